@@ -1,0 +1,208 @@
+"""ctypes wrapper of the CPU oracle (oracle/oracle.cpp).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module.  The product path
+(paper_1909_00145_b200/) never imports it and shares no code with it.
+
+Every function takes/returns numpy arrays in the layouts of include/csc.h:
+x[N][H][W], d[K][s][s], z[N][K][H+s-1][W+s-1] (C-contiguous).  dtype float32
+selects the fp32-state oracle (parity with the GPU), float64 the exact-arithmetic
+build used by the pins.  Sums always accumulate in fp64.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+_c_i64 = ctypes.c_int64
+_c_dbl = ctypes.c_double
+_c_u64 = ctypes.c_uint64
+_c_u32 = ctypes.c_uint32
+_vp = ctypes.c_void_p
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with the oracle's own Makefile (g++ -O2 -fopenmp)."""
+    src = os.path.join(_HERE, "oracle.cpp")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE, "liboracle.so"], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB_PATH)
+            L.oracle_num_threads.restype = ctypes.c_int
+            L.oracle_philox4x32_10.argtypes = [_vp, _vp, _vp]
+            L.oracle_philox_batch.argtypes = [_c_i64, _vp, _vp, _vp]
+            L.oracle_mask_threshold.argtypes = [_c_dbl]
+            L.oracle_mask_threshold.restype = _c_u64
+            L.oracle_mask_bits.argtypes = [_c_i64, _c_i64, _c_i64, _c_dbl, _c_u64, _c_u32, _vp]
+            L.oracle_soft_threshold.argtypes = [_c_dbl, _c_dbl]
+            L.oracle_soft_threshold.restype = _c_dbl
+            for suf in ("f32", "f64"):
+                getattr(L, f"oracle_residual_{suf}").argtypes = [_c_i64] * 5 + [_vp] * 4
+                getattr(L, f"oracle_dtr_{suf}").argtypes = [_c_i64] * 5 + [_vp] * 3
+                getattr(L, f"oracle_filter_grad_{suf}").argtypes = [_c_i64] * 5 + [_vp] * 3
+                f = getattr(L, f"oracle_lipschitz_{suf}")
+                f.argtypes = [_c_i64, _c_i64, _vp]
+                f.restype = _c_dbl
+                getattr(L, f"oracle_code_step_{suf}").argtypes = (
+                    [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, _c_u64, _c_u32, _vp])
+                getattr(L, f"oracle_filter_step_{suf}").argtypes = (
+                    [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _vp, _vp, _vp])
+                getattr(L, f"oracle_objective_{suf}").argtypes = [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _vp]
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_vp)
+
+
+def _suf(dtype) -> str:
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return "f32"
+    if dt == np.float64:
+        return "f64"
+    raise TypeError(f"oracle supports float32/float64 state, got {dt}")
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    ctr = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
+    key = np.ascontiguousarray(key, dtype=np.uint32).reshape(-1, 2)
+    out = np.empty_like(ctr)
+    lib().oracle_philox_batch(ctr.shape[0], _p(ctr), _p(key), _p(out))
+    return out
+
+
+def mask_threshold(p: float) -> int:
+    return int(lib().oracle_mask_threshold(float(p)))
+
+
+def mask_bits(K: int, Hc: int, Wc: int, p: float, seed: int, t: int) -> np.ndarray:
+    total = K * Hc * Wc
+    out = np.zeros((total + 31) // 32, dtype=np.uint32)
+    lib().oracle_mask_bits(K, Hc, Wc, float(p), int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(out))
+    return out
+
+
+def unpack_mask(bits: np.ndarray, K: int, Hc: int, Wc: int) -> np.ndarray:
+    """Bool mask [K][Hc][Wc] from the ABI bit layout (bit l of word l>>5, LSB first)."""
+    b = np.unpackbits(bits.view(np.uint8), bitorder="little")[: K * Hc * Wc]
+    return b.reshape(K, Hc, Wc).astype(bool)
+
+
+def soft_threshold(w: float, kappa: float) -> float:
+    return float(lib().oracle_soft_threshold(float(w), float(kappa)))
+
+
+def residual(x, d, z, dtype=np.float32) -> np.ndarray:
+    """r = sum_k d_k * z_k - x (valid true convolution).  x may be None (-> Dz)."""
+    d = _c(d, dtype); z = _c(z, dtype)
+    N, K, Hc, Wc = z.shape
+    s = d.shape[-1]
+    H, W = Hc - s + 1, Wc - s + 1
+    xx = _c(x, dtype) if x is not None else None
+    r = np.empty((N, H, W), dtype=dtype)
+    getattr(lib(), f"oracle_residual_{_suf(dtype)}")(N, K, s, H, W, _p(xx) if xx is not None else None,
+                                                   _p(d), _p(z), _p(r))
+    return r
+
+
+def dtr(d, r, dtype=np.float64) -> np.ndarray:
+    """D^T r for all codes: out[n,k,u,v] = sum_ab d[k,a,b] r[n,u-P+a,v-P+b]."""
+    d = _c(d, dtype); r = _c(r, dtype)
+    N, H, W = r.shape
+    K, s, _ = d.shape
+    out = np.empty((N, K, H + s - 1, W + s - 1), dtype=dtype)
+    getattr(lib(), f"oracle_dtr_{_suf(dtype)}")(N, K, s, H, W, _p(d), _p(r), _p(out))
+    return out
+
+
+def filter_grad(r, z, dtype=np.float64) -> np.ndarray:
+    """g[k,a,b] = sum_n sum_ij r[n,i,j] z[n,k,i+P-a,j+P-b] (fp64)."""
+    r = _c(r, dtype); z = _c(z, dtype)
+    N, K, Hc, Wc = z.shape
+    H, W = r.shape[1:]
+    s = Hc - H + 1
+    g = np.empty((K, s, s), dtype=np.float64)
+    getattr(lib(), f"oracle_filter_grad_{_suf(dtype)}")(N, K, s, H, W, _p(r), _p(z), _p(g))
+    return g
+
+
+def lipschitz(d, dtype=np.float32) -> float:
+    d = _c(d, dtype)
+    K, s, _ = d.shape
+    return float(getattr(lib(), f"oracle_lipschitz_{_suf(dtype)}")(K, s, _p(d)))
+
+
+def code_step(x, d, z, lam, step_z, p, seed, t, dtype=np.float32):
+    """One masked prox-gradient code step.  Returns (z_new, tau_used)."""
+    x = _c(x, dtype); d = _c(d, dtype)
+    z = np.array(z, dtype=dtype, copy=True, order="C")
+    N, K, Hc, Wc = z.shape
+    s = d.shape[-1]
+    H, W = Hc - s + 1, Wc - s + 1
+    tau = np.zeros(1, dtype=np.float64)
+    getattr(lib(), f"oracle_code_step_{_suf(dtype)}")(
+        N, K, s, H, W, _p(x), _p(d), _p(z), float(lam), float(step_z), float(p),
+        int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(tau))
+    return z, float(tau[0])
+
+
+def filter_step(x, d, z, step_d=0.0, dtype=np.float32):
+    """One projected-gradient filter step.  Returns (d_new, tau_used, g_fp64, ||Zg||^2)."""
+    x = _c(x, dtype); z = _c(z, dtype)
+    d = np.array(d, dtype=dtype, copy=True, order="C")
+    N, K, Hc, Wc = z.shape
+    s = d.shape[-1]
+    H, W = Hc - s + 1, Wc - s + 1
+    tau = np.zeros(1, dtype=np.float64)
+    g = np.zeros((K, s, s), dtype=np.float64)
+    zg2 = np.zeros(1, dtype=np.float64)
+    getattr(lib(), f"oracle_filter_step_{_suf(dtype)}")(
+        N, K, s, H, W, _p(x), _p(d), _p(z), float(step_d), _p(tau), _p(g), _p(zg2))
+    return d, float(tau[0]), g, float(zg2[0])
+
+
+def objective(x, d, z, lam, dtype=np.float32):
+    """(F, 1/2||Dz-x||^2, lam*||z||_1) in fp64."""
+    x = _c(x, dtype); d = _c(d, dtype); z = _c(z, dtype)
+    N, K, Hc, Wc = z.shape
+    s = d.shape[-1]
+    H, W = Hc - s + 1, Wc - s + 1
+    out = np.zeros(3, dtype=np.float64)
+    getattr(lib(), f"oracle_objective_{_suf(dtype)}")(N, K, s, H, W, _p(x), _p(d), _p(z), float(lam),
+                                                     _p(out))
+    return float(out[0]), float(out[1]), float(out[2])
+
+
+def iteration(x, d, z, lam, p, seed, t, step_z=0.0, step_d=0.0, dtype=np.float32):
+    """One SBCSC outer iteration (Alg.1): code step with mask t,
+    filter step, then the Eq.1 objective with the new (z, d).  Returns a dict."""
+    z1, tau_z = code_step(x, d, z, lam, step_z, p, seed, t, dtype=dtype)
+    d1, tau_d, g, zg2 = filter_step(x, d, z1, step_d, dtype=dtype)
+    F = objective(x, d1, z1, lam, dtype=dtype)
+    return {"z": z1, "d": d1, "tau_z": tau_z, "tau_d": tau_d, "g": g, "zg2": zg2, "F": F}

@@ -1,0 +1,387 @@
+// oracle/oracle.cpp -- CPU ORACLE FOR THE STOCHASTIC SPATIAL-DOMAIN CSC HOT PATH.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+// cpu_baseline / --impl reference legs of bench.py may load this library.  The
+// product path (paper_1909_00145_b200/) never links, imports or executes it,
+// and this file shares no code, header, table or constant generator with it.
+//
+// Plain nested loops in the paper's order and notation.  State (x, d, z, r) is
+// stored in T (float for parity with the GPU, double for the exact-arithmetic
+// pins); every sum accumulates in double; each stored value is rounded once.
+//
+// Citations: P:n = PAPER.md line n (arxiv 1909.00145 LaTeX), with section /
+// equation.  Readings R1..R9 and #1..#17 are listed in DESIGN.md §3.
+//
+// Notation (§2-3): N images x_n (H x W), K filters d_k (s x s,
+// M = s^2), codes z_{n,k} of (H+s-1) x (W+s-1) (reading R3: "valid" true
+// convolution, non-circular boundary), P = s-1.
+//
+// Pinned by tests/test_oracle_*.py (curand Philox, dense Toeplitz brute force,
+// scipy convolve2d/correlate2d, adjoint identities, closed-form shrinkage,
+// textbook ISTA at p=1, monotone descent, 1-D line-search optimality, numpy FFT
+// for the DTFT bound).  The 50-iteration trajectory as a whole is "parity
+// unpinned" beyond those pins: the paper prints no per-iteration value.
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+#include <omp.h>
+
+namespace {
+
+struct Dims {
+  int64_t N, K, s, H, W, Hc, Wc, P;
+  Dims(int64_t N_, int64_t K_, int64_t s_, int64_t H_, int64_t W_)
+      : N(N_), K(K_), s(s_), H(H_), W(W_), Hc(H_ + s_ - 1), Wc(W_ + s_ - 1), P(s_ - 1) {}
+  int64_t xi(int64_t n, int64_t i, int64_t j) const { return (n * H + i) * W + j; }
+  int64_t di(int64_t k, int64_t a, int64_t b) const { return (k * s + a) * s + b; }
+  int64_t zi(int64_t n, int64_t k, int64_t u, int64_t v) const {
+    return ((n * K + k) * Hc + u) * Wc + v;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11), written from the
+// algorithm: 10 rounds of  (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2,
+// c <- (hi1^c1^k0, lo1, hi0^c3^k1, lo0), with the Weyl key bump (W0, W1)
+// between rounds.  Pinned bit-exact against curand_Philox4x32_10.
+// ---------------------------------------------------------------------------
+void philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+  uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) { k0 += W0; k1 += W1; }
+    const uint64_t p0 = (uint64_t)M0 * (uint64_t)c0;
+    const uint64_t p1 = (uint64_t)M1 * (uint64_t)c2;
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// Domain tag of the mask counter (reading R4 / DESIGN.md #13): the 4th counter
+// word.  Arbitrary, chosen once ("CSCM").
+const uint32_t kMaskTag = 0x4353434Du;
+
+// thr = floor(p * 2^32) in double, as uint64 (p = 1 -> 2^32: everything selected,
+// M^t = identity).
+uint64_t mask_threshold(double p) { return (uint64_t)std::floor(p * 4294967296.0); }
+
+// Eq.2, reading R4/R5: i.i.d. Bernoulli(p) per code coordinate
+// l = (k*Hc + u)*Wc + v, one mask per iteration t shared by all images.
+bool mask_bit(uint64_t seed, uint32_t t, uint64_t l, uint64_t thr) {
+  const uint64_t q = l >> 2;
+  const uint32_t ctr[4] = {(uint32_t)(q & 0xffffffffu), (uint32_t)(q >> 32), t, kMaskTag};
+  const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+  uint32_t w[4];
+  philox4x32_10(ctr, key, w);
+  return (uint64_t)w[l & 3] < thr;
+}
+
+// Dz - x  (Sec.3.1 P:191-197 "D z = sum_k d_k * z_k", fit term of Eq.1):
+//   r[n,i,j] = sum_k sum_{a,b} d[k,a,b] z[n,k,i+P-a,j+P-b] - x[n,i,j]
+// a "valid" true convolution: every tap lands inside the code map.
+template <typename T>
+void residual(const Dims& D, const T* x, const T* d, const T* z, T* r) {
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < D.N; ++n)
+    for (int64_t i = 0; i < D.H; ++i)
+      for (int64_t j = 0; j < D.W; ++j) {
+        double acc = 0.0;
+        for (int64_t k = 0; k < D.K; ++k)
+          for (int64_t a = 0; a < D.s; ++a)
+            for (int64_t b = 0; b < D.s; ++b)
+              acc += (double)d[D.di(k, a, b)] * (double)z[D.zi(n, k, i + D.P - a, j + D.P - b)];
+        r[D.xi(n, i, j)] = (T)(acc - (x ? (double)x[D.xi(n, i, j)] : 0.0));
+      }
+}
+
+// (D^T r)[n,k,u,v] = sum_{a,b} d[k,a,b] r[n, u-P+a, v-P+b]  (r == 0 outside the
+// image): the gradient of the fit term of Eq.3 w.r.t. code (k,u,v).
+inline double dtr_at(const Dims& D, const double* dk, const double* rn, int64_t u, int64_t v) {
+  double c = 0.0;
+  for (int64_t a = 0; a < D.s; ++a) {
+    const int64_t i = u - D.P + a;
+    if (i < 0 || i >= D.H) continue;
+    for (int64_t b = 0; b < D.s; ++b) {
+      const int64_t j = v - D.P + b;
+      if (j < 0 || j >= D.W) continue;
+      c += dk[a * D.s + b] * rn[i * D.W + j];
+    }
+  }
+  return c;
+}
+
+// D^T r for every code coordinate (all n, k, u, v), stored in T.
+template <typename T>
+void dtr_all(const Dims& D, const T* d, const T* r, T* out) {
+  std::vector<double> dd((size_t)(D.K * D.s * D.s)), rd((size_t)(D.N * D.H * D.W));
+  for (size_t q = 0; q < dd.size(); ++q) dd[q] = (double)d[q];
+  for (size_t q = 0; q < rd.size(); ++q) rd[q] = (double)r[q];
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t n = 0; n < D.N; ++n)
+    for (int64_t k = 0; k < D.K; ++k)
+      for (int64_t u = 0; u < D.Hc; ++u)
+        for (int64_t v = 0; v < D.Wc; ++v)
+          out[D.zi(n, k, u, v)] = (T)dtr_at(D, &dd[k * D.s * D.s], &rd[n * D.H * D.W], u, v);
+}
+
+// Soft threshold, the prox of kappa*||.||_1 ("point-wise shrinkage"):
+// S(w,kappa) = w-kappa (w>kappa), w+kappa (w<-kappa), +0.0 otherwise (#12).
+inline double soft_threshold(double w, double kappa) {
+  if (w > kappa) return w - kappa;
+  if (w < -kappa) return w + kappa;
+  return 0.0;
+}
+
+// Lipschitz bound of the code gradient (reading R8, #7):
+//   L_D = max_{m1,m2 in [0,64)} sum_k | sum_{a,b} d[k,a,b] e^{-2 pi i (a m1 + b m2)/64} |^2
+template <typename T>
+double lipschitz_dtft(const Dims& D, const T* d) {
+  const int G = 64;
+  double best = 0.0;
+  for (int m1 = 0; m1 < G; ++m1)
+    for (int m2 = 0; m2 < G; ++m2) {
+      double tot = 0.0;
+      for (int64_t k = 0; k < D.K; ++k) {
+        double re = 0.0, im = 0.0;
+        for (int64_t a = 0; a < D.s; ++a)
+          for (int64_t b = 0; b < D.s; ++b) {
+            const double ang = -2.0 * M_PI * (double)((a * m1 + b * m2) % G) / (double)G;
+            const double v = (double)d[D.di(k, a, b)];
+            re += v * std::cos(ang);
+            im += v * std::sin(ang);
+          }
+        tot += re * re + im * im;
+      }
+      best = std::max(best, tot);
+    }
+  return best;
+}
+
+// One masked proximal-gradient step on the codes (reading R1): Eq.3
+// restricted by M^t (Eq.2) and upsampled in place (Eq.4, reading R2: unsampled
+// codes keep their values).
+template <typename T>
+void code_step(const Dims& D, const T* x, const T* d, T* z, double lam, double step_z, double p,
+               uint64_t seed, uint32_t t, double* tau_used) {
+  std::vector<T> r((size_t)(D.N * D.H * D.W));
+  residual<T>(D, x, d, z, r.data());
+  const T tau_t = step_z > 0.0 ? (T)step_z : (T)(1.0 / lipschitz_dtft<T>(D, d));
+  const double tau = (double)tau_t;
+  const double kappa = tau * lam;
+  const uint64_t thr = mask_threshold(p);
+  std::vector<double> rd(r.size());
+  for (size_t q = 0; q < r.size(); ++q) rd[q] = (double)r[q];
+  std::vector<double> dd((size_t)(D.K * D.s * D.s));
+  for (size_t q = 0; q < dd.size(); ++q) dd[q] = (double)d[q];
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t n = 0; n < D.N; ++n)
+    for (int64_t k = 0; k < D.K; ++k)
+      for (int64_t u = 0; u < D.Hc; ++u)
+        for (int64_t v = 0; v < D.Wc; ++v) {
+          const uint64_t l = (uint64_t)((k * D.Hc + u) * D.Wc + v);
+          if (!mask_bit(seed, t, l, thr)) continue;
+          const double c = dtr_at(D, &dd[k * D.s * D.s], &rd[n * D.H * D.W], u, v);
+          const int64_t zi = D.zi(n, k, u, v);
+          const double w = (double)z[zi] - tau * c;
+          z[zi] = (T)soft_threshold(w, kappa);
+        }
+  if (tau_used) *tau_used = tau;
+}
+
+// g[k,a,b] = sum_n sum_{i,j} r[n,i,j] z[n,k,i+P-a,j+P-b]: the gradient of the
+// Eq.5 fit term 1/2||x - Z d||^2 with r = Z d - x.
+void filter_grad(const Dims& D, const double* r, const double* zd, double* g) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < D.K; ++k)
+    for (int64_t a = 0; a < D.s; ++a)
+      for (int64_t b = 0; b < D.s; ++b) {
+        double acc = 0.0;
+        for (int64_t n = 0; n < D.N; ++n)
+          for (int64_t i = 0; i < D.H; ++i)
+            for (int64_t j = 0; j < D.W; ++j)
+              acc += r[(n * D.H + i) * D.W + j] *
+                     zd[((n * D.K + k) * D.Hc + i + D.P - a) * D.Wc + j + D.P - b];
+        g[D.di(k, a, b)] = acc;
+      }
+}
+
+// ||Z g||^2 with (Z g)[n,i,j] = sum_k sum_{a,b} g[k,a,b] z[n,k,i+P-a,j+P-b].
+double zg_sq(const Dims& D, const double* g, const double* zd) {
+  std::vector<double> part((size_t)D.N, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < D.N; ++n) {
+    double s2 = 0.0;
+    for (int64_t i = 0; i < D.H; ++i)
+      for (int64_t j = 0; j < D.W; ++j) {
+        double acc = 0.0;
+        for (int64_t k = 0; k < D.K; ++k)
+          for (int64_t a = 0; a < D.s; ++a)
+            for (int64_t b = 0; b < D.s; ++b)
+              acc += g[D.di(k, a, b)] * zd[((n * D.K + k) * D.Hc + i + D.P - a) * D.Wc + j + D.P - b];
+        s2 += acc * acc;
+      }
+    part[n] = s2;
+  }
+  double tot = 0.0;
+  for (int64_t n = 0; n < D.N; ++n) tot += part[n];
+  return tot;
+}
+
+// One projected-gradient step on the filters (reading R6) for Eq.5 with the
+// unit-ball constraint of Eq.1 (reading R7), exact line search (R8).
+template <typename T>
+void filter_step(const Dims& D, const T* x, T* d, const T* z, double step_d, double* tau_used,
+                 double* g_out, double* zg2_out) {
+  std::vector<T> rt((size_t)(D.N * D.H * D.W));
+  residual<T>(D, x, d, z, rt.data());
+  std::vector<double> r(rt.size());
+  for (size_t q = 0; q < r.size(); ++q) r[q] = (double)rt[q];
+  const size_t nz = (size_t)(D.N * D.K * D.Hc * D.Wc);
+  std::vector<double> zd(nz);
+  for (size_t q = 0; q < nz; ++q) zd[q] = (double)z[q];
+  const size_t nd = (size_t)(D.K * D.s * D.s);
+  std::vector<double> g(nd);
+  filter_grad(D, r.data(), zd.data(), g.data());
+  double tau;
+  double zg2 = 0.0;
+  if (step_d > 0.0) {
+    tau = (double)(T)step_d;
+  } else {
+    double gg = 0.0;
+    for (size_t q = 0; q < nd; ++q) gg += g[q] * g[q];
+    zg2 = zg_sq(D, g.data(), zd.data());
+    tau = zg2 > 0.0 ? (double)(T)(gg / zg2) : 0.0;
+  }
+  const int64_t M = D.s * D.s;
+  for (int64_t k = 0; k < D.K; ++k) {
+    std::vector<double> e((size_t)M);
+    double nrm2 = 0.0;
+    for (int64_t m = 0; m < M; ++m) {
+      e[m] = (double)d[k * M + m] - tau * g[k * M + m];
+      nrm2 += e[m] * e[m];
+    }
+    const double scale = std::max(1.0, std::sqrt(nrm2));
+    for (int64_t m = 0; m < M; ++m) d[k * M + m] = (T)(e[m] / scale);
+  }
+  if (tau_used) *tau_used = tau;
+  if (g_out) std::memcpy(g_out, g.data(), nd * sizeof(double));
+  if (zg2_out) *zg2_out = zg2;
+}
+
+// Eq.1 objective: F = sum_n 1/2||x_n - sum_k d_k * z_{n,k}||^2 + lam sum ||z||_1.
+template <typename T>
+void objective(const Dims& D, const T* x, const T* d, const T* z, double lam, double out[3]) {
+  std::vector<double> h((size_t)D.N, 0.0), l1((size_t)D.N, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < D.N; ++n) {
+    double s2 = 0.0;
+    for (int64_t i = 0; i < D.H; ++i)
+      for (int64_t j = 0; j < D.W; ++j) {
+        double acc = 0.0;
+        for (int64_t k = 0; k < D.K; ++k)
+          for (int64_t a = 0; a < D.s; ++a)
+            for (int64_t b = 0; b < D.s; ++b)
+              acc += (double)d[D.di(k, a, b)] * (double)z[D.zi(n, k, i + D.P - a, j + D.P - b)];
+        const double rr = acc - (double)x[D.xi(n, i, j)];
+        s2 += rr * rr;
+      }
+    double a1 = 0.0;
+    for (int64_t k = 0; k < D.K; ++k)
+      for (int64_t u = 0; u < D.Hc; ++u)
+        for (int64_t v = 0; v < D.Wc; ++v) a1 += std::fabs((double)z[D.zi(n, k, u, v)]);
+    h[n] = 0.5 * s2;
+    l1[n] = a1;
+  }
+  double hs = 0.0, ls = 0.0;
+  for (int64_t n = 0; n < D.N; ++n) { hs += h[n]; ls += l1[n]; }
+  out[1] = hs;
+  out[2] = lam * ls;
+  out[0] = out[1] + out[2];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C interface (ctypes).  All pointers are host pointers to contiguous arrays:
+// x[N][H][W], d[K][s][s], z[N][K][H+s-1][W+s-1], r[N][H][W].
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int oracle_num_threads() { return omp_get_max_threads(); }
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  philox4x32_10(ctr, key, out);
+}
+
+void oracle_philox_batch(int64_t count, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+  for (int64_t q = 0; q < count; ++q) philox4x32_10(ctr + 4 * q, key + 2 * q, out + 4 * q);
+}
+
+uint64_t oracle_mask_threshold(double p) { return mask_threshold(p); }
+
+// Mask bits in the ABI layout: bit l of word l>>5 (LSB first).
+void oracle_mask_bits(int64_t K, int64_t Hc, int64_t Wc, double p, uint64_t seed, uint32_t t,
+                      uint32_t* bits) {
+  const uint64_t total = (uint64_t)(K * Hc * Wc);
+  const uint64_t nwords = (total + 31) / 32;
+  const uint64_t thr = mask_threshold(p);
+#pragma omp parallel for schedule(static)
+  for (int64_t wi = 0; wi < (int64_t)nwords; ++wi) {
+    uint32_t word = 0;
+    for (uint64_t bit = 0; bit < 32; ++bit) {
+      const uint64_t l = (uint64_t)wi * 32 + bit;
+      if (l < total && mask_bit(seed, t, l, thr)) word |= (1u << bit);
+    }
+    bits[wi] = word;
+  }
+}
+
+double oracle_soft_threshold(double w, double kappa) { return soft_threshold(w, kappa); }
+
+#define ORACLE_EXPORTS(T, SUF)                                                                    \
+  void oracle_residual_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W, const T* x,  \
+                             const T* d, const T* z, T* r) {                                     \
+    residual<T>(Dims(N, K, s, H, W), x, d, z, r);                                                \
+  }                                                                                              \
+  void oracle_dtr_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W, const T* d,       \
+                        const T* r, T* out) {                                                    \
+    dtr_all<T>(Dims(N, K, s, H, W), d, r, out);                                                  \
+  }                                                                                              \
+  void oracle_filter_grad_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,           \
+                                const T* r, const T* z, double* g) {                             \
+    Dims D(N, K, s, H, W);                                                                       \
+    std::vector<double> rd((size_t)(N * H * W)), zd((size_t)(N * K * D.Hc * D.Wc));              \
+    for (size_t q = 0; q < rd.size(); ++q) rd[q] = (double)r[q];                                  \
+    for (size_t q = 0; q < zd.size(); ++q) zd[q] = (double)z[q];                                  \
+    filter_grad(D, rd.data(), zd.data(), g);                                                     \
+  }                                                                                              \
+  double oracle_lipschitz_##SUF(int64_t K, int64_t s, const T* d) {                              \
+    return lipschitz_dtft<T>(Dims(1, K, s, s, s), d);                                            \
+  }                                                                                              \
+  void oracle_code_step_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W, const T* x, \
+                              const T* d, T* z, double lam, double step_z, double p,             \
+                              uint64_t seed, uint32_t t, double* tau_used) {                     \
+    code_step<T>(Dims(N, K, s, H, W), x, d, z, lam, step_z, p, seed, t, tau_used);              \
+  }                                                                                              \
+  void oracle_filter_step_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,           \
+                                const T* x, T* d, const T* z, double step_d, double* tau_used,   \
+                                double* g_out, double* zg2_out) {                                \
+    filter_step<T>(Dims(N, K, s, H, W), x, d, z, step_d, tau_used, g_out, zg2_out);             \
+  }                                                                                              \
+  void oracle_objective_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W, const T* x, \
+                              const T* d, const T* z, double lam, double out[3]) {               \
+    objective<T>(Dims(N, K, s, H, W), x, d, z, lam, out);                                        \
+  }
+
+ORACLE_EXPORTS(float, f32)
+ORACLE_EXPORTS(double, f64)
+
+}  // extern "C"
