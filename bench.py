@@ -1,0 +1,337 @@
+"""bench.py -- CSC iterations/s on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config sweep] [--p 0.1] [--impl ours|reference]
+
+A step is one SBCSC outer iteration (Alg.1) over the whole
+hot path (every SURVEY.md §8(a) row): Philox mask + masked prox-gradient code
+step, filter gradient + exact line search + unit-ball projection, Eq.1
+objective -- through the C ABI call csc_iterate.
+
+Default workload: config 3 "sweep" (BASELINE.json configs[2]) at p = 0.1:
+K=100 filters 11x11, N=40 images 256x256, codes 100x266x266 per image (1.13 GB,
+larger than the 126 MB L2, so no L2 flush is needed between steps).  It is the
+largest configuration whose iteration fits one GPU in a few ms and the one
+SURVEY.md §8(d) designates for HBM claims; configs[1] ("batch", 48 MB of codes)
+is L2-resident and is reported with --config batch.  See DESIGN.md §6.
+
+Multi-GPU (torchrun, one process per GPU): the N images are sharded across
+ranks (strong scaling of the fixed problem); the filter gradient and the
+objective parts are all-reduced with NCCL inside the library.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+SMS = 148
+FP32_LANES_PER_SM = 128
+
+
+def _peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), float(pk.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, flag in zip(names, parts[5:9]):
+                    if flag.lower().startswith("active"):
+                        reasons.add(nm)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only)."""
+    import numpy as np
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    import oracle
+    from synth import config_by_name, make_codes, make_filters, make_images, mask_seed
+    cfg = config_by_name(args.config, args.p)
+    n_img = max(1, min(cfg.N, args.ref_images))
+    sub = cfg.with_(N=n_img)
+    x, d, z = make_images(sub), make_filters(sub), make_codes(sub)
+    seed = mask_seed(cfg)
+    for t in range(1, args.warmup + 1):
+        it = oracle.iteration(x, d, z, cfg.lam, cfg.p, seed, t)
+        z, d = it["z"], it["d"]
+    times = []
+    for t in range(args.warmup + 1, args.warmup + 1 + args.steps):
+        t0 = time.perf_counter()
+        it = oracle.iteration(x, d, z, cfg.lam, cfg.p, seed, t)
+        times.append(time.perf_counter() - t0)
+        z, d = it["z"], it["d"]
+    per_sample = sum(times) / len(times)
+    per_full = per_sample * cfg.N / n_img  # the per-image passes dominate; scaled to the full workload
+    value = 1.0 / per_full
+    cores = oracle.num_threads()
+    line = {
+        "impl": "reference", "metric": "csc_iterations_per_s", "value": value, "unit": "it/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_full * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64-accum/f32-state",
+        "data": "synthetic", "config": _config_dict(cfg, ws),
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} oracle iterations on {n_img} of {cfg.N} images "
+                                   f"(scaled x{cfg.N / n_img:g}); {per_sample:.2f} s per sampled iteration"},
+        "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(cfg, ws):
+    return {"workload": f"{cfg.name} (BASELINE.json configs[{cfg.index - 1}]) p={cfg.p:g}",
+            "K": cfg.K, "s": cfg.s, "N": cfg.N, "H": cfg.H, "W": cfg.W, "p": cfg.p, "lambda": cfg.lam,
+            "codes_bytes": 4 * cfg.N * cfg.K * cfg.Hc * cfg.Wc, "global_batch": cfg.N,
+            "parallelism": f"dp{ws} (images sharded)",
+            "l2": "inputs larger than L2 (no flush)" if 4 * cfg.N * cfg.K * cfg.Hc * cfg.Wc > 126e6 * 2
+            else "L2 flushed between steps"}
+
+
+def _cpu_baseline(cfg, n_img=2):
+    """Oracle on a bounded sample (rank 0, N=1 only): one iteration on n_img images, scaled."""
+    import oracle
+    from synth import make_codes, make_filters, make_images, mask_seed
+    sub = cfg.with_(N=n_img)
+    x, d, z = make_images(sub), make_filters(sub), make_codes(sub)
+    t0 = time.perf_counter()
+    oracle.iteration(x, d, z, cfg.lam, cfg.p, mask_seed(cfg), 1)
+    dt = time.perf_counter() - t0
+    per_full = dt * cfg.N / n_img
+    return {"value": 1.0 / per_full, "unit": "it/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"1 oracle iteration (iteration 1) on {n_img} of {cfg.N} images, {dt:.2f} s, "
+                      f"scaled x{cfg.N / n_img:g} to the full workload"}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1909_00145_b200 as pkg
+    from synth import config_by_name, make_codes, make_filters, make_images, mask_seed
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = config_by_name(args.config, args.p)
+    n0 = (rank * cfg.N) // ws
+    n1 = ((rank + 1) * cfg.N) // ws
+    nl = n1 - n0
+    x_np = make_images(cfg, n0, nl)
+    d_np = make_filters(cfg)
+    seed = mask_seed(cfg)
+    x = torch.from_numpy(x_np).to(dev)
+    d = torch.from_numpy(d_np).to(dev)
+    z = torch.zeros((nl, cfg.K, cfg.Hc, cfg.Wc), dtype=torch.float32, device=dev)
+    nccl_id = None
+    if ws > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(pkg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    stream = torch.cuda.current_stream(dev)
+    ctx = pkg.Context(nl, cfg.K, cfg.s, cfg.H, cfg.W, world=ws, rank=rank, device=local, stream=stream,
+                      nccl_id=nccl_id)
+    l2_flush = None
+    if 4 * cfg.N * cfg.K * cfg.Hc * cfg.Wc <= 2 * 126e6:
+        l2_flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier(device_ids=[local])
+
+    it = 0
+    for _ in range(args.warmup):
+        it += 1
+        ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs
+    ctx.profile_enable(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count
+    t_total = 0.0
+    objs = []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        it += 1
+        if l2_flush is not None:
+            l2_flush.fill_(float(it))
+        ev0.record(stream)
+        obj, taus = ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it)
+        ev1.record(stream)
+        ev1.synchronize()
+        t_total += ev0.elapsed_time(ev1)
+        objs.append(obj[0])
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launch_count - l0
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    value = args.steps / (t_ms / 1e3)
+
+    # ---- e2e: same iteration through the C ABI with the step's images uploaded from pinned host memory
+    x_host = torch.from_numpy(x_np).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        it += 1
+        if l2_flush is not None:
+            l2_flush.fill_(float(it))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it, x_host=x_host)
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = args.steps / (float(te.item()) / 1e3)
+
+    if rank == 0:
+        hbm_gbs, sm_max_mhz, peak_kind = _peaks()
+        # dominant kernel: the dense convolution pass (3 launches per iteration)
+        conv_ms, conv_n = prof["conv"]
+        conv_avg_ms = conv_ms / max(conv_n, 1)
+        flops_per_launch = 2.0 * nl * cfg.K * cfg.s * cfg.s * cfg.H * cfg.W
+        fp32_peak = SMS * FP32_LANES_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12
+        achieved = flops_per_launch / (conv_avg_ms / 1e3) / 1e12
+        # masked code step against HBM (sector model of SURVEY.md §8(d))
+        cs_ms, cs_n = prof["code_step"]
+        cs_avg = cs_ms / max(cs_n, 1)
+        codes = nl * cfg.K * cfg.Hc * cfg.Wc
+        sector_bytes = 8.0 * (1.0 - (1.0 - cfg.p) ** 8) * codes + 12.0 * nl * cfg.H * cfg.W
+        cs_gbs = sector_bytes / (cs_avg / 1e3) / 1e9
+        step_ms = t_ms / args.steps
+        kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                       "share": v[0] / max(t_total, 1e-9)} for k, v in prof.items()}
+        line = {
+            "metric": "csc_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": _config_dict(cfg, ws),
+            "roofline": {"kernel": "conv_fwd_kernel (dense residual / Zg pass, SIMT FP32)", "bound": "alu",
+                         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                         "frac": achieved / fp32_peak, "traffic": None,
+                         "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived, DESIGN.md §5)",
+                         "algorithmic_per_launch": flops_per_launch, "avg_launch_ms": conv_avg_ms},
+            "code_step_roofline": {"bound": "hbm", "achieved": cs_gbs, "peak": hbm_gbs, "unit": "GB/s",
+                                   "frac": cs_gbs / hbm_gbs, "peak_kind": peak_kind,
+                                   "algorithmic_bytes_per_launch": sector_bytes, "avg_launch_ms": cs_avg,
+                                   "model": "sector: 8(1-(1-p)^8) N K Hc Wc + 12 N H W"},
+            "kernels": kernels,
+            "objective_last": objs[-1] if objs else None,
+            "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": 4 * nl * cfg.H * cfg.W,
+                    "d2h_bytes_per_step": 80},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = _cpu_baseline(cfg, args.cpu_images)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="sweep")
+    ap.add_argument("--p", type=float, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-images", type=int, default=1)
+    ap.add_argument("--cpu-images", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,176 @@
+/* include/csc.h -- C ABI of the B200-native stochastic spatial-domain CSC hot path.
+ *
+ * Method: arxiv 1909.00145 ("Stochastic Convolutional Sparse Coding"), PAPER.md.
+ * Citations "P:n" are PAPER.md line numbers with section/equation; readings
+ * R1..R9 and #1..#17 are listed in DESIGN.md §3.
+ *
+ * Problem (Eq.1):  min_{d,z} sum_n 1/2||x_n - sum_k d_k * z_{n,k}||^2
+ *                                       + lambda sum_{n,k} ||z_{n,k}||_1,  ||d_k||_2 <= 1.
+ *
+ * LAYOUTS (all row-major, contiguous, fp32, 16-byte aligned device pointers):
+ *   x  [n_local][H][W]                    images of THIS rank
+ *   d  [K][s][s]                          filters, replicated on every rank
+ *   z  [n_local][K][H+s-1][W+s-1]         codes of THIS rank (reading R3: the
+ *                                         reconstruction is a "valid" true
+ *                                         convolution, no circular boundary)
+ *   residual r = sum_k d_k * z_k - x      [n_local][H][W], library-owned cache.
+ *
+ * OWNERSHIP: x, d, z are caller-owned DEVICE pointers (e.g. torch
+ * data_ptr()).  csc_code_step mutates z in place, csc_filter_step mutates d in
+ * place.  The library owns all scratch, allocated once in csc_init; steps never
+ * allocate, so a step sequence can be captured in a CUDA graph.
+ *
+ * ASYNCHRONY: everything is enqueued on dims.stream (a cudaStream_t).  Only
+ * csc_objective, csc_iterate and a non-NULL step_used pointer synchronise.
+ *
+ * COLLECTIVES (world > 1): every rank must call csc_filter_step, csc_objective
+ * and csc_iterate in the same order; csc_code_step is rank-local.  The mask is a
+ * counter-based function of (seed, iter, k, u, v), identical on every rank with
+ * no communication.
+ *
+ * ERRORS: every call returns csc_status.  Argument violations return
+ * CSC_ERR_ARG and have no side effects; csc_last_error(ctx) gives a message.
+ * There is NO CPU fallback: without a CUDA device csc_init fails with
+ * CSC_ERR_CUDA.
+ *
+ * RESIDUAL CACHE: the library caches r with the (x, d, z) pointers it was
+ * computed from.  A different pointer, or csc_invalidate, forces a dense
+ * recompute.  A caller that modifies x/d/z outside the API must call
+ * csc_invalidate.
+ */
+#ifndef CSC_H_
+#define CSC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSC_ABI_VERSION 1
+
+typedef enum {
+  CSC_OK = 0,
+  CSC_ERR_ARG = 1,       /* invalid argument (no side effects) */
+  CSC_ERR_SHAPE = 2,     /* unsupported shape (e.g. filter size not compiled) */
+  CSC_ERR_CUDA = 3,      /* CUDA runtime error (message in csc_last_error) */
+  CSC_ERR_NCCL = 4,      /* NCCL error or NCCL not loadable for world > 1 */
+  CSC_ERR_OOM = 5,       /* device allocation failed in csc_init */
+  CSC_ERR_NONFINITE = 6  /* a reduced scalar (objective, step) is not finite */
+} csc_status;
+
+typedef struct csc_ctx csc_ctx; /* opaque; one per (rank, device, stream) */
+
+typedef struct {
+  int32_t n_local;          /* images on this rank, >= 0 */
+  int32_t K;                /* filters, >= 1 */
+  int32_t s;                /* filter side, odd, 1 <= s <= 11 (compiled set: 1,3,5,7,9,11) */
+  int32_t H, W;             /* image size, H >= s, W >= s; codes are K x (H+s-1) x (W+s-1) */
+  int32_t world, rank;      /* world in {1,2,4,8}; 0 <= rank < world */
+  int32_t device;           /* CUDA device ordinal */
+  void* stream;             /* cudaStream_t (0 = legacy default stream) */
+  const uint8_t* nccl_id;   /* 128-byte ncclUniqueId from csc_nccl_unique_id on rank 0,
+                               broadcast by the caller; NULL when world == 1 */
+} csc_dims;
+
+/* Create a context: validates dims, binds device+stream, allocates scratch, and
+ * (world > 1) joins the NCCL communicator.  *out is set only on CSC_OK. */
+csc_status csc_init(const csc_dims* dims, csc_ctx** out);
+
+/* One masked proximal-gradient step on the codes (reading R1), Eq.2-4
+ * with readings R2 (unsampled codes keep their value),
+ * R4/R5 (i.i.d. Bernoulli(p) per code coordinate, one mask per iteration shared
+ * by all images, counter-based Philox4x32-10 generated in-kernel):
+ *   for every image n and every (k,u,v) with mask bit 1:
+ *     c = sum_{a,b} d[k,a,b] r[n, u-s+1+a, v-s+1+b]     (r == 0 outside the image)
+ *     z[n,k,u,v] <- S_{tau*lambda}(z[n,k,u,v] - tau*c)  (shrinkage)
+ * lambda >= 0; step_z > 0 is used as tau, step_z == 0 selects tau = 1/L_D(d)
+ * (reading R8: L_D = max over the 64x64 DFT grid of sum_k |d_k^|^2); 0 < p <= 1;
+ * iter is the mask counter t.  step_used (HOST, nullable) receives tau (syncs). */
+csc_status csc_code_step(csc_ctx* ctx, const float* x, const float* d, float* z, float lambda,
+                         float step_z, double p, uint64_t seed, uint32_t iter, float* step_used);
+
+/* One projected-gradient step on the filters (reading R6) for Eq.5:
+ *   g = sum_n Z_n^T (Z_n d - x_n)  (all-reduced over ranks, fp64)
+ *   tau = step_d > 0 ? step_d : <g,g>/||Z g||^2  (exact line search, R8; 0 if ||Zg|| = 0)
+ *   d_k <- (d_k - tau g_k) / max(1, ||d_k - tau g_k||_2)  (unit ball, R7)
+ * Collective.  step_used (HOST, nullable) receives tau (syncs). */
+csc_status csc_filter_step(csc_ctx* ctx, const float* x, float* d, const float* z, float step_d,
+                           float* step_used);
+
+/* Eq.1 objective over ALL ranks' images: out[0] = F,
+ * out[1] = 1/2||Dz - x||^2, out[2] = lambda*||z||_1 (fp64, HOST).  Refreshes the
+ * residual cache.  Collective; synchronises the stream. */
+csc_status csc_objective(csc_ctx* ctx, const float* x, const float* d, const float* z,
+                         float lambda, double out[3]);
+
+/* One SBCSC outer iteration (Alg.1): [x_host -> x upload] ->
+ * csc_code_step(iter) -> csc_filter_step -> csc_objective.  x_host (HOST,
+ * nullable, ideally pinned) is copied into the device buffer x first (the step's
+ * input for the end-to-end measurement); obj_out[3] (HOST) as csc_objective;
+ * taus_out[2] (HOST, nullable) = {tau_z, tau_d}.  Collective. */
+csc_status csc_iterate(csc_ctx* ctx, const float* x_host, float* x, float* d, float* z,
+                       float lambda, float step_z, float step_d, double p, uint64_t seed,
+                       uint32_t iter, double obj_out[3], float taus_out[2]);
+
+/* Forget the residual cache (caller changed x, d or z outside the API). */
+csc_status csc_invalidate(csc_ctx* ctx);
+
+/* SOCSC (Alg.2) fresh mini-batch: z <- 0 and r <- -x exactly, no dense pass. */
+csc_status csc_zero_codes(csc_ctx* ctx, const float* x, float* z);
+
+csc_status csc_destroy(csc_ctx* ctx);
+
+/* Last error message of ctx (or of the last failed csc_init when ctx is NULL). */
+const char* csc_last_error(const csc_ctx* ctx);
+
+/* ncclGetUniqueId into out[128] (rank 0, before csc_init with world > 1). */
+csc_status csc_nccl_unique_id(uint8_t out[128]);
+
+int csc_abi_version(void);
+
+/* ---- test hooks (parity) ---- */
+
+/* Mask of iteration iter in the canonical layout: bit l = (k*Hc+u)*Wc+v lives in
+ * word l>>5 at bit l&31 (LSB first); ceil(K*Hc*Wc/32) words into bits_dev (DEVICE).
+ * Bit = Philox4x32-10(ctr={q lo, q hi, iter, 0x4353434D}, key={seed lo, seed hi})[l&3]
+ *       < floor(p*2^32), q = l>>2. */
+csc_status csc_mask_bits(csc_ctx* ctx, uint32_t iter, double p, uint64_t seed, uint32_t* bits_dev);
+
+/* Copy the cached residual [n_local][H][W] into r_dev (DEVICE). */
+csc_status csc_read_residual(csc_ctx* ctx, float* r_dev);
+
+/* Copy the last all-reduced filter gradient [K][s][s] (fp64) into g_dev (DEVICE). */
+csc_status csc_read_grad(csc_ctx* ctx, double* g_dev);
+
+/* L_D(d) (reading R8) computed on the device; result to *out (HOST, syncs). */
+csc_status csc_lipschitz(csc_ctx* ctx, const float* d, double* out);
+
+/* Number of kernel launches this context has enqueued (for bench accounting). */
+uint64_t csc_launch_count(const csc_ctx* ctx);
+
+/* ---- profiling (CUDA events around every launch, on the context stream) ---- */
+typedef enum {
+  CSC_K_CONV = 0,          /* dense pass: residual / Zg convolution (conv_fwd_kernel) */
+  CSC_K_CONV_FINALIZE = 1, /* k-split partial sum + reduction */
+  CSC_K_WGRAD = 2,         /* filter-gradient correlation (wgrad_kernel) */
+  CSC_K_CODE_STEP = 3,     /* masked prox-gradient code step (code_step_kernel) */
+  CSC_K_MASK = 4,          /* Philox mask generation */
+  CSC_K_LIPSCHITZ = 5,     /* DTFT bound */
+  CSC_K_SMALL = 6,         /* reductions, step size, update/projection */
+  CSC_K_NCLASS = 7
+} csc_kernel_class;
+
+/* Enable (1) / disable (0) per-launch event timing; enabling resets the totals. */
+csc_status csc_profile_enable(csc_ctx* ctx, int enable);
+
+/* Synchronises the stream, then returns the accumulated device time (ms) and the
+ * number of launches of kernel class cls since csc_profile_enable(ctx, 1). */
+csc_status csc_profile_read(csc_ctx* ctx, int cls, double* total_ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSC_H_ */

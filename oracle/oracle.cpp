@@ -145,6 +145,14 @@ inline double soft_threshold(double w, double kappa) {
 template <typename T>
 double lipschitz_dtft(const Dims& D, const T* d) {
   const int G = 64;
+  // e^{-2 pi i n/64}, n = 0..63: the same cos/sin values the direct formula evaluates,
+  // tabulated once (the exponent (a m1 + b m2) is taken mod 64).
+  double cs[G], sn[G];
+  for (int q = 0; q < G; ++q) {
+    const double ang = -2.0 * M_PI * (double)q / (double)G;
+    cs[q] = std::cos(ang);
+    sn[q] = std::sin(ang);
+  }
   double best = 0.0;
   for (int m1 = 0; m1 < G; ++m1)
     for (int m2 = 0; m2 < G; ++m2) {
@@ -153,10 +161,10 @@ double lipschitz_dtft(const Dims& D, const T* d) {
         double re = 0.0, im = 0.0;
         for (int64_t a = 0; a < D.s; ++a)
           for (int64_t b = 0; b < D.s; ++b) {
-            const double ang = -2.0 * M_PI * (double)((a * m1 + b * m2) % G) / (double)G;
+            const int q = (int)((a * m1 + b * m2) % G);
             const double v = (double)d[D.di(k, a, b)];
-            re += v * std::cos(ang);
-            im += v * std::sin(ang);
+            re += v * cs[q];
+            im += v * sn[q];
           }
         tot += re * re + im * im;
       }

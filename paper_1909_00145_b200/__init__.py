@@ -1,0 +1,257 @@
+"""B200-native stochastic spatial-domain CSC hot path (arxiv 1909.00145).
+
+Thin Python binding over the C ABI in include/csc.h (libcsc_b200.so, built with
+nvcc for sm_100a).  Argument marshalling only: every step of the path runs in
+the library's CUDA kernels.  There is NO CPU fallback: if the extension is
+missing or no B200 is visible, construction fails loudly.
+
+PyTorch is used for device memory and streams only.  Tensors passed in must be
+contiguous float32 CUDA tensors in the layouts of include/csc.h:
+  x [n_local, H, W], d [K, s, s], z [n_local, K, H+s-1, W+s-1].
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Optional, Sequence, Tuple
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcsc_b200.so")
+
+CSC_OK = 0
+_STATUS = {0: "CSC_OK", 1: "CSC_ERR_ARG", 2: "CSC_ERR_SHAPE", 3: "CSC_ERR_CUDA", 4: "CSC_ERR_NCCL",
+           5: "CSC_ERR_OOM", 6: "CSC_ERR_NONFINITE"}
+
+# Every symbol include/csc.h declares (checked by tests/test_abi.py).
+ABI_SYMBOLS = (
+    "csc_init", "csc_code_step", "csc_filter_step", "csc_objective", "csc_iterate", "csc_invalidate",
+    "csc_zero_codes", "csc_destroy", "csc_last_error", "csc_nccl_unique_id", "csc_abi_version",
+    "csc_mask_bits", "csc_read_residual", "csc_read_grad", "csc_lipschitz", "csc_launch_count",
+    "csc_profile_enable", "csc_profile_read",
+)
+
+# csc_kernel_class (include/csc.h)
+KERNEL_CLASSES = ("conv", "conv_finalize", "wgrad", "code_step", "mask", "lipschitz", "small")
+
+
+class CSCError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Dims(ctypes.Structure):
+    _fields_ = [("n_local", ctypes.c_int32), ("K", ctypes.c_int32), ("s", ctypes.c_int32),
+                ("H", ctypes.c_int32), ("W", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
+                ("nccl_id", ctypes.c_void_p)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: Optional[str] = None):
+    """Load libcsc_b200.so (raises if it is missing -- build with __graft_entry__.build())."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise ImportError(f"{p} not found: the CUDA extension is not built "
+                              "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
+        L = ctypes.CDLL(p)
+        vp, f32, f64, u32, u64 = ctypes.c_void_p, ctypes.c_float, ctypes.c_double, ctypes.c_uint32, ctypes.c_uint64
+        L.csc_init.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(vp)]
+        L.csc_code_step.argtypes = [vp, vp, vp, vp, f32, f32, f64, u64, u32, vp]
+        L.csc_filter_step.argtypes = [vp, vp, vp, vp, f32, vp]
+        L.csc_objective.argtypes = [vp, vp, vp, vp, f32, vp]
+        L.csc_iterate.argtypes = [vp, vp, vp, vp, vp, f32, f32, f32, f64, u64, u32, vp, vp]
+        L.csc_invalidate.argtypes = [vp]
+        L.csc_zero_codes.argtypes = [vp, vp, vp]
+        L.csc_destroy.argtypes = [vp]
+        L.csc_last_error.argtypes = [vp]
+        L.csc_last_error.restype = ctypes.c_char_p
+        L.csc_nccl_unique_id.argtypes = [vp]
+        L.csc_abi_version.restype = ctypes.c_int
+        L.csc_mask_bits.argtypes = [vp, u32, f64, u64, vp]
+        L.csc_read_residual.argtypes = [vp, vp]
+        L.csc_read_grad.argtypes = [vp, vp]
+        L.csc_lipschitz.argtypes = [vp, vp, vp]
+        L.csc_launch_count.argtypes = [vp]
+        L.csc_launch_count.restype = u64
+        L.csc_profile_enable.argtypes = [vp, ctypes.c_int]
+        L.csc_profile_read.argtypes = [vp, ctypes.c_int, ctypes.POINTER(f64), ctypes.POINTER(u64)]
+        for name in ABI_SYMBOLS:
+            if name not in ("csc_last_error", "csc_abi_version", "csc_launch_count"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+        return L
+
+
+def nccl_unique_id() -> bytes:
+    L = load_library()
+    buf = (ctypes.c_uint8 * 128)()
+    st = L.csc_nccl_unique_id(buf)
+    if st != CSC_OK:
+        raise CSCError(st, L.csc_last_error(None).decode())
+    return bytes(buf)
+
+
+def _ptr(t, name: str, numel: Optional[int] = None) -> int:
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
+    return t.data_ptr()
+
+
+class Context:
+    """One csc_ctx: (rank, device, stream).  See include/csc.h for semantics."""
+
+    def __init__(self, n_local: int, K: int, s: int, H: int, W: int, *, world: int = 1, rank: int = 0,
+                 device: Optional[int] = None, stream=None, nccl_id: Optional[bytes] = None):
+        import torch
+        self._L = load_library()
+        if device is None:
+            device = torch.cuda.current_device()
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        self.n_local, self.K, self.s, self.H, self.W = n_local, K, s, H, W
+        self.Hc, self.Wc = H + s - 1, W + s - 1
+        self.world, self.rank, self.device = world, rank, device
+        self._idbuf = None
+        if nccl_id is not None:
+            self._idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+        dims = _Dims(n_local, K, s, H, W, world, rank, device, ctypes.c_void_p(stream.cuda_stream),
+                     ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf is not None else None)
+        h = ctypes.c_void_p()
+        st = self._L.csc_init(ctypes.byref(dims), ctypes.byref(h))
+        if st != CSC_OK:
+            raise CSCError(st, self._L.csc_last_error(None).decode())
+        self._h = h
+
+    # -- helpers
+    def _check(self, st: int):
+        if st != CSC_OK:
+            raise CSCError(st, self._L.csc_last_error(self._h).decode())
+
+    def _xdz(self, x, d, z):
+        nx = self.n_local * self.H * self.W
+        nz = self.n_local * self.K * self.Hc * self.Wc
+        return (_ptr(x, "x", nx) if self.n_local else 0, _ptr(d, "d", self.K * self.s * self.s),
+                _ptr(z, "z", nz) if self.n_local else 0)
+
+    # -- ABI
+    def code_step(self, x, d, z, lam: float, p: float, seed: int, it: int, step_z: float = 0.0,
+                  want_step: bool = False) -> Optional[float]:
+        px, pd, pz = self._xdz(x, d, z)
+        out = ctypes.c_float(0.0)
+        self._check(self._L.csc_code_step(self._h, px, pd, pz, float(lam), float(step_z), float(p),
+                                          int(seed) & (2**64 - 1), int(it) & 0xffffffff,
+                                          ctypes.byref(out) if want_step else None))
+        return float(out.value) if want_step else None
+
+    def filter_step(self, x, d, z, step_d: float = 0.0, want_step: bool = False) -> Optional[float]:
+        px, pd, pz = self._xdz(x, d, z)
+        out = ctypes.c_float(0.0)
+        self._check(self._L.csc_filter_step(self._h, px, pd, pz, float(step_d),
+                                            ctypes.byref(out) if want_step else None))
+        return float(out.value) if want_step else None
+
+    def objective(self, x, d, z, lam: float) -> Tuple[float, float, float]:
+        px, pd, pz = self._xdz(x, d, z)
+        out = (ctypes.c_double * 3)()
+        self._check(self._L.csc_objective(self._h, px, pd, pz, float(lam), out))
+        return float(out[0]), float(out[1]), float(out[2])
+
+    def iterate(self, x, d, z, lam: float, p: float, seed: int, it: int, *, x_host=None,
+                step_z: float = 0.0, step_d: float = 0.0):
+        """One SBCSC iteration (code step, filter step, objective).  x_host: optional pinned CPU
+        float32 tensor uploaded into x first.  Returns ((F, fit, l1), (tau_z, tau_d))."""
+        px, pd, pz = self._xdz(x, d, z)
+        ph = None
+        if x_host is not None:
+            if x_host.is_cuda or x_host.dtype.itemsize != 4 or not x_host.is_contiguous():
+                raise ValueError("x_host must be a contiguous float32 CPU tensor")
+            if x_host.numel() != self.n_local * self.H * self.W:
+                raise ValueError("x_host has the wrong size")
+            ph = x_host.data_ptr()
+        obj = (ctypes.c_double * 3)()
+        taus = (ctypes.c_float * 2)()
+        self._check(self._L.csc_iterate(self._h, ph, px, pd, pz, float(lam), float(step_z), float(step_d),
+                                        float(p), int(seed) & (2**64 - 1), int(it) & 0xffffffff, obj, taus))
+        return (float(obj[0]), float(obj[1]), float(obj[2])), (float(taus[0]), float(taus[1]))
+
+    def invalidate(self):
+        self._check(self._L.csc_invalidate(self._h))
+
+    def zero_codes(self, x, z):
+        px = _ptr(x, "x") if self.n_local else 0
+        pz = _ptr(z, "z") if self.n_local else 0
+        self._check(self._L.csc_zero_codes(self._h, px, pz))
+
+    def mask_bits(self, it: int, p: float, seed: int, out):
+        import torch
+        nwords = (self.K * self.Hc * self.Wc + 31) // 32
+        if not (out.is_cuda and out.dtype == torch.int32 and out.numel() == nwords and out.is_contiguous()):
+            raise ValueError(f"out must be a contiguous int32 CUDA tensor of {nwords} words")
+        self._check(self._L.csc_mask_bits(self._h, int(it) & 0xffffffff, float(p), int(seed) & (2**64 - 1),
+                                          out.data_ptr()))
+
+    def read_residual(self, out):
+        self._check(self._L.csc_read_residual(self._h, _ptr(out, "out", self.n_local * self.H * self.W)
+                                              if self.n_local else 0))
+
+    def read_grad(self, out):
+        import torch
+        if not (out.is_cuda and out.dtype == torch.float64 and out.numel() == self.K * self.s * self.s):
+            raise ValueError("out must be a float64 CUDA tensor of K*s*s elements")
+        self._check(self._L.csc_read_grad(self._h, out.data_ptr()))
+
+    def lipschitz(self, d) -> float:
+        out = ctypes.c_double(0.0)
+        self._check(self._L.csc_lipschitz(self._h, _ptr(d, "d"), ctypes.byref(out)))
+        return float(out.value)
+
+    def profile_enable(self, on: bool = True):
+        self._check(self._L.csc_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        """{class: (total_ms, launches)} accumulated since profile_enable(True) (syncs)."""
+        out = {}
+        for i, name in enumerate(KERNEL_CLASSES):
+            ms, n = ctypes.c_double(0.0), ctypes.c_uint64(0)
+            self._check(self._L.csc_profile_read(self._h, i, ctypes.byref(ms), ctypes.byref(n)))
+            out[name] = (float(ms.value), int(n.value))
+        return out
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._L.csc_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._L.csc_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+__all__: Sequence[str] = ["Context", "CSCError", "load_library", "nccl_unique_id", "LIB_PATH", "ABI_SYMBOLS"]

@@ -1,0 +1,90 @@
+"""Build the sm_100a C-ABI library libcsc_b200.so in-tree with nvcc.
+
+    python -m paper_1909_00145_b200.build [--force] [--verbose]
+
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo, no fast-math (the
+projection and the step sizes need IEEE sqrt/div).  NCCL headers come from the
+torch wheel (nvidia/nccl/include); the library dlopens libnccl.so.2 only when a
+context with world > 1 is created.
+"""
+from __future__ import annotations
+
+import argparse
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libcsc_b200.so")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: the CUDA 12.9 toolkit is required to build libcsc_b200.so")
+
+
+def _nccl_include() -> str:
+    try:
+        import nvidia.nccl  # type: ignore
+        base = list(nvidia.nccl.__path__)[0]
+    except Exception:  # pragma: no cover
+        import site
+        base = None
+        for sp in site.getsitepackages():
+            cand = os.path.join(sp, "nvidia", "nccl")
+            if os.path.isdir(cand):
+                base = cand
+                break
+        if base is None:
+            raise RuntimeError("nvidia-nccl headers not found (torch wheel)")
+    inc = os.path.join(base, "include")
+    if not os.path.exists(os.path.join(inc, "nccl.h")):
+        raise RuntimeError(f"nccl.h not found under {inc}")
+    return inc
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "csc.h")]
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    nvcc = _nvcc()
+    host_cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
+           "-ccbin", host_cxx, "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(),
+           "-o", LIB + ".tmp", *sources(), "-ldl"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.verbose))
+
+
+if __name__ == "__main__":
+    main()

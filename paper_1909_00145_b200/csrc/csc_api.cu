@@ -1,0 +1,619 @@
+// csc_api.cu -- the C ABI (include/csc.h) over the sm_100a kernels.
+//
+// Iteration structure (Alg.1):
+//   csc_code_step   [r cache invalid -> dense residual] -> [tau_z = 1/L_D] -> mask -> masked step
+//   csc_filter_step dense residual r' -> Z^T r' -> allreduce g -> ||Zg||^2 -> allreduce
+//                   -> tau_d -> update + ball projection
+//   csc_objective   dense residual r'' (refreshes the cache) + ||z||_1 -> allreduce -> F
+// NCCL (world > 1) is loaded with dlopen("libnccl.so.2") at csc_init; single-GPU
+// contexts never touch it.
+#include "../../include/csc.h"
+#include "csc_internal.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using csc::Geom;
+
+namespace {
+
+std::mutex g_err_mu;
+std::string g_init_err;
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string* err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      *err = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
+      return false;
+    }
+    GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(h, "ncclAllReduce"));
+    GetErrorString = reinterpret_cast<decltype(GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!GetUniqueId || !CommInitRank || !CommDestroy || !AllReduce || !GetErrorString) {
+      *err = "libnccl.so.2 lacks required symbols";
+      return false;
+    }
+    return true;
+  }
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+// device scalar slots
+enum DSlot { kSqR = 0, kL1 = 1, kZg2 = 2, kGG = 3, kLhat = 4, kNumD = 8 };
+enum FSlot { kTauZ = 0, kTauD = 1, kNumF = 4 };
+
+}  // namespace
+
+struct csc_ctx {
+  Geom g{};
+  int world = 1, rank = 0, device = 0;
+  cudaStream_t st = nullptr;
+  // scratch
+  float* r = nullptr;          // [N][H][W] residual cache
+  float* part = nullptr;       // conv k-split partials
+  int ksplit = 1;              // dense-pass k split
+  double* sq_part = nullptr;   // per-block partials
+  double* l1_part = nullptr;
+  int part_cap = 0;
+  double* gpart = nullptr;     // [G][K][S*S]
+  int G = 1;
+  double* gsum = nullptr;      // [K][S*S]
+  float* g32 = nullptr;
+  uint32_t* colw = nullptr;    // mask column words
+  double* lip_part = nullptr;
+  double* dscal = nullptr;
+  float* fscal = nullptr;
+  double* h_dscal = nullptr;   // pinned host mirrors
+  float* h_fscal = nullptr;
+  // residual cache
+  bool cache_valid = false;
+  const float* cx = nullptr;
+  const float* cd = nullptr;
+  const float* cz = nullptr;
+  ncclComm_t comm = nullptr;
+  uint64_t launches = 0;
+  std::string err;
+  // profiling
+  struct Rec { cudaEvent_t a, b; int cls; };
+  bool prof_on = false;
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[CSC_K_NCLASS] = {0};
+  uint64_t prof_n[CSC_K_NCLASS] = {0};
+};
+
+namespace {
+
+csc_status fail(csc_ctx* c, csc_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+#define CSC_CUDA(ctx, call)                                                                      \
+  do {                                                                                           \
+    cudaError_t _e = (call);                                                                     \
+    if (_e != cudaSuccess)                                                                       \
+      return fail((ctx), CSC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));      \
+  } while (0)
+
+cudaEvent_t prof_event(csc_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Launch `call` (nk kernels of class cls); with profiling on, bracket it with events.
+#define CSC_LAUNCH_C(ctx, cls, nk, call)                                                         \
+  do {                                                                                           \
+    cudaEvent_t _ea = nullptr, _eb = nullptr;                                                    \
+    if ((ctx)->prof_on) {                                                                        \
+      _ea = prof_event(ctx);                                                                     \
+      _eb = prof_event(ctx);                                                                     \
+      cudaEventRecord(_ea, (ctx)->st);                                                           \
+    }                                                                                            \
+    cudaError_t _e = (call);                                                                     \
+    if (_e != cudaSuccess)                                                                       \
+      return fail((ctx), CSC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));      \
+    if ((ctx)->prof_on) {                                                                        \
+      cudaEventRecord(_eb, (ctx)->st);                                                           \
+      (ctx)->pending.push_back({_ea, _eb, (cls)});                                               \
+    }                                                                                            \
+    (ctx)->launches += (nk);                                                                     \
+  } while (0)
+#define CSC_LAUNCH(ctx, nk, call) CSC_LAUNCH_C(ctx, CSC_K_SMALL, nk, call)
+
+#define CSC_NCCL(ctx, call)                                                                      \
+  do {                                                                                           \
+    ncclResult_t _r = (call);                                                                    \
+    if (_r != ncclSuccess)                                                                       \
+      return fail((ctx), CSC_ERR_NCCL, std::string(#call) + ": " + g_nccl.GetErrorString(_r));   \
+  } while (0)
+
+bool aligned4(const void* p) { return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+
+int64_t n_pix(const Geom& g) { return static_cast<int64_t>(g.N) * g.H * g.W; }
+
+csc_status allreduce_d(csc_ctx* c, double* buf, size_t count) {
+  if (c->world <= 1) return CSC_OK;
+  CSC_NCCL(c, g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->st));
+  return CSC_OK;
+}
+
+// Dense residual pass r = Dz - x, plus sum r^2 -> dscal[kSqR] and (optional)
+// ||z||_1 -> dscal[kL1]; both local to this rank.
+csc_status dense_residual(csc_ctx* c, const float* x, const float* d, const float* z, bool want_l1) {
+  const Geom& g = c->g;
+  int nb = 0;
+  double* l1p = want_l1 ? c->l1_part : nullptr;
+  if (g.N == 0) {
+    CSC_CUDA(c, cudaMemsetAsync(c->dscal, 0, sizeof(double) * 2, c->st));
+    return CSC_OK;
+  }
+  CSC_LAUNCH_C(c, CSC_K_CONV, 1, csc::launch_conv_fwd(g, z, d, x, c->r, c->part, c->ksplit, csc::kConvResidual, c->sq_part, l1p,
+                                        c->st, &nb));
+  if (c->ksplit == 1) {
+    CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, nb, c->dscal + kSqR, 1.0, c->st));
+  } else {
+    CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1, csc::launch_conv_finalize(g, c->part, c->ksplit, x, c->r, csc::kConvResidual, c->sq_part, c->st));
+    CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kSqR, 1.0, c->st));
+  }
+  if (want_l1) CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->l1_part, nb, c->dscal + kL1, 1.0, c->st));
+  c->cache_valid = true;
+  c->cx = x;
+  c->cd = d;
+  c->cz = z;
+  return CSC_OK;
+}
+
+bool cache_ok(const csc_ctx* c, const float* x, const float* d, const float* z) {
+  return c->cache_valid && c->cx == x && c->cd == d && c->cz == z;
+}
+
+csc_status check_ptrs(csc_ctx* c, const void* x, const void* d, const void* z) {
+  if (!c) return CSC_ERR_ARG;
+  if (!aligned4(d)) return fail(c, CSC_ERR_ARG, "d must be a non-null 4-byte aligned device pointer");
+  if (c->g.N > 0 && (!aligned4(x) || !aligned4(z)))
+    return fail(c, CSC_ERR_ARG, "x and z must be non-null 4-byte aligned device pointers");
+  return CSC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int csc_abi_version(void) { return CSC_ABI_VERSION; }
+
+const char* csc_last_error(const csc_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  return g_init_err.c_str();
+}
+
+uint64_t csc_launch_count(const csc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+csc_status csc_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return CSC_ERR_ARG;
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  std::string err;
+  if (!g_nccl.load(&err)) {
+    std::lock_guard<std::mutex> lk2(g_err_mu);
+    g_init_err = err;
+    return CSC_ERR_NCCL;
+  }
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return CSC_ERR_NCCL;
+  std::memcpy(out, id.internal, 128);
+  return CSC_OK;
+}
+
+csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
+  auto init_fail = [](csc_status s, const std::string& m) {
+    std::lock_guard<std::mutex> lk(g_err_mu);
+    g_init_err = m;
+    return s;
+  };
+  if (!dims || !out) return init_fail(CSC_ERR_ARG, "null dims/out");
+  const csc_dims& D = *dims;
+  if (D.K < 1 || D.n_local < 0 || D.s < 1 || (D.s % 2) == 0 || D.H < D.s || D.W < D.s)
+    return init_fail(CSC_ERR_ARG, "invalid dims: need K>=1, n_local>=0, odd s>=1, H,W>=s");
+  if (!(D.world == 1 || D.world == 2 || D.world == 4 || D.world == 8) || D.rank < 0 || D.rank >= D.world)
+    return init_fail(CSC_ERR_ARG, "world must be 1,2,4,8 and 0<=rank<world");
+  if (D.world > 1 && D.nccl_id == nullptr) return init_fail(CSC_ERR_ARG, "nccl_id required for world>1");
+  if (!csc::filter_size_supported(D.s)) return init_fail(CSC_ERR_SHAPE, "filter size s not compiled (1,3,5,7,9,11)");
+  if (static_cast<int64_t>(D.H + D.s - 1) * (D.W + D.s - 1) * D.K > (int64_t(1) << 31))
+    return init_fail(CSC_ERR_SHAPE, "K*(H+s-1)*(W+s-1) exceeds 2^31 per image");
+
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0)
+    return init_fail(CSC_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(ce));
+  if (D.device < 0 || D.device >= ndev) return init_fail(CSC_ERR_ARG, "device ordinal out of range");
+  ce = cudaSetDevice(D.device);
+  if (ce != cudaSuccess) return init_fail(CSC_ERR_CUDA, cudaGetErrorString(ce));
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, D.device);
+  if (prop.major != 10)
+    return init_fail(CSC_ERR_CUDA, "kernels are compiled for sm_100a only (B200); found sm_" +
+                                       std::to_string(prop.major) + std::to_string(prop.minor));
+
+  csc_ctx* c = new csc_ctx();
+  c->g.N = D.n_local;
+  c->g.K = D.K;
+  c->g.S = D.s;
+  c->g.H = D.H;
+  c->g.W = D.W;
+  c->g.Hc = D.H + D.s - 1;
+  c->g.Wc = D.W + D.s - 1;
+  c->g.P = D.s - 1;
+  c->world = D.world;
+  c->rank = D.rank;
+  c->device = D.device;
+  c->st = static_cast<cudaStream_t>(D.stream);
+  const Geom& g = c->g;
+
+  // dense-pass k split: aim for >= ~8 CTAs per SM over the grid
+  const int tiles = csc::ceil_div(g.W, csc::kConvTW) * csc::ceil_div(g.H, csc::kConvTH) * (g.N > 0 ? g.N : 1);
+  int ks = csc::ceil_div(prop.multiProcessorCount * 8, tiles);
+  if (ks > g.K) ks = g.K;
+  if (ks > 32) ks = 32;
+  if (ks < 1) ks = 1;
+  c->ksplit = ks;
+  // filter-gradient tile groups
+  const int wtiles = csc::ceil_div(g.W, csc::kWgTW) * csc::ceil_div(g.H, csc::kWgTH) * (g.N > 0 ? g.N : 1);
+  int G = csc::ceil_div(prop.multiProcessorCount * 8, g.K);
+  if (G > wtiles) G = wtiles;
+  if (G < 1) G = 1;
+  c->G = G;
+
+  const int64_t npix = n_pix(g);
+  const int M = g.S * g.S;
+  const int NB = csc::ceil_div(g.Hc, 32);
+  int cap = csc::conv_fwd_blocks(g, ks);
+  if (cap < csc::kFinalizeBlocks) cap = csc::kFinalizeBlocks;
+  c->part_cap = cap;
+  auto alloc = [&](void** p, size_t bytes) -> bool {
+    if (bytes == 0) bytes = 16;
+    return cudaMalloc(p, bytes) == cudaSuccess;
+  };
+  bool ok = true;
+  ok = ok && alloc(reinterpret_cast<void**>(&c->r), sizeof(float) * npix);
+  if (ks > 1) ok = ok && alloc(reinterpret_cast<void**>(&c->part), sizeof(float) * npix * ks);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->sq_part), sizeof(double) * cap);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->l1_part), sizeof(double) * cap);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->gpart), sizeof(double) * static_cast<size_t>(G) * g.K * M);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->gsum), sizeof(double) * g.K * M);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->g32), sizeof(float) * g.K * M);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->colw), sizeof(uint32_t) * static_cast<size_t>(g.K) * NB * g.Wc);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->lip_part), sizeof(double) * 64 * 64 * csc::ceil_div(g.K, 16));
+  ok = ok && alloc(reinterpret_cast<void**>(&c->dscal), sizeof(double) * kNumD);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->fscal), sizeof(float) * kNumF);
+  ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_dscal), sizeof(double) * kNumD) == cudaSuccess;
+  ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_fscal), sizeof(float) * kNumF) == cudaSuccess;
+  if (!ok) {
+    csc_destroy(c);
+    return init_fail(CSC_ERR_OOM, "device allocation failed in csc_init");
+  }
+  cudaMemsetAsync(c->dscal, 0, sizeof(double) * kNumD, c->st);
+  cudaMemsetAsync(c->fscal, 0, sizeof(float) * kNumF, c->st);
+  cudaMemsetAsync(c->gsum, 0, sizeof(double) * g.K * M, c->st);
+
+  if (c->world > 1) {
+    std::string err;
+    {
+      std::lock_guard<std::mutex> lk(g_nccl_mu);
+      if (!g_nccl.load(&err)) {
+        csc_destroy(c);
+        return init_fail(CSC_ERR_NCCL, err);
+      }
+    }
+    ncclUniqueId id;
+    std::memcpy(id.internal, D.nccl_id, 128);
+    ncclResult_t nr = g_nccl.CommInitRank(&c->comm, c->world, id, c->rank);
+    if (nr != ncclSuccess) {
+      const std::string m = std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(nr);
+      c->comm = nullptr;
+      csc_destroy(c);
+      return init_fail(CSC_ERR_NCCL, m);
+    }
+  }
+  ce = cudaStreamSynchronize(c->st);
+  if (ce != cudaSuccess) {
+    csc_destroy(c);
+    return init_fail(CSC_ERR_CUDA, cudaGetErrorString(ce));
+  }
+  *out = c;
+  return CSC_OK;
+}
+
+csc_status csc_profile_enable(csc_ctx* c, int enable) {
+  if (!c) return CSC_ERR_ARG;
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  for (auto& r : c->pending) {
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->pending.clear();
+  for (int i = 0; i < CSC_K_NCLASS; ++i) {
+    c->prof_ms[i] = 0.0;
+    c->prof_n[i] = 0;
+  }
+  c->prof_on = enable != 0;
+  return CSC_OK;
+}
+
+csc_status csc_profile_read(csc_ctx* c, int cls, double* total_ms, uint64_t* launches) {
+  if (!c || cls < 0 || cls >= CSC_K_NCLASS) return fail(c, CSC_ERR_ARG, "bad kernel class");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  for (auto& r : c->pending) {
+    float ms = 0.f;
+    CSC_CUDA(c, cudaEventElapsedTime(&ms, r.a, r.b));
+    c->prof_ms[r.cls] += ms;
+    c->prof_n[r.cls] += 1;
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->pending.clear();
+  if (total_ms) *total_ms = c->prof_ms[cls];
+  if (launches) *launches = c->prof_n[cls];
+  return CSC_OK;
+}
+
+csc_status csc_destroy(csc_ctx* c) {
+  if (!c) return CSC_OK;
+  for (auto& r : c->pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->comm) g_nccl.CommDestroy(c->comm);
+  cudaFree(c->r);
+  cudaFree(c->part);
+  cudaFree(c->sq_part);
+  cudaFree(c->l1_part);
+  cudaFree(c->gpart);
+  cudaFree(c->gsum);
+  cudaFree(c->g32);
+  cudaFree(c->colw);
+  cudaFree(c->lip_part);
+  cudaFree(c->dscal);
+  cudaFree(c->fscal);
+  cudaFreeHost(c->h_dscal);
+  cudaFreeHost(c->h_fscal);
+  delete c;
+  return CSC_OK;
+}
+
+csc_status csc_invalidate(csc_ctx* c) {
+  if (!c) return CSC_ERR_ARG;
+  c->cache_valid = false;
+  return CSC_OK;
+}
+
+csc_status csc_zero_codes(csc_ctx* c, const float* x, float* z) {
+  if (!c) return CSC_ERR_ARG;
+  if (c->g.N > 0 && (!aligned4(x) || !aligned4(z))) return fail(c, CSC_ERR_ARG, "x, z must be device pointers");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  if (g.N > 0) {
+    CSC_CUDA(c, cudaMemsetAsync(z, 0, sizeof(float) * static_cast<size_t>(g.N) * g.K * g.Hc * g.Wc, c->st));
+    CSC_LAUNCH(c, 1, csc::launch_neg_copy(x, c->r, n_pix(g), c->st));
+  }
+  c->cache_valid = true;
+  c->cx = x;
+  c->cz = z;
+  c->cd = nullptr;  // r = -x holds for any d when z = 0
+  return CSC_OK;
+}
+
+csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, float lambda, float step_z,
+                         double p, uint64_t seed, uint32_t iter, float* step_used) {
+  csc_status s = check_ptrs(c, x, d, z);
+  if (s != CSC_OK) return s;
+  if (!(lambda >= 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and >= 0");
+  if (!(step_z >= 0.f) || !std::isfinite(step_z)) return fail(c, CSC_ERR_ARG, "step_z must be finite and >= 0");
+  if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  // zero-code shortcut of csc_zero_codes: r = -x for any d
+  const bool zero_ok = c->cache_valid && c->cd == nullptr && c->cx == x && c->cz == z;
+  if (!zero_ok && !cache_ok(c, x, d, z)) {
+    s = dense_residual(c, x, d, z, false);
+    if (s != CSC_OK) return s;
+  }
+  if (step_z > 0.f) {
+    CSC_CUDA(c, cudaMemcpyAsync(c->fscal + kTauZ, &step_z, sizeof(float), cudaMemcpyHostToDevice, c->st));
+  } else {
+    CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 2, csc::launch_lipschitz(g, d, c->lip_part, c->dscal + kLhat, c->fscal + kTauZ, c->st));
+  }
+  const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
+  const int all_selected = thr >= (uint64_t(1) << 32) ? 1 : 0;
+  if (g.N > 0) {
+    if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st));
+    CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, c->fscal + kTauZ, lambda, c->st));
+  }
+  c->cache_valid = false;  // r no longer matches z
+  if (step_used) {
+    CSC_CUDA(c, cudaMemcpyAsync(c->h_fscal + kTauZ, c->fscal + kTauZ, sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    CSC_CUDA(c, cudaStreamSynchronize(c->st));
+    *step_used = c->h_fscal[kTauZ];
+    if (!std::isfinite(*step_used)) return fail(c, CSC_ERR_NONFINITE, "tau_z is not finite");
+  }
+  return CSC_OK;
+}
+
+csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z, float step_d, float* step_used) {
+  csc_status s = check_ptrs(c, x, d, z);
+  if (s != CSC_OK) return s;
+  if (!(step_d >= 0.f) || !std::isfinite(step_d)) return fail(c, CSC_ERR_ARG, "step_d must be finite and >= 0");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  const int M = g.S * g.S;
+  if (!cache_ok(c, x, d, z)) {
+    s = dense_residual(c, x, d, z, false);
+    if (s != CSC_OK) return s;
+  }
+  if (g.N > 0) {
+    CSC_LAUNCH_C(c, CSC_K_WGRAD, 1, csc::launch_wgrad(g, z, c->r, c->G, c->gpart, c->st));
+    CSC_LAUNCH(c, 1, csc::launch_wgrad_reduce(g, c->gpart, c->G, c->gsum, c->st));
+  } else {
+    CSC_CUDA(c, cudaMemsetAsync(c->gsum, 0, sizeof(double) * g.K * M, c->st));
+  }
+  s = allreduce_d(c, c->gsum, static_cast<size_t>(g.K) * M);
+  if (s != CSC_OK) return s;
+  CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->st));
+  if (step_d == 0.f) {
+    if (g.N > 0) {
+      int nb = 0;
+      CSC_LAUNCH_C(c, CSC_K_CONV, 1, csc::launch_conv_fwd(g, z, c->g32, nullptr, nullptr, c->part, c->ksplit, csc::kConvSumSq,
+                                            c->sq_part, nullptr, c->st, &nb));
+      if (c->ksplit == 1) {
+        CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, nb, c->dscal + kZg2, 1.0, c->st));
+      } else {
+        CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1, csc::launch_conv_finalize(g, c->part, c->ksplit, nullptr, nullptr, csc::kConvSumSq,
+                                                   c->sq_part, c->st));
+        CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));
+      }
+    } else {
+      CSC_CUDA(c, cudaMemsetAsync(c->dscal + kZg2, 0, sizeof(double), c->st));
+    }
+    s = allreduce_d(c, c->dscal + kZg2, 1);
+    if (s != CSC_OK) return s;
+  }
+  CSC_LAUNCH(c, 1, csc::launch_filter_tau(c->dscal + kGG, c->dscal + kZg2, step_d, c->fscal + kTauD, c->st));
+  CSC_LAUNCH(c, 1, csc::launch_filter_update(g, d, c->gsum, c->fscal + kTauD, c->st));
+  c->cache_valid = false;  // d changed
+  if (step_used) {
+    CSC_CUDA(c, cudaMemcpyAsync(c->h_fscal + kTauD, c->fscal + kTauD, sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    CSC_CUDA(c, cudaStreamSynchronize(c->st));
+    *step_used = c->h_fscal[kTauD];
+    if (!std::isfinite(*step_used)) return fail(c, CSC_ERR_NONFINITE, "tau_d is not finite");
+  }
+  return CSC_OK;
+}
+
+static csc_status objective_enqueue(csc_ctx* c, const float* x, const float* d, const float* z) {
+  csc_status s = dense_residual(c, x, d, z, true);
+  if (s != CSC_OK) return s;
+  s = allreduce_d(c, c->dscal + kSqR, 2);
+  if (s != CSC_OK) return s;
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal, c->dscal, sizeof(double) * kNumD, cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_fscal, c->fscal, sizeof(float) * kNumF, cudaMemcpyDeviceToHost, c->st));
+  return CSC_OK;
+}
+
+static csc_status objective_finish(csc_ctx* c, float lambda, double out[3]) {
+  CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  const double half = 0.5 * c->h_dscal[kSqR];
+  const double l1 = static_cast<double>(lambda) * c->h_dscal[kL1];
+  out[0] = half + l1;
+  out[1] = half;
+  out[2] = l1;
+  if (!std::isfinite(out[0])) return fail(c, CSC_ERR_NONFINITE, "objective is not finite");
+  return CSC_OK;
+}
+
+csc_status csc_objective(csc_ctx* c, const float* x, const float* d, const float* z, float lambda, double out[3]) {
+  csc_status s = check_ptrs(c, x, d, z);
+  if (s != CSC_OK) return s;
+  if (!out) return fail(c, CSC_ERR_ARG, "out must be a host pointer to 3 doubles");
+  if (!(lambda >= 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and >= 0");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  s = objective_enqueue(c, x, d, z);
+  if (s != CSC_OK) return s;
+  return objective_finish(c, lambda, out);
+}
+
+csc_status csc_iterate(csc_ctx* c, const float* x_host, float* x, float* d, float* z, float lambda, float step_z,
+                       float step_d, double p, uint64_t seed, uint32_t iter, double obj_out[3], float taus_out[2]) {
+  csc_status s = check_ptrs(c, x, d, z);
+  if (s != CSC_OK) return s;
+  if (!obj_out) return fail(c, CSC_ERR_ARG, "obj_out must be a host pointer to 3 doubles");
+  if (!(lambda >= 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and >= 0");
+  if (!(step_z >= 0.f) || !std::isfinite(step_z) || !(step_d >= 0.f) || !std::isfinite(step_d))
+    return fail(c, CSC_ERR_ARG, "steps must be finite and >= 0");
+  if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  if (x_host && c->g.N > 0) {
+    CSC_CUDA(c, cudaMemcpyAsync(x, x_host, sizeof(float) * n_pix(c->g), cudaMemcpyHostToDevice, c->st));
+    c->cache_valid = false;
+  }
+  s = csc_code_step(c, x, d, z, lambda, step_z, p, seed, iter, nullptr);
+  if (s != CSC_OK) return s;
+  s = csc_filter_step(c, x, d, z, step_d, nullptr);
+  if (s != CSC_OK) return s;
+  s = objective_enqueue(c, x, d, z);
+  if (s != CSC_OK) return s;
+  s = objective_finish(c, lambda, obj_out);
+  if (taus_out) {
+    taus_out[0] = c->h_fscal[kTauZ];
+    taus_out[1] = c->h_fscal[kTauD];
+  }
+  return s;
+}
+
+csc_status csc_mask_bits(csc_ctx* c, uint32_t iter, double p, uint64_t seed, uint32_t* bits_dev) {
+  if (!c || !aligned4(bits_dev)) return fail(c, CSC_ERR_ARG, "bits_dev must be a device pointer");
+  if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
+  CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_bits(c->g, seed, iter, thr, bits_dev, c->st));
+  return CSC_OK;
+}
+
+csc_status csc_read_residual(csc_ctx* c, float* r_dev) {
+  if (!c || (c->g.N > 0 && !aligned4(r_dev))) return fail(c, CSC_ERR_ARG, "r_dev must be a device pointer");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  if (c->g.N > 0)
+    CSC_CUDA(c, cudaMemcpyAsync(r_dev, c->r, sizeof(float) * n_pix(c->g), cudaMemcpyDeviceToDevice, c->st));
+  return CSC_OK;
+}
+
+csc_status csc_read_grad(csc_ctx* c, double* g_dev) {
+  if (!c || !g_dev) return fail(c, CSC_ERR_ARG, "g_dev must be a device pointer");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  CSC_CUDA(c, cudaMemcpyAsync(g_dev, c->gsum, sizeof(double) * c->g.K * c->g.S * c->g.S, cudaMemcpyDeviceToDevice,
+                              c->st));
+  return CSC_OK;
+}
+
+csc_status csc_lipschitz(csc_ctx* c, const float* d, double* out) {
+  if (!c || !aligned4(d) || !out) return fail(c, CSC_ERR_ARG, "d (device) and out (host) required");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 2, csc::launch_lipschitz(c->g, d, c->lip_part, c->dscal + kLhat, nullptr, c->st));
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal + kLhat, c->dscal + kLhat, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  *out = c->h_dscal[kLhat];
+  return CSC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// csc_internal.cuh -- internal launch interface between the C ABI (csc_api.cu)
+// and the sm_100a kernels (csc_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace csc {
+
+struct Geom {
+  int N, K, S, H, W, Hc, Wc, P;
+};
+
+// ---- tiling constants shared by launcher and kernels ----
+constexpr int kConvTX = 8, kConvTY = 16, kConvR = 4, kConvC = 8;
+constexpr int kConvTW = kConvTX * kConvC;  // 64 output columns per tile
+constexpr int kConvTH = kConvTY * kConvR;  // 64 output rows per tile
+constexpr int kConvThreads = kConvTX * kConvTY;
+
+constexpr int kWgTX = 8, kWgTY = 16, kWgRB = 4, kWgC = 8;
+constexpr int kWgTW = kWgTX * kWgC;  // 64
+constexpr int kWgTH = kWgTY * kWgRB; // 64
+constexpr int kWgThreads = kWgTX * kWgTY;
+
+constexpr int kCodeWarps = 4;
+constexpr int kCodeThreads = 32 * kCodeWarps;
+constexpr int kCodePitch = 64;  // r-tile pitch in floats; multiple of 32 => lane L hits bank L+b
+
+constexpr int kReduceThreads = 256;
+constexpr int kFinalizeBlocks = 148 * 4;
+
+inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Filter sizes with compiled kernels.
+inline bool filter_size_supported(int s) {
+  return s == 1 || s == 3 || s == 5 || s == 7 || s == 9 || s == 11;
+}
+
+// All launchers return cudaGetLastError() of their launch.
+enum ConvMode : int { kConvResidual = 0, kConvSumSq = 1 };
+
+// y = sum_{k in [k0,k1)} f_k * z_k (valid true convolution) for all images.
+// ksplit == 1: out = y - x (mode residual, stored to r) or nothing (sumsq);
+//   per-block fp64 partials of sum(out^2) -> sq_part[blocks], of |z| over owned
+//   code positions -> l1_part[blocks] (if l1_part != nullptr).
+// ksplit > 1: y of split ks -> part[ks][N][H][W]; finalize with launch_conv_finalize.
+cudaError_t launch_conv_fwd(const Geom& g, const float* z, const float* filt, const float* x,
+                            float* r, float* part, int ksplit, int mode, double* sq_part,
+                            double* l1_part, cudaStream_t st, int* nblocks_out);
+int conv_fwd_blocks(const Geom& g, int ksplit);
+cudaError_t launch_conv_finalize(const Geom& g, const float* part, int ksplit, const float* x,
+                                 float* r, int mode, double* sq_part, cudaStream_t st);
+
+// Fixed-order fp64 sum of n partials -> *out (single block).  scale applied to result.
+cudaError_t launch_reduce_sum(const double* part, int n, double* out, double scale,
+                              cudaStream_t st);
+
+// Filter-gradient partials: gpart[G][K][S*S] (fp64); grid (G, K).
+cudaError_t launch_wgrad(const Geom& g, const float* z, const float* r, int G, double* gpart,
+                         cudaStream_t st);
+// gsum[K*S*S] = sum_G gpart (fixed order, fp64).
+cudaError_t launch_wgrad_reduce(const Geom& g, const double* gpart, int G, double* gsum,
+                                cudaStream_t st);
+// g32 = (float)gsum, gg_out = sum gsum^2 (fp64) -- after the cross-rank all-reduce.
+cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, double* gg_out,
+                               cudaStream_t st);
+
+// Mask (Philox4x32-10) -- internal column-word layout for the code step:
+//   colw[(k*NB + ub)*Wc + v] bit r = mask(k, 32*ub + r, v), NB = ceil(Hc/32).
+cudaError_t launch_mask_colwords(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr,
+                                 uint32_t* colw, cudaStream_t st);
+// Canonical layout for the test hook.
+cudaError_t launch_mask_bits(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr,
+                             uint32_t* bits, cudaStream_t st);
+
+// Masked proximal-gradient code step.
+cudaError_t launch_code_step(const Geom& g, const float* r, const float* d, float* z,
+                             const uint32_t* colw, int all_selected, const float* tau_dev,
+                             float lam, cudaStream_t st);
+
+// L_D(d) = max over 64x64 DFT grid of sum_k |d^_k|^2 -> lhat (fp64), and
+// tau_out = (float)(1/L) if tau_out != nullptr.  part: >= 64 doubles scratch.
+cudaError_t launch_lipschitz(const Geom& g, const float* d, double* part, double* lhat,
+                             float* tau_out, cudaStream_t st);
+
+// tau_d = step > 0 ? step : (zg2 > 0 ? (float)(gg/zg2) : 0)  (device scalar).
+cudaError_t launch_filter_tau(const double* gg, const double* zg2, float step, float* tau_d,
+                              cudaStream_t st);
+// d_k <- (float)((d_k - tau g_k) / max(1, ||d_k - tau g_k||)) in fp64.
+cudaError_t launch_filter_update(const Geom& g, float* d, const double* gsum, const float* tau_d,
+                                 cudaStream_t st);
+
+// r = -x (zero codes).
+cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st);
+
+}  // namespace csc

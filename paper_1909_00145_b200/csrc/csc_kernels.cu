@@ -1,0 +1,830 @@
+// csc_kernels.cu -- sm_100a kernels of the stochastic spatial-domain CSC hot path.
+//
+// Method: arxiv 1909.00145, PAPER.md (citations P:n = line n).  Readings
+// R1..R9 / #1..#17: DESIGN.md §3.  Layouts: include/csc.h.
+//
+//   conv_fwd_kernel      r = sum_k d_k * z_k - x  (also Zg with g for d)
+//   wgrad_kernel         g = Z^T r                 (gradient of the Eq.5 fit term)
+//   code_step_kernel     masked prox-gradient step on the codes (Eq.2-4)
+//   mask_*_kernel        Bernoulli(p) mask from counter-based Philox4x32-10 (Eq.2, R4/R5)
+//   lipschitz_*_kernel   L_D on the 64x64 DFT grid (R8)
+//   filter_*_kernel      exact line search + unit-ball projection (R6-R8)
+//
+// Everything is FP32 state with FP64 cross-thread/cross-block sums in a fixed
+// order (deterministic run to run).  This file shares no code with oracle/.
+#include "csc_internal.cuh"
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace csc {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ void cp_async_f32(float* smem_dst, const float* gmem_src, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int bytes = valid ? 4 : 0;  // src-size 0 => zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem_src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed shuffle tree, then warp partials in order).
+// Result valid in thread 0.  Requires blockDim.x % 32 == 0, <= 1024.
+__device__ double block_sum_d(double v) {
+  __shared__ double red[32];
+  v = warp_sum_d(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int i = 0; i < nw; ++i) t += red[i];
+  }
+  return t;
+}
+
+__device__ double block_max_d(double v) {
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int i = 0; i < nw; ++i) t = fmax(t, red[i]);
+  }
+  return t;
+}
+
+// ------------------------------------------------------------------ Philox
+// Philox4x32-10 (Salmon et al., SC'11): 10 rounds of two 32x32->64 multiplies
+// with the Weyl key schedule.  Independent of oracle/ (pinned against it and,
+// through it, against curand).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+constexpr uint32_t kMaskTag = 0x4353434Du;  // 4th counter word, "CSCM" (#13)
+
+__device__ __forceinline__ uint4 mask_block(uint64_t seed, uint32_t iter, uint64_t q) {
+  return philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), iter, kMaskTag),
+                       make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)));
+}
+__device__ __forceinline__ uint32_t pick(const uint4& w, int i) {
+  return i == 0 ? w.x : (i == 1 ? w.y : (i == 2 ? w.z : w.w));
+}
+
+// Canonical layout: one 32-bit word per thread, bit l = (k*Hc+u)*Wc+v.
+__global__ void mask_bits_kernel(uint64_t total, uint64_t seed, uint32_t iter, uint64_t thr,
+                                 uint32_t* __restrict__ bits) {
+  const uint64_t wi = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nwords = (total + 31) / 32;
+  if (wi >= nwords) return;
+  uint32_t word = 0;
+#pragma unroll 1
+  for (int qq = 0; qq < 8; ++qq) {
+    const uint64_t q = wi * 8 + qq;
+    if (q * 4 >= total) break;
+    const uint4 w = mask_block(seed, iter, q);
+    const uint32_t v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t l = q * 4 + j;
+      if (l < total && static_cast<uint64_t>(v[j]) < thr) word |= 1u << (qq * 4 + j);
+    }
+  }
+  bits[wi] = word;
+}
+
+// Column-word layout for the code step: thread per (k, ub, quad of 4 columns);
+// colw[(k*NB+ub)*Wc+v] bit r = mask(k, 32*ub+r, v).  Rows >= Hc are 0.
+__global__ void mask_colwords_kernel(Geom g, int NB, uint64_t seed, uint32_t iter, uint64_t thr,
+                                     uint32_t* __restrict__ colw) {
+  const int nq = (g.Wc + 3) / 4;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = static_cast<int64_t>(g.K) * NB * nq;
+  if (tid >= total) return;
+  const int vq = static_cast<int>(tid % nq);
+  const int64_t kb = tid / nq;
+  const int ub = static_cast<int>(kb % NB);
+  const int k = static_cast<int>(kb / NB);
+  const int v0 = vq * 4;
+  uint32_t out[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 1
+  for (int r = 0; r < 32; ++r) {
+    const int u = ub * 32 + r;
+    if (u >= g.Hc) break;
+    const uint64_t l0 = (static_cast<uint64_t>(k) * g.Hc + u) * g.Wc + v0;
+    const uint64_t qa = l0 >> 2;
+    const uint4 wa = mask_block(seed, iter, qa);
+    uint4 wb = wa;
+    if ((l0 & 3) != 0) wb = mask_block(seed, iter, qa + 1);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (v0 + c >= g.Wc) break;
+      const uint64_t l = l0 + c;
+      const uint32_t w = ((l >> 2) == qa) ? pick(wa, static_cast<int>(l & 3)) : pick(wb, static_cast<int>(l & 3));
+      if (static_cast<uint64_t>(w) < thr) out[c] |= 1u << r;
+    }
+  }
+  uint32_t* dst = colw + (static_cast<int64_t>(k) * NB + ub) * g.Wc + v0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (v0 + c < g.Wc) dst[c] = out[c];
+}
+
+// ------------------------------------------------------------------ conv fwd
+// y[n,i,j] = sum_{k in split} sum_{a,b} f[k,a,b] z[n,k,i+P-a,j+P-b]
+// Tile 64x64 outputs, 128 threads, each thread a 4x8 register block.  The z
+// halo tile (64+P)^2 and the filter are double-buffered in shared memory with
+// cp.async; the filter tap row a for (z row rho, output row r_) is a = r_+P-rho.
+template <int S>
+struct ConvTile {
+  static constexpr int P = S - 1;
+  static constexpr int ZH = kConvTH + P;
+  static constexpr int ZW = kConvTW + P;
+  static constexpr int ZP = ((ZW + 3) / 4) * 4;
+  static constexpr int FP = ((S + 3) / 4) * 4;
+  static constexpr int ZR = ((kConvC + P + 3) / 4) * 4;
+  static constexpr int ZTILE = ZH * ZP;
+  static constexpr int FTILE = S * FP;
+  static constexpr int SMEM_FLOATS = 2 * (ZTILE + FTILE);
+};
+
+template <int S>
+__device__ __forceinline__ void conv_load_stage(float* zs, float* fs, const float* __restrict__ zk,
+                                                const float* __restrict__ fk, const Geom& g, int i0, int j0) {
+  using T = ConvTile<S>;
+  for (int e = threadIdx.x; e < T::ZH * T::ZW; e += kConvThreads) {
+    const int rr = e / T::ZW, cc = e - rr * T::ZW;
+    const int u = i0 + rr, v = j0 + cc;
+    const bool ok = (u < g.Hc) && (v < g.Wc);
+    cp_async_f32(zs + rr * T::ZP + cc, ok ? zk + static_cast<int64_t>(u) * g.Wc + v : zk, ok);
+  }
+  for (int e = threadIdx.x; e < S * S; e += kConvThreads) {
+    const int a = e / S, b = e - a * S;
+    cp_async_f32(fs + a * T::FP + b, fk + e, true);
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(kConvThreads, 4)
+conv_fwd_kernel(const float* __restrict__ z, const float* __restrict__ filt, const float* __restrict__ x,
+                float* __restrict__ out, int mode, int ksplit, Geom g, int tilesX,
+                double* __restrict__ sq_part, double* __restrict__ l1_part) {
+  using T = ConvTile<S>;
+  constexpr int P = T::P;
+  constexpr int R = kConvR, C = kConvC;
+  extern __shared__ __align__(16) float smem[];
+  float* zbuf[2] = {smem, smem + T::ZTILE};
+  float* fbuf[2] = {smem + 2 * T::ZTILE, smem + 2 * T::ZTILE + T::FTILE};
+
+  const int tile = blockIdx.x;
+  const int n = blockIdx.y;
+  const int ks = blockIdx.z;
+  const int i0 = (tile / tilesX) * kConvTH;
+  const int j0 = (tile % tilesX) * kConvTW;
+  const int k0 = static_cast<int>((static_cast<int64_t>(ks) * g.K) / ksplit);
+  const int k1 = static_cast<int>((static_cast<int64_t>(ks + 1) * g.K) / ksplit);
+  const int tx = threadIdx.x % kConvTX, ty = threadIdx.x / kConvTX;
+  const int64_t zimg = static_cast<int64_t>(n) * g.K * g.Hc * g.Wc;
+  const int64_t kstride = static_cast<int64_t>(g.Hc) * g.Wc;
+
+  // owned code positions for the L1 norm (each code counted once over all tiles)
+  const int u_end = (i0 + kConvTH >= g.H) ? g.Hc : i0 + kConvTH;
+  const int v_end = (j0 + kConvTW >= g.W) ? g.Wc : j0 + kConvTW;
+  double l1 = 0.0;
+
+  float acc[R][C];
+#pragma unroll
+  for (int r_ = 0; r_ < R; ++r_)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[r_][c] = 0.f;
+
+  if (k0 < k1) {
+    conv_load_stage<S>(zbuf[0], fbuf[0], z + zimg + k0 * kstride, filt + static_cast<int64_t>(k0) * S * S, g, i0, j0);
+    cp_async_commit();
+  }
+  for (int k = k0; k < k1; ++k) {
+    const int buf = (k - k0) & 1;
+    if (k + 1 < k1) {
+      conv_load_stage<S>(zbuf[buf ^ 1], fbuf[buf ^ 1], z + zimg + (k + 1) * kstride,
+                         filt + static_cast<int64_t>(k + 1) * S * S, g, i0, j0);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float* zs = zbuf[buf];
+    const float* fs = fbuf[buf];
+    if (l1_part != nullptr) {
+      float s1 = 0.f;
+      for (int e = threadIdx.x; e < T::ZH * T::ZW; e += kConvThreads) {
+        const int rr = e / T::ZW, cc = e - rr * T::ZW;
+        const int u = i0 + rr, v = j0 + cc;
+        if (u < u_end && v < v_end) s1 += fabsf(zs[rr * T::ZP + cc]);
+      }
+      l1 += static_cast<double>(s1);
+    }
+    const float* zt = zs + (ty * R) * T::ZP + tx * C;
+#pragma unroll 1
+    for (int rho = 0; rho < R + P; ++rho) {
+      float zr[T::ZR];
+#pragma unroll
+      for (int q = 0; q < T::ZR / 4; ++q) {
+        const float4 v4 = *reinterpret_cast<const float4*>(zt + rho * T::ZP + 4 * q);
+        zr[4 * q + 0] = v4.x; zr[4 * q + 1] = v4.y; zr[4 * q + 2] = v4.z; zr[4 * q + 3] = v4.w;
+      }
+#pragma unroll
+      for (int r_ = 0; r_ < R; ++r_) {
+        const int a = r_ + P - rho;
+        if (a >= 0 && a <= P) {
+          float fr[T::FP];
+#pragma unroll
+          for (int q = 0; q < T::FP / 4; ++q) {
+            const float4 v4 = *reinterpret_cast<const float4*>(fs + a * T::FP + 4 * q);
+            fr[4 * q + 0] = v4.x; fr[4 * q + 1] = v4.y; fr[4 * q + 2] = v4.z; fr[4 * q + 3] = v4.w;
+          }
+#pragma unroll
+          for (int b = 0; b < S; ++b)
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[r_][c] = fmaf(fr[b], zr[c + P - b], acc[r_][c]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  const int bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  double sq = 0.0;
+  const int64_t img = static_cast<int64_t>(n) * g.H * g.W;
+  if (ksplit == 1) {
+#pragma unroll
+    for (int r_ = 0; r_ < R; ++r_) {
+      const int i = i0 + ty * R + r_;
+      if (i >= g.H) continue;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int j = j0 + tx * C + c;
+        if (j >= g.W) continue;
+        const int64_t idx = img + static_cast<int64_t>(i) * g.W + j;
+        float v = acc[r_][c];
+        if (mode == kConvResidual) {
+          v = v - x[idx];
+          out[idx] = v;
+        }
+        sq += static_cast<double>(v) * static_cast<double>(v);
+      }
+    }
+    const double t = block_sum_d(sq);
+    if (threadIdx.x == 0 && sq_part != nullptr) sq_part[bid] = t;
+  } else {
+    float* dst = out + static_cast<int64_t>(ks) * g.N * g.H * g.W + img;
+#pragma unroll
+    for (int r_ = 0; r_ < R; ++r_) {
+      const int i = i0 + ty * R + r_;
+      if (i >= g.H) continue;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int j = j0 + tx * C + c;
+        if (j < g.W) dst[static_cast<int64_t>(i) * g.W + j] = acc[r_][c];
+      }
+    }
+  }
+  if (l1_part != nullptr) {
+    const double t = block_sum_d(l1);
+    if (threadIdx.x == 0) l1_part[bid] = t;
+  }
+}
+
+__global__ void conv_finalize_kernel(const float* __restrict__ part, int ksplit, int64_t npix,
+                                     const float* __restrict__ x, float* __restrict__ r, int mode,
+                                     double* __restrict__ sq_part) {
+  double sq = 0.0;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < npix;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float v = 0.f;
+    for (int ks = 0; ks < ksplit; ++ks) v += part[ks * npix + idx];
+    if (mode == kConvResidual) {
+      v = v - x[idx];
+      r[idx] = v;
+    }
+    sq += static_cast<double>(v) * static_cast<double>(v);
+  }
+  const double t = block_sum_d(sq);
+  if (threadIdx.x == 0) sq_part[blockIdx.x] = t;
+}
+
+__global__ void reduce_sum_kernel(const double* __restrict__ part, int n, double* __restrict__ out,
+                                  double scale) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  const double t = block_sum_d(s);
+  if (threadIdx.x == 0) *out = t * scale;
+}
+
+// ------------------------------------------------------------------ wgrad
+// g[k,a,b] = sum_n sum_ij r[n,i,j] z[n,k,i+P-a,j+P-b].  Grid (G, K): the CTA for
+// (gi, k) loops over tiles t = gi, gi+G, ... of all images, accumulating the
+// full s x s tap block per thread in registers; one fixed-order reduction at the end.
+template <int S>
+struct WgTile {
+  static constexpr int P = S - 1;
+  static constexpr int ZH = kWgTH + P;
+  static constexpr int ZW = kWgTW + P;
+  static constexpr int ZP = ((ZW + 3) / 4) * 4;
+  static constexpr int RP = kWgTW;
+  static constexpr int ZR = ((kWgC + P + 3) / 4) * 4;
+  static constexpr int SMEM_FLOATS = ZH * ZP + kWgTH * RP;
+};
+
+template <int S>
+__global__ void __launch_bounds__(kWgThreads, 2)
+wgrad_kernel(const float* __restrict__ z, const float* __restrict__ r, Geom g, int tilesX, int tilesY,
+             int G, double* __restrict__ gpart) {
+  using T = WgTile<S>;
+  constexpr int P = T::P;
+  constexpr int C = kWgC, RB = kWgRB;
+  extern __shared__ __align__(16) float smem[];
+  float* zs = smem;
+  float* rs = smem + T::ZH * T::ZP;
+  const int gi = blockIdx.x, k = blockIdx.y;
+  const int tx = threadIdx.x % kWgTX, ty = threadIdx.x / kWgTX;
+  const int ntiles = g.N * tilesX * tilesY;
+
+  float acc[S][S];
+#pragma unroll
+  for (int a = 0; a < S; ++a)
+#pragma unroll
+    for (int b = 0; b < S; ++b) acc[a][b] = 0.f;
+
+  for (int t = gi; t < ntiles; t += G) {
+    const int n = t / (tilesX * tilesY);
+    const int tt = t - n * tilesX * tilesY;
+    const int i0 = (tt / tilesX) * kWgTH, j0 = (tt % tilesX) * kWgTW;
+    const float* zk = z + (static_cast<int64_t>(n) * g.K + k) * g.Hc * g.Wc;
+    const float* rn = r + static_cast<int64_t>(n) * g.H * g.W;
+    __syncthreads();
+    for (int e = threadIdx.x; e < T::ZH * T::ZW; e += kWgThreads) {
+      const int rr = e / T::ZW, cc = e - rr * T::ZW;
+      const int u = i0 + rr, v = j0 + cc;
+      const bool ok = (u < g.Hc) && (v < g.Wc);
+      cp_async_f32(zs + rr * T::ZP + cc, ok ? zk + static_cast<int64_t>(u) * g.Wc + v : zk, ok);
+    }
+    for (int e = threadIdx.x; e < kWgTH * kWgTW; e += kWgThreads) {
+      const int rr = e / kWgTW, cc = e - rr * kWgTW;
+      const int i = i0 + rr, j = j0 + cc;
+      const bool ok = (i < g.H) && (j < g.W);
+      cp_async_f32(rs + rr * T::RP + cc, ok ? rn + static_cast<int64_t>(i) * g.W + j : rn, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll 1
+    for (int rr = 0; rr < RB; ++rr) {
+      const int il = ty * RB + rr;
+      float rv[C];
+#pragma unroll
+      for (int q = 0; q < C / 4; ++q) {
+        const float4 v4 = *reinterpret_cast<const float4*>(rs + il * T::RP + tx * C + 4 * q);
+        rv[4 * q + 0] = v4.x; rv[4 * q + 1] = v4.y; rv[4 * q + 2] = v4.z; rv[4 * q + 3] = v4.w;
+      }
+      const float* zrow0 = zs + (il + P) * T::ZP + tx * C;
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        float zr[T::ZR];
+#pragma unroll
+        for (int q = 0; q < T::ZR / 4; ++q) {
+          const float4 v4 = *reinterpret_cast<const float4*>(zrow0 - a * T::ZP + 4 * q);
+          zr[4 * q + 0] = v4.x; zr[4 * q + 1] = v4.y; zr[4 * q + 2] = v4.z; zr[4 * q + 3] = v4.w;
+        }
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[a][b] = fmaf(rv[c], zr[c + P - b], acc[a][b]);
+      }
+    }
+  }
+
+  // fixed-order reduction of the per-thread tap blocks
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(smem);  // [warps][S*S]
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int a = 0; a < S; ++a)
+#pragma unroll
+    for (int b = 0; b < S; ++b) {
+      const double v = warp_sum_d(static_cast<double>(acc[a][b]));
+      if (l == 0) red[w * S * S + a * S + b] = v;
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < S * S; e += kWgThreads) {
+    double s = 0.0;
+    for (int ww = 0; ww < kWgThreads / 32; ++ww) s += red[ww * S * S + e];
+    gpart[(static_cast<int64_t>(gi) * g.K + k) * S * S + e] = s;
+  }
+}
+
+__global__ void wgrad_reduce_kernel(const double* __restrict__ gpart, int G, int nel, double* __restrict__ gsum) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nel) return;
+  double s = 0.0;
+  for (int gi = 0; gi < G; ++gi) s += gpart[static_cast<int64_t>(gi) * nel + e];
+  gsum[e] = s;
+}
+
+__global__ void grad_finish_kernel(const double* __restrict__ gsum, int nel, float* __restrict__ g32,
+                                   double* __restrict__ gg_out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nel; i += blockDim.x) {
+    const double v = gsum[i];
+    g32[i] = static_cast<float>(v);
+    s += v * v;
+  }
+  const double t = block_sum_d(s);
+  if (threadIdx.x == 0) *gg_out = t;
+}
+
+// ------------------------------------------------------------------ code step
+// CTA = (32-column strip, TH-row band, image n, k group); lane L owns column
+// v0+L; the 4 warps take k = kb+w, kb+w+4, ...  Each lane walks the masked rows
+// of its column (bits from the column-word mask) and, per masked code, does the
+// s^2-tap correlation with the residual tile in shared memory (pitch 64 => the
+// 32 lanes always hit 32 distinct banks), the step and the shrinkage.  Codes
+// whose value does not change are not written back.
+template <int S>
+__global__ void __launch_bounds__(kCodeThreads, 3)
+code_step_kernel(const float* __restrict__ r, const float* __restrict__ d, float* __restrict__ z,
+                 const uint32_t* __restrict__ colw, int all_selected, const float* __restrict__ tau_dev,
+                 float lam, Geom g, int TH, int kgroups, int NB) {
+  constexpr int P = S - 1;
+  extern __shared__ __align__(16) float rs[];
+  const int v0 = blockIdx.x * 32;
+  const int u0 = blockIdx.y * TH;
+  const int n = blockIdx.z / kgroups;
+  const int kg = blockIdx.z - n * kgroups;
+  const int kb = static_cast<int>((static_cast<int64_t>(kg) * g.K) / kgroups);
+  const int ke = static_cast<int>((static_cast<int64_t>(kg + 1) * g.K) / kgroups);
+  const float* rn = r + static_cast<int64_t>(n) * g.H * g.W;
+
+  // residual tile: rows [u0-P, u0+TH), cols [v0-P, v0+32), zero outside the image
+  const int tw = 32 + P;
+  for (int e = threadIdx.x; e < (TH + P) * tw; e += kCodeThreads) {
+    const int lr = e / tw, lc = e - lr * tw;
+    const int i = u0 - P + lr, j = v0 - P + lc;
+    float v = 0.f;
+    if (i >= 0 && i < g.H && j >= 0 && j < g.W) v = rn[static_cast<int64_t>(i) * g.W + j];
+    rs[lr * kCodePitch + lc] = v;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int v = v0 + lane;
+  const bool col_ok = v < g.Wc;
+  const float tau = *tau_dev;
+  const float kappa = tau * lam;
+  const int nblk = TH / 32;
+  const int ub0 = u0 / 32;
+
+  for (int k = kb + warp; k < ke; k += kCodeWarps) {
+    float dk[S * S];
+#pragma unroll
+    for (int i = 0; i < S * S; ++i) dk[i] = __ldg(d + static_cast<int64_t>(k) * S * S + i);
+    uint32_t q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ub = ub0 + j;
+      uint32_t wbits = 0u;
+      if (j < nblk && ub < NB && col_ok) {
+        if (all_selected) {
+          const int rows = g.Hc - ub * 32;
+          wbits = rows >= 32 ? kFull : ((1u << rows) - 1u);
+        } else {
+          wbits = __ldg(colw + (static_cast<int64_t>(k) * NB + ub) * g.Wc + v);
+        }
+      }
+      q[j] = wbits;
+    }
+    float* zk = z + (static_cast<int64_t>(n) * g.K + k) * g.Hc * g.Wc;
+    uint32_t bits = q[0];
+    int blk = 0;
+    while (true) {
+      while (bits == 0u && blk < 3) {
+        bits = q[1]; q[1] = q[2]; q[2] = q[3]; q[3] = 0u; ++blk;
+      }
+      const bool have = bits != 0u;
+      if (!__any_sync(kFull, have)) break;
+      if (have) {
+        const int rbit = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const int ul = blk * 32 + rbit;
+        const int u = u0 + ul;
+        const int64_t zi = static_cast<int64_t>(u) * g.Wc + v;
+        const float zv = zk[zi];
+        const float* rp = rs + ul * kCodePitch + lane;
+        float c = 0.f;
+#pragma unroll
+        for (int a = 0; a < S; ++a)
+#pragma unroll
+          for (int b = 0; b < S; ++b) c = fmaf(dk[a * S + b], rp[a * kCodePitch + b], c);
+        const float w = fmaf(-tau, c, zv);
+        const float nz = (w > kappa) ? (w - kappa) : ((w < -kappa) ? (w + kappa) : 0.f);
+        if (nz != zv) zk[zi] = nz;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ Lipschitz
+// part[kc][m1*64+m2] = sum_{k in chunk kc} |sum_{a,b} d[k,a,b] w^(a m1 + b m2)|^2, w = e^{-2 pi i/64}
+constexpr int kLipG = 64;
+constexpr int kLipKChunk = 16;
+__global__ void lipschitz_partial_kernel(const float* __restrict__ d, Geom g, double* __restrict__ part) {
+  __shared__ double twc[kLipG], tws[kLipG];
+  const int m1 = blockIdx.x, kc = blockIdx.y, m2 = threadIdx.x;
+  {
+    double sv, cv;
+    sincospi(-2.0 * static_cast<double>(threadIdx.x) / kLipG, &sv, &cv);
+    twc[threadIdx.x] = cv;
+    tws[threadIdx.x] = sv;
+  }
+  __syncthreads();
+  const int S = g.S;
+  const int k0 = kc * kLipKChunk, k1 = min(g.K, k0 + kLipKChunk);
+  double tot = 0.0;
+  for (int k = k0; k < k1; ++k) {
+    double re = 0.0, im = 0.0;
+    for (int a = 0; a < S; ++a) {
+      double ra = 0.0, ia = 0.0;
+      for (int b = 0; b < S; ++b) {
+        const double dv = static_cast<double>(__ldg(d + (static_cast<int64_t>(k) * S + a) * S + b));
+        const int idx = (b * m2) & (kLipG - 1);
+        ra += dv * twc[idx];
+        ia += dv * tws[idx];
+      }
+      const int ia_idx = (a * m1) & (kLipG - 1);
+      const double c = twc[ia_idx], s = tws[ia_idx];
+      re += ra * c - ia * s;
+      im += ra * s + ia * c;
+    }
+    tot += re * re + im * im;
+  }
+  part[static_cast<int64_t>(kc) * kLipG * kLipG + m1 * kLipG + m2] = tot;
+}
+
+__global__ void lipschitz_final_kernel(const double* __restrict__ part, int nkc, double* __restrict__ lhat,
+                                       float* __restrict__ tau_out) {
+  double best = 0.0;
+  for (int e = threadIdx.x; e < kLipG * kLipG; e += blockDim.x) {
+    double s = 0.0;
+    for (int kc = 0; kc < nkc; ++kc) s += part[static_cast<int64_t>(kc) * kLipG * kLipG + e];
+    best = fmax(best, s);
+  }
+  const double m = block_max_d(best);
+  if (threadIdx.x == 0) {
+    *lhat = m;
+    if (tau_out != nullptr) *tau_out = m > 0.0 ? static_cast<float>(1.0 / m) : 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ filter update
+__global__ void filter_tau_kernel(const double* __restrict__ gg, const double* __restrict__ zg2, float step,
+                                  float* __restrict__ tau_d) {
+  if (step > 0.f) {
+    *tau_d = step;
+  } else {
+    const double den = *zg2;
+    *tau_d = den > 0.0 ? static_cast<float>(*gg / den) : 0.f;
+  }
+}
+
+__global__ void filter_update_kernel(float* __restrict__ d, const double* __restrict__ gsum,
+                                     const float* __restrict__ tau_d, int M) {
+  const int k = blockIdx.x;
+  const double tau = static_cast<double>(*tau_d);
+  double e_loc[8];
+  double s2 = 0.0;
+  int cnt = 0;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    const double e = static_cast<double>(d[static_cast<int64_t>(k) * M + i]) - tau * gsum[static_cast<int64_t>(k) * M + i];
+    e_loc[cnt++] = e;
+    s2 += e * e;
+  }
+  __shared__ double scale_sh;
+  const double t = block_sum_d(s2);
+  if (threadIdx.x == 0) scale_sh = fmax(1.0, sqrt(t));
+  __syncthreads();
+  const double scale = scale_sh;
+  cnt = 0;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) d[static_cast<int64_t>(k) * M + i] = static_cast<float>(e_loc[cnt++] / scale);
+}
+
+__global__ void neg_copy_kernel(const float* __restrict__ x, float* __restrict__ r, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    r[i] = -x[i];
+}
+
+template <template <int> class F, typename... Args>
+cudaError_t dispatch_s(int s, Args&&... args) {
+  switch (s) {
+    case 1: return F<1>::run(args...);
+    case 3: return F<3>::run(args...);
+    case 5: return F<5>::run(args...);
+    case 7: return F<7>::run(args...);
+    case 9: return F<9>::run(args...);
+    case 11: return F<11>::run(args...);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int S>
+struct ConvRun {
+  static cudaError_t run(const Geom& g, const float* z, const float* filt, const float* x, float* out, int ksplit,
+                         int mode, double* sq_part, double* l1_part, cudaStream_t st) {
+    using T = ConvTile<S>;
+    const int tilesX = ceil_div(g.W, kConvTW), tilesY = ceil_div(g.H, kConvTH);
+    const size_t smem = sizeof(float) * T::SMEM_FLOATS;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(conv_fwd_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      attr = true;
+    }
+    dim3 grid(tilesX * tilesY, g.N, ksplit);
+    conv_fwd_kernel<S><<<grid, kConvThreads, smem, st>>>(z, filt, x, out, mode, ksplit, g, tilesX, sq_part, l1_part);
+    return cudaGetLastError();
+  }
+};
+
+template <int S>
+struct WgRun {
+  static cudaError_t run(const Geom& g, const float* z, const float* r, int G, double* gpart, cudaStream_t st) {
+    using T = WgTile<S>;
+    const int tilesX = ceil_div(g.W, kWgTW), tilesY = ceil_div(g.H, kWgTH);
+    size_t smem = sizeof(float) * T::SMEM_FLOATS;
+    const size_t red = sizeof(double) * (kWgThreads / 32) * S * S;
+    if (red > smem) smem = red;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(wgrad_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      attr = true;
+    }
+    dim3 grid(G, g.K);
+    wgrad_kernel<S><<<grid, kWgThreads, smem, st>>>(z, r, g, tilesX, tilesY, G, gpart);
+    return cudaGetLastError();
+  }
+};
+
+inline int code_tile_rows(int Hc) {
+  // rows per band: a multiple of 32 (column words are 32-row aligned), <= 128,
+  // chosen to minimise padding rows.
+  int best = 32, best_waste = 1 << 30;
+  for (int th = 32; th <= 128; th += 32) {
+    const int waste = ceil_div(Hc, th) * th - Hc;
+    if (waste < best_waste || (waste == best_waste && th > best)) {
+      best = th;
+      best_waste = waste;
+    }
+  }
+  return best;
+}
+
+template <int S>
+struct CodeRun {
+  static cudaError_t run(const Geom& g, const float* r, const float* d, float* z, const uint32_t* colw,
+                         int all_selected, const float* tau_dev, float lam, cudaStream_t st) {
+    const int TH = code_tile_rows(g.Hc);
+    const int strips = ceil_div(g.Wc, 32), bands = ceil_div(g.Hc, TH);
+    const int base = strips * bands * g.N;
+    int kgroups = ceil_div(148 * 6, base > 0 ? base : 1);
+    const int kmax = ceil_div(g.K, kCodeWarps);
+    if (kgroups > kmax) kgroups = kmax;
+    if (kgroups < 1) kgroups = 1;
+    const size_t smem = sizeof(float) * (TH + S - 1) * kCodePitch;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(code_step_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      attr = true;
+    }
+    const int NB = ceil_div(g.Hc, 32);
+    dim3 grid(strips, bands, g.N * kgroups);
+    code_step_kernel<S><<<grid, kCodeThreads, smem, st>>>(r, d, z, colw, all_selected, tau_dev, lam, g, TH, kgroups, NB);
+    return cudaGetLastError();
+  }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+int conv_fwd_blocks(const Geom& g, int ksplit) {
+  return ceil_div(g.W, kConvTW) * ceil_div(g.H, kConvTH) * g.N * ksplit;
+}
+
+cudaError_t launch_conv_fwd(const Geom& g, const float* z, const float* filt, const float* x, float* r,
+                            float* part, int ksplit, int mode, double* sq_part, double* l1_part,
+                            cudaStream_t st, int* nblocks_out) {
+  if (nblocks_out) *nblocks_out = conv_fwd_blocks(g, ksplit);
+  float* out = ksplit == 1 ? r : part;
+  return dispatch_s<ConvRun>(g.S, g, z, filt, x, out, ksplit, mode, sq_part, l1_part, st);
+}
+
+cudaError_t launch_conv_finalize(const Geom& g, const float* part, int ksplit, const float* x, float* r, int mode,
+                                 double* sq_part, cudaStream_t st) {
+  const int64_t npix = static_cast<int64_t>(g.N) * g.H * g.W;
+  conv_finalize_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, ksplit, npix, x, r, mode, sq_part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_sum(const double* part, int n, double* out, double scale, cudaStream_t st) {
+  reduce_sum_kernel<<<1, kReduceThreads, 0, st>>>(part, n, out, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wgrad(const Geom& g, const float* z, const float* r, int G, double* gpart, cudaStream_t st) {
+  return dispatch_s<WgRun>(g.S, g, z, r, G, gpart, st);
+}
+
+cudaError_t launch_wgrad_reduce(const Geom& g, const double* gpart, int G, double* gsum, cudaStream_t st) {
+  const int nel = g.K * g.S * g.S;
+  wgrad_reduce_kernel<<<ceil_div(nel, 256), 256, 0, st>>>(gpart, G, nel, gsum);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, double* gg_out, cudaStream_t st) {
+  const int nel = g.K * g.S * g.S;
+  grad_finish_kernel<<<1, 1024, 0, st>>>(gsum, nel, g32, gg_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mask_colwords(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr, uint32_t* colw,
+                                 cudaStream_t st) {
+  const int NB = ceil_div(g.Hc, 32);
+  const int64_t total = static_cast<int64_t>(g.K) * NB * ceil_div(g.Wc, 4);
+  mask_colwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g, NB, seed, iter, thr, colw);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mask_bits(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr, uint32_t* bits,
+                             cudaStream_t st) {
+  const uint64_t total = static_cast<uint64_t>(g.K) * g.Hc * g.Wc;
+  const uint64_t nwords = (total + 31) / 32;
+  mask_bits_kernel<<<static_cast<unsigned>((nwords + 255) / 256), 256, 0, st>>>(total, seed, iter, thr, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_code_step(const Geom& g, const float* r, const float* d, float* z, const uint32_t* colw,
+                             int all_selected, const float* tau_dev, float lam, cudaStream_t st) {
+  return dispatch_s<CodeRun>(g.S, g, r, d, z, colw, all_selected, tau_dev, lam, st);
+}
+
+cudaError_t launch_lipschitz(const Geom& g, const float* d, double* part, double* lhat, float* tau_out,
+                             cudaStream_t st) {
+  const int nkc = ceil_div(g.K, kLipKChunk);
+  lipschitz_partial_kernel<<<dim3(kLipG, nkc), kLipG, 0, st>>>(d, g, part);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  lipschitz_final_kernel<<<1, 256, 0, st>>>(part, nkc, lhat, tau_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_filter_tau(const double* gg, const double* zg2, float step, float* tau_d, cudaStream_t st) {
+  filter_tau_kernel<<<1, 1, 0, st>>>(gg, zg2, step, tau_d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_filter_update(const Geom& g, float* d, const double* gsum, const float* tau_d, cudaStream_t st) {
+  const int M = g.S * g.S;  // <= 121 <= 128 threads * 8 slots
+  filter_update_kernel<<<g.K, 128, 0, st>>>(d, gsum, tau_d, M);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st) {
+  neg_copy_kernel<<<kFinalizeBlocks, 256, 0, st>>>(x, r, n);
+  return cudaGetLastError();
+}
+
+}  // namespace csc

@@ -1,0 +1,266 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): masks bit-exact; codes, filters and objective
+within 1e-5 relative (norm-wise, reading R9) per iteration over 50 iterations;
+the residual r and gradient g within 1e-5; the step sizes within 1e-6.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import CONFIGS, make_codes, make_filters, make_images, mask_seed, random_problem
+from tests.conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+TOL_TAU = 1e-6
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+    from paper_1909_00145_b200 import build as b
+    b.build()
+    torch.cuda.set_device(0)
+    return torch.device("cuda:0")
+
+
+def _ctx(N, K, s, H, W):
+    import paper_1909_00145_b200 as pkg
+    return pkg.Context(N, K, s, H, W, device=0)
+
+
+def _t(a, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+@pytest.mark.parametrize("K,Hc,Wc", [(8, 36, 36), (3, 7, 9), (5, 41, 67), (100, 110, 110), (2, 33, 29)])
+@pytest.mark.parametrize("p", [0.05, 0.1, 0.5, 1.0])
+def test_mask_bits_bit_exact(torch_dev, K, Hc, Wc, p):
+    import torch
+    s = 3
+    ctx = _ctx(1, K, s, Hc - s + 1, Wc - s + 1)
+    nwords = (K * Hc * Wc + 31) // 32
+    out = torch.zeros(nwords, dtype=torch.int32, device=torch_dev)
+    for seed, it in [(0, 0), (0x0123456789ABCDEF, 7), (2**64 - 1, 2**32 - 1)]:
+        ctx.mask_bits(it, p, seed, out)
+        torch.cuda.synchronize()
+        ref = oracle.mask_bits(K, Hc, Wc, p, seed, it)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+    ctx.close()
+
+
+def test_lipschitz_parity(torch_dev):
+    for K, s in [(8, 5), (100, 11), (3, 1), (17, 7)]:
+        d = np.random.default_rng(K).standard_normal((K, s, s)).astype(np.float32)
+        ctx = _ctx(1, K, s, s + 3, s + 3)
+        L = ctx.lipschitz(_t(d, torch_dev))
+        assert abs(L - oracle.lipschitz(d)) <= 1e-12 * L
+        ctx.close()
+
+
+@pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (4, 8, 5, 32, 32),
+                                   (1, 3, 1, 9, 65), (2, 6, 3, 129, 64), (1, 2, 9, 9, 9)])
+def test_residual_and_objective_parity(torch_dev, shape):
+    N, K, s, H, W = shape
+    x, d, z = random_problem(100 + K, N, K, s, H, W, code_density=0.3)
+    ctx = _ctx(N, K, s, H, W)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    lam = 0.7
+    F = ctx.objective(xt, dt, zt, lam)
+    r = _t(np.zeros_like(x), torch_dev)
+    ctx.read_residual(r)
+    import torch
+    torch.cuda.synchronize()
+    assert rel_err(r.cpu().numpy(), oracle.residual(x, d, z)) < TOL
+    Fo = oracle.objective(x, d, z, lam)
+    for a, b_ in zip(F, Fo):
+        assert abs(a - b_) <= TOL * abs(b_)
+    ctx.close()
+
+
+@pytest.mark.parametrize("shape,p", [((3, 5, 5, 70, 130), 0.1), ((2, 17, 11, 100, 100), 0.2),
+                                     ((4, 8, 5, 32, 32), 1.0), ((1, 9, 3, 33, 47), 0.5), ((2, 4, 11, 11, 11), 0.05)])
+def test_code_step_parity(torch_dev, shape, p):
+    import torch
+    N, K, s, H, W = shape
+    x, d, z = random_problem(200 + K, N, K, s, H, W, code_density=0.3)
+    seed, it, lam = 12345, 3, 0.2
+    ctx = _ctx(N, K, s, H, W)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    tau = ctx.code_step(xt, dt, zt, lam, p, seed, it, want_step=True)
+    zg = zt.cpu().numpy()
+    zo, tau_o = oracle.code_step(x, d, z, lam, 0.0, p, seed, it)
+    assert abs(tau - tau_o) <= TOL_TAU * tau_o
+    assert rel_err(zg, zo) < TOL
+    Hc, Wc = H + s - 1, W + s - 1
+    m = oracle.unpack_mask(oracle.mask_bits(K, Hc, Wc, p, seed, it), K, Hc, Wc)
+    for n in range(N):
+        assert np.array_equal(zg[n][~m], z[n][~m])  # unsampled codes bit-identical (R2)
+    # explicit step size
+    zt2 = _t(z, torch_dev)
+    ctx.invalidate()
+    ctx.code_step(xt, dt, zt2, lam, p, seed, it, step_z=0.01)
+    zo2, _ = oracle.code_step(x, d, z, lam, 0.01, p, seed, it)
+    torch.cuda.synchronize()
+    assert rel_err(zt2.cpu().numpy(), zo2) < TOL
+    ctx.close()
+
+
+@pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (1, 3, 3, 9, 9)])
+def test_filter_step_parity(torch_dev, shape):
+    import torch
+    N, K, s, H, W = shape
+    x, d, z = random_problem(300 + K, N, K, s, H, W, code_density=0.3)
+    ctx = _ctx(N, K, s, H, W)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    tau = ctx.filter_step(xt, dt, zt, want_step=True)
+    g = torch.zeros(K * s * s, dtype=torch.float64, device=torch_dev)
+    ctx.read_grad(g)
+    torch.cuda.synchronize()
+    do, tau_o, go, _ = oracle.filter_step(x, d, z)
+    assert rel_err(g.cpu().numpy(), go.ravel()) < TOL
+    assert abs(tau - tau_o) <= TOL_TAU * tau_o
+    assert rel_err(dt.cpu().numpy(), do) < TOL
+    assert (np.sqrt((dt.cpu().numpy().astype(np.float64) ** 2).sum(axis=(1, 2))) <= 1 + 1e-6).all()
+    ctx.close()
+
+
+def _trajectory(torch_dev, cfg, iters, p=None, check_every=1):
+    import torch
+    p = cfg.p if p is None else p
+    x, d, z = make_images(cfg), make_filters(cfg), make_codes(cfg)
+    seed = mask_seed(cfg)
+    ctx = _ctx(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    worst = {"z": 0.0, "d": 0.0, "F": 0.0, "tau_z": 0.0, "tau_d": 0.0}
+    for t in range(1, iters + 1):
+        F, taus = ctx.iterate(xt, dt, zt, cfg.lam, p, seed, t)
+        it = oracle.iteration(x, d, z, cfg.lam, p, seed, t)
+        z, d = it["z"], it["d"]
+        if t % check_every == 0 or t == iters:
+            torch.cuda.synchronize()
+            errs = {"z": rel_err(zt.cpu().numpy(), z), "d": rel_err(dt.cpu().numpy(), d),
+                    "F": abs(F[0] - it["F"][0]) / abs(it["F"][0]),
+                    "tau_z": abs(taus[0] - it["tau_z"]) / it["tau_z"],
+                    "tau_d": abs(taus[1] - it["tau_d"]) / max(it["tau_d"], 1e-30)}
+            for k_, v in errs.items():
+                worst[k_] = max(worst[k_], v)
+            assert errs["z"] < TOL and errs["d"] < TOL and errs["F"] < TOL, (t, errs)
+            assert errs["tau_z"] < TOL_TAU and errs["tau_d"] < TOL_TAU, (t, errs)
+    ctx.close()
+    return worst
+
+
+def test_trajectory_tiny_50_iterations(torch_dev):
+    """Config 1 (BASELINE.json configs[0]): 50 code+filter iterations, every iteration compared."""
+    w = _trajectory(torch_dev, CONFIGS["tiny"], 50)
+    print("tiny worst", w)
+
+
+def test_trajectory_ragged_multitile(torch_dev):
+    """Several 64x64 tiles with ragged tails, s=11, p=0.2, 20 iterations."""
+    cfg = CONFIGS["batch"].with_(name="ragged", N=3, K=12, H=70, W=135, p=0.2)
+    _trajectory(torch_dev, cfg, 20)
+
+
+@pytest.mark.parametrize("p", [0.1, 1.0])
+def test_trajectory_batch_config(torch_dev, p):
+    """Config 2 (BASELINE.json configs[1]) at full size: first 5 iterations, every one compared."""
+    _trajectory(torch_dev, CONFIGS["batch"], 5, p=p)
+
+
+def test_zero_codes_and_online_step(torch_dev):
+    """SOCSC step (Alg.2): zero codes -> 10 masked code steps -> filter step -> objective."""
+    import torch
+    cfg = CONFIGS["online"].with_(K=24, N=3, H=40, W=44)
+    x = make_images(cfg)
+    d = make_filters(cfg)
+    seed = mask_seed(cfg)
+    ctx = _ctx(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W)
+    xt, dt = _t(x, torch_dev), _t(d, torch_dev)
+    zt = torch.full((cfg.N, cfg.K, cfg.Hc, cfg.Wc), 3.0, device=torch_dev)
+    ctx.zero_codes(xt, zt)
+    r = torch.zeros_like(xt)
+    ctx.read_residual(r)
+    torch.cuda.synchronize()
+    assert not zt.any() and torch.equal(r, -xt)
+    z = np.zeros((cfg.N, cfg.K, cfg.Hc, cfg.Wc), np.float32)
+    for i in range(10):
+        ctx.code_step(xt, dt, zt, cfg.lam, cfg.p, seed, i)
+        z, _ = oracle.code_step(x, d, z, cfg.lam, 0.0, cfg.p, seed, i)
+    ctx.filter_step(xt, dt, zt)
+    d1, _, _, _ = oracle.filter_step(x, d, z)
+    F = ctx.objective(xt, dt, zt, cfg.lam)
+    Fo = oracle.objective(x, d1, z, cfg.lam)
+    torch.cuda.synchronize()
+    assert rel_err(zt.cpu().numpy(), z) < TOL
+    assert rel_err(dt.cpu().numpy(), d1) < TOL
+    assert abs(F[0] - Fo[0]) < TOL * Fo[0]
+    ctx.close()
+
+
+def test_empty_local_batch(torch_dev):
+    """n_local = 0 (a rank with no images): steps are no-ops on codes, filters get a zero gradient."""
+    import torch
+    ctx = _ctx(0, 4, 3, 8, 8)
+    d = _t(make_filters(CONFIGS["tiny"].with_(K=4, s=3)), torch_dev)
+    d0 = d.clone()
+    e = torch.zeros(0, device=torch_dev)
+    ctx.code_step(e, d, e, 1.0, 0.5, 1, 1)
+    ctx.filter_step(e, d, e)
+    F = ctx.objective(e, d, e, 1.0)
+    torch.cuda.synchronize()
+    assert F == (0.0, 0.0, 0.0)
+    assert torch.equal(d, d0)
+    ctx.close()
+
+
+def test_argument_errors(torch_dev):
+    import torch
+    import paper_1909_00145_b200 as pkg
+    x, d, z = random_problem(1, 1, 2, 3, 8, 8)
+    ctx = _ctx(1, 2, 3, 8, 8)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    z0 = zt.clone()
+    for bad in [dict(p=0.0), dict(p=1.5), dict(lam=-1.0), dict(lam=float("nan"))]:
+        kw = dict(lam=1.0, p=0.5)
+        kw.update(bad)
+        with pytest.raises(pkg.CSCError) as ei:
+            ctx.code_step(xt, dt, zt, kw["lam"], kw["p"], 1, 1)
+        assert ei.value.status == 1
+    torch.cuda.synchronize()
+    assert torch.equal(zt, z0)  # no side effects
+    ctx.close()
+
+
+@pytest.mark.slow
+def test_full_size_sweep_config_sampled(torch_dev):
+    """Config 3 (N=40, 256x256, K=100, s=11, p=0.1) in the launch configuration bench.py times:
+    one full iteration on the GPU; the oracle checks sampled images for the code step (per-image
+    independent), the full filter gradient / step and the objective."""
+    import torch
+    cfg = CONFIGS["sweep"]
+    x, d, z = make_images(cfg), make_filters(cfg), make_codes(cfg)
+    seed = mask_seed(cfg)
+    ctx = _ctx(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    # iteration 1 from the initial state, codes first
+    ctx.code_step(xt, dt, zt, cfg.lam, cfg.p, seed, 1)
+    torch.cuda.synchronize()
+    zg = zt.cpu().numpy()
+    sample = [0, cfg.N - 1]
+    zo, _ = oracle.code_step(x[sample], d, z[sample], cfg.lam, 0.0, cfg.p, seed, 1)
+    assert rel_err(zg[sample], zo) < TOL
+    # filter step + objective on the GPU's codes (all 40 images)
+    tau = ctx.filter_step(xt, dt, zt, want_step=True)
+    do, tau_o, _, _ = oracle.filter_step(x, d, zg)
+    torch.cuda.synchronize()
+    assert abs(tau - tau_o) <= TOL_TAU * tau_o
+    assert rel_err(dt.cpu().numpy(), do) < TOL
+    F = ctx.objective(xt, dt, zt, cfg.lam)
+    Fo = oracle.objective(x, do, zg, cfg.lam)
+    assert abs(F[0] - Fo[0]) <= TOL * Fo[0]
+    ctx.close()
