@@ -39,13 +39,63 @@ SMS = 148
 FP32_LANES_PER_SM = 128
 
 
+FALLBACK_BF16_TFLOPS = 1590.0
+TF32_PER_BF16 = 1.1 / 2.25   # guide's nominal dense ratio (B200_PROFILING.md)
+
+
 def _peaks():
     try:
         with open(PEAKS_PATH) as f:
             pk = json.load(f)
-        return float(pk["hbm_gbs"]), float(pk.get("sm_max_mhz", 1965.0)), "measured"
+        return (float(pk["hbm_gbs"]), float(pk.get("sm_max_mhz", 1965.0)), float(pk["bf16_tflops"]),
+                "measured")
     except Exception:
-        return FALLBACK_HBM_GBS, 1965.0, "fallback"
+        return FALLBACK_HBM_GBS, 1965.0, FALLBACK_BF16_TFLOPS, "fallback"
+
+
+def kernel_rooflines(prof, cfg, nl, steps, tc_dense):
+    """Per kernel class: algorithmic work per launch / measured average launch time vs its roof.
+    Algorithmic units: dense pass 2*N*K*s^2*H*W FLOP; masked step sector-model bytes."""
+    hbm_gbs, sm_max_mhz, bf16_tflops, kind = _peaks()
+    fp32_peak = SMS * FP32_LANES_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12
+    tf32_peak = bf16_tflops * TF32_PER_BF16
+    dense_flops = 2.0 * nl * cfg.K * cfg.s * cfg.s * cfg.H * cfg.W
+    codes = nl * cfg.K * cfg.Hc * cfg.Wc
+    out = {}
+    for name, (ms, n) in prof.items():
+        if n == 0:
+            continue
+        avg = ms / n
+        if name == "conv":
+            if tc_dense:
+                peak = tf32_peak / 3.0
+                out[name] = {"kernel": "conv_tc_kernel (tcgen05 3xTF32 implicit GEMM + col2im)", "bound": "tensor",
+                             "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                             "peak_note": f"{kind} bf16 {bf16_tflops:.0f} TF/s x {TF32_PER_BF16:.3f} (tf32/bf16 nominal) / 3 (3xTF32 products per FMA)"}
+            else:
+                out[name] = {"kernel": "conv_fwd_kernel (SIMT FP32)", "bound": "alu",
+                             "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+                             "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
+            out[name]["hbm_frac"] = 4.0 * codes / (avg / 1e3) / 1e9 / hbm_gbs
+        elif name == "wgrad":
+            out[name] = {"kernel": "wgrad_kernel (SIMT FP32)", "bound": "alu",
+                         "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+                         "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
+        elif name == "code_step":
+            sector_bytes = 8.0 * (1.0 - (1.0 - cfg.p) ** 8) * codes + 12.0 * nl * cfg.H * cfg.W
+            out[name] = {"kernel": "code_step_kernel (masked prox step)", "bound": "hbm",
+                         "achieved": sector_bytes / (avg / 1e3) / 1e9, "peak": hbm_gbs, "unit": "GB/s",
+                         "peak_note": f"{kind} copy bandwidth (MEASURED_PEAKS.json)",
+                         "model": "sector: 8(1-(1-p)^8) N K Hc Wc + 12 N H W"}
+        else:
+            continue
+        r = out[name]
+        r["frac"] = r["achieved"] / r["peak"]
+        r["avg_launch_ms"] = avg
+        r["launches_per_step"] = n / steps
+        r["ms_per_step"] = ms / steps
+        r["traffic"] = None
+    return out
 
 
 class ClockSampler:
@@ -270,20 +320,9 @@ def run_ours(args):
     e2e_value = args.steps / (float(te.item()) / 1e3)
 
     if rank == 0:
-        hbm_gbs, sm_max_mhz, peak_kind = _peaks()
-        # dominant kernel: the dense convolution pass (3 launches per iteration)
-        conv_ms, conv_n = prof["conv"]
-        conv_avg_ms = conv_ms / max(conv_n, 1)
-        flops_per_launch = 2.0 * nl * cfg.K * cfg.s * cfg.s * cfg.H * cfg.W
-        fp32_peak = SMS * FP32_LANES_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12
-        achieved = flops_per_launch / (conv_avg_ms / 1e3) / 1e12
-        # masked code step against HBM (sector model of SURVEY.md §8(d))
-        cs_ms, cs_n = prof["code_step"]
-        cs_avg = cs_ms / max(cs_n, 1)
-        codes = nl * cfg.K * cfg.Hc * cfg.Wc
-        sector_bytes = 8.0 * (1.0 - (1.0 - cfg.p) ** 8) * codes + 12.0 * nl * cfg.H * cfg.W
-        cs_gbs = sector_bytes / (cs_avg / 1e3) / 1e9
         step_ms = t_ms / args.steps
+        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.tc_dense)
+        dom = max(rl, key=lambda k: rl[k]["ms_per_step"])
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                        "share": v[0] / max(t_total, 1e-9)} for k, v in prof.items()}
         line = {
@@ -291,15 +330,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": _config_dict(cfg, ws),
-            "roofline": {"kernel": "conv_fwd_kernel (dense residual / Zg pass, SIMT FP32)", "bound": "alu",
-                         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                         "frac": achieved / fp32_peak, "traffic": None,
-                         "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived, DESIGN.md §5)",
-                         "algorithmic_per_launch": flops_per_launch, "avg_launch_ms": conv_avg_ms},
-            "code_step_roofline": {"bound": "hbm", "achieved": cs_gbs, "peak": hbm_gbs, "unit": "GB/s",
-                                   "frac": cs_gbs / hbm_gbs, "peak_kind": peak_kind,
-                                   "algorithmic_bytes_per_launch": sector_bytes, "avg_launch_ms": cs_avg,
-                                   "model": "sector: 8(1-(1-p)^8) N K Hc Wc + 12 N H W"},
+            "roofline": dict(rl[dom], dominant_class=dom),
+            "kernel_rooflines": rl,
             "kernels": kernels,
             "objective_last": objs[-1] if objs else None,
             "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": 4 * nl * cfg.H * cfg.W,

@@ -233,6 +233,13 @@ class Context:
         return out
 
     @property
+    def tc_dense(self) -> bool:
+        """True when the dense passes run on the tcgen05 3xTF32 kernel (s in {5,7,9,11}, W+s-1 >= 32,
+        CSC_DENSE_PATH != simt)."""
+        return (os.environ.get("CSC_DENSE_PATH", "") != "simt" and self.n_local > 0 and self.s in (5, 7, 9, 11)
+                and self.Wc >= 32)
+
+    @property
     def launch_count(self) -> int:
         return int(self._L.csc_launch_count(self._h))
 

@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -93,6 +94,11 @@ struct csc_ctx {
   const float* cx = nullptr;
   const float* cd = nullptr;
   const float* cz = nullptr;
+  // tensor-core dense path (csc_tc.cu)
+  bool tc_on = false;
+  csc::TcPlan tc{};
+  float* tc_part = nullptr;
+  float* tc_bimg = nullptr;
   ncclComm_t comm = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -175,6 +181,20 @@ csc_status dense_residual(csc_ctx* c, const float* x, const float* d, const floa
   double* l1p = want_l1 ? c->l1_part : nullptr;
   if (g.N == 0) {
     CSC_CUDA(c, cudaMemsetAsync(c->dscal, 0, sizeof(double) * 2, c->st));
+    return CSC_OK;
+  }
+  if (c->tc_on) {
+    CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks,
+                 csc::launch_conv_tc(g, c->tc, z, d, c->tc_bimg, c->tc_part, l1p, c->st));
+    CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
+                 csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, x, c->r, csc::kConvResidual, c->sq_part, c->st));
+    CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kSqR, 1.0, c->st));
+    if (want_l1)
+      CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->l1_part, c->tc.nks * c->tc.grid, c->dscal + kL1, 1.0, c->st));
+    c->cache_valid = true;
+    c->cx = x;
+    c->cd = d;
+    c->cz = z;
     return CSC_OK;
   }
   CSC_LAUNCH_C(c, CSC_K_CONV, 1, csc::launch_conv_fwd(g, z, d, x, c->r, c->part, c->ksplit, csc::kConvResidual, c->sq_part, l1p,
@@ -317,6 +337,23 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   ok = ok && alloc(reinterpret_cast<void**>(&c->fscal), sizeof(float) * kNumF);
   ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_dscal), sizeof(double) * kNumD) == cudaSuccess;
   ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_fscal), sizeof(float) * kNumF) == cudaSuccess;
+  // tensor-core dense path unless CSC_DENSE_PATH=simt
+  {
+    const char* ev = std::getenv("CSC_DENSE_PATH");
+    const bool force_simt = ev != nullptr && std::string(ev) == "simt";
+    if (!force_simt && g.N > 0 && csc::conv_tc_supported(g)) {
+      c->tc = csc::conv_tc_plan(g, prop.multiProcessorCount);
+      c->tc_on = true;
+      ok = ok && alloc(reinterpret_cast<void**>(&c->tc_part), sizeof(float) * c->tc.part_floats);
+      ok = ok && alloc(reinterpret_cast<void**>(&c->tc_bimg), sizeof(float) * c->tc.bimg_floats);
+      const int need = c->tc.nks * c->tc.grid;
+      if (need > cap) {
+        cudaFree(c->l1_part);
+        c->l1_part = nullptr;
+        ok = ok && alloc(reinterpret_cast<void**>(&c->l1_part), sizeof(double) * need);
+      }
+    }
+  }
   if (!ok) {
     csc_destroy(c);
     return init_fail(CSC_ERR_OOM, "device allocation failed in csc_init");
@@ -405,6 +442,8 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->g32);
   cudaFree(c->colw);
   cudaFree(c->lip_part);
+  cudaFree(c->tc_part);
+  cudaFree(c->tc_bimg);
   cudaFree(c->dscal);
   cudaFree(c->fscal);
   cudaFreeHost(c->h_dscal);
@@ -492,7 +531,13 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
   if (s != CSC_OK) return s;
   CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->st));
   if (step_d == 0.f) {
-    if (g.N > 0) {
+    if (g.N > 0 && c->tc_on) {
+      CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks,
+                   csc::launch_conv_tc(g, c->tc, z, c->g32, c->tc_bimg, c->tc_part, nullptr, c->st));
+      CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
+                   csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, nullptr, csc::kConvSumSq, c->sq_part, c->st));
+      CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));
+    } else if (g.N > 0) {
       int nb = 0;
       CSC_LAUNCH_C(c, CSC_K_CONV, 1, csc::launch_conv_fwd(g, z, c->g32, nullptr, nullptr, c->part, c->ksplit, csc::kConvSumSq,
                                             c->sq_part, nullptr, c->st, &nb));

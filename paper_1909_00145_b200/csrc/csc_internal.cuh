@@ -92,4 +92,19 @@ cudaError_t launch_filter_update(const Geom& g, float* d, const double* gsum, co
 // r = -x (zero codes).
 cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st);
 
+// ---- tensor-core (tcgen05, 3xTF32) dense pass, csc_tc.cu
+constexpr int kTcMaxKC = 104;  // filters per k-split held resident in shared memory
+struct TcPlan {
+  int NT, natoms, nks, KC, NCH, SEGR, RW, BR, nbands, nitems, grid, smem;
+  size_t part_floats, bimg_floats;
+};
+bool conv_tc_supported(const Geom& g);
+TcPlan conv_tc_plan(const Geom& g, int num_sms);
+// y (all k-splits) -> band partial windows in part; per-CTA |z| partials -> l1_part[nks*grid] if non-null.
+cudaError_t launch_conv_tc(const Geom& g, const TcPlan& p, const float* z, const float* filt, float* bimg,
+                           float* part, double* l1_part, cudaStream_t st);
+// part -> r = y - x (residual mode) or sum y^2 (sum-of-squares mode); per-block partials -> sq_part[kFinalizeBlocks].
+cudaError_t launch_conv_tc_fixup(const Geom& g, const TcPlan& p, const float* part, const float* x, float* r,
+                                 int mode, double* sq_part, cudaStream_t st);
+
 }  // namespace csc
