@@ -33,7 +33,7 @@ namespace csc {
 namespace {
 
 constexpr unsigned kFullMask = 0xffffffffu;
-constexpr int kNS = 4;            // TMEM A slots: 4 K-steps (32 filters) each, 64 columns (32 hi + 32 lo)
+constexpr int kNS = 4;            // TMEM A slots: kKSteps K-steps each, 64 columns (32 hi + 32 lo)
 constexpr int kKSteps = 4;        // K-steps (8 filters each) per slot
 constexpr int kEpiWarps = 8;      // epilogue warps (2 per TMEM lane quarter, disjoint tap rows)
 constexpr int kConvPerQ = 4;        // converter warps per TMEM lane quarter
@@ -64,6 +64,15 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsi
   const unsigned long long t0 = clock64();
   mbar_wait(bar, parity);
   acc += clock64() - t0;
+}
+// Wait with a suspend-time hint: the warp sleeps in the barrier unit instead of re-issuing
+// try_wait, leaving issue slots to the MMA / converter warps sharing its SMSP.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n@!P1 bra WAIT_%=;\n}\n" ::"r"(
+          su32(bar)),
+      "r"(parity), "r"(20000)
+      : "memory");
 }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -106,6 +115,23 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(su32(bar))
       : "memory");
 }
+
+// One K-step of 3xTF32 MMAs (3 products) issued by one elected lane in a single asm block: the
+// operand arithmetic stays inside PTX, so the issue loop costs a few instructions per MMA
+// instead of an elect + uniform-register moves per MMA.
+__device__ __forceinline__ void mma_kstep3(uint32_t d, uint32_t ah, uint64_t bh, uint64_t bl, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred e, p, t;\n.reg .b32 al;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 1, 1;\nadd.u32 al, %1, %6;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %4, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], %2, %4, t;\n"
+      "}\n" ::"r"(d), "r"(ah), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "n"(8 * kKSteps)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
                : "memory");
@@ -258,17 +284,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
           mbar_wait_t(&a_full[slot], ph, w_full, tim);
           tc_after();
           const int ns = min(kKSteps, A.NCH - c0);
-          const uint32_t a0 = tbase + 256u + slot * 64u;
+          const uint32_t a0 = tbase + 256u + slot * (16u * kKSteps);
           const unsigned long long t_is = tim ? clock64() : 0ull;
 #pragma unroll
           for (int e = 0; e < kKSteps; ++e) {
             if (e < ns) {
-              const uint32_t ah = a0 + e * 8u;
-              mma_ts_elect(d, ah, bh, idesc, (c0 + e) > 0 ? 1u : 0u);
-              if (three) {
-                mma_ts_elect(d, ah, bl, idesc, 1u);
-                mma_ts_elect(d, ah + 32u, bh, idesc, 1u);
-              }
+              const uint32_t acc = (c0 + e) > 0 ? 1u : 0u;
+              if (three) mma_kstep3(d, a0 + e * 8u, bh, bl, idesc, acc);
+              else mma_ts_elect(d, a0 + e * 8u, bh, idesc, acc);
               bh += 64u;
               bl += 64u;
             }
@@ -299,7 +322,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
       const ItemInfo it = decode_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
-        mbar_wait_t(&acc_full[buf], use & 1u, w_epi, (A.dbg & 8) != 0);
+        if (A.dbg & 8) mbar_wait_t(&acc_full[buf], use & 1u, w_epi, true);
+        else mbar_wait_sleep(&acc_full[buf], use & 1u);
         tc_after();
         const int sg = t * 4 + q;
         const int u = it.u0 + sg / A.SEGR;
@@ -310,6 +334,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
         for (int a = a_beg; a < a_end; a += 2) {
           const bool two = a + 1 < a_end;
           float y0[16], y1[16];
+          if (A.dbg & 32) continue;
           tmem_ld16_nowait(tacc + a * S, y0);
           if (two) tmem_ld16_nowait(tacc + (a + 1) * S, y1);
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
@@ -440,7 +465,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
       for (int i = 0; i < D; ++i) {
         if (cur.done) break;
         const uint32_t slot = cur.g % kNS, ph = (cur.g / kNS) & 1u;
-        mbar_wait_t(&a_empty[slot], ph ^ 1u, w_cv, (A.dbg & 8) != 0);
+        if (A.dbg & 8) mbar_wait_t(&a_empty[slot], ph ^ 1u, w_cv, true);
+        else mbar_wait_sleep(&a_empty[slot], ph ^ 1u);
         tc_after();
 #pragma unroll
         for (int m = 0; m < kKPerConv; ++m) {
@@ -452,10 +478,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
             tf32_split(x, h8[jj], l8[jj]);
             if (want_l1) l1 += fabsf(x);
           }
-          if (kk < A.NCH) {
-            const uint32_t ta = tq + 256u + slot * 64u + static_cast<uint32_t>(e + m * kConvPerQ) * 8u;
+          if (kk < A.NCH && !(A.dbg & 16)) {
+            const uint32_t ta = tq + 256u + slot * (16u * kKSteps) + static_cast<uint32_t>(e + m * kConvPerQ) * 8u;
             tmem_st8(ta, h8);
-            tmem_st8(ta + 32u, l8);
+            tmem_st8(ta + 8u * kKSteps, l8);
           }
         }
         load(pre, v[i]);
