@@ -53,7 +53,7 @@ def _peaks():
         return FALLBACK_HBM_GBS, 1965.0, FALLBACK_BF16_TFLOPS, "fallback"
 
 
-def kernel_rooflines(prof, cfg, nl, steps, tc_dense):
+def kernel_rooflines(prof, cfg, nl, steps, tc_dense, tc_wgrad=False):
     """Per kernel class: algorithmic work per launch / measured average launch time vs its roof.
     Algorithmic units: dense pass 2*N*K*s^2*H*W FLOP; masked step sector-model bytes."""
     hbm_gbs, sm_max_mhz, bf16_tflops, kind = _peaks()
@@ -77,6 +77,11 @@ def kernel_rooflines(prof, cfg, nl, steps, tc_dense):
                              "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
                              "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
             out[name]["hbm_frac"] = 4.0 * codes / (avg / 1e3) / 1e9 / hbm_gbs
+        elif name == "wgrad" and tc_wgrad:
+            out[name] = {"kernel": "wgrad_tc_kernel (tcgen05 3xTF32, TMA z + TMEM im2col(r))", "bound": "tensor",
+                         "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": tf32_peak / 3.0, "unit": "TFLOP/s",
+                         "peak_note": f"{kind} bf16 {bf16_tflops:.0f} TF/s x {TF32_PER_BF16:.3f} (tf32/bf16 nominal) / 3 (3xTF32 products per FMA)",
+                         "hbm_frac": 4.0 * codes / (avg / 1e3) / 1e9 / hbm_gbs}
         elif name == "wgrad":
             out[name] = {"kernel": "wgrad_kernel (SIMT FP32)", "bound": "alu",
                          "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -321,7 +326,7 @@ def run_ours(args):
 
     if rank == 0:
         step_ms = t_ms / args.steps
-        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.tc_dense)
+        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.tc_dense, ctx.tc_wgrad)
         dom = max(rl, key=lambda k: rl[k]["ms_per_step"])
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                        "share": v[0] / max(t_total, 1e-9)} for k, v in prof.items()}

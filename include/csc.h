@@ -169,6 +169,12 @@ csc_status csc_profile_enable(csc_ctx* ctx, int enable);
  * number of launches of kernel class cls since csc_profile_enable(ctx, 1). */
 csc_status csc_profile_read(csc_ctx* ctx, int cls, double* total_ms, uint64_t* launches);
 
+/* Which sm_100a kernel variant this context runs (bit set = tensor-core variant):
+ *   bit 0  dense passes (residual, ||Zg||^2, objective) on tcgen05 3xTF32 (csc_tc.cu)
+ *   bit 1  filter gradient Z^T r on tcgen05 3xTF32 (csc_wgrad_tc.cu)
+ * The choice is fixed at csc_init from the shape (and CSC_DENSE_PATH / CSC_WGRAD_PATH = simt). */
+uint32_t csc_kernel_variants(const csc_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,7 @@ ABI_SYMBOLS = (
     "csc_init", "csc_code_step", "csc_filter_step", "csc_objective", "csc_iterate", "csc_invalidate",
     "csc_zero_codes", "csc_destroy", "csc_last_error", "csc_nccl_unique_id", "csc_abi_version",
     "csc_mask_bits", "csc_read_residual", "csc_read_grad", "csc_lipschitz", "csc_launch_count",
-    "csc_profile_enable", "csc_profile_read",
+    "csc_profile_enable", "csc_profile_read", "csc_kernel_variants",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -84,8 +84,10 @@ def load_library(path: Optional[str] = None):
         L.csc_launch_count.restype = u64
         L.csc_profile_enable.argtypes = [vp, ctypes.c_int]
         L.csc_profile_read.argtypes = [vp, ctypes.c_int, ctypes.POINTER(f64), ctypes.POINTER(u64)]
+        L.csc_kernel_variants.argtypes = [vp]
+        L.csc_kernel_variants.restype = u32
         for name in ABI_SYMBOLS:
-            if name not in ("csc_last_error", "csc_abi_version", "csc_launch_count"):
+            if name not in ("csc_last_error", "csc_abi_version", "csc_launch_count", "csc_kernel_variants"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L
@@ -234,10 +236,13 @@ class Context:
 
     @property
     def tc_dense(self) -> bool:
-        """True when the dense passes run on the tcgen05 3xTF32 kernel (s in {5,7,9,11}, W+s-1 >= 32,
-        CSC_DENSE_PATH != simt)."""
-        return (os.environ.get("CSC_DENSE_PATH", "") != "simt" and self.n_local > 0 and self.s in (5, 7, 9, 11)
-                and self.Wc >= 32)
+        """True when the dense passes run on the tcgen05 3xTF32 kernel (csc_kernel_variants bit 0)."""
+        return bool(self._L.csc_kernel_variants(self._h) & 1)
+
+    @property
+    def tc_wgrad(self) -> bool:
+        """True when the filter gradient runs on the tcgen05 3xTF32 kernel (csc_kernel_variants bit 1)."""
+        return bool(self._L.csc_kernel_variants(self._h) & 2)
 
     @property
     def launch_count(self) -> int:

@@ -99,6 +99,9 @@ struct csc_ctx {
   csc::TcPlan tc{};
   float* tc_part = nullptr;
   float* tc_bimg = nullptr;
+  // tensor-core filter gradient (csc_wgrad_tc.cu)
+  bool wg_tc_on = false;
+  csc::WgTcPlan wg{};
   ncclComm_t comm = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -239,6 +242,11 @@ const char* csc_last_error(const csc_ctx* ctx) {
 
 uint64_t csc_launch_count(const csc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+uint32_t csc_kernel_variants(const csc_ctx* ctx) {
+  if (!ctx) return 0;
+  return (ctx->tc_on ? 1u : 0u) | (ctx->wg_tc_on ? 2u : 0u);
+}
+
 csc_status csc_nccl_unique_id(uint8_t out[128]) {
   if (!out) return CSC_ERR_ARG;
   std::lock_guard<std::mutex> lk(g_nccl_mu);
@@ -328,7 +336,17 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   if (ks > 1) ok = ok && alloc(reinterpret_cast<void**>(&c->part), sizeof(float) * npix * ks);
   ok = ok && alloc(reinterpret_cast<void**>(&c->sq_part), sizeof(double) * cap);
   ok = ok && alloc(reinterpret_cast<void**>(&c->l1_part), sizeof(double) * cap);
-  ok = ok && alloc(reinterpret_cast<void**>(&c->gpart), sizeof(double) * static_cast<size_t>(G) * g.K * M);
+  // tensor-core filter gradient unless CSC_WGRAD_PATH=simt (needs Hc*Wc % 4 == 0 for the TMA view of z)
+  {
+    const char* ev = std::getenv("CSC_WGRAD_PATH");
+    const bool force_simt = ev != nullptr && std::string(ev) == "simt";
+    if (!force_simt && csc::wgrad_tc_supported(g)) {
+      c->wg = csc::wgrad_tc_plan(g, prop.multiProcessorCount);
+      c->wg_tc_on = true;
+    }
+  }
+  const int gpart_groups = c->wg_tc_on && c->wg.G > G ? c->wg.G : G;
+  ok = ok && alloc(reinterpret_cast<void**>(&c->gpart), sizeof(double) * static_cast<size_t>(gpart_groups) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->gsum), sizeof(double) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->g32), sizeof(float) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->colw), sizeof(uint32_t) * static_cast<size_t>(g.K) * NB * g.Wc);
@@ -522,8 +540,13 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
     if (s != CSC_OK) return s;
   }
   if (g.N > 0) {
-    CSC_LAUNCH_C(c, CSC_K_WGRAD, 1, csc::launch_wgrad(g, z, c->r, c->G, c->gpart, c->st));
-    CSC_LAUNCH(c, 1, csc::launch_wgrad_reduce(g, c->gpart, c->G, c->gsum, c->st));
+    if (c->wg_tc_on && (reinterpret_cast<uintptr_t>(z) & 15u) == 0) {
+      CSC_LAUNCH_C(c, CSC_K_WGRAD, 1, csc::launch_wgrad_tc(g, c->wg, z, c->r, c->gpart, c->st));
+      CSC_LAUNCH(c, 1, csc::launch_wgrad_reduce(g, c->gpart, c->wg.G, c->gsum, c->st));
+    } else {
+      CSC_LAUNCH_C(c, CSC_K_WGRAD, 1, csc::launch_wgrad(g, z, c->r, c->G, c->gpart, c->st));
+      CSC_LAUNCH(c, 1, csc::launch_wgrad_reduce(g, c->gpart, c->G, c->gsum, c->st));
+    }
   } else {
     CSC_CUDA(c, cudaMemsetAsync(c->gsum, 0, sizeof(double) * g.K * M, c->st));
   }

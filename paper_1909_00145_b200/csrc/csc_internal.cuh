@@ -107,4 +107,17 @@ cudaError_t launch_conv_tc(const Geom& g, const TcPlan& p, const float* z, const
 cudaError_t launch_conv_tc_fixup(const Geom& g, const TcPlan& p, const float* part, const float* x, float* r,
                                  int mode, double* sq_part, cudaStream_t st);
 
+
+// ---- tensor-core (tcgen05, 3xTF32) filter gradient, csc_wgrad_tc.cu
+struct WgTcPlan {
+  int KC, Npad, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, stage_bytes;
+  int grid, smem;
+};
+bool wgrad_tc_supported(const Geom& g);
+WgTcPlan wgrad_tc_plan(const Geom& g, int num_sms);
+// Per-CTA fp64 partials gpart[p.G][K][S*S] (reduce with launch_wgrad_reduce(g, gpart, p.G, ...)).
+// z must be 16-byte aligned.
+cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, const float* z, const float* r, double* gpart,
+                            cudaStream_t st);
+
 }  // namespace csc

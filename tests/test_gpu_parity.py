@@ -111,9 +111,15 @@ def test_code_step_parity(torch_dev, shape, p):
     ctx.close()
 
 
-@pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (1, 3, 3, 9, 9)])
-def test_filter_step_parity(torch_dev, shape):
+@pytest.mark.parametrize("wg", ["tc", "simt"])
+@pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (1, 3, 3, 9, 9), (2, 130, 5, 36, 40),
+                                   (1, 8, 7, 26, 22), (2, 40, 11, 256, 56), (5, 24, 9, 48, 63), (1, 100, 11, 12, 300)])
+def test_filter_step_parity(torch_dev, shape, wg, monkeypatch):
+    """Filter gradient g = Z^T r (tcgen05 3xTF32 kernel, or SIMT), exact line search, projection.
+    Shapes cover several k-groups (K=130), one partial chunk per row (Wc < 32), many bands,
+    rows of 9-10 chunks, and Hc*Wc % 4 != 0 (TMA view impossible: SIMT path either way)."""
     import torch
+    monkeypatch.setenv("CSC_WGRAD_PATH", wg)
     N, K, s, H, W = shape
     x, d, z = random_problem(300 + K, N, K, s, H, W, code_density=0.3)
     ctx = _ctx(N, K, s, H, W)
