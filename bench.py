@@ -53,7 +53,7 @@ def _peaks():
         return FALLBACK_HBM_GBS, 1965.0, FALLBACK_BF16_TFLOPS, "fallback"
 
 
-def kernel_rooflines(prof, cfg, nl, steps, tc_dense, tc_wgrad=False):
+def kernel_rooflines(prof, cfg, nl, steps, tc_dense, tc_wgrad=False, tc_code=False):
     """Per kernel class: algorithmic work per launch / measured average launch time vs its roof.
     Algorithmic units: dense pass 2*N*K*s^2*H*W FLOP; masked step sector-model bytes."""
     hbm_gbs, sm_max_mhz, bf16_tflops, kind = _peaks()
@@ -88,7 +88,8 @@ def kernel_rooflines(prof, cfg, nl, steps, tc_dense, tc_wgrad=False):
                          "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
         elif name == "code_step":
             sector_bytes = 8.0 * (1.0 - (1.0 - cfg.p) ** 8) * codes + 12.0 * nl * cfg.H * cfg.W
-            out[name] = {"kernel": "code_step_kernel (masked prox step)", "bound": "hbm",
+            out[name] = {"kernel": "code_tc_kernel (tcgen05 3xTF32 dense-then-mask prox step)" if tc_code
+                         else "code_step_kernel (SIMT masked prox step)", "bound": "hbm",
                          "achieved": sector_bytes / (avg / 1e3) / 1e9, "peak": hbm_gbs, "unit": "GB/s",
                          "peak_note": f"{kind} copy bandwidth (MEASURED_PEAKS.json)",
                          "model": "sector: 8(1-(1-p)^8) N K Hc Wc + 12 N H W"}
@@ -326,7 +327,7 @@ def run_ours(args):
 
     if rank == 0:
         step_ms = t_ms / args.steps
-        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.tc_dense, ctx.tc_wgrad)
+        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.tc_dense, ctx.tc_wgrad, ctx.tc_code)
         dom = max(rl, key=lambda k: rl[k]["ms_per_step"])
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                        "share": v[0] / max(t_total, 1e-9)} for k, v in prof.items()}

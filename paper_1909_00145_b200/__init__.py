@@ -245,6 +245,11 @@ class Context:
         return bool(self._L.csc_kernel_variants(self._h) & 2)
 
     @property
+    def tc_code(self) -> bool:
+        """True when the masked code step runs as the tcgen05 dense-then-mask kernel (bit 2)."""
+        return bool(self._L.csc_kernel_variants(self._h) & 4)
+
+    @property
     def launch_count(self) -> int:
         return int(self._L.csc_launch_count(self._h))
 

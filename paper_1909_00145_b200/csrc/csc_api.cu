@@ -102,6 +102,10 @@ struct csc_ctx {
   // tensor-core filter gradient (csc_wgrad_tc.cu)
   bool wg_tc_on = false;
   csc::WgTcPlan wg{};
+  // tensor-core dense-then-mask code step (csc_code_tc.cu)
+  bool ct_on = false;
+  csc::CodeTcPlan ct{};
+  uint32_t* mwords = nullptr;  // plane-word mask [K][Wk]
   ncclComm_t comm = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -244,7 +248,7 @@ uint64_t csc_launch_count(const csc_ctx* ctx) { return ctx ? ctx->launches : 0; 
 
 uint32_t csc_kernel_variants(const csc_ctx* ctx) {
   if (!ctx) return 0;
-  return (ctx->tc_on ? 1u : 0u) | (ctx->wg_tc_on ? 2u : 0u);
+  return (ctx->tc_on ? 1u : 0u) | (ctx->wg_tc_on ? 2u : 0u) | (ctx->ct_on ? 4u : 0u);
 }
 
 csc_status csc_nccl_unique_id(uint8_t out[128]) {
@@ -343,6 +347,18 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
     if (!force_simt && csc::wgrad_tc_supported(g)) {
       c->wg = csc::wgrad_tc_plan(g, prop.multiProcessorCount);
       c->wg_tc_on = true;
+    }
+  }
+  // tensor-core code step unless CSC_CODE_PATH=simt
+  {
+    const char* ev = std::getenv("CSC_CODE_PATH");
+    const bool force_simt = ev != nullptr && std::string(ev) == "simt";
+    if (!force_simt && csc::code_tc_supported(g)) {
+      c->ct = csc::code_tc_plan(g, prop.multiProcessorCount);
+      if (c->ct.ok) {
+        c->ct_on = true;
+        ok = ok && alloc(reinterpret_cast<void**>(&c->mwords), sizeof(uint32_t) * static_cast<size_t>(g.K) * c->ct.Wk);
+      }
     }
   }
   const int gpart_groups = c->wg_tc_on && c->wg.G > G ? c->wg.G : G;
@@ -459,6 +475,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->gsum);
   cudaFree(c->g32);
   cudaFree(c->colw);
+  cudaFree(c->mwords);
   cudaFree(c->lip_part);
   cudaFree(c->tc_part);
   cudaFree(c->tc_bimg);
@@ -515,8 +532,16 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
   const int all_selected = thr >= (uint64_t(1) << 32) ? 1 : 0;
   if (g.N > 0) {
-    if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st));
-    CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, c->fscal + kTauZ, lambda, c->st));
+    if (c->ct_on) {
+      if (!all_selected)
+        CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_planewords(g, c->ct, seed, iter, thr, c->mwords, c->st));
+      CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
+                   csc::launch_code_tc(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, c->fscal + kTauZ, lambda,
+                                       c->st));
+    } else {
+      if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st));
+      CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, c->fscal + kTauZ, lambda, c->st));
+    }
   }
   c->cache_valid = false;  // r no longer matches z
   if (step_used) {

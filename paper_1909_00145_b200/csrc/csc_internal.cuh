@@ -120,4 +120,20 @@ WgTcPlan wgrad_tc_plan(const Geom& g, int num_sms);
 cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, const float* z, const float* r, double* gpart,
                             cudaStream_t st);
 
+
+// ---- tensor-core (tcgen05, 3xTF32) dense-then-mask code step, csc_code_tc.cu
+struct CodeTcPlan {
+  int KC, Npad, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, b_bytes, Wk;
+  int grid, smem;
+  bool ok;
+};
+bool code_tc_supported(const Geom& g);
+CodeTcPlan code_tc_plan(const Geom& g, int num_sms);
+// Mask in plane-word layout words[K][Wk], Wk = ceil(Hc*Wc/32): bit j of word w = mask(k, p = 32w+j).
+cudaError_t launch_mask_planewords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
+                                   uint32_t* words, cudaStream_t st);
+// words == nullptr: every code selected (p = 1).
+cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
+                           const uint32_t* words, const float* tau_dev, float lam, cudaStream_t st);
+
 }  // namespace csc

@@ -168,8 +168,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&f)[16]) {
 // tf32, so the tensor core's operand truncation is exact; lo has a random sign relative to x, so
 // the dropped lo*lo term (~2^-22 relative) carries no systematic bias.
 __device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hi) : "f"(x));
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(lo) : "f"(x - __uint_as_float(hi)));
+  // cvt.rna.tf32.f32 (round to nearest, ties away) written as integer add + mask: identical
+  // results for finite x, 2 integer ops instead of the ~5-instruction emulation ptxas emits
+  hi = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+  lo = (__float_as_uint(x - __uint_as_float(hi)) + 0x1000u) & 0xFFFFE000u;
 }
 __device__ __forceinline__ float ldg_stream(const float* p) {
   float v;

@@ -227,7 +227,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
         const int pk = it.p0 + 32 * c + 16 * h;
         int u = pk / A.Wc;
         int v = pk - u * A.Wc;
-        mbar_wait(&z_full[slot], ph);
+        mbar_wait_sleep(&z_full[slot], ph);
         // (1) lo copy of the z stage (elementwise, the swizzle is irrelevant)
         if (!(A.dbg & 16)) {
           float4* hi4 = reinterpret_cast<float4*>(stages + slot * 2 * A.stage_bytes);

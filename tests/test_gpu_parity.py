@@ -83,10 +83,15 @@ def test_residual_and_objective_parity(torch_dev, shape):
     ctx.close()
 
 
+@pytest.mark.parametrize("path", ["tc", "simt"])
 @pytest.mark.parametrize("shape,p", [((3, 5, 5, 70, 130), 0.1), ((2, 17, 11, 100, 100), 0.2),
-                                     ((4, 8, 5, 32, 32), 1.0), ((1, 9, 3, 33, 47), 0.5), ((2, 4, 11, 11, 11), 0.05)])
-def test_code_step_parity(torch_dev, shape, p):
+                                     ((4, 8, 5, 32, 32), 1.0), ((1, 9, 3, 33, 47), 0.5), ((2, 4, 11, 11, 11), 0.05),
+                                     ((2, 130, 7, 20, 300), 0.1), ((1, 100, 11, 40, 11), 0.3), ((3, 16, 9, 61, 9), 1.0)])
+def test_code_step_parity(torch_dev, shape, p, path, monkeypatch):
+    """Masked prox-gradient code step: tcgen05 dense-then-mask kernel or SIMT.  Shapes: several
+    k-groups (K=130), tiles that wrap many short rows (Wc=21, 17), ragged plane tails, p=1 shortcut."""
     import torch
+    monkeypatch.setenv("CSC_CODE_PATH", path)
     N, K, s, H, W = shape
     x, d, z = random_problem(200 + K, N, K, s, H, W, code_density=0.3)
     seed, it, lam = 12345, 3, 0.2
