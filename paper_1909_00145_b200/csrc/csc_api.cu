@@ -105,7 +105,7 @@ struct csc_ctx {
   // tensor-core dense-then-mask code step (csc_code_tc.cu)
   bool ct_on = false;
   csc::CodeTcPlan ct{};
-  uint32_t* mwords = nullptr;  // plane-word mask [K][Wk]
+  uint32_t* mwords = nullptr;  // selection-word mask [4*nkg][Hc*Wc]
   ncclComm_t comm = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -357,7 +357,7 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
       c->ct = csc::code_tc_plan(g, prop.multiProcessorCount);
       if (c->ct.ok) {
         c->ct_on = true;
-        ok = ok && alloc(reinterpret_cast<void**>(&c->mwords), sizeof(uint32_t) * static_cast<size_t>(g.K) * c->ct.Wk);
+        ok = ok && alloc(reinterpret_cast<void**>(&c->mwords), sizeof(uint32_t) * c->ct.sw_words);
       }
     }
   }
@@ -534,7 +534,7 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   if (g.N > 0) {
     if (c->ct_on) {
       if (!all_selected)
-        CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_planewords(g, c->ct, seed, iter, thr, c->mwords, c->st));
+        CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(g, c->ct, seed, iter, thr, c->mwords, c->st));
       CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
                    csc::launch_code_tc(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, c->fscal + kTauZ, lambda,
                                        c->st));

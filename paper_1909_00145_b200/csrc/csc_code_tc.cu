@@ -47,10 +47,10 @@ struct CtArgs {
   const float* r;        // [N][H][W]
   const float* d;        // [K][S][S]
   float* z;              // [N][K][Hc][Wc]
-  const uint32_t* mask;  // [K][Wk] plane words (bit j of word w = mask(k, p = 32 w + j)), or nullptr = all
+  const uint32_t* mask;  // selection words [nkg*4][plane]: bit i = mask(k = kg*KC + cb*NC + i, p); nullptr = all
   const float* tau;      // device scalar
   float lam;
-  int N, K, S, H, W, Hc, Wc, P, Wk;
+  int N, K, S, H, W, Hc, Wc, P;
   int KC, Npad, nkg, G;
   int L, nseg, nitems;   // item = (image, segment of L flattened positions, L % 128 == 0)
   int pitch, rs_rows, rs_floats;
@@ -259,18 +259,9 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
           const bool ok = pok && (k0 + i) < kend;
           zv[i] = ok ? zb[static_cast<size_t>(i) * plane] : 0.f;
         }
-        // selection bits: lane i loads the mask word of filter k0 + i for these 32 positions, the
-        // warp transposes it with shuffles into one bit per (filter, lane): sel bit i of lane l
-        uint32_t sel = 0u;
-        {
-          uint32_t mword = 0xffffffffu;
-          if (A.mask != nullptr)
-            mword = (lane < NC && pw < it.p1 && k0 + lane < kend) ? __ldg(A.mask + static_cast<size_t>(k0 + lane) * A.Wk + (pw >> 5)) : 0u;
-#pragma unroll
-          for (int i = 0; i < NC; ++i) sel |= ((__shfl_sync(kFullMask, mword, i) >> lane) & 1u) << i;
-          if (!pok) sel = 0u;
-          if (kend - k0 < NC) sel &= (kend - k0 > 0) ? ((1u << (kend - k0)) - 1u) : 0u;
-        }
+        // selection word of this position: bit i = mask(k0 + i, p) (coalesced, L2-resident)
+        const uint32_t sel = A.mask == nullptr ? (pok ? 0xffffffffu : 0u)
+                                               : (pok ? __ldg(A.mask + static_cast<size_t>(kg * 4 + cb) * plane + p) : 0u);
         mbar_wait_sleep(&acc_full[buf], use & 1u);
         tc_after();
         const uint32_t colb = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
@@ -284,7 +275,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
             const int i = 4 * j4 + i4;
             const float w = fmaf(-tau, c4[i4], zv[i]);
             const float nz = (w > kappa) ? (w - kappa) : ((w < -kappa) ? (w + kappa) : 0.f);
-            if (((sel >> i) & 1u) && nz != zv[i]) zb[static_cast<size_t>(i) * plane] = nz;
+            if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv[i]) zb[static_cast<size_t>(i) * plane] = nz;
           }
         }
         tc_before();
@@ -300,9 +291,12 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
-// Plane-word mask layout for the tensor-core code step:
-// words[k][w] bit j = mask(k, u, v) for the flattened position p = 32 w + j = u Wc + v
-// (canonical index l = (k Hc + u) Wc + v = k Hc Wc + p, Philox block l >> 2, word l & 3).
+// Selection-word mask layout for the tensor-core code step: one 32-bit word per (filter block,
+// position), the block being the NC filters one epilogue warp owns:
+//   sw[(kg*4 + cb)][p] bit i = mask(k, u, v),  k = kg*KC + cb*NC + i,  p = u*Wc + v,
+// with the canonical index l = (k*Hc + u)*Wc + v = k*Hc*Wc + p, Philox block l >> 2, word l & 3
+// (#13).  A thread makes 4 consecutive positions of one block: each Philox call of a
+// filter yields the 4 positions' words when l is 4-aligned.
 constexpr uint32_t kMaskTag = 0x4353434Du;
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 #pragma unroll
@@ -315,30 +309,40 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   }
   return c;
 }
-__global__ void mask_planewords_kernel(int K, int64_t plane, int Wk, uint64_t seed, uint32_t iter, uint64_t thr,
-                                       uint32_t* __restrict__ words) {
+__device__ __forceinline__ uint32_t word_of(const uint4& b, int i) {
+  return i == 0 ? b.x : (i == 1 ? b.y : (i == 2 ? b.z : b.w));
+}
+__global__ void mask_selwords_kernel(int K, int KC, int NC, int nblk, int64_t plane, uint64_t seed, uint32_t iter,
+                                     uint64_t thr, uint32_t* __restrict__ sw) {
+  const int64_t nq = (plane + 3) / 4;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (tid >= static_cast<int64_t>(K) * Wk) return;
-  const int k = static_cast<int>(tid / Wk);
-  const int w = static_cast<int>(tid - static_cast<int64_t>(k) * Wk);
-  const uint64_t l0 = static_cast<uint64_t>(k) * plane + 32u * static_cast<uint64_t>(w);
+  if (tid >= static_cast<int64_t>(nblk) * nq) return;
+  const int blk = static_cast<int>(tid / nq);
+  const int64_t p0 = (tid - static_cast<int64_t>(blk) * nq) * 4;
+  const int kg = blk >> 2, cb = blk & 3;
   const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
-  uint32_t out = 0u;
-  uint64_t qcur = ~0ull;
-  uint4 blk = make_uint4(0, 0, 0, 0);
-#pragma unroll 1
-  for (int j = 0; j < 32; ++j) {
-    if (32 * static_cast<int64_t>(w) + j >= plane) break;
-    const uint64_t l = l0 + j;
-    const uint64_t qq = l >> 2;
-    if (qq != qcur) {
-      blk = philox4x32_10(make_uint4(static_cast<uint32_t>(qq), static_cast<uint32_t>(qq >> 32), iter, kMaskTag), key);
-      qcur = qq;
+  uint32_t out[4] = {0u, 0u, 0u, 0u};
+  for (int i = 0; i < NC; ++i) {
+    const int kl = cb * NC + i;
+    const int k = kg * KC + kl;
+    if (kl >= KC || k >= K) break;
+    const uint64_t l0 = static_cast<uint64_t>(k) * plane + p0;
+    const uint64_t qa = l0 >> 2;
+    const uint4 ba = philox4x32_10(make_uint4(static_cast<uint32_t>(qa), static_cast<uint32_t>(qa >> 32), iter, kMaskTag), key);
+    uint4 bb = ba;
+    if ((l0 & 3) != 0)
+      bb = philox4x32_10(make_uint4(static_cast<uint32_t>(qa + 1), static_cast<uint32_t>((qa + 1) >> 32), iter, kMaskTag), key);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t l = l0 + j;
+      const uint32_t rnd = (l >> 2) == qa ? word_of(ba, static_cast<int>(l & 3)) : word_of(bb, static_cast<int>(l & 3));
+      if (static_cast<uint64_t>(rnd) < thr) out[j] |= 1u << i;
     }
-    const uint32_t rnd = (l & 3) == 0 ? blk.x : ((l & 3) == 1 ? blk.y : ((l & 3) == 2 ? blk.z : blk.w));
-    if (static_cast<uint64_t>(rnd) < thr) out |= 1u << j;
   }
-  words[tid] = out;
+  uint32_t* dst = sw + static_cast<int64_t>(blk) * plane + p0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (p0 + j < plane) dst[j] = out[j];
 }
 
 template <int S, int NC>
@@ -384,7 +388,7 @@ CodeTcPlan code_tc_plan(const Geom& g, int num_sms) {
   while (pitch % 32 != 0) ++pitch;  // lanes are consecutive positions: any pitch is conflict-free within a row
   p.pitch = pitch;
   const int plane = g.Hc * g.Wc;
-  p.Wk = ceil_div(plane, 32);
+  p.sw_words = static_cast<size_t>(4 * p.nkg) * plane;
   const int G = num_sms / p.nkg > 0 ? num_sms / p.nkg : 1;
   const int64_t total = static_cast<int64_t>(g.N > 0 ? g.N : 1) * plane;
   int64_t L = total / (8 * static_cast<int64_t>(G));
@@ -406,11 +410,13 @@ CodeTcPlan code_tc_plan(const Geom& g, int num_sms) {
   return p;
 }
 
-cudaError_t launch_mask_planewords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
-                                   uint32_t* words, cudaStream_t st) {
-  const int64_t total = static_cast<int64_t>(g.K) * p.Wk;
-  mask_planewords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-      g.K, static_cast<int64_t>(g.Hc) * g.Wc, p.Wk, seed, iter, thr, words);
+cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
+                                 uint32_t* words, cudaStream_t st) {
+  const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
+  const int nblk = 4 * p.nkg;
+  const int64_t total = static_cast<int64_t>(nblk) * ((plane + 3) / 4);
+  mask_selwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g.K, p.KC, p.Npad / 4, nblk, plane,
+                                                                                 seed, iter, thr, words);
   return cudaGetLastError();
 }
 
@@ -418,7 +424,7 @@ cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, c
                            const uint32_t* words, const float* tau_dev, float lam, cudaStream_t st) {
   CtArgs a{};
   a.r = r; a.d = d; a.z = z; a.mask = words; a.tau = tau_dev; a.lam = lam;
-  a.N = g.N; a.K = g.K; a.S = g.S; a.H = g.H; a.W = g.W; a.Hc = g.Hc; a.Wc = g.Wc; a.P = g.P; a.Wk = p.Wk;
+  a.N = g.N; a.K = g.K; a.S = g.S; a.H = g.H; a.W = g.W; a.Hc = g.Hc; a.Wc = g.Wc; a.P = g.P;
   a.KC = p.KC; a.Npad = p.Npad; a.nkg = p.nkg; a.G = p.G;
   a.L = p.L; a.nseg = p.nseg; a.nitems = p.nitems;
   a.pitch = p.pitch; a.rs_rows = p.rs_rows; a.rs_floats = p.rs_floats; a.b_bytes = p.b_bytes;

@@ -123,15 +123,16 @@ cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, const float* z, co
 
 // ---- tensor-core (tcgen05, 3xTF32) dense-then-mask code step, csc_code_tc.cu
 struct CodeTcPlan {
-  int KC, Npad, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, b_bytes, Wk;
+  int KC, Npad, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, b_bytes;
+  size_t sw_words;  // selection-word mask size (4 * nkg * Hc * Wc words)
   int grid, smem;
   bool ok;
 };
 bool code_tc_supported(const Geom& g);
 CodeTcPlan code_tc_plan(const Geom& g, int num_sms);
-// Mask in plane-word layout words[K][Wk], Wk = ceil(Hc*Wc/32): bit j of word w = mask(k, p = 32w+j).
-cudaError_t launch_mask_planewords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
-                                   uint32_t* words, cudaStream_t st);
+// Mask as selection words sw[4*nkg][Hc*Wc]: bit i of sw[kg*4+cb][p] = mask(kg*KC + cb*(Npad/4) + i, p).
+cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
+                                 uint32_t* words, cudaStream_t st);
 // words == nullptr: every code selected (p = 1).
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                            const uint32_t* words, const float* tau_dev, float lam, cudaStream_t st);
