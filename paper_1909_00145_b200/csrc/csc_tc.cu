@@ -262,53 +262,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
 
   if (warp == 0) {
     // ================================ MMA issuer
-    // The whole warp runs the loop (so the operands stay warp-uniform, in uniform registers);
-    // one elected lane issues each tcgen05.mma / commit.  Descriptors advance incrementally.
-    const bool tim = (A.dbg & 8) != 0 && lane == 0;
-    unsigned long long w_acc = 0, w_full = 0, w_issue = 0;
-    const unsigned long long t_start = clock64();
+    // The whole warp runs the loop with warp-uniform values only (no lane-dependent branches), so
+    // every operand stays in the uniform datapath; one elected lane issues each tcgen05.mma.
     const uint32_t idesc = idesc_tf32_ts(A.NT);
     const uint32_t lbo = static_cast<uint32_t>(A.KC) * 128u;
-    const uint64_t bh_base = sdesc_b32(su32(bsm), lbo, 512u);
-    const uint64_t bl_base = sdesc_b32(su32(bsm + bbytes), lbo, 512u);
-    const bool three = !(A.dbg & 4);
+    const uint32_t sbh = su32(bsm), sbl = su32(bsm + bbytes);
     uint32_t g = 0, tcount = 0;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
       const ItemInfo it = decode_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
-        mbar_wait_t(&acc_empty[buf], (use & 1u) ^ 1u, w_acc, tim);
+        mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
         tc_after();
         const uint32_t d = tbase + buf * 128u;
-        uint64_t bh = bh_base, bl = bl_base;  // K-step c: start address + c*1024 B (= +64 in 16-B units)
         for (int c0 = 0; c0 < A.NCH; c0 += kKSteps, ++g) {
           const uint32_t slot = g % kNS, ph = (g / kNS) & 1u;
-          mbar_wait_t(&a_full[slot], ph, w_full, tim);
+          mbar_wait(&a_full[slot], ph);
           tc_after();
           const int ns = min(kKSteps, A.NCH - c0);
           const uint32_t a0 = tbase + 256u + slot * (16u * kKSteps);
-          const unsigned long long t_is = tim ? clock64() : 0ull;
 #pragma unroll
           for (int e = 0; e < kKSteps; ++e) {
             if (e < ns) {
+              // K-step c0 + e: B start address + (c0 + e) * 1024 B (8 K-rows of 128 B)
+              const uint32_t koff = static_cast<uint32_t>(c0 + e) * 1024u;
+              const uint64_t bh = sdesc_b32(sbh + koff, lbo, 512u);
+              const uint64_t bl = sdesc_b32(sbl + koff, lbo, 512u);
               const uint32_t acc = (c0 + e) > 0 ? 1u : 0u;
-              if (three) mma_kstep3(d, a0 + e * 8u, bh, bl, idesc, acc);
-              else mma_ts_elect(d, a0 + e * 8u, bh, idesc, acc);
-              bh += 64u;
-              bl += 64u;
+              mma_kstep3(d, a0 + e * 8u, bh, bl, idesc, acc);
             }
           }
           mma_commit_elect(&a_empty[slot]);
-          if (tim) w_issue += clock64() - t_is;
         }
         mma_commit_elect(&acc_full[buf]);
       }
-    }
-    if (tim) {
-      A.dbgbuf[blockIdx.x * 8 + 0] = clock64() - t_start;
-      A.dbgbuf[blockIdx.x * 8 + 1] = w_acc;
-      A.dbgbuf[blockIdx.x * 8 + 2] = w_full;
-      A.dbgbuf[blockIdx.x * 8 + 5] = w_issue;
     }
     __syncwarp();
   } else if (warp >= kEpiBase && warp < kConvBase) {
@@ -325,6 +312,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
         if (A.dbg & 8) mbar_wait_t(&acc_full[buf], use & 1u, w_epi, true);
+        else if (A.dbg & 64) mbar_wait(&acc_full[buf], use & 1u);
         else mbar_wait_sleep(&acc_full[buf], use & 1u);
         tc_after();
         const int sg = t * 4 + q;
@@ -468,6 +456,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
         if (cur.done) break;
         const uint32_t slot = cur.g % kNS, ph = (cur.g / kNS) & 1u;
         if (A.dbg & 8) mbar_wait_t(&a_empty[slot], ph ^ 1u, w_cv, true);
+        else if (A.dbg & 64) mbar_wait(&a_empty[slot], ph ^ 1u);
         else mbar_wait_sleep(&a_empty[slot], ph ^ 1u);
         tc_after();
 #pragma unroll
@@ -477,7 +466,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const TcArgs A) 
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
             const float x = v[i][m * 8 + jj];
-            tf32_split(x, h8[jj], l8[jj]);
+            if (A.dbg & 128) {
+              h8[jj] = __float_as_uint(x);
+              l8[jj] = __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+            } else {
+              tf32_split(x, h8[jj], l8[jj]);
+            }
             if (want_l1) l1 += fabsf(x);
           }
           if (kk < A.NCH && !(A.dbg & 16)) {

@@ -27,7 +27,9 @@ def rep(path):
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out = []
-    extra = [h for h in hdr if ("tensor" in h or "tmem" in h.lower()) and "pct" in h and h not in KEYS]
+    extra = [h for h in hdr if ("pipe_tensor_cycles_active.avg" in h or "pipe_tensor_cycles_active_realtime" in h
+                                or "utchmma_src_tf32_dst_fp32_sparsity_off.avg" in h or "inst_executed_pipe_tmem.avg" in h)
+             and h not in KEYS]
     for vals in rows[2:]:
         name = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
         out.append(f"kernel: {name}")
