@@ -173,6 +173,7 @@ csc_status csc_profile_read(csc_ctx* ctx, int cls, double* total_ms, uint64_t* l
  *   bit 0  dense passes (residual, ||Zg||^2, objective) on tcgen05 3xTF32 (csc_tc.cu)
  *   bit 1  filter gradient Z^T r on tcgen05 3xTF32 (csc_wgrad_tc.cu)
  *   bit 2  masked code step as tcgen05 3xTF32 dense-then-mask (csc_code_tc.cu)
+ *   bit 3  the dense passes use the TMA-fed shared-memory-operand kernel (csc_conv_ss.cu)
  * The choice is fixed at csc_init from the shape (and CSC_DENSE_PATH / CSC_WGRAD_PATH /
  * CSC_CODE_PATH = simt). */
 uint32_t csc_kernel_variants(const csc_ctx* ctx);

@@ -180,6 +180,17 @@ csc_status allreduce_d(csc_ctx* c, double* buf, size_t count) {
   return CSC_OK;
 }
 
+// Tensor-core dense pass y = sum_k f_k * z_k into the band partials (TMA-fed SS kernel when the
+// plan says so, else the TMEM-fed kernel).
+cudaError_t conv_tc_any(csc_ctx* c, const float* z, const float* filt, double* l1p) {
+  if (c->tc.ss) {
+    cudaError_t e = csc::launch_tc_bimg(c->g, c->tc, filt, c->tc_bimg, c->st);
+    if (e != cudaSuccess) return e;
+    return csc::launch_conv_ss(c->g, c->tc, z, c->tc_bimg, c->tc_part, l1p, c->st);
+  }
+  return csc::launch_conv_tc(c->g, c->tc, z, filt, c->tc_bimg, c->tc_part, l1p, c->st);
+}
+
 // Dense residual pass r = Dz - x, plus sum r^2 -> dscal[kSqR] and (optional)
 // ||z||_1 -> dscal[kL1]; both local to this rank.
 csc_status dense_residual(csc_ctx* c, const float* x, const float* d, const float* z, bool want_l1) {
@@ -191,8 +202,7 @@ csc_status dense_residual(csc_ctx* c, const float* x, const float* d, const floa
     return CSC_OK;
   }
   if (c->tc_on) {
-    CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks,
-                 csc::launch_conv_tc(g, c->tc, z, d, c->tc_bimg, c->tc_part, l1p, c->st));
+    CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, z, d, l1p));
     CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
                  csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, x, c->r, csc::kConvResidual, c->sq_part, c->st));
     CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kSqR, 1.0, c->st));
@@ -248,7 +258,8 @@ uint64_t csc_launch_count(const csc_ctx* ctx) { return ctx ? ctx->launches : 0; 
 
 uint32_t csc_kernel_variants(const csc_ctx* ctx) {
   if (!ctx) return 0;
-  return (ctx->tc_on ? 1u : 0u) | (ctx->wg_tc_on ? 2u : 0u) | (ctx->ct_on ? 4u : 0u);
+  return (ctx->tc_on ? 1u : 0u) | (ctx->wg_tc_on ? 2u : 0u) | (ctx->ct_on ? 4u : 0u) |
+         (ctx->tc_on && ctx->tc.ss ? 8u : 0u);
 }
 
 csc_status csc_nccl_unique_id(uint8_t out[128]) {
@@ -376,7 +387,10 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
     const char* ev = std::getenv("CSC_DENSE_PATH");
     const bool force_simt = ev != nullptr && std::string(ev) == "simt";
     if (!force_simt && g.N > 0 && csc::conv_tc_supported(g)) {
-      c->tc = csc::conv_tc_plan(g, prop.multiProcessorCount);
+      const char* ev2 = std::getenv("CSC_CONV_PATH");
+      const bool force_tmem = ev2 != nullptr && std::string(ev2) == "tmem";
+      if (force_tmem || !csc::conv_ss_supported(g) || !csc::conv_ss_plan(g, prop.multiProcessorCount, c->tc))
+        c->tc = csc::conv_tc_plan(g, prop.multiProcessorCount);
       c->tc_on = true;
       ok = ok && alloc(reinterpret_cast<void**>(&c->tc_part), sizeof(float) * c->tc.part_floats);
       ok = ok && alloc(reinterpret_cast<void**>(&c->tc_bimg), sizeof(float) * c->tc.bimg_floats);
@@ -580,8 +594,7 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
   CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->st));
   if (step_d == 0.f) {
     if (g.N > 0 && c->tc_on) {
-      CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks,
-                   csc::launch_conv_tc(g, c->tc, z, c->g32, c->tc_bimg, c->tc_part, nullptr, c->st));
+      CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, z, c->g32, nullptr));
       CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
                    csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, nullptr, csc::kConvSumSq, c->sq_part, c->st));
       CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));

@@ -97,7 +97,17 @@ constexpr int kTcMaxKC = 104;  // filters per k-split held resident in shared me
 struct TcPlan {
   int NT, natoms, nks, KC, NCH, SEGR, RW, BR, nbands, nitems, grid, smem;
   size_t part_floats, bimg_floats;
+  int WL;    // SS kernel: band window length (floats)
+  bool ss;   // true: the TMA-fed SS kernel (csc_conv_ss.cu) runs this plan
 };
+int tc_ntaps_padded(int S);
+// filter taps -> B image bimg[nks][hi|lo][natoms][KC][32] (MN-major SWIZZLE_128B_BASE32B)
+cudaError_t launch_tc_bimg(const Geom& g, const TcPlan& p, const float* filt, float* bimg, cudaStream_t st);
+// TMA-fed SS dense pass (csc_conv_ss.cu): Hc*Wc % 4 == 0, s in {5,7,9,11}
+bool conv_ss_supported(const Geom& g);
+bool conv_ss_plan(const Geom& g, int num_sms, TcPlan& p);
+cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, const float* z, const float* bimg, float* part,
+                           double* l1_part, cudaStream_t st);
 bool conv_tc_supported(const Geom& g);
 TcPlan conv_tc_plan(const Geom& g, int num_sms);
 // y (all k-splits) -> band partial windows in part; per-CTA |z| partials -> l1_part[nks*grid] if non-null.

@@ -685,6 +685,11 @@ cudaError_t launch_conv_tc(const Geom& g, const TcPlan& p, const float* z, const
   return cudaSuccess;
 }
 
+cudaError_t launch_tc_bimg(const Geom& g, const TcPlan& p, const float* filt, float* bimg, cudaStream_t st) {
+  tc_bimg_kernel<<<64, 256, 0, st>>>(filt, g.K, g.S * g.S, p.KC, p.nks, p.natoms, bimg);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_conv_tc_fixup(const Geom& g, const TcPlan& p, const float* part, const float* x, float* r,
                                  int mode, double* sq_part, cudaStream_t st) {
   tc_fixup_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, g.N, g.H, g.W, g.P, p.BR, p.nbands, p.nks, x, r, mode,

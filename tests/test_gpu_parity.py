@@ -63,9 +63,15 @@ def test_lipschitz_parity(torch_dev):
         ctx.close()
 
 
+@pytest.mark.parametrize("conv", ["ss", "tmem"])
 @pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (4, 8, 5, 32, 32),
-                                   (1, 3, 1, 9, 65), (2, 6, 3, 129, 64), (1, 2, 9, 9, 9)])
-def test_residual_and_objective_parity(torch_dev, shape):
+                                   (1, 3, 1, 9, 65), (2, 6, 3, 129, 64), (1, 2, 9, 9, 9), (2, 130, 7, 41, 61),
+                                   (1, 100, 11, 150, 40)])
+def test_residual_and_objective_parity(torch_dev, shape, conv, monkeypatch):
+    """Dense pass r = Dz - x and the Eq.1 objective: TMA-fed SS tensor-core kernel (default where
+    Hc*Wc % 4 == 0), TMEM-fed kernel, or SIMT (s < 5, W+s-1 < 32).  Shapes: k-splits (K=130),
+    bands that end mid-tile, many bands (H=150)."""
+    monkeypatch.setenv("CSC_CONV_PATH", conv)
     N, K, s, H, W = shape
     x, d, z = random_problem(100 + K, N, K, s, H, W, code_density=0.3)
     ctx = _ctx(N, K, s, H, W)
