@@ -99,6 +99,10 @@ struct csc_ctx {
   csc::TcPlan tc{};
   float* tc_part = nullptr;
   float* tc_bimg = nullptr;
+  // fp16-split dense pass: scale bounds (float bits): [0] = bound of max|z|, [1] = max|filter|
+  uint32_t* smax = nullptr;
+  bool zmax_known = false;
+  const float* zmax_ptr = nullptr;
   // tensor-core filter gradient (csc_wgrad_tc.cu)
   bool wg_tc_on = false;
   csc::WgTcPlan wg{};
@@ -183,6 +187,17 @@ csc_status allreduce_d(csc_ctx* c, double* buf, size_t count) {
 // Tensor-core dense pass y = sum_k f_k * z_k into the band partials (TMA-fed SS kernel when the
 // plan says so, else the TMEM-fed kernel).
 cudaError_t conv_tc_any(csc_ctx* c, const float* z, const float* filt, double* l1p) {
+  if (c->tc.half) {
+    // the fp16 split needs a bound of max|z|: exact after csc_zero_codes or an absmax pass, then
+    // raised by every code step (T6)
+    if (!c->zmax_known || c->zmax_ptr != z) {
+      cudaError_t e = csc::launch_absmax(z, static_cast<int64_t>(c->g.N) * c->g.K * c->g.Hc * c->g.Wc, c->smax, c->st);
+      if (e != cudaSuccess) return e;
+      c->zmax_known = true;
+      c->zmax_ptr = z;
+    }
+    return csc::launch_conv_h(c->g, c->tc, z, filt, c->tc_bimg, c->smax, c->smax + 1, c->tc_part, l1p, c->st);
+  }
   if (c->tc.ss) {
     cudaError_t e = csc::launch_tc_bimg(c->g, c->tc, filt, c->tc_bimg, c->st);
     if (e != cudaSuccess) return e;
@@ -230,6 +245,13 @@ csc_status dense_residual(csc_ctx* c, const float* x, const float* d, const floa
   return CSC_OK;
 }
 
+// The code step raises the max|z| bound of the fp16-split dense pass when it writes the tracked z.
+uint32_t* zbound(csc_ctx* c, const float* z) {
+  if (c->smax == nullptr) return nullptr;
+  if (c->zmax_ptr != z) c->zmax_known = false;
+  return c->zmax_known ? c->smax : nullptr;
+}
+
 bool cache_ok(const csc_ctx* c, const float* x, const float* d, const float* z) {
   return c->cache_valid && c->cx == x && c->cd == d && c->cz == z;
 }
@@ -259,7 +281,7 @@ uint64_t csc_launch_count(const csc_ctx* ctx) { return ctx ? ctx->launches : 0; 
 uint32_t csc_kernel_variants(const csc_ctx* ctx) {
   if (!ctx) return 0;
   return (ctx->tc_on ? 1u : 0u) | (ctx->wg_tc_on ? 2u : 0u) | (ctx->ct_on ? 4u : 0u) |
-         (ctx->tc_on && ctx->tc.ss ? 8u : 0u);
+         (ctx->tc_on && ctx->tc.ss ? 8u : 0u) | (ctx->tc_on && ctx->tc.half ? 16u : 0u);
 }
 
 csc_status csc_nccl_unique_id(uint8_t out[128]) {
@@ -377,7 +399,7 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   ok = ok && alloc(reinterpret_cast<void**>(&c->gsum), sizeof(double) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->g32), sizeof(float) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->colw), sizeof(uint32_t) * static_cast<size_t>(g.K) * NB * g.Wc);
-  ok = ok && alloc(reinterpret_cast<void**>(&c->lip_part), sizeof(double) * 64 * 64 * csc::ceil_div(g.K, 16));
+  ok = ok && alloc(reinterpret_cast<void**>(&c->lip_part), sizeof(double) * 64 * 64 * csc::ceil_div(g.K, 2));
   ok = ok && alloc(reinterpret_cast<void**>(&c->dscal), sizeof(double) * kNumD);
   ok = ok && alloc(reinterpret_cast<void**>(&c->fscal), sizeof(float) * kNumF);
   ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_dscal), sizeof(double) * kNumD) == cudaSuccess;
@@ -389,11 +411,15 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
     if (!force_simt && g.N > 0 && csc::conv_tc_supported(g)) {
       const char* ev2 = std::getenv("CSC_CONV_PATH");
       const bool force_tmem = ev2 != nullptr && std::string(ev2) == "tmem";
-      if (force_tmem || !csc::conv_ss_supported(g) || !csc::conv_ss_plan(g, prop.multiProcessorCount, c->tc))
-        c->tc = csc::conv_tc_plan(g, prop.multiProcessorCount);
+      const bool force_ss = ev2 != nullptr && std::string(ev2) == "ss";
+      bool planned = false;
+      if (!force_tmem && !force_ss && csc::conv_h_supported(g)) planned = csc::conv_h_plan(g, prop.multiProcessorCount, c->tc);
+      if (!planned && !force_tmem && csc::conv_ss_supported(g)) planned = csc::conv_ss_plan(g, prop.multiProcessorCount, c->tc);
+      if (!planned) c->tc = csc::conv_tc_plan(g, prop.multiProcessorCount);
       c->tc_on = true;
       ok = ok && alloc(reinterpret_cast<void**>(&c->tc_part), sizeof(float) * c->tc.part_floats);
       ok = ok && alloc(reinterpret_cast<void**>(&c->tc_bimg), sizeof(float) * c->tc.bimg_floats);
+      ok = ok && alloc(reinterpret_cast<void**>(&c->smax), sizeof(uint32_t) * 2);
       const int need = c->tc.nks * c->tc.grid;
       if (need > cap) {
         cudaFree(c->l1_part);
@@ -493,6 +519,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->lip_part);
   cudaFree(c->tc_part);
   cudaFree(c->tc_bimg);
+  cudaFree(c->smax);
   cudaFree(c->dscal);
   cudaFree(c->fscal);
   cudaFreeHost(c->h_dscal);
@@ -504,6 +531,7 @@ csc_status csc_destroy(csc_ctx* c) {
 csc_status csc_invalidate(csc_ctx* c) {
   if (!c) return CSC_ERR_ARG;
   c->cache_valid = false;
+  c->zmax_known = false;
   return CSC_OK;
 }
 
@@ -514,6 +542,11 @@ csc_status csc_zero_codes(csc_ctx* c, const float* x, float* z) {
   const Geom& g = c->g;
   if (g.N > 0) {
     CSC_CUDA(c, cudaMemsetAsync(z, 0, sizeof(float) * static_cast<size_t>(g.N) * g.K * g.Hc * g.Wc, c->st));
+    if (c->smax != nullptr) {
+      CSC_CUDA(c, cudaMemsetAsync(c->smax, 0, sizeof(uint32_t), c->st));
+      c->zmax_known = true;
+      c->zmax_ptr = z;
+    }
     CSC_LAUNCH(c, 1, csc::launch_neg_copy(x, c->r, n_pix(g), c->st));
   }
   c->cache_valid = true;
@@ -551,10 +584,11 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
         CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(g, c->ct, seed, iter, thr, c->mwords, c->st));
       CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
                    csc::launch_code_tc(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, c->fscal + kTauZ, lambda,
-                                       c->st));
+                                       zbound(c, z), c->st));
     } else {
       if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st));
-      CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, c->fscal + kTauZ, lambda, c->st));
+      CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, c->fscal + kTauZ, lambda,
+                                                                zbound(c, z), c->st));
     }
   }
   c->cache_valid = false;  // r no longer matches z

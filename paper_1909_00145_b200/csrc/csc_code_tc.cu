@@ -49,6 +49,7 @@ struct CtArgs {
   float* z;              // [N][K][Hc][Wc]
   const uint32_t* mask;  // selection words [nkg*4][plane]: bit i = mask(k = kg*KC + cb*NC + i, p); nullptr = all
   const float* tau;      // device scalar
+  uint32_t* zmax;        // bound of max|z| raised by every written code (float bits), or nullptr
   float lam;
   int N, K, S, H, W, Hc, Wc, P;
   int KC, Npad, nkg, G;
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
     const size_t plane = static_cast<size_t>(A.Hc) * A.Wc;
     const int k0 = kg * A.KC + cb * NC;  // first filter of this warp
     const int kend = min(kg * A.KC + A.KC, A.K);
+    float wmax = 0.f;  // largest |code| this thread writes
     uint32_t tcount = 0;
     for (int item = gi; item < A.nitems; item += A.G) {
       const CtItem it = ct_item(A, item);
@@ -275,7 +277,10 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
             const int i = 4 * j4 + i4;
             const float w = fmaf(-tau, c4[i4], zv[i]);
             const float nz = (w > kappa) ? (w - kappa) : ((w < -kappa) ? (w + kappa) : 0.f);
-            if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv[i]) zb[static_cast<size_t>(i) * plane] = nz;
+            if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv[i]) {
+              zb[static_cast<size_t>(i) * plane] = nz;
+              wmax = fmaxf(wmax, fabsf(nz));
+            }
           }
         }
         tc_before();
@@ -283,6 +288,10 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
       }
     }
+    uint32_t wb = __float_as_uint(wmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wb = max(wb, __shfl_xor_sync(kFullMask, wb, o));
+    if (lane == 0 && A.zmax != nullptr && wb != 0u) atomicMax(A.zmax, wb);
   }
 
   tc_before();
@@ -421,9 +430,9 @@ cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t se
 }
 
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
-                           const uint32_t* words, const float* tau_dev, float lam, cudaStream_t st) {
+                           const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st) {
   CtArgs a{};
-  a.r = r; a.d = d; a.z = z; a.mask = words; a.tau = tau_dev; a.lam = lam;
+  a.r = r; a.d = d; a.z = z; a.mask = words; a.tau = tau_dev; a.lam = lam; a.zmax = zmax;
   a.N = g.N; a.K = g.K; a.S = g.S; a.H = g.H; a.W = g.W; a.Hc = g.Hc; a.Wc = g.Wc; a.P = g.P;
   a.KC = p.KC; a.Npad = p.Npad; a.nkg = p.nkg; a.G = p.G;
   a.L = p.L; a.nseg = p.nseg; a.nitems = p.nitems;

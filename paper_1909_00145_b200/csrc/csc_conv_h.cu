@@ -1,0 +1,512 @@
+// csc_conv_h.cu -- dense pass y = sum_k f_k * z_k on the sm_100a tensor cores, 3-term fp16 split
+// (tcgen05.mma kind::f16, fp32 accumulate), TMA-fed shared-memory operands.
+//
+// Same mathematics and tiling as csc_conv_ss.cu: Y[pos][tap] =
+// sum_k z[k][pos] f[k][tap] on flattened 128-position tiles, warp-shuffle col2im into one band
+// window.  The operands are split into two fp16 halves after an exact power-of-two scaling
+// (reading T6):
+//   x_s = x * 2^e,  hi = rn11(x_s) (rounded to 11 significant bits in fp32, exactly an fp16),
+//   lo = fp16_rn(x_s - hi),   Y_s += A_hi B_hi + A_hi B_lo + A_lo B_hi,   Y = Y_s * 2^-(e_z + e_f)
+// which carries the same 2^-22 per-product error as the 3xTF32 split while the tensor core runs at
+// the fp16 rate (2x tf32) with half the shared-memory bytes per MAC.  e_f comes from max|f|
+// (computed by the B-image kernel), e_z from a running upper bound of max|z| that the code step
+// raises whenever it writes a code (csc_api.cu keeps it); both put the largest scaled magnitude
+// at <= 2^14, so no value overflows fp16 and values below 2^-24 of the maximum lose nothing that
+// survives the fp32 sum.
+//
+// Stage = 16 filter planes of one tile: 4 TMA boxes {32 positions, 16 planes} (fp32, no swizzle,
+// 8 KB), converted by one converter warp into fp16 hi/lo tiles in the canonical MN-major
+// SWIZZLE_128B layout (2 atoms of 64 positions x 16 rows of 128 B, 16-B chunks XOR row).
+// CTA (persistent, 14 warps): warp 0 MMA, warp 1 TMA, warps 2..5 converters, warps 6..13 epilogue.
+#include "csc_internal.cuh"
+#include "csc_tc_ptx.cuh"
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <cuda_runtime.h>
+
+namespace csc {
+namespace {
+
+using namespace tcx;
+
+constexpr int kHNS = 8;             // stages (16 filters of one tile each)
+constexpr int kHConvWarps = 4;
+constexpr int kHEpiWarps = 8;
+constexpr int kHConvBase = 2, kHEpiBase = kHConvBase + kHConvWarps;
+constexpr int kHWarps = kHEpiBase + kHEpiWarps;
+constexpr int kHThreads = 32 * kHWarps;
+constexpr int kHRawBytes = 8192;    // 4 boxes x 16 rows x 128 B (fp32)
+constexpr int kHHalfBytes = 4096;   // 2 atoms x 16 rows x 128 B (fp16), one of hi / lo
+constexpr int kHStageBytes = kHRawBytes + 2 * kHHalfBytes;
+constexpr int kHSmemMax = 220 * 1024;
+
+// instruction descriptor kind::f16: fp32 accumulate, fp16 A/B, both MN-major
+__host__ __device__ constexpr uint32_t idesc_f16_mn(int M, int N) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// scale exponent for a magnitude bound m (float bits): 2^e with m * 2^e <= 2^14
+__device__ __forceinline__ int scale_exp(uint32_t mbits) {
+  if ((mbits & 0x7FFFFFFFu) == 0u) return 0;
+  const int E = static_cast<int>((mbits >> 23) & 0xFFu) - 127;  // m in [2^E, 2^(E+1))
+  int e = 13 - E;                                                 // m * 2^e < 2^14
+  return e < -100 ? -100 : (e > 100 ? 100 : e);
+}
+__device__ __forceinline__ float exp2i(int e) { return __uint_as_float(static_cast<uint32_t>(e + 127) << 23); }
+
+__device__ __forceinline__ float rn11(float x) {  // round to 11 significant bits (an fp16 mantissa)
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+struct HArgs {
+  const uint16_t* bimg;      // [nks][2][2 atoms][KC][64] fp16, SW128
+  const uint32_t* zmax;      // bound on max |z| (float bits)
+  const uint32_t* fmax;      // max |f| (float bits), written by the B-image kernel
+  float* part;               // [N][nbands][BR+P][W]
+  double* l1_part;           // [nks * grid] or nullptr
+  int N, K, S, H, W, Hc, Wc, P;
+  int KC, NCH, NT, ks;       // NCH = KC / 16
+  int BR, nbands, nitems, WL;
+};
+
+struct HItem {
+  int n, u0, u1, p0, pend, ntiles;
+};
+__device__ __forceinline__ HItem h_item(const HArgs& A, int item) {
+  HItem it;
+  it.n = item / A.nbands;
+  const int b = item - it.n * A.nbands;
+  it.u0 = b * A.BR;
+  it.u1 = min(it.u0 + A.BR, A.Hc);
+  it.p0 = it.u0 * A.Wc;
+  it.pend = it.u1 * A.Wc;
+  it.ntiles = (it.pend - it.p0 + 127) / 128;
+  return it;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+  return v;
+}
+
+template <int S>
+__global__ void __launch_bounds__(kHThreads, 1)
+conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
+  constexpr int P = S - 1;
+  extern __shared__ uint8_t smraw[];
+  __shared__ __align__(8) uint64_t full[kHNS], ready[kHNS], empty[kHNS], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ double l1_warp[kHConvWarps];
+
+  const int tid = threadIdx.x, warp = __shfl_sync(kFullMask, tid >> 5, 0), lane = tid & 31;
+  const uint32_t raw = su32(smraw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* sm = smraw + (base - raw);
+  const int bbytes = 2 * A.KC * 128;                   // one of hi / lo: 2 atoms x KC rows x 128 B
+  uint8_t* bsm = sm;                                   // [hi | lo]
+  uint8_t* stg = sm + 2 * bbytes;                      // [NS][raw 8 KB | hi 4 KB | lo 4 KB]
+  float* win = reinterpret_cast<float*>(stg + kHNS * kHStageBytes);  // [WL]
+  const int ez = scale_exp(*A.zmax), ef = scale_exp(*A.fmax);
+
+  {
+    const int4* src = reinterpret_cast<const int4*>(A.bimg + static_cast<size_t>(A.ks) * 2 * 2 * A.KC * 64);
+    int4* dst = reinterpret_cast<int4*>(bsm);
+    for (int e = tid; e < 2 * bbytes / 16; e += kHThreads) dst[e] = src[e];
+    for (int e = tid; e < A.WL; e += kHThreads) win[e] = 0.f;
+  }
+  fence_async_shared();
+  if (tid == 0) {
+    for (int i = 0; i < kHNS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&ready[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kHEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(&tmem_base_sh, 256);
+  if (warp == 1 && lane == 0) tma_prefetch_desc(&tmap_z);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tbase = __shfl_sync(kFullMask, tmem_base_sh, 0);
+
+  if (warp == 0) {
+    // ================================ MMA issuer
+    const uint32_t idesc = idesc_f16_mn(128, A.NT);
+    const uint32_t lbo_b = static_cast<uint32_t>(A.KC) * 128u;  // N atom (64 taps) stride
+    const uint32_t sbh = su32(bsm), sbl = su32(bsm + bbytes), sst = su32(stg);
+    uint32_t g = 0, tcount = 0;
+    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+      const HItem it = h_item(A, item);
+      for (int t = 0; t < it.ntiles; ++t, ++tcount) {
+        const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
+        tc_after();
+        const uint32_t d = tbase + buf * 128u;
+        for (int c = 0; c < A.NCH; ++c, ++g) {
+          const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+          mbar_wait(&ready[slot], ph);
+          tc_after();
+          const uint32_t ah = sst + slot * kHStageBytes + kHRawBytes;
+          // A: MN-major SW128, 2 atoms of 64 positions at LBO = 16 rows x 128 B, 8-row K groups at SBO
+          const uint64_t dah = sdesc(ah, 2048u, 1024u, kLayout128B);
+          const uint64_t dal = sdesc(ah + kHHalfBytes, 2048u, 1024u, kLayout128B);
+          // B: K-step c = filter rows 16c..16c+15 of the resident image
+          const uint64_t dbh = sdesc(sbh + static_cast<uint32_t>(c) * 2048u, lbo_b, 1024u, kLayout128B);
+          const uint64_t dbl = sdesc(sbl + static_cast<uint32_t>(c) * 2048u, lbo_b, 1024u, kLayout128B);
+          const uint32_t acc0 = c > 0 ? 1u : 0u;
+          asm volatile(
+              "{\n.reg .pred e, p, t;\n"
+              "elect.sync _|e, 0xffffffff;\n"
+              "setp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 1, 1;\n"
+              "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, p;\n"
+              "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %6, %4, t;\n"
+              "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %4, t;\n"
+              "}\n" ::"r"(d),
+              "l"(dah), "l"(dal), "l"(dbh), "r"(idesc), "r"(acc0), "l"(dbl)
+              : "memory");
+          mma_commit_elect(&empty[slot]);
+        }
+        mma_commit_elect(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ================================ TMA producer: 4 boxes {32 positions, 16 planes} per stage
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+        const HItem it = h_item(A, item);
+        const int plane0 = it.n * A.K + A.ks * A.KC;
+        for (int t = 0; t < it.ntiles; ++t) {
+          const int pt = it.p0 + 128 * t;  // multiple of 4 floats (BR % 4 == 0): 16-B aligned box start
+          for (int c = 0; c < A.NCH; ++c, ++g) {
+            const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+            mbar_wait(&empty[slot], ph ^ 1u);
+            mbar_arrive_expect_tx(&full[slot], kHRawBytes);
+            const uint32_t dst = su32(stg + slot * kHStageBytes);
+#pragma unroll
+            for (int at = 0; at < 4; ++at)
+              tma_load_2d(dst + at * 2048u, &tmap_z, pt + 32 * at, plane0 + 16 * c, &full[slot]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < kHEpiBase) {
+    // ================================ converters: one warp per stage (stages g = cw mod 4)
+    // thread job (row k, 8 positions 8j..8j+7): raw = box j/4, floats 8(j%4).. of row k;
+    // fp16 chunk j%8 of atom j/8, row k, at 16-B chunk (j%8) ^ (k%8)
+    const int cw = warp - kHConvBase;
+    const bool want_l1 = A.l1_part != nullptr;
+    const float sz = exp2i(ez);
+    double l1 = 0.0;
+    uint32_t g = 0;
+    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+      const HItem it = h_item(A, item);
+      for (int t = 0; t < it.ntiles; ++t) {
+        const int pt = it.p0 + 128 * t;
+        for (int c = 0; c < A.NCH; ++c, ++g) {
+          if (static_cast<int>(g % kHConvWarps) != cw) continue;
+          const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+          mbar_wait(&full[slot], ph);
+          const uint8_t* rawp = stg + slot * kHStageBytes;
+          uint8_t* hip = stg + slot * kHStageBytes + kHRawBytes;
+          uint8_t* lop = hip + kHHalfBytes;
+          float s1 = 0.f;
+#pragma unroll 2
+          for (int rep = 0; rep < 8; ++rep) {
+            const int job = lane + 32 * rep;   // 0..255
+            const int k = job >> 4, j = job & 15;
+            const float4* src = reinterpret_cast<const float4*>(rawp + (j >> 2) * 2048 + k * 128 + (j & 3) * 32);
+            const float4 x0 = src[0], x1 = src[1];
+            float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            uint32_t hv[4], lv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float a = v[2 * i] * sz, b = v[2 * i + 1] * sz;
+              const float ha = rn11(a), hb = rn11(b);
+              hv[i] = pack_h2(ha, hb);
+              lv[i] = pack_h2(a - ha, b - hb);
+            }
+            const int off = (j >> 3) * 2048 + k * 128 + (((j & 7) ^ (k & 7)) << 4);
+            *reinterpret_cast<uint4*>(hip + off) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+            *reinterpret_cast<uint4*>(lop + off) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+            if (want_l1) {
+              const int kk = A.ks * A.KC + 16 * c + k;
+              const int p = pt + 8 * j;
+              if (kk < A.K) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  if (p + i < it.pend) s1 += fabsf(v[i]);
+              }
+            }
+          }
+          if (want_l1) l1 += static_cast<double>(s1);
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ready[slot]);
+        }
+      }
+    }
+    const double tsum = warp_sum_d(l1);
+    if (lane == 0) l1_warp[cw] = tsum;
+  } else {
+    // ================================ epilogue (as csc_conv_ss.cu: one band window, Wc >= 128)
+    const int q = warp & 3;
+    const int h = (warp - kHEpiBase) >> 2;
+    constexpr int AH = (S + 1) / 2;
+    const int a_beg = h == 0 ? 0 : AH;
+    const int na = h == 0 ? AH : S - AH;
+    const float inv = exp2i(-(ez + ef));
+    uint32_t tcount = 0;
+    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+      const HItem it = h_item(A, item);
+      for (int t = 0; t < it.ntiles; ++t, ++tcount) {
+        const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        mbar_wait_sleep(&acc_full[buf], use & 1u);
+        tc_after();
+        const int pq = 128 * t + 32 * q;
+        const bool pvalid = it.p0 + pq + lane < it.pend;
+        const uint32_t tacc = tbase + buf * 128u + (static_cast<uint32_t>(32 * q) << 16);
+        float* rowb = win + pq + lane + a_beg * A.Wc;
+        float dnv[AH];
+#pragma unroll
+        for (int i = 0; i < AH; ++i) {
+          dnv[i] = 0.f;
+          if (i >= na) continue;
+          const int a = a_beg + i;
+          float y[16];
+          tmem_ld16_nowait(tacc + a * S, y);
+          tmem_ld_wait();
+          float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
+#pragma unroll
+          for (int b = 0; b < S; ++b) {
+            const float yv = pvalid ? y[b] : 0.f;
+            const float up = __shfl_up_sync(kFullMask, yv, b);
+            const float dn = __shfl_down_sync(kFullMask, yv, 32 - b);
+            const float uv = lane >= b ? up : 0.f;
+            const float dv = (b > 0 && lane < b) ? dn : 0.f;
+            if (b & 1) { u1s += uv; d1s += dv; } else { u0s += uv; d0s += dv; }
+          }
+          rowb[i * A.Wc] += u0s + u1s;
+          dnv[i] = d0s + d1s;
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        named_sync(1, 32 * kHEpiWarps);
+        if (lane < P) {
+#pragma unroll
+          for (int i = 0; i < AH; ++i)
+            if (i < na) rowb[i * A.Wc + 32] += dnv[i];
+        }
+        named_sync(1, 32 * kHEpiWarps);
+      }
+      float* dst = A.part + (static_cast<size_t>(it.n) * A.nbands + (it.u0 / A.BR)) *
+                                static_cast<size_t>(A.BR + P) * A.W;
+      const int rows = A.BR + P;
+      const int et = tid - 32 * kHEpiBase;
+      for (int e = et; e < rows * A.W; e += 32 * kHEpiWarps) {
+        const int r = e / A.W, j = e - r * A.W;
+        const float v = win[r * A.Wc + j + P] * inv;  // exact: power of two
+        dst[e] = A.ks == 0 ? v : dst[e] + v;
+      }
+      named_sync(1, 32 * kHEpiWarps);
+      for (int e = et; e < A.WL; e += 32 * kHEpiWarps) win[e] = 0.f;
+      named_sync(1, 32 * kHEpiWarps);
+    }
+  }
+
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+  if (tid == 0 && A.l1_part != nullptr) {
+    double s = 0.0;
+    for (int i = 0; i < kHConvWarps; ++i) s += l1_warp[i];
+    A.l1_part[static_cast<size_t>(A.ks) * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// B image (one block): max |f| -> fmax (float bits); then, with 2^ef, the fp16 hi/lo image
+// bimg[ks][hl][atom][k][64 taps] in the MN-major SW128 layout (16-B chunk (t%64)/8 XOR (k%8)).
+__global__ void __launch_bounds__(1024) bimg_h_kernel(const float* __restrict__ f, int K, int S2, int KC, int nks,
+                                                      uint16_t* __restrict__ bimg, uint32_t* __restrict__ fmax) {
+  __shared__ uint32_t mx;
+  if (threadIdx.x == 0) mx = 0u;
+  __syncthreads();
+  uint32_t m = 0u;
+  for (int e = threadIdx.x; e < K * S2; e += blockDim.x) m = max(m, __float_as_uint(fabsf(f[e])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFullMask, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&mx, m);
+  __syncthreads();
+  const uint32_t mbits = mx;
+  if (threadIdx.x == 0) *fmax = mbits;
+  const float sf = exp2i(scale_exp(mbits));
+  const int total = nks * KC * 128;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int t = e & 127;
+    const int k = (e >> 7) % KC, ks = (e >> 7) / KC;
+    const int kg = ks * KC + k;
+    const float v = (kg < K && t < S2) ? f[static_cast<size_t>(kg) * S2 + t] * sf : 0.f;
+    const float hv = rn11(v);
+    const __half hh = __float2half_rn(hv), hl = __float2half_rn(v - hv);
+    const int atom = t >> 6, tt = t & 63;
+    const size_t blk = static_cast<size_t>(2) * KC * 64;  // halves per (ks, hl)
+    const size_t off = static_cast<size_t>(atom) * KC * 64 + static_cast<size_t>(k) * 64 +
+                       ((((tt >> 3) ^ (k & 7))) << 3) + (tt & 7);
+    bimg[(static_cast<size_t>(ks) * 2 + 0) * blk + off] = *reinterpret_cast<const uint16_t*>(&hh);
+    bimg[(static_cast<size_t>(ks) * 2 + 1) * blk + off] = *reinterpret_cast<const uint16_t*>(&hl);
+  }
+}
+
+__global__ void absmax_kernel(const float* __restrict__ x, int64_t n, uint32_t* __restrict__ out) {
+  uint32_t m = 0u;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(x[i])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFullMask, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+typedef CUresult (*PFN_encodeTiled_h)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled_h encode_fn_h() {
+  static PFN_encodeTiled_h fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_h>(p);
+  }
+  return fn;
+}
+
+template <int S>
+cudaError_t run_conv_h(const CUtensorMap& tm, const HArgs& a, int grid, int smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(conv_h_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHSmemMax);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  conv_h_kernel<S><<<grid, kHThreads, smem, st>>>(tm, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+bool conv_h_supported(const Geom& g) {
+  return (g.S == 5 || g.S == 7 || g.S == 9 || g.S == 11) && g.N > 0 && g.Wc >= 128 &&
+         (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 && tc_ntaps_padded(g.S) <= 128 && encode_fn_h() != nullptr;
+}
+
+bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p) {
+  p = TcPlan{};
+  p.NT = 128;  // taps padded to 2 atoms of 64
+  p.natoms = 2;
+  const int stages = kHNS * kHStageBytes;
+  const int n = g.N > 0 ? g.N : 1;
+  int BR = (g.Hc * n) / (6 * num_sms);
+  BR = (BR / 4) * 4;
+  if (BR < 4) BR = 4;
+  if (BR > 32) BR = 32;
+  auto wl = [&](int br) { return (br + g.P) * g.Wc + 192; };
+  int kc_fit = (kHSmemMax - 2048 - stages - wl(4) * 4) / (2 * 2 * 128);
+  kc_fit = kc_fit / 16 * 16;
+  if (kc_fit > 128) kc_fit = 128;
+  if (kc_fit < 16) return false;
+  p.nks = ceil_div(g.K, kc_fit);
+  p.KC = (ceil_div(g.K, p.nks) + 15) / 16 * 16;
+  p.NCH = p.KC / 16;
+  const int bsm = 2 * 2 * p.KC * 128;
+  while (BR > 4 && 2048 + bsm + stages + wl(BR) * 4 > kHSmemMax) BR -= 4;
+  if (2048 + bsm + stages + wl(BR) * 4 > kHSmemMax) return false;
+  p.BR = BR;
+  p.WL = wl(BR);
+  p.nbands = ceil_div(g.Hc, BR);
+  p.nitems = g.N * p.nbands;
+  p.grid = p.nitems < num_sms ? p.nitems : num_sms;
+  if (p.grid < 1) p.grid = 1;
+  p.smem = 1024 + bsm + stages + p.WL * 4;
+  p.part_floats = static_cast<size_t>(g.N) * p.nbands * (p.BR + g.P) * g.W;
+  p.bimg_floats = static_cast<size_t>(p.nks) * 2 * 2 * p.KC * 64 / 2 + 16;  // fp16 image, in floats
+  p.ss = false;
+  p.half = true;
+  return true;
+}
+
+cudaError_t launch_absmax(const float* x, int64_t n, uint32_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  if (n > 0) absmax_kernel<<<148 * 4, 256, 0, st>>>(x, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const float* filt, float* bimg_f,
+                          const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part, cudaStream_t st) {
+  static const float* cached_z = nullptr;
+  static Geom cached_g{};
+  static CUtensorMap tm;
+  if (z != cached_z || std::memcmp(&cached_g, &g, sizeof(Geom)) != 0) {
+    PFN_encodeTiled_h enc = encode_fn_h();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Hc) * g.Wc, static_cast<cuuint64_t>(g.N) * g.K};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Hc) * g.Wc * 4};
+    const cuuint32_t box[2] = {32u, 16u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(z), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return cudaErrorInvalidPitchValue;
+    cached_z = z;
+    cached_g = g;
+  }
+  uint16_t* bimg = reinterpret_cast<uint16_t*>(bimg_f);
+  bimg_h_kernel<<<1, 1024, 0, st>>>(filt, g.K, g.S * g.S, p.KC, p.nks, bimg, fmax);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  HArgs a{};
+  a.bimg = bimg;
+  a.zmax = zmax;
+  a.fmax = fmax;
+  a.part = part;
+  a.l1_part = l1_part;
+  a.N = g.N; a.K = g.K; a.S = g.S; a.H = g.H; a.W = g.W; a.Hc = g.Hc; a.Wc = g.Wc; a.P = g.P;
+  a.KC = p.KC; a.NCH = p.NCH; a.NT = p.NT;
+  a.BR = p.BR; a.nbands = p.nbands; a.nitems = p.nitems; a.WL = p.WL;
+  for (int ks = 0; ks < p.nks; ++ks) {
+    a.ks = ks;
+    switch (g.S) {
+      case 5: e = run_conv_h<5>(tm, a, p.grid, p.smem, st); break;
+      case 7: e = run_conv_h<7>(tm, a, p.grid, p.smem, st); break;
+      case 9: e = run_conv_h<9>(tm, a, p.grid, p.smem, st); break;
+      case 11: e = run_conv_h<11>(tm, a, p.grid, p.smem, st); break;
+      default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace csc

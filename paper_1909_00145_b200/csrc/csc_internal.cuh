@@ -73,9 +73,10 @@ cudaError_t launch_mask_bits(const Geom& g, uint64_t seed, uint32_t iter, uint64
                              uint32_t* bits, cudaStream_t st);
 
 // Masked proximal-gradient code step.
+// zmax (may be null): raised (atomicMax of float bits) to >= |z| of every code written.
 cudaError_t launch_code_step(const Geom& g, const float* r, const float* d, float* z,
                              const uint32_t* colw, int all_selected, const float* tau_dev,
-                             float lam, cudaStream_t st);
+                             float lam, uint32_t* zmax, cudaStream_t st);
 
 // L_D(d) = max over 64x64 DFT grid of sum_k |d^_k|^2 -> lhat (fp64), and
 // tau_out = (float)(1/L) if tau_out != nullptr.  part: >= 64 doubles scratch.
@@ -97,8 +98,9 @@ constexpr int kTcMaxKC = 104;  // filters per k-split held resident in shared me
 struct TcPlan {
   int NT, natoms, nks, KC, NCH, SEGR, RW, BR, nbands, nitems, grid, smem;
   size_t part_floats, bimg_floats;
-  int WL;    // SS kernel: band window length (floats)
+  int WL;    // SS kernels: band window length (floats)
   bool ss;   // true: the TMA-fed SS kernel (csc_conv_ss.cu) runs this plan
+  bool half; // true: the fp16-split SS kernel (csc_conv_h.cu) runs this plan
 };
 int tc_ntaps_padded(int S);
 // filter taps -> B image bimg[nks][hi|lo][natoms][KC][32] (MN-major SWIZZLE_128B_BASE32B)
@@ -108,6 +110,14 @@ bool conv_ss_supported(const Geom& g);
 bool conv_ss_plan(const Geom& g, int num_sms, TcPlan& p);
 cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, const float* z, const float* bimg, float* part,
                            double* l1_part, cudaStream_t st);
+// fp16-split SS dense pass (csc_conv_h.cu): Wc >= 128, Hc*Wc % 4 == 0.  zmax: upper bound of max|z|
+// (float bits, device); fmax: written with max|filt| (float bits, device).
+bool conv_h_supported(const Geom& g);
+bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p);
+cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const float* filt, float* bimg,
+                          const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part, cudaStream_t st);
+// *out = bits of max |x[i]| (atomicMax over non-negative float bits; resets *out first)
+cudaError_t launch_absmax(const float* x, int64_t n, uint32_t* out, cudaStream_t st);
 bool conv_tc_supported(const Geom& g);
 TcPlan conv_tc_plan(const Geom& g, int num_sms);
 // y (all k-splits) -> band partial windows in part; per-CTA |z| partials -> l1_part[nks*grid] if non-null.
@@ -145,6 +155,6 @@ cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t se
                                  uint32_t* words, cudaStream_t st);
 // words == nullptr: every code selected (p = 1).
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
-                           const uint32_t* words, const float* tau_dev, float lam, cudaStream_t st);
+                           const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st);
 
 }  // namespace csc

@@ -480,7 +480,7 @@ template <int S>
 __global__ void __launch_bounds__(kCodeThreads, 3)
 code_step_kernel(const float* __restrict__ r, const float* __restrict__ d, float* __restrict__ z,
                  const uint32_t* __restrict__ colw, int all_selected, const float* __restrict__ tau_dev,
-                 float lam, Geom g, int TH, int kgroups, int NB) {
+                 float lam, Geom g, int TH, int kgroups, int NB, uint32_t* __restrict__ zmax) {
   constexpr int P = S - 1;
   extern __shared__ __align__(16) float rs[];
   const int v0 = blockIdx.x * 32;
@@ -509,6 +509,7 @@ code_step_kernel(const float* __restrict__ r, const float* __restrict__ d, float
   const float kappa = tau * lam;
   const int nblk = TH / 32;
   const int ub0 = u0 / 32;
+  float wmax = 0.f;
 
   for (int k = kb + warp; k < ke; k += kCodeWarps) {
     float dk[S * S];
@@ -553,51 +554,77 @@ code_step_kernel(const float* __restrict__ r, const float* __restrict__ d, float
           for (int b = 0; b < S; ++b) c = fmaf(dk[a * S + b], rp[a * kCodePitch + b], c);
         const float w = fmaf(-tau, c, zv);
         const float nz = (w > kappa) ? (w - kappa) : ((w < -kappa) ? (w + kappa) : 0.f);
-        if (nz != zv) zk[zi] = nz;
+        if (nz != zv) {
+          zk[zi] = nz;
+          wmax = fmaxf(wmax, fabsf(nz));
+        }
       }
     }
   }
+  uint32_t wb = __float_as_uint(wmax);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wb = max(wb, __shfl_xor_sync(kFull, wb, o));
+  if (lane == 0 && zmax != nullptr && wb != 0u) atomicMax(zmax, wb);
 }
 
 // ------------------------------------------------------------------ Lipschitz
-// part[kc][m1*64+m2] = sum_{k in chunk kc} |sum_{a,b} d[k,a,b] w^(a m1 + b m2)|^2, w = e^{-2 pi i/64}
+// part[kc][m1*64+m2] = sum_{k in chunk kc} |d^_k(m1, m2)|^2, d^_k(m1,m2) = sum_{a,b} d[k,a,b] w^(a m1 + b m2),
+// w = e^{-2 pi i/64}, evaluated separably: R[k][a][m2] = sum_b d[k,a,b] w^(b m2) (shared memory), then
+// d^_k(m1,m2) = sum_a R[k][a][m2] w^(a m1).  Block = kLipKChunk filters, thread = 16 grid points.
 constexpr int kLipG = 64;
-constexpr int kLipKChunk = 16;
-__global__ void lipschitz_partial_kernel(const float* __restrict__ d, Geom g, double* __restrict__ part) {
+constexpr int kLipKChunk = 2;
+constexpr int kLipThreads = 256;
+__global__ void __launch_bounds__(kLipThreads) lipschitz_partial_kernel(const float* __restrict__ d, Geom g,
+                                                                      double* __restrict__ part) {
   __shared__ double twc[kLipG], tws[kLipG];
-  const int m1 = blockIdx.x, kc = blockIdx.y, m2 = threadIdx.x;
-  {
+  __shared__ double rre[kLipKChunk][11][kLipG], rim[kLipKChunk][11][kLipG];
+  const int kc = blockIdx.x;
+  const int S = g.S;
+  const int k0 = kc * kLipKChunk, k1 = min(g.K, k0 + kLipKChunk);
+  if (threadIdx.x < kLipG) {
     double sv, cv;
     sincospi(-2.0 * static_cast<double>(threadIdx.x) / kLipG, &sv, &cv);
     twc[threadIdx.x] = cv;
     tws[threadIdx.x] = sv;
   }
   __syncthreads();
-  const int S = g.S;
-  const int k0 = kc * kLipKChunk, k1 = min(g.K, k0 + kLipKChunk);
-  double tot = 0.0;
-  for (int k = k0; k < k1; ++k) {
+  // row transforms
+  for (int e = threadIdx.x; e < (k1 - k0) * S * kLipG; e += kLipThreads) {
+    const int m2 = e % kLipG;
+    const int r = e / kLipG;
+    const int a = r % S, kk = r / S;
+    const float* da = d + (static_cast<int64_t>(k0 + kk) * S + a) * S;
     double re = 0.0, im = 0.0;
-    for (int a = 0; a < S; ++a) {
-      double ra = 0.0, ia = 0.0;
-      for (int b = 0; b < S; ++b) {
-        const double dv = static_cast<double>(__ldg(d + (static_cast<int64_t>(k) * S + a) * S + b));
-        const int idx = (b * m2) & (kLipG - 1);
-        ra += dv * twc[idx];
-        ia += dv * tws[idx];
-      }
-      const int ia_idx = (a * m1) & (kLipG - 1);
-      const double c = twc[ia_idx], s = tws[ia_idx];
-      re += ra * c - ia * s;
-      im += ra * s + ia * c;
+    for (int b = 0; b < S; ++b) {
+      const double dv = static_cast<double>(__ldg(da + b));
+      const int idx = (b * m2) & (kLipG - 1);
+      re += dv * twc[idx];
+      im += dv * tws[idx];
     }
-    tot += re * re + im * im;
+    rre[kk][a][m2] = re;
+    rim[kk][a][m2] = im;
   }
-  part[static_cast<int64_t>(kc) * kLipG * kLipG + m1 * kLipG + m2] = tot;
+  __syncthreads();
+  for (int pt = threadIdx.x; pt < kLipG * kLipG; pt += kLipThreads) {
+    const int m1 = pt / kLipG, m2 = pt % kLipG;
+    double tot = 0.0;
+    for (int kk = 0; kk < k1 - k0; ++kk) {
+      double re = 0.0, im = 0.0;
+      for (int a = 0; a < S; ++a) {
+        const int ia = (a * m1) & (kLipG - 1);
+        const double c = twc[ia], sn = tws[ia];
+        const double ra = rre[kk][a][m2], ib = rim[kk][a][m2];
+        re += ra * c - ib * sn;
+        im += ra * sn + ib * c;
+      }
+      tot += re * re + im * im;
+    }
+    part[static_cast<int64_t>(kc) * kLipG * kLipG + pt] = tot;
+  }
 }
 
-__global__ void lipschitz_final_kernel(const double* __restrict__ part, int nkc, double* __restrict__ lhat,
-                                       float* __restrict__ tau_out) {
+__global__ void __launch_bounds__(1024) lipschitz_final_kernel(const double* __restrict__ part, int nkc,
+                                                              double* __restrict__ lhat, float* __restrict__ tau_out) {
   double best = 0.0;
   for (int e = threadIdx.x; e < kLipG * kLipG; e += blockDim.x) {
     double s = 0.0;
@@ -716,7 +743,7 @@ inline int code_tile_rows(int Hc) {
 template <int S>
 struct CodeRun {
   static cudaError_t run(const Geom& g, const float* r, const float* d, float* z, const uint32_t* colw,
-                         int all_selected, const float* tau_dev, float lam, cudaStream_t st) {
+                         int all_selected, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st) {
     const int TH = code_tile_rows(g.Hc);
     const int strips = ceil_div(g.Wc, 32), bands = ceil_div(g.Hc, TH);
     const int base = strips * bands * g.N;
@@ -732,7 +759,8 @@ struct CodeRun {
     }
     const int NB = ceil_div(g.Hc, 32);
     dim3 grid(strips, bands, g.N * kgroups);
-    code_step_kernel<S><<<grid, kCodeThreads, smem, st>>>(r, d, z, colw, all_selected, tau_dev, lam, g, TH, kgroups, NB);
+    code_step_kernel<S><<<grid, kCodeThreads, smem, st>>>(r, d, z, colw, all_selected, tau_dev, lam, g, TH, kgroups, NB,
+                                                          zmax);
     return cudaGetLastError();
   }
 };
@@ -797,17 +825,17 @@ cudaError_t launch_mask_bits(const Geom& g, uint64_t seed, uint32_t iter, uint64
 }
 
 cudaError_t launch_code_step(const Geom& g, const float* r, const float* d, float* z, const uint32_t* colw,
-                             int all_selected, const float* tau_dev, float lam, cudaStream_t st) {
-  return dispatch_s<CodeRun>(g.S, g, r, d, z, colw, all_selected, tau_dev, lam, st);
+                             int all_selected, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st) {
+  return dispatch_s<CodeRun>(g.S, g, r, d, z, colw, all_selected, tau_dev, lam, zmax, st);
 }
 
 cudaError_t launch_lipschitz(const Geom& g, const float* d, double* part, double* lhat, float* tau_out,
                              cudaStream_t st) {
   const int nkc = ceil_div(g.K, kLipKChunk);
-  lipschitz_partial_kernel<<<dim3(kLipG, nkc), kLipG, 0, st>>>(d, g, part);
+  lipschitz_partial_kernel<<<nkc, kLipThreads, 0, st>>>(d, g, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  lipschitz_final_kernel<<<1, 256, 0, st>>>(part, nkc, lhat, tau_out);
+  lipschitz_final_kernel<<<1, 1024, 0, st>>>(part, nkc, lhat, tau_out);
   return cudaGetLastError();
 }
 

@@ -536,26 +536,25 @@ __global__ void tc_bimg_kernel(const float* __restrict__ f, int K, int S2, int K
 __global__ void tc_fixup_kernel(const float* __restrict__ part, int N, int H, int W, int P, int BR, int nbands,
                                 int nks, const float* __restrict__ x, float* __restrict__ r, int mode,
                                 double* __restrict__ sq_part) {
-  const int64_t npix = static_cast<int64_t>(N) * H * W;
+  // one output row per block iteration (row index decoded once; threads run along the row)
   const size_t win = static_cast<size_t>(BR + P) * W;
   double sq = 0.0;
-  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < npix;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(idx % W);
-    const int64_t ni = idx / W;
-    const int i = static_cast<int>(ni % H);
-    const int n = static_cast<int>(ni / H);
+  for (int row = blockIdx.x; row < N * H; row += gridDim.x) {
+    const int n = row / H, i = row - n * H;
     const int b0 = i / BR;
     int b1 = (i + P) / BR;
     if (b1 > nbands - 1) b1 = nbands - 1;
-    float v = 0.f;
     const float* pk = part + static_cast<size_t>(n) * nbands * win;
-    for (int b = b0; b <= b1; ++b) v += pk[b * win + static_cast<size_t>(i - b * BR + P) * W + j];
-    if (mode == kConvResidual) {
-      v = v - x[idx];
-      r[idx] = v;
+    const size_t orow = static_cast<size_t>(row) * W;
+    for (int j = threadIdx.x; j < W; j += blockDim.x) {
+      float v = 0.f;
+      for (int b = b0; b <= b1; ++b) v += pk[b * win + static_cast<size_t>(i - b * BR + P) * W + j];
+      if (mode == kConvResidual) {
+        v = v - x[orow + j];
+        r[orow + j] = v;
+      }
+      sq += static_cast<double>(v) * static_cast<double>(v);
     }
-    sq += static_cast<double>(v) * static_cast<double>(v);
   }
   // block reduction (fixed tree)
   __shared__ double red[32];

@@ -63,7 +63,7 @@ def test_lipschitz_parity(torch_dev):
         ctx.close()
 
 
-@pytest.mark.parametrize("conv", ["ss", "tmem"])
+@pytest.mark.parametrize("conv", ["half", "ss", "tmem"])
 @pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (4, 8, 5, 32, 32),
                                    (1, 3, 1, 9, 65), (2, 6, 3, 129, 64), (1, 2, 9, 9, 9), (2, 130, 7, 41, 61),
                                    (1, 100, 11, 150, 40)])
