@@ -17,7 +17,8 @@
 // Stage = 16 filter planes of one tile: 4 TMA boxes {32 positions, 16 planes} (fp32, no swizzle,
 // 8 KB), converted by one converter warp into fp16 hi/lo tiles in the canonical MN-major
 // SWIZZLE_128B layout (2 atoms of 64 positions x 16 rows of 128 B, 16-B chunks XOR row).
-// CTA (persistent, 14 warps): warp 0 MMA, warp 1 TMA, warps 2..5 converters, warps 6..13 epilogue.
+// CTA (persistent, 18 warps): warp 0 MMA, warp 1 TMA, warps 2..9 converters (one stage each, round
+// robin), warps 10..17 epilogue.
 #include "csc_internal.cuh"
 #include "csc_tc_ptx.cuh"
 
@@ -34,7 +35,7 @@ namespace {
 using namespace tcx;
 
 constexpr int kHNS = 8;             // stages (16 filters of one tile each)
-constexpr int kHConvWarps = 4;
+constexpr int kHConvWarps = 8;
 constexpr int kHEpiWarps = 8;
 constexpr int kHConvBase = 2, kHEpiBase = kHConvBase + kHConvWarps;
 constexpr int kHWarps = kHEpiBase + kHEpiWarps;
@@ -228,7 +229,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           uint8_t* hip = stg + slot * kHStageBytes + kHRawBytes;
           uint8_t* lop = hip + kHHalfBytes;
           float s1 = 0.f;
-#pragma unroll 2
+#pragma unroll 4
           for (int rep = 0; rep < 8; ++rep) {
             const int job = lane + 32 * rep;   // 0..255
             const int k = job >> 4, j = job & 15;
