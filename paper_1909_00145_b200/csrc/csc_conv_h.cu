@@ -17,8 +17,8 @@
 // Stage = 16 filter planes of one tile: 4 TMA boxes {32 positions, 16 planes} (fp32, no swizzle,
 // 8 KB), converted by one converter warp into fp16 hi/lo tiles in the canonical MN-major
 // SWIZZLE_128B layout (2 atoms of 64 positions x 16 rows of 128 B, 16-B chunks XOR row).
-// CTA (persistent, 18 warps): warp 0 MMA, warp 1 TMA, warps 2..9 converters (one stage each, round
-// robin), warps 10..17 epilogue.
+// CTA (persistent, 26 warps): warp 0 MMA, warp 1 TMA, warps 2..17 converters (a pair per stage slot),
+// warps 18..25 epilogue.
 #include "csc_internal.cuh"
 #include "csc_tc_ptx.cuh"
 
@@ -35,7 +35,7 @@ namespace {
 using namespace tcx;
 
 constexpr int kHNS = 8;             // stages (16 filters of one tile each)
-constexpr int kHConvWarps = 8;
+constexpr int kHConvWarps = 16;  // 2 per stage slot (kHNS slots): a slot is always converted by the same pair
 constexpr int kHEpiWarps = 8;
 constexpr int kHConvBase = 2, kHEpiBase = kHConvBase + kHConvWarps;
 constexpr int kHWarps = kHEpiBase + kHEpiWarps;
@@ -129,7 +129,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
   if (tid == 0) {
     for (int i = 0; i < kHNS; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&ready[i], 1);
+      mbar_init(&ready[i], 2);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -222,7 +222,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       for (int t = 0; t < it.ntiles; ++t) {
         const int pt = it.p0 + 128 * t;
         for (int c = 0; c < A.NCH; ++c, ++g) {
-          if (static_cast<int>(g % kHConvWarps) != cw) continue;
+          if (static_cast<int>(g % kHNS) != (cw >> 1)) continue;
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
           mbar_wait(&full[slot], ph);
           const uint8_t* rawp = stg + slot * kHStageBytes;
@@ -230,8 +230,8 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           uint8_t* lop = hip + kHHalfBytes;
           float s1 = 0.f;
 #pragma unroll 4
-          for (int rep = 0; rep < 8; ++rep) {
-            const int job = lane + 32 * rep;   // 0..255
+          for (int rep = 0; rep < 4; ++rep) {
+            const int job = lane + 32 * (2 * rep + (cw & 1));   // 0..255, the pair splits the stage
             const int k = job >> 4, j = job & 15;
             const float4* src = reinterpret_cast<const float4*>(rawp + (j >> 2) * 2048 + k * 128 + (j & 3) * 32);
             const float4 x0 = src[0], x1 = src[1];
