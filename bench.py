@@ -53,46 +53,77 @@ def _peaks():
         return FALLBACK_HBM_GBS, 1965.0, FALLBACK_BF16_TFLOPS, "fallback"
 
 
-def kernel_rooflines(prof, cfg, nl, steps, tc_dense, tc_wgrad=False, tc_code=False):
-    """Per kernel class: algorithmic work per launch / measured average launch time vs its roof.
-    Algorithmic units: dense pass 2*N*K*s^2*H*W FLOP; masked step sector-model bytes."""
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def _traffic():
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of each kernel class
+    from the committed ncu --set full captures (profiles/traffic.json, written by
+    scripts/ncu_traffic.py from profiles/*_ncu_*.txt); {} if absent."""
+    try:
+        with open(TRAFFIC_PATH) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def kernel_rooflines(prof, cfg, nl, steps, variants):
+    """Per kernel class: algorithmic work per launch / measured average launch time vs its roofs.
+    Algorithmic units: dense pass / filter gradient 2*N*K*s^2*H*W FLOP and a read of
+    all codes (4*N*K*Hc*Wc B); masked code step: sector-model bytes.  Tensor peaks: the measured
+    bf16 peak (fp16 split kernels) or x 0.489 (nominal tf32/bf16, 3xTF32 kernels), / 3 products.
+    "bound" is the roof with the larger fraction (the one the kernel is closest to)."""
     hbm_gbs, sm_max_mhz, bf16_tflops, kind = _peaks()
     fp32_peak = SMS * FP32_LANES_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12
     tf32_peak = bf16_tflops * TF32_PER_BF16
     dense_flops = 2.0 * nl * cfg.K * cfg.s * cfg.s * cfg.H * cfg.W
     codes = nl * cfg.K * cfg.Hc * cfg.Wc
+    traffic = _traffic()
     out = {}
+
+    def two_roofs(kernel, avg, tpeak, tnote):
+        t_ach = dense_flops / (avg / 1e3) / 1e12
+        h_ach = 4.0 * codes / (avg / 1e3) / 1e9
+        tensor = {"bound": "tensor", "achieved": t_ach, "peak": tpeak, "unit": "TFLOP/s", "peak_note": tnote,
+                  "frac": t_ach / tpeak}
+        hbm = {"bound": "hbm", "achieved": h_ach, "peak": hbm_gbs, "unit": "GB/s", "frac": h_ach / hbm_gbs,
+               "peak_note": f"{kind} copy bandwidth (MEASURED_PEAKS.json)", "bytes_model": "4 N K Hc Wc (codes read once)"}
+        best = dict(tensor if tensor["frac"] >= hbm["frac"] else hbm)
+        best["kernel"] = kernel
+        best["other_roof"] = hbm if best["bound"] == "tensor" else tensor
+        return best
+
     for name, (ms, n) in prof.items():
         if n == 0:
             continue
         avg = ms / n
         if name == "conv":
-            if tc_dense:
-                peak = tf32_peak / 3.0
-                out[name] = {"kernel": "conv_tc_kernel (tcgen05 3xTF32 implicit GEMM + col2im)", "bound": "tensor",
-                             "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": peak, "unit": "TFLOP/s",
-                             "peak_note": f"{kind} bf16 {bf16_tflops:.0f} TF/s x {TF32_PER_BF16:.3f} (tf32/bf16 nominal) / 3 (3xTF32 products per FMA)"}
+            if variants & 16:
+                out[name] = two_roofs("conv_h_kernel (tcgen05 kind::f16, 3-term fp16 split, TMA-fed SS)", avg,
+                                      bf16_tflops / 3.0, f"{kind} bf16/fp16 {bf16_tflops:.0f} TF/s / 3 products")
+            elif variants & 1:
+                nm = "conv_ss_kernel (tcgen05 3xTF32, TMA-fed SS)" if variants & 8 else \
+                    "conv_tc_kernel (tcgen05 3xTF32, TMEM A)"
+                out[name] = two_roofs(nm, avg, tf32_peak / 3.0,
+                                      f"{kind} bf16 {bf16_tflops:.0f} TF/s x {TF32_PER_BF16:.3f} (tf32/bf16 nominal) / 3")
             else:
                 out[name] = {"kernel": "conv_fwd_kernel (SIMT FP32)", "bound": "alu",
                              "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
                              "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
-            out[name]["hbm_frac"] = 4.0 * codes / (avg / 1e3) / 1e9 / hbm_gbs
-        elif name == "wgrad" and tc_wgrad:
-            out[name] = {"kernel": "wgrad_tc_kernel (tcgen05 3xTF32, TMA z + TMEM im2col(r))", "bound": "tensor",
-                         "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": tf32_peak / 3.0, "unit": "TFLOP/s",
-                         "peak_note": f"{kind} bf16 {bf16_tflops:.0f} TF/s x {TF32_PER_BF16:.3f} (tf32/bf16 nominal) / 3 (3xTF32 products per FMA)",
-                         "hbm_frac": 4.0 * codes / (avg / 1e3) / 1e9 / hbm_gbs}
+        elif name == "wgrad" and variants & 2:
+            out[name] = two_roofs("wgrad_tc_kernel (tcgen05 3xTF32, TMA z + TMEM im2col(r))", avg, tf32_peak / 3.0,
+                                  f"{kind} bf16 {bf16_tflops:.0f} TF/s x {TF32_PER_BF16:.3f} (tf32/bf16 nominal) / 3")
         elif name == "wgrad":
             out[name] = {"kernel": "wgrad_kernel (SIMT FP32)", "bound": "alu",
                          "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
                          "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
         elif name == "code_step":
             sector_bytes = 8.0 * (1.0 - (1.0 - cfg.p) ** 8) * codes + 12.0 * nl * cfg.H * cfg.W
-            out[name] = {"kernel": "code_tc_kernel (tcgen05 3xTF32 dense-then-mask prox step)" if tc_code
+            out[name] = {"kernel": "code_tc_kernel (tcgen05 dense-then-mask prox step)" if variants & 4
                          else "code_step_kernel (SIMT masked prox step)", "bound": "hbm",
                          "achieved": sector_bytes / (avg / 1e3) / 1e9, "peak": hbm_gbs, "unit": "GB/s",
                          "peak_note": f"{kind} copy bandwidth (MEASURED_PEAKS.json)",
-                         "model": "sector: 8(1-(1-p)^8) N K Hc Wc + 12 N H W"}
+                         "bytes_model": "sector: 8(1-(1-p)^8) N K Hc Wc + 12 N H W"}
         else:
             continue
         r = out[name]
@@ -100,7 +131,10 @@ def kernel_rooflines(prof, cfg, nl, steps, tc_dense, tc_wgrad=False, tc_code=Fal
         r["avg_launch_ms"] = avg
         r["launches_per_step"] = n / steps
         r["ms_per_step"] = ms / steps
-        r["traffic"] = None
+        tr = traffic.get(name, {}).get(cfg.name)
+        r["traffic"] = tr["bytes_per_launch"] if tr else None
+        if tr:
+            r["traffic_source"] = tr["source"]
     return out
 
 
@@ -325,7 +359,7 @@ def run_ours(args):
 
     if rank == 0:
         step_ms = t_ms / args.steps
-        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.tc_dense, ctx.tc_wgrad, ctx.tc_code)
+        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.variants)
         dom = max(rl, key=lambda k: rl[k]["ms_per_step"])
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                        "share": v[0] / max(t_total, 1e-9)} for k, v in prof.items()}

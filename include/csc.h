@@ -175,6 +175,7 @@ csc_status csc_profile_read(csc_ctx* ctx, int cls, double* total_ms, uint64_t* l
  *   bit 2  masked code step as tcgen05 3xTF32 dense-then-mask (csc_code_tc.cu)
  *   bit 3  the dense passes use the TMA-fed shared-memory-operand kernel (csc_conv_ss.cu)
  *   bit 4  the dense passes use the fp16-split TMA-fed kernel (csc_conv_h.cu, T6)
+ *   bit 5  the code step uses the fp16-split kernel with TMA-fed code tiles (csc_code_h.cu)
  * The choice is fixed at csc_init from the shape (and CSC_DENSE_PATH / CSC_WGRAD_PATH /
  * CSC_CODE_PATH = simt). */
 uint32_t csc_kernel_variants(const csc_ctx* ctx);

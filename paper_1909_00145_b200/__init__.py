@@ -245,6 +245,11 @@ class Context:
         return bool(self._L.csc_kernel_variants(self._h) & 2)
 
     @property
+    def variants(self) -> int:
+        """csc_kernel_variants bit set (include/csc.h)."""
+        return int(self._L.csc_kernel_variants(self._h))
+
+    @property
     def tc_code(self) -> bool:
         """True when the masked code step runs as the tcgen05 dense-then-mask kernel (bit 2)."""
         return bool(self._L.csc_kernel_variants(self._h) & 4)

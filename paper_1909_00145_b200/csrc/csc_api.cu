@@ -110,6 +110,7 @@ struct csc_ctx {
   bool ct_on = false;
   csc::CodeTcPlan ct{};
   uint32_t* mwords = nullptr;  // selection-word mask [4*nkg][Hc*Wc]
+  uint32_t* rmax = nullptr;    // max|r| (float bits) for the fp16-split code step
   ncclComm_t comm = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -281,7 +282,8 @@ uint64_t csc_launch_count(const csc_ctx* ctx) { return ctx ? ctx->launches : 0; 
 uint32_t csc_kernel_variants(const csc_ctx* ctx) {
   if (!ctx) return 0;
   return (ctx->tc_on ? 1u : 0u) | (ctx->wg_tc_on ? 2u : 0u) | (ctx->ct_on ? 4u : 0u) |
-         (ctx->tc_on && ctx->tc.ss ? 8u : 0u) | (ctx->tc_on && ctx->tc.half ? 16u : 0u);
+         (ctx->tc_on && ctx->tc.ss ? 8u : 0u) | (ctx->tc_on && ctx->tc.half ? 16u : 0u) |
+         (ctx->ct_on && ctx->ct.half ? 32u : 0u);
 }
 
 csc_status csc_nccl_unique_id(uint8_t out[128]) {
@@ -386,11 +388,18 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   {
     const char* ev = std::getenv("CSC_CODE_PATH");
     const bool force_simt = ev != nullptr && std::string(ev) == "simt";
-    if (!force_simt && csc::code_tc_supported(g)) {
+    const bool force_tc = ev != nullptr && std::string(ev) == "tc";
+    if (!force_simt && !force_tc && csc::code_h_supported(g)) {
+      c->ct = csc::code_h_plan(g, prop.multiProcessorCount);
+      if (!c->ct.ok) c->ct = csc::code_tc_plan(g, prop.multiProcessorCount);
+    } else if (!force_simt && csc::code_tc_supported(g)) {
       c->ct = csc::code_tc_plan(g, prop.multiProcessorCount);
+    }
+    if (!force_simt && (csc::code_h_supported(g) || csc::code_tc_supported(g))) {
       if (c->ct.ok) {
         c->ct_on = true;
         ok = ok && alloc(reinterpret_cast<void**>(&c->mwords), sizeof(uint32_t) * c->ct.sw_words);
+        ok = ok && alloc(reinterpret_cast<void**>(&c->rmax), sizeof(uint32_t) * 4);
       }
     }
   }
@@ -516,6 +525,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->g32);
   cudaFree(c->colw);
   cudaFree(c->mwords);
+  cudaFree(c->rmax);
   cudaFree(c->lip_part);
   cudaFree(c->tc_part);
   cudaFree(c->tc_bimg);
@@ -582,9 +592,16 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
     if (c->ct_on) {
       if (!all_selected)
         CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(g, c->ct, seed, iter, thr, c->mwords, c->st));
-      CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
-                   csc::launch_code_tc(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, c->fscal + kTauZ, lambda,
-                                       zbound(c, z), c->st));
+      if (c->ct.half) {
+        CSC_LAUNCH(c, 1, csc::launch_absmax(c->r, n_pix(g), c->rmax, c->st));
+        CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
+                     csc::launch_code_h(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, c->fscal + kTauZ,
+                                        lambda, c->rmax, zbound(c, z), c->st));
+      } else {
+        CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
+                     csc::launch_code_tc(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, c->fscal + kTauZ,
+                                         lambda, zbound(c, z), c->st));
+      }
     } else {
       if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st));
       CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, c->fscal + kTauZ, lambda,

@@ -147,12 +147,19 @@ struct CodeTcPlan {
   size_t sw_words;  // selection-word mask size (4 * nkg * Hc * Wc words)
   int grid, smem;
   bool ok;
+  bool half;        // true: the fp16-split kernel (csc_code_h.cu)
 };
 bool code_tc_supported(const Geom& g);
 CodeTcPlan code_tc_plan(const Geom& g, int num_sms);
 // Mask as selection words sw[4*nkg][Hc*Wc]: bit i of sw[kg*4+cb][p] = mask(kg*KC + cb*(Npad/4) + i, p).
 cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
                                  uint32_t* words, cudaStream_t st);
+// fp16-split variant (csc_code_h.cu): Hc*Wc % 4 == 0 (TMA view of z); rmax = max|r| (float bits).
+bool code_h_supported(const Geom& g);
+CodeTcPlan code_h_plan(const Geom& g, int num_sms);
+cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
+                          const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
+                          uint32_t* zmax, cudaStream_t st);
 // words == nullptr: every code selected (p = 1).
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                            const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st);

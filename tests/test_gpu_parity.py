@@ -89,7 +89,7 @@ def test_residual_and_objective_parity(torch_dev, shape, conv, monkeypatch):
     ctx.close()
 
 
-@pytest.mark.parametrize("path", ["tc", "simt"])
+@pytest.mark.parametrize("path", ["half", "tc", "simt"])
 @pytest.mark.parametrize("shape,p", [((3, 5, 5, 70, 130), 0.1), ((2, 17, 11, 100, 100), 0.2),
                                      ((4, 8, 5, 32, 32), 1.0), ((1, 9, 3, 33, 47), 0.5), ((2, 4, 11, 11, 11), 0.05),
                                      ((2, 130, 7, 20, 300), 0.1), ((1, 100, 11, 40, 11), 0.3), ((3, 16, 9, 61, 9), 1.0)])
