@@ -119,7 +119,7 @@ def kernel_rooflines(prof, cfg, nl, steps, variants):
                          "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
         elif name == "code_step":
             sector_bytes = 8.0 * (1.0 - (1.0 - cfg.p) ** 8) * codes + 12.0 * nl * cfg.H * cfg.W
-            out[name] = {"kernel": "code_tc_kernel (tcgen05 dense-then-mask prox step)" if variants & 4
+            out[name] = {"kernel": ("code_h_kernel (tcgen05 kind::f16 3-term split, dense-then-mask, TMA code slices)" if variants & 32 else "code_tc_kernel (tcgen05 3xTF32 dense-then-mask)") if variants & 4
                          else "code_step_kernel (SIMT masked prox step)", "bound": "hbm",
                          "achieved": sector_bytes / (avg / 1e3) / 1e9, "peak": hbm_gbs, "unit": "GB/s",
                          "peak_note": f"{kind} copy bandwidth (MEASURED_PEAKS.json)",
