@@ -58,6 +58,7 @@ struct WgArgs {
   int pitch, rs_rows, rs_floats;  // residual tile
   int stage_bytes;       // one of hi / lo
   int cpt;               // chunks (32 positions) per accumulator tile
+  unsigned long long* tdbg;  // CSC_WG_TIMING: per-CTA role timings [grid][8] or nullptr
   int dbg;  // CSC_WG_DEBUG development switches: 1 no MMA, 2 no TMA, 4 no tmem st, 8 no tmem ld, 16 no lo copy
 };
 
@@ -91,7 +92,8 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* sm = smraw + (base - raw);
   uint8_t* stages = sm;                                   // [NS][hi | lo], each stage_bytes
-  float* rs = reinterpret_cast<float*>(sm + 2 * kWgNS * A.stage_bytes);  // [2][rs_rows][pitch]
+  float* rs = reinterpret_cast<float*>(sm + 2 * kWgNS * A.stage_bytes);  // [2][rs_rows][pitch]: r, then hi
+  float* rsl = rs + 2 * A.rs_floats;                                      // [2][rs_rows][pitch]: lo
 
   // ---- setup: zero the z stages (rows >= KC are never written by TMA), barriers, TMEM
   for (int e = tid; e < 2 * kWgNS * A.stage_bytes / 16; e += kWgThreadsTc)
@@ -100,7 +102,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
   if (tid == 0) {
     for (int i = 0; i < kWgNS; ++i) {
       mbar_init(&z_full[i], 1);
-      mbar_init(&ready[i], kWgConvWarps);
+      mbar_init(&ready[i], 4);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -121,19 +123,25 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
   if (warp == 0) {
     // ================================ MMA issuer
     const uint32_t idesc = idesc_tf32(128, A.Npad, 0, 0);
+    unsigned long long w_acc = 0, w_rdy = 0;
+    const unsigned long long t_beg = clock64();
     uint32_t g = 0, tcount = 0;
     for (int item = gi; item < A.nitems; item += A.G) {
       const WgItem it = wg_item(A, item);
       const int ntl = wg_ntiles(it.nch, A.cpt);
       for (int tl = 0; tl < ntl; ++tl, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        const unsigned long long tw0 = clock64();
         mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
+        w_acc += clock64() - tw0;
         tc_after();
         const uint32_t d = t_acc + buf * static_cast<uint32_t>(A.Npad);
         const int c0 = tl * A.cpt, c1 = min(c0 + A.cpt, it.nch);
         for (int c = c0; c < c1; ++c, ++g) {
           const uint32_t slot = g % kWgNS, ph = (g / kWgNS) & 1u;
+          const unsigned long long tw1 = clock64();
           mbar_wait(&ready[slot], ph);
+          w_rdy += clock64() - tw1;
           tc_after();
           const int nks = min(4, (it.p1 - it.p0 - 32 * c + 7) >> 3);
           const uint32_t sh = su32(stages + slot * 2 * A.stage_bytes);
@@ -161,6 +169,11 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
         }
         mma_commit_elect(&acc_full[buf]);
       }
+    }
+    if (A.tdbg != nullptr && lane == 0) {
+      A.tdbg[blockIdx.x * 8 + 0] = clock64() - t_beg;
+      A.tdbg[blockIdx.x * 8 + 1] = w_acc;
+      A.tdbg[blockIdx.x * 8 + 2] = w_rdy;
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -190,7 +203,9 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
     // ================================ converters
     const int cw = warp - kWgConvBase;  // 0..7
     const int q = warp & 3;             // TMEM lane quarter
-    const int h = cw >> 2;              // K-steps {2h, 2h+1} of every chunk
+    const int grp = cw >> 2;            // the two groups of 4 warps take alternate chunks (whole chunks),
+                                        // so two chunks are converted concurrently
+    const int ctg = (cw & 3) * 32 + lane;  // 0..127 within the group
     const int t = 32 * q + lane;        // tap of this lane
     const int S2 = A.S * A.S;
     const bool tap_ok = t < S2;
@@ -212,6 +227,8 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
       cp_async_commit();
     };
     uint32_t g = 0;
+    unsigned long long w_zf = 0;
+    const unsigned long long t_cv = clock64();
     int ibuf = 0;
     if (gi < A.nitems) stage_r(gi, 0);
     for (int item = gi; item < A.nitems; item += A.G, ibuf ^= 1) {
@@ -220,20 +237,37 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
       else cp_async_commit();
       cp_async_wait<1>();
       named_sync(1, 32 * kWgConvWarps);
+      // split the staged residual tile once (hi in place, lo beside it): the im2col below reads
+      // every value once per tap, so this removes ~121 redundant splits per value
+      {
+        float* th = rs + ibuf * A.rs_floats;
+        float* tl = rsl + ibuf * A.rs_floats;
+        for (int e = ct; e < A.rs_floats; e += 32 * kWgConvWarps) {
+          float hf, lf;
+          tf32_split_rn(th[e], hf, lf);
+          th[e] = hf;
+          tl[e] = lf;
+        }
+      }
+      named_sync(1, 32 * kWgConvWarps);
       const float* rtile = rs + ibuf * A.rs_floats + tap_off;
+      const float* rtilel = rsl + ibuf * A.rs_floats + tap_off;
       for (int c = 0; c < it.nch; ++c, ++g) {
+        if (static_cast<int>(g & 1u) != grp) continue;
         const uint32_t slot = g % kWgNS, ph = (g / kWgNS) & 1u;
-        // first position of this warp's K-steps, as (row, column) -- warp-uniform
-        const int pk = it.p0 + 32 * c + 16 * h;
+        // first position of the chunk, as (row, column) -- warp-uniform
+        const int pk = it.p0 + 32 * c;
         int u = pk / A.Wc;
         int v = pk - u * A.Wc;
+        const unsigned long long tw2 = clock64();
         mbar_wait_sleep(&z_full[slot], ph);
+        w_zf += clock64() - tw2;
         // (1) lo copy of the z stage (elementwise, the swizzle is irrelevant)
         if (!(A.dbg & 16)) {
           float4* hi4 = reinterpret_cast<float4*>(stages + slot * 2 * A.stage_bytes);
           float4* lo4 = reinterpret_cast<float4*>(stages + slot * 2 * A.stage_bytes + A.stage_bytes);
           const int n4 = A.KC * 8;  // KC rows x 32 floats / 4
-          for (int e = ct; e < n4; e += 32 * kWgConvWarps) {
+          for (int e = ctg; e < n4; e += 128) {
             const float4 x = hi4[e];
             float4 h, l;
             tf32_split_rn(x.x, h.x, l.x);
@@ -244,23 +278,21 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
             lo4[e] = l;
           }
         }
-        // (2) im2col of r into the A slot: K-steps 2h, 2h+1 of this chunk.
+        // (2) im2col of r into the A slot: the 4 K-steps of this chunk for this lane quarter.
         // R[(u,v)][(a,b)] = r[u-P+a][v-P+b] = rs[u - u_first + a][v + b]
 #pragma unroll
-        for (int ee = 0; ee < 2; ++ee) {
-          const int e = 2 * h + ee;
-          const int p = pk + 8 * ee;  // first position of K-step e
+        for (int e = 0; e < 4; ++e) {
+          const int p = pk + 8 * e;  // first position of K-step e
           if (p < it.p1) {
             uint32_t hv[8], lv[8];
             if (v + 7 < A.Wc && p + 7 < it.p1) {
-              const float* src = rtile + (u - it.u_first) * A.pitch + v;
+              const int o = (u - it.u_first) * A.pitch + v;
+              const float* srch = rtile + o;
+              const float* srcl = rtilel + o;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float x = tap_ok ? src[j] : 0.f;
-                float hf, lf;
-                tf32_split_rn(x, hf, lf);
-                hv[j] = __float_as_uint(hf);
-                lv[j] = __float_as_uint(lf);
+                hv[j] = tap_ok ? __float_as_uint(srch[j]) : 0u;
+                lv[j] = tap_ok ? __float_as_uint(srcl[j]) : 0u;
               }
             } else {
               // row wrap (Wc >= 8: at most one) or end of the item
@@ -269,11 +301,10 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
                 const int vj = v + j;
                 const bool wrap = vj >= A.Wc;
                 const int uu = wrap ? u + 1 : u, vv = wrap ? vj - A.Wc : vj;
-                const float x = (tap_ok && p + j < it.p1) ? rtile[(uu - it.u_first) * A.pitch + vv] : 0.f;
-                float hf, lf;
-                tf32_split_rn(x, hf, lf);
-                hv[j] = __float_as_uint(hf);
-                lv[j] = __float_as_uint(lf);
+                const bool ok = tap_ok && p + j < it.p1;
+                const int o = (uu - it.u_first) * A.pitch + vv;
+                hv[j] = ok ? __float_as_uint(rtile[o]) : 0u;
+                lv[j] = ok ? __float_as_uint(rtilel[o]) : 0u;
               }
             }
             const uint32_t ta_col = t_a + slot * 64u + 8u * e;
@@ -297,6 +328,10 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
       named_sync(1, 32 * kWgConvWarps);  // everyone is done reading rs[ibuf] before it is restaged
     }
     cp_async_wait<0>();
+    if (A.tdbg != nullptr && warp == kWgConvBase && lane == 0) {
+      A.tdbg[blockIdx.x * 8 + 3] = w_zf;
+      A.tdbg[blockIdx.x * 8 + 4] = clock64() - t_cv;
+    }
   } else {
     // ================================ epilogue
     const int ew = warp - kWgEpiBase;  // 0..15
@@ -306,13 +341,16 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
 #pragma unroll
     for (int i = 0; i < NC; ++i) acc[i] = 0.0;
     const uint32_t tq = (static_cast<uint32_t>(32 * q) << 16);
+    unsigned long long w_af = 0;
     uint32_t tcount = 0;
     for (int item = gi; item < A.nitems; item += A.G) {
       const WgItem it = wg_item(A, item);
       const int ntl = wg_ntiles(it.nch, A.cpt);
       for (int tl = 0; tl < ntl; ++tl, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        const unsigned long long tw3 = clock64();
         mbar_wait_sleep(&acc_full[buf], use & 1u);
+        w_af += clock64() - tw3;
         tc_after();
         const uint32_t col = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
 #pragma unroll
@@ -330,6 +368,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
       }
     }
+    if (A.tdbg != nullptr && warp == kWgEpiBase && lane == 0) A.tdbg[blockIdx.x * 8 + 5] = w_af;
     // per-CTA partial: gpart[gi][k][t]
     const int t = 32 * q + lane;
     const int S2 = A.S * A.S;
@@ -407,7 +446,7 @@ WgTcPlan wgrad_tc_plan(const Geom& g, int num_sms) {
   if (L > 4096) L = 4096;
   const int smem_fixed = 1024 + 2 * kWgNS * p.stage_bytes;
   auto rows_for = [&](int64_t len) { return static_cast<int>((len + g.Wc - 1) / g.Wc) + 1 + g.P; };
-  while (L > 32 && smem_fixed + 2 * rows_for(L) * pitch * 4 > kWgSmemMax) L -= 32;
+  while (L > 32 && smem_fixed + 4 * rows_for(L) * pitch * 4 > kWgSmemMax) L -= 32;
   p.L = static_cast<int>(L);
   p.rs_rows = rows_for(L);
   p.rs_floats = p.rs_rows * pitch;
@@ -415,7 +454,7 @@ WgTcPlan wgrad_tc_plan(const Geom& g, int num_sms) {
   p.nitems = g.N * p.nseg;
   p.G = p.nitems < G ? (p.nitems > 0 ? p.nitems : 1) : G;
   p.grid = p.G * p.nkg;
-  p.smem = smem_fixed + 2 * p.rs_floats * 4;
+  p.smem = smem_fixed + 4 * p.rs_floats * 4;
   return p;
 }
 
@@ -461,6 +500,28 @@ cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, const float* z, co
       if (cpt < 1) cpt = 1;
     }
     a.cpt = cpt;
+  }
+  {
+    static int tmode = -1;
+    static unsigned long long* tbuf = nullptr;
+    static int ncalls = 0;
+    if (tmode < 0) {
+      const char* ev = std::getenv("CSC_WG_TIMING");
+      tmode = ev ? std::atoi(ev) : 0;
+      if (tmode) cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 2048);
+    }
+    a.tdbg = tmode ? tbuf : nullptr;
+    if (tmode && ++ncalls == 5) {
+      cudaStreamSynchronize(st);
+      unsigned long long h[8 * 2048];
+      cudaMemcpy(h, tbuf, sizeof(unsigned long long) * 8 * p.grid, cudaMemcpyDeviceToHost);
+      double tot[8] = {0};
+      for (int b = 0; b < p.grid; ++b)
+        for (int r = 0; r < 6; ++r) tot[r] += static_cast<double>(h[b * 8 + r]);
+      fprintf(stderr, "[wgrad_tc] per CTA cycles: total %.0f | mma wait acc_empty %.0f, wait ready %.0f | conv0 wait z "
+                      "%.0f of %.0f | epi wait acc_full %.0f\n",
+              tot[0] / p.grid, tot[1] / p.grid, tot[2] / p.grid, tot[3] / p.grid, tot[4] / p.grid, tot[5] / p.grid);
+    }
   }
   switch (p.Npad / 4) {
     case 4: return run_wgrad_tc<4>(tm, a, p.grid, p.smem, st);
