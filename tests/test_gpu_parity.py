@@ -289,3 +289,75 @@ def test_full_size_sweep_config_sampled(torch_dev):
     Fo = oracle.objective(x, do, zg, cfg.lam)
     assert abs(F[0] - Fo[0]) <= TOL * Fo[0]
     ctx.close()
+
+
+@pytest.mark.slow
+def test_full_size_online_config_step():
+    """Config 4 (BASELINE.json configs[3]) at full size: K=400 filters (4 filter groups in the
+    tensor-core kernels), a mini-batch of 8 images 100x100, p=0.1 -- one SOCSC step (Alg.2,
+    P:336-346; reading #14): zero codes, 10 masked code steps (mask t = 10 step + i), filter step,
+    objective; codes, filters and F against the oracle."""
+    import torch
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda:0")
+    cfg = CONFIGS["online"]
+    x = make_images(cfg, 0, cfg.N)
+    d = make_filters(cfg)
+    seed = mask_seed(cfg)
+    ctx = _ctx(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W)
+    xt, dt = _t(x, dev), _t(d, dev)
+    zt = torch.empty((cfg.N, cfg.K, cfg.Hc, cfg.Wc), dtype=torch.float32, device=dev)
+    ctx.zero_codes(xt, zt)
+    z = np.zeros((cfg.N, cfg.K, cfg.Hc, cfg.Wc), np.float32)
+    step = 3
+    for i in range(10):
+        ctx.code_step(xt, dt, zt, cfg.lam, cfg.p, seed, 10 * step + i)
+        z, _ = oracle.code_step(x, d, z, cfg.lam, 0.0, cfg.p, seed, 10 * step + i)
+    ctx.filter_step(xt, dt, zt)
+    d1, _, _, _ = oracle.filter_step(x, d, z)
+    F = ctx.objective(xt, dt, zt, cfg.lam)
+    Fo = oracle.objective(x, d1, z, cfg.lam)
+    torch.cuda.synchronize()
+    assert rel_err(zt.cpu().numpy(), z) < TOL
+    assert rel_err(dt.cpu().numpy(), d1) < TOL
+    assert abs(F[0] - Fo[0]) < TOL * Fo[0]
+    ctx.close()
+
+
+@pytest.mark.slow
+def test_full_size_large_config_sampled():
+    """Config 5 (BASELINE.json configs[4]) at full size on one B200: K=1024 filters (10 filter
+    groups), 64 images 512x512, 71 GB of codes, p=0.1, in the launch configuration bench.py uses.
+    Two iterations on the GPU; the code steps are checked on sampled images against the oracle
+    (codes are independent per image given d), the filter step by properties that hold at any
+    size: unit-ball filters and a decreasing objective."""
+    import torch
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda:0")
+    cfg = CONFIGS["large"]
+    x = make_images(cfg)
+    d = make_filters(cfg)
+    seed = mask_seed(cfg)
+    ctx = _ctx(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W)
+    xt, dt = _t(x, dev), _t(d, dev)
+    zt = torch.empty((cfg.N, cfg.K, cfg.Hc, cfg.Wc), dtype=torch.float32, device=dev)
+    ctx.zero_codes(xt, zt)
+    sample = [0, cfg.N - 1]
+    F_prev = 0.5 * float((x.astype(np.float64) ** 2).sum())
+    z_s = np.zeros((len(sample), cfg.K, cfg.Hc, cfg.Wc), np.float32)
+    for t in (1, 2):
+        d_before = dt.cpu().numpy()
+        ctx.code_step(xt, dt, zt, cfg.lam, cfg.p, seed, t)
+        torch.cuda.synchronize()
+        zo, _ = oracle.code_step(x[sample], d_before, z_s, cfg.lam, 0.0, cfg.p, seed, t)
+        zg = torch.stack([zt[i] for i in sample]).cpu().numpy()
+        assert rel_err(zg, zo) < TOL, (t, rel_err(zg, zo))
+        z_s = zg
+        ctx.filter_step(xt, dt, zt)
+        F = ctx.objective(xt, dt, zt, cfg.lam)
+        dn = np.sqrt((dt.cpu().numpy().astype(np.float64) ** 2).sum(axis=(1, 2)))
+        assert (dn <= 1 + 1e-6).all()
+        assert F[0] < F_prev, (t, F, F_prev)
+        F_prev = F[0]
+    del zt
+    ctx.close()
