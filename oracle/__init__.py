@@ -61,6 +61,9 @@ def lib():
                 f.restype = _c_dbl
                 getattr(L, f"oracle_code_step_{suf}").argtypes = (
                     [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, _c_u64, _c_u32, _vp])
+                getattr(L, f"oracle_admm_code_step_{suf}").argtypes = (
+                    [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, ctypes.c_int, ctypes.c_int, _c_dbl, _c_u64,
+                                                _c_u32])
                 getattr(L, f"oracle_filter_step_{suf}").argtypes = (
                     [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _vp, _vp, _vp])
                 getattr(L, f"oracle_objective_{suf}").argtypes = [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _vp]
@@ -170,6 +173,27 @@ def code_step(x, d, z, lam, step_z, p, seed, t, dtype=np.float32):
         N, K, s, H, W, _p(x), _p(d), _p(z), float(lam), float(step_z), float(p),
         int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(tau))
     return z, float(tau[0])
+
+
+ADMM_ITERS = 10      # P:317-318 "the ADMM iteration fixed to 10"
+ADMM_ALPHA = 1.8     # P:319-320 over-relaxation
+ADMM_CG_ITERS = 5    # reading A3: the paper leaves the CG length to its supplement
+
+
+def admm_code_step(x, d, z, lam, p, seed, t, rho=None, alpha=ADMM_ALPHA, n_admm=ADMM_ITERS, n_cg=ADMM_CG_ITERS,
+                   dtype=np.float32):
+    """ADMM masked-LASSO code step, rho = 10 lambda by default
+    (P:318-319).  Returns z_new."""
+    x = _c(x, dtype); d = _c(d, dtype)
+    z = np.array(z, dtype=dtype, copy=True, order="C")
+    N, K, Hc, Wc = z.shape
+    s = d.shape[-1]
+    H, W = Hc - s + 1, Wc - s + 1
+    rho = 10.0 * lam if rho is None else rho
+    getattr(lib(), f"oracle_admm_code_step_{_suf(dtype)}")(
+        N, K, s, H, W, _p(x), _p(d), _p(z), float(lam), float(rho), float(alpha), int(n_admm), int(n_cg),
+        float(p), int(seed) & (2**64 - 1), int(t) & 0xffffffff)
+    return z
 
 
 def filter_step(x, d, z, step_d=0.0, dtype=np.float32):

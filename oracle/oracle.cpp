@@ -204,6 +204,107 @@ void code_step(const Dims& D, const T* x, const T* d, T* z, double lam, double s
   if (tau_used) *tau_used = tau;
 }
 
+// ADMM code step (§3.2): Eq.3, the LASSO for the codes
+// selected by M^t with the filters held fixed, solved by ADMM with the data term and the L1 term
+// split: a quadratic substep solved by Conjugate Gradient ("when N is
+// relatively small") and a point-wise shrinkage; 10 iterations, rho = 10 lambda,
+// over-relaxation alpha = 1.8.  Readings (A1-A6): scaled form; per image
+// (the images are independent problems, Alg.1 lines 5-6); w = y = the current selected codes and
+// u = 0 at the start of every outer iteration; CG warm-started at the current w with n_cg
+// iterations; the output is the shrunk variable y; unselected codes are untouched (R2).
+//   b = x - D z_fix (z_fix: codes with the selected ones zeroed), A = D M^T
+//   repeat n_admm:  (A^T A + rho I) w = A^T b + rho (y - u)      [CG]
+//                   w^ = alpha w + (1 - alpha) y
+//                   y  = S_{lam/rho}(w^ + u),   u = u + w^ - y
+template <typename T>
+void admm_code_step(const Dims& D, const T* x, const T* d, T* z, double lam, double rho, double alpha,
+                    int n_admm, int n_cg, double p, uint64_t seed, uint32_t t) {
+  const uint64_t thr = mask_threshold(p);
+  const int64_t nc = D.K * D.Hc * D.Wc;
+  std::vector<double> dd((size_t)(D.K * D.s * D.s));
+  for (size_t q = 0; q < dd.size(); ++q) dd[q] = (double)d[q];
+  std::vector<char> msk((size_t)nc);
+  for (int64_t l = 0; l < nc; ++l) msk[l] = mask_bit(seed, t, (uint64_t)l, thr) ? 1 : 0;
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t n = 0; n < D.N; ++n) {
+    // image-n views: codes c[l] (l = (k Hc + u) Wc + v), images [i W + j]
+    const T* zn = z + n * nc;
+    const T* xn = x + n * D.H * D.W;
+    // D applied to a code vector (valid true convolution), and D^T at the selected codes
+    auto apply_D = [&](const std::vector<double>& c, std::vector<double>& img) {
+      for (int64_t i = 0; i < D.H; ++i)
+        for (int64_t j = 0; j < D.W; ++j) {
+          double acc = 0.0;
+          for (int64_t k = 0; k < D.K; ++k)
+            for (int64_t a = 0; a < D.s; ++a)
+              for (int64_t b = 0; b < D.s; ++b)
+                acc += dd[(k * D.s + a) * D.s + b] * c[(k * D.Hc + i + D.P - a) * D.Wc + j + D.P - b];
+          img[i * D.W + j] = acc;
+        }
+    };
+    auto apply_Dt_masked = [&](const std::vector<double>& img, std::vector<double>& c) {
+      for (int64_t k = 0; k < D.K; ++k)
+        for (int64_t u = 0; u < D.Hc; ++u)
+          for (int64_t v = 0; v < D.Wc; ++v) {
+            const int64_t l = (k * D.Hc + u) * D.Wc + v;
+            c[l] = msk[l] ? dtr_at(D, &dd[k * D.s * D.s], img.data(), u, v) : 0.0;
+          }
+    };
+    std::vector<double> zfix((size_t)nc), w((size_t)nc), y((size_t)nc), u((size_t)nc, 0.0);
+    for (int64_t l = 0; l < nc; ++l) {
+      zfix[l] = msk[l] ? 0.0 : (double)zn[l];
+      w[l] = y[l] = msk[l] ? (double)zn[l] : 0.0;
+    }
+    std::vector<double> img((size_t)(D.H * D.W)), bimg((size_t)(D.H * D.W));
+    apply_D(zfix, img);
+    for (int64_t q = 0; q < D.H * D.W; ++q) bimg[q] = (double)xn[q] - img[q];  // b = x - D z_fix
+    std::vector<double> atb((size_t)nc), r((size_t)nc), pv((size_t)nc), qv((size_t)nc), tmp((size_t)nc);
+    apply_Dt_masked(bimg, atb);                                                  // A^T b
+    auto apply_op = [&](const std::vector<double>& v, std::vector<double>& out) {  // (A^T A + rho I) v
+      apply_D(v, img);
+      apply_Dt_masked(img, out);
+      for (int64_t l = 0; l < nc; ++l) out[l] = msk[l] ? out[l] + rho * v[l] : 0.0;
+    };
+    for (int it = 0; it < n_admm; ++it) {
+      // CG on (A^T A + rho I) w = A^T b + rho (y - u), warm start at w
+      apply_op(w, tmp);
+      double rr = 0.0;
+      for (int64_t l = 0; l < nc; ++l) {
+        r[l] = msk[l] ? atb[l] + rho * (y[l] - u[l]) - tmp[l] : 0.0;
+        pv[l] = r[l];
+        rr += r[l] * r[l];
+      }
+      for (int c = 0; c < n_cg && rr > 0.0; ++c) {
+        apply_op(pv, qv);
+        double pq = 0.0;
+        for (int64_t l = 0; l < nc; ++l) pq += pv[l] * qv[l];
+        if (!(pq > 0.0)) break;
+        const double a = rr / pq;
+        double rr2 = 0.0;
+        for (int64_t l = 0; l < nc; ++l) {
+          w[l] += a * pv[l];
+          r[l] -= a * qv[l];
+          rr2 += r[l] * r[l];
+        }
+        const double beta = rr2 / rr;
+        for (int64_t l = 0; l < nc; ++l) pv[l] = r[l] + beta * pv[l];
+        rr = rr2;
+      }
+      // over-relaxation, shrinkage, dual update (selected coordinates only)
+      for (int64_t l = 0; l < nc; ++l) {
+        if (!msk[l]) continue;
+        const double wh = alpha * w[l] + (1.0 - alpha) * y[l];
+        const double yn = soft_threshold(wh + u[l], lam / rho);
+        u[l] += wh - yn;
+        y[l] = yn;
+      }
+    }
+    T* zo = z + n * nc;
+    for (int64_t l = 0; l < nc; ++l)
+      if (msk[l]) zo[l] = (T)y[l];
+  }
+}
+
 // g[k,a,b] = sum_n sum_{i,j} r[n,i,j] z[n,k,i+P-a,j+P-b]: the gradient of the
 // Eq.5 fit term 1/2||x - Z d||^2 with r = Z d - x.
 void filter_grad(const Dims& D, const double* r, const double* zd, double* g) {
@@ -378,6 +479,12 @@ double oracle_soft_threshold(double w, double kappa) { return soft_threshold(w, 
                               const T* d, T* z, double lam, double step_z, double p,             \
                               uint64_t seed, uint32_t t, double* tau_used) {                     \
     code_step<T>(Dims(N, K, s, H, W), x, d, z, lam, step_z, p, seed, t, tau_used);              \
+  }                                                                                              \
+  void oracle_admm_code_step_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,          \
+                                   const T* x, const T* d, T* z, double lam, double rho,           \
+                                   double alpha, int n_admm, int n_cg, double p, uint64_t seed,    \
+                                   uint32_t t) {                                                   \
+    admm_code_step<T>(Dims(N, K, s, H, W), x, d, z, lam, rho, alpha, n_admm, n_cg, p, seed, t);   \
   }                                                                                              \
   void oracle_filter_step_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,           \
                                 const T* x, T* d, const T* z, double step_d, double* tau_used,   \
