@@ -114,6 +114,22 @@ csc_status csc_iterate(csc_ctx* ctx, const float* x_host, float* x, float* d, fl
                        float lambda, float step_z, float step_d, double p, uint64_t seed,
                        uint32_t iter, double obj_out[3], float taus_out[2]);
 
+/* ADMM code update of the paper (§3.2), in place of the
+ * one-step prox-gradient csc_code_step.  Per image n, with M = mask(seed, iter, p) (Eq.2),
+ * A = D M^T and b = x_n - D z_n|off M, the selected codes w solve the masked LASSO (Eq.3)
+ *   min_w 1/2||A w - b||^2 + lambda ||w||_1
+ * by n_admm iterations of scaled over-relaxed ADMM started at w = y = z_n[M], u = 0:
+ *   w <- n_cg conjugate-gradient steps (warm start) on (A^T A + rho I) w = A^T b + rho (y - u)
+ *   w^ = alpha w + (1 - alpha) y;  y <- S_{lambda/rho}(w^ + u);  u <- u + w^ - y
+ * and z_n[M] <- y; codes off M are untouched (readings A1-A6).  rho = 0 selects
+ * rho = 10 lambda.  Requires lambda > 0, rho >= 0, 0 < alpha < 2, n_admm >= 1,
+ * n_cg >= 1, 0 < p <= 1.  Rank-local (images are independent).  Scratch (7 code-sized fp32
+ * buffers + mask bits) is allocated on the first call and kept; it is the only call that
+ * allocates, so capture it in a graph only after one warm-up call. */
+csc_status csc_code_step_admm(csc_ctx* ctx, const float* x, const float* d, float* z, float lambda,
+                              float rho, float alpha, int n_admm, int n_cg, double p, uint64_t seed,
+                              uint32_t iter);
+
 /* Forget the residual cache (caller changed x, d or z outside the API). */
 csc_status csc_invalidate(csc_ctx* ctx);
 
@@ -159,7 +175,8 @@ typedef enum {
   CSC_K_MASK = 4,          /* Philox mask generation */
   CSC_K_LIPSCHITZ = 5,     /* DTFT bound */
   CSC_K_SMALL = 6,         /* reductions, step size, update/projection */
-  CSC_K_NCLASS = 7
+  CSC_K_ADMM = 7,          /* ADMM solver: masked D^T and CG / ADMM vector kernels */
+  CSC_K_NCLASS = 8
 } csc_kernel_class;
 
 /* Enable (1) / disable (0) per-launch event timing; enabling resets the totals. */

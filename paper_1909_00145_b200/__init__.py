@@ -28,11 +28,11 @@ ABI_SYMBOLS = (
     "csc_init", "csc_code_step", "csc_filter_step", "csc_objective", "csc_iterate", "csc_invalidate",
     "csc_zero_codes", "csc_destroy", "csc_last_error", "csc_nccl_unique_id", "csc_abi_version",
     "csc_mask_bits", "csc_read_residual", "csc_read_grad", "csc_lipschitz", "csc_launch_count",
-    "csc_profile_enable", "csc_profile_read", "csc_kernel_variants",
+    "csc_profile_enable", "csc_profile_read", "csc_kernel_variants", "csc_code_step_admm",
 )
 
 # csc_kernel_class (include/csc.h)
-KERNEL_CLASSES = ("conv", "conv_finalize", "wgrad", "code_step", "mask", "lipschitz", "small")
+KERNEL_CLASSES = ("conv", "conv_finalize", "wgrad", "code_step", "mask", "lipschitz", "small", "admm")
 
 
 class CSCError(RuntimeError):
@@ -67,6 +67,7 @@ def load_library(path: Optional[str] = None):
         L.csc_init.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(vp)]
         L.csc_code_step.argtypes = [vp, vp, vp, vp, f32, f32, f64, u64, u32, vp]
         L.csc_filter_step.argtypes = [vp, vp, vp, vp, f32, vp]
+        L.csc_code_step_admm.argtypes = [vp, vp, vp, vp, f32, f32, f32, ctypes.c_int, ctypes.c_int, f64, u64, u32]
         L.csc_objective.argtypes = [vp, vp, vp, vp, f32, vp]
         L.csc_iterate.argtypes = [vp, vp, vp, vp, vp, f32, f32, f32, f64, u64, u32, vp, vp]
         L.csc_invalidate.argtypes = [vp]
@@ -159,6 +160,14 @@ class Context:
                                           int(seed) & (2**64 - 1), int(it) & 0xffffffff,
                                           ctypes.byref(out) if want_step else None))
         return float(out.value) if want_step else None
+
+    def code_step_admm(self, x, d, z, lam: float, p: float, seed: int, it: int, rho: float = 0.0,
+                       alpha: float = 1.8, n_admm: int = 10, n_cg: int = 5) -> None:
+        """ADMM masked-LASSO code update (include/csc.h csc_code_step_admm)."""
+        px, pd, pz = self._xdz(x, d, z)
+        self._check(self._L.csc_code_step_admm(self._h, px, pd, pz, float(lam), float(rho), float(alpha),
+                                               int(n_admm), int(n_cg), float(p), int(seed) & (2**64 - 1),
+                                               int(it) & 0xffffffff))
 
     def filter_step(self, x, d, z, step_d: float = 0.0, want_step: bool = False) -> Optional[float]:
         px, pd, pz = self._xdz(x, d, z)

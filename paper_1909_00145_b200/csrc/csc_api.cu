@@ -111,6 +111,12 @@ struct csc_ctx {
   csc::CodeTcPlan ct{};
   uint32_t* mwords = nullptr;  // selection-word mask [4*nkg][Hc*Wc]
   uint32_t* rmax = nullptr;    // max|r| (float bits) for the fp16-split code step
+  // ADMM code solver scratch (csc_admm.cu), allocated by the first csc_code_step_admm
+  float* adm = nullptr;        // 7 code-sized buffers W Y U R PV Q ATB
+  float* adm_e = nullptr;      // image-sized operator output
+  uint32_t* adm_bits = nullptr;
+  double* adm_part = nullptr;  // [N][blocks]
+  double* adm_s = nullptr;     // rr, rr_new, pq  [3][N]
   ncclComm_t comm = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -251,6 +257,23 @@ uint32_t* zbound(csc_ctx* c, const float* z) {
   if (c->smax == nullptr) return nullptr;
   if (c->zmax_ptr != z) c->zmax_known = false;
   return c->zmax_known ? c->smax : nullptr;
+}
+
+// out = D v - x (plain D v when x == nullptr) for a code-shaped v: the dense pass of
+// dense_residual into a caller buffer, without touching the residual cache.
+csc_status dense_apply(csc_ctx* c, const float* x, const float* d, const float* v, float* out, int cls) {
+  const Geom& g = c->g;
+  if (c->tc_on) {
+    CSC_LAUNCH_C(c, cls, 1 + c->tc.nks, conv_tc_any(c, v, d, nullptr));
+    CSC_LAUNCH_C(c, cls, 1, csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, x, out, csc::kConvResidual, c->sq_part, c->st));
+    return CSC_OK;
+  }
+  int nb = 0;
+  CSC_LAUNCH_C(c, cls, 1, csc::launch_conv_fwd(g, v, d, x, out, c->part, c->ksplit, csc::kConvResidual, c->sq_part,
+                                               nullptr, c->st, &nb));
+  if (c->ksplit > 1)
+    CSC_LAUNCH_C(c, cls, 1, csc::launch_conv_finalize(g, c->part, c->ksplit, x, out, csc::kConvResidual, c->sq_part, c->st));
+  return CSC_OK;
 }
 
 bool cache_ok(const csc_ctx* c, const float* x, const float* d, const float* z) {
@@ -526,6 +549,11 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->colw);
   cudaFree(c->mwords);
   cudaFree(c->rmax);
+  cudaFree(c->adm);
+  cudaFree(c->adm_e);
+  cudaFree(c->adm_bits);
+  cudaFree(c->adm_part);
+  cudaFree(c->adm_s);
   cudaFree(c->lip_part);
   cudaFree(c->tc_part);
   cudaFree(c->tc_bimg);
@@ -615,6 +643,78 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
     *step_used = c->h_fscal[kTauZ];
     if (!std::isfinite(*step_used)) return fail(c, CSC_ERR_NONFINITE, "tau_z is not finite");
   }
+  return CSC_OK;
+}
+
+csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float* z, float lambda, float rho,
+                              float alpha, int n_admm, int n_cg, double p, uint64_t seed, uint32_t iter) {
+  csc_status s = check_ptrs(c, x, d, z);
+  if (s != CSC_OK) return s;
+  if (!(lambda > 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and > 0");
+  if (!(rho >= 0.f) || !std::isfinite(rho)) return fail(c, CSC_ERR_ARG, "rho must be finite and >= 0");
+  if (!(alpha > 0.f && alpha < 2.f)) return fail(c, CSC_ERR_ARG, "alpha must be in (0, 2)");
+  if (n_admm < 1 || n_cg < 1) return fail(c, CSC_ERR_ARG, "n_admm and n_cg must be >= 1");
+  if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  if (g.N == 0) return CSC_OK;
+  const int64_t ncode = static_cast<int64_t>(g.N) * g.K * g.Hc * g.Wc;
+  const int64_t nper = static_cast<int64_t>(g.K) * g.Hc * g.Wc;
+  const int nb = csc::admm_blocks_per_image(g);
+  if (c->adm == nullptr) {
+    bool ok = cudaMalloc(reinterpret_cast<void**>(&c->adm), sizeof(float) * 7 * ncode) == cudaSuccess;
+    ok = ok && cudaMalloc(reinterpret_cast<void**>(&c->adm_e), sizeof(float) * n_pix(g)) == cudaSuccess;
+    ok = ok && cudaMalloc(reinterpret_cast<void**>(&c->adm_bits), sizeof(uint32_t) * ((nper + 31) / 32)) == cudaSuccess;
+    ok = ok && cudaMalloc(reinterpret_cast<void**>(&c->adm_part), sizeof(double) * g.N * nb) == cudaSuccess;
+    ok = ok && cudaMalloc(reinterpret_cast<void**>(&c->adm_s), sizeof(double) * 3 * g.N) == cudaSuccess;
+    if (!ok) {
+      cudaFree(c->adm); cudaFree(c->adm_e); cudaFree(c->adm_bits); cudaFree(c->adm_part); cudaFree(c->adm_s);
+      c->adm = c->adm_e = nullptr;
+      c->adm_bits = nullptr;
+      c->adm_part = c->adm_s = nullptr;
+      cudaGetLastError();
+      return fail(c, CSC_ERR_OOM, "ADMM scratch allocation failed");
+    }
+  }
+  float* W = c->adm;
+  float* Y = W + ncode;
+  float* U = Y + ncode;
+  float* R = U + ncode;
+  float* PV = R + ncode;
+  float* Q = PV + ncode;
+  float* ATB = Q + ncode;
+  double* rr = c->adm_s;
+  double* rr_new = rr + g.N;
+  double* pq = rr_new + g.N;
+  const float rh = rho > 0.f ? rho : 10.f * lambda;
+  const float kappa = lambda / rh;
+  const int A = CSC_K_ADMM;
+  const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
+  CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_bits(g, seed, iter, thr, c->adm_bits, c->st));
+  // W = Y = z[M], U = 0, Q <- z off M;  ATB = M D^T (x - D z_off)
+  CSC_LAUNCH_C(c, A, 1, csc::launch_admm_init(g, z, c->adm_bits, W, Y, U, Q, c->st));
+  s = dense_apply(c, x, d, Q, c->adm_e, A);
+  if (s != CSC_OK) return s;
+  CSC_LAUNCH_C(c, A, 1, csc::launch_masked_dtr(g, c->adm_e, d, c->adm_bits, nullptr, 0.f, -1.f, ATB, nullptr, c->st));
+  for (int it = 0; it < n_admm; ++it) {
+    // R = ATB + rho (Y - U) - (A^T A + rho I) W,  PV = R,  rr = |R|^2
+    s = dense_apply(c, nullptr, d, W, c->adm_e, A);
+    if (s != CSC_OK) return s;
+    CSC_LAUNCH_C(c, A, 1, csc::launch_masked_dtr(g, c->adm_e, d, c->adm_bits, W, rh, 1.f, Q, nullptr, c->st));
+    CSC_LAUNCH_C(c, A, 2, csc::launch_cg_start(g, ATB, Y, U, Q, rh, R, PV, c->adm_part, rr, c->st));
+    for (int j = 0; j < n_cg; ++j) {
+      s = dense_apply(c, nullptr, d, PV, c->adm_e, A);
+      if (s != CSC_OK) return s;
+      CSC_LAUNCH_C(c, A, 1, csc::launch_masked_dtr(g, c->adm_e, d, c->adm_bits, PV, rh, 1.f, Q, c->adm_part, c->st));
+      CSC_LAUNCH_C(c, A, 1, csc::launch_image_sum(g, c->adm_part, pq, c->st));
+      CSC_LAUNCH_C(c, A, 2, csc::launch_cg_step(g, rr, pq, W, R, PV, Q, c->adm_part, rr_new, c->st));
+      CSC_LAUNCH_C(c, A, 2, csc::launch_cg_dir(g, rr, rr_new, R, PV, c->st));
+    }
+    CSC_LAUNCH_C(c, A, 1, csc::launch_admm_update(g, c->adm_bits, W, Y, U, alpha, kappa, c->st));
+  }
+  CSC_LAUNCH_C(c, A, 1, csc::launch_admm_finish(g, c->adm_bits, Y, z, nullptr, c->st));
+  c->cache_valid = false;  // r no longer matches z
+  c->zmax_known = false;   // the fp16 dense pass re-derives max|z| (T6)
   return CSC_OK;
 }
 

@@ -36,6 +36,7 @@ inline bool filter_size_supported(int s) {
 }
 
 // All launchers return cudaGetLastError() of their launch.
+// kConvResidual: out = y - x (plain y when x == nullptr); kConvSumSq: only sum y^2.
 enum ConvMode : int { kConvResidual = 0, kConvSumSq = 1 };
 
 // y = sum_{k in [k0,k1)} f_k * z_k (valid true convolution) for all images.
@@ -163,5 +164,24 @@ cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, co
 // words == nullptr: every code selected (p = 1).
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                            const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st);
+
+// ADMM masked-LASSO code solver (csc_admm.cu): grid (admm_blocks_per_image, N); `part` holds
+// N * admm_blocks_per_image doubles; per-image scalars rr / rr_new / pq are N doubles.
+int admm_blocks_per_image(const Geom& g);
+cudaError_t launch_masked_dtr(const Geom& g, const float* e, const float* d, const uint32_t* bits, const float* v,
+                              float rho, float sign, float* out, double* part, cudaStream_t st);
+cudaError_t launch_admm_init(const Geom& g, const float* z, const uint32_t* bits, float* W, float* Y, float* U,
+                             float* Zf, cudaStream_t st);
+cudaError_t launch_cg_start(const Geom& g, const float* ATB, const float* Y, const float* U, const float* Q,
+                            float rho, float* R, float* PV, double* part, double* rr, cudaStream_t st);
+cudaError_t launch_image_sum(const Geom& g, const double* part, double* out, cudaStream_t st);
+cudaError_t launch_cg_step(const Geom& g, const double* rr, const double* pq, float* W, float* R, const float* PV,
+                           const float* Q, double* part, double* rr_new, cudaStream_t st);
+cudaError_t launch_cg_dir(const Geom& g, double* rr, const double* rr_new, const float* R, float* PV,
+                          cudaStream_t st);
+cudaError_t launch_admm_update(const Geom& g, const uint32_t* bits, const float* W, float* Y, float* U, float alpha,
+                               float kappa, cudaStream_t st);
+cudaError_t launch_admm_finish(const Geom& g, const uint32_t* bits, const float* Y, float* z, uint32_t* zmax,
+                               cudaStream_t st);
 
 }  // namespace csc

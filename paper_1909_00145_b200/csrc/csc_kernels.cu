@@ -294,7 +294,7 @@ conv_fwd_kernel(const float* __restrict__ z, const float* __restrict__ filt, con
         const int64_t idx = img + static_cast<int64_t>(i) * g.W + j;
         float v = acc[r_][c];
         if (mode == kConvResidual) {
-          v = v - x[idx];
+          if (x != nullptr) v = v - x[idx];
           out[idx] = v;
         }
         sq += static_cast<double>(v) * static_cast<double>(v);
@@ -330,7 +330,7 @@ __global__ void conv_finalize_kernel(const float* __restrict__ part, int ksplit,
     float v = 0.f;
     for (int ks = 0; ks < ksplit; ++ks) v += part[ks * npix + idx];
     if (mode == kConvResidual) {
-      v = v - x[idx];
+      if (x != nullptr) v = v - x[idx];
       r[idx] = v;
     }
     sq += static_cast<double>(v) * static_cast<double>(v);

@@ -550,7 +550,7 @@ __global__ void tc_fixup_kernel(const float* __restrict__ part, int N, int H, in
       float v = 0.f;
       for (int b = b0; b <= b1; ++b) v += pk[b * win + static_cast<size_t>(i - b * BR + P) * W + j];
       if (mode == kConvResidual) {
-        v = v - x[orow + j];
+        if (x != nullptr) v = v - x[orow + j];
         r[orow + j] = v;
       }
       sq += static_cast<double>(v) * static_cast<double>(v);

@@ -1,0 +1,106 @@
+"""GPU parity of the ADMM masked-LASSO code solver (
+include/csc.h csc_code_step_admm) against oracle.admm_code_step (pinned in tests/test_oracle_admm.py).
+
+Bar: codes within TOL_ADMM relative (norm-wise, reading R9) after one step of 10 ADMM x 5 CG
+iterations; codes off the mask bit-identical (R2).  TOL_ADMM is derived in DESIGN.md A7: the
+operator runs through the same dense pass as the hot path (relative ~1e-6 per application), and
+CG amplifies the per-application error by at most the condition number of A^T A + rho I over
+the 60 applications, which rho = 10 lambda keeps small.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import random_problem
+from tests.conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL_ADMM = 1e-5
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+    from paper_1909_00145_b200 import build as b
+    b.build()
+    torch.cuda.set_device(0)
+    return torch.device("cuda:0")
+
+
+def _t(a, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+SHAPES = [((3, 5, 5, 70, 130), 0.1), ((2, 17, 11, 100, 100), 0.2), ((4, 8, 5, 32, 32), 1.0),
+          ((1, 9, 3, 33, 47), 0.5), ((2, 4, 11, 11, 11), 0.05), ((2, 130, 7, 20, 300), 0.1),
+          ((1, 100, 11, 40, 11), 0.3)]
+
+
+@pytest.mark.parametrize("dense", ["half", "simt"])
+@pytest.mark.parametrize("shape,p", SHAPES)
+def test_admm_code_step_parity(torch_dev, shape, p, dense, monkeypatch):
+    import torch
+    import paper_1909_00145_b200 as pkg
+    if dense == "simt":
+        monkeypatch.setenv("CSC_DENSE_PATH", "simt")
+    N, K, s, H, W = shape
+    x, d, z = random_problem(300 + K, N, K, s, H, W, code_density=0.3)
+    seed, it, lam = 777, 5, 0.2
+    ctx = pkg.Context(N, K, s, H, W, device=0)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    ctx.code_step_admm(xt, dt, zt, lam, p, seed, it)
+    torch.cuda.synchronize()
+    zg = zt.cpu().numpy()
+    zo = oracle.admm_code_step(x, d, z, lam, p, seed, it, dtype=np.float64)
+    err = rel_err(zg, zo)
+    print(f"admm {shape} p={p} {dense}: rel err {err:.3e}")
+    assert err < TOL_ADMM, err
+    Hc, Wc = H + s - 1, W + s - 1
+    m = oracle.unpack_mask(oracle.mask_bits(K, Hc, Wc, p, seed, it), K, Hc, Wc)
+    for n in range(N):
+        assert np.array_equal(zg[n][~m], z[n][~m])
+    ctx.close()
+
+
+def test_admm_parameters_and_objective(torch_dev):
+    """Explicit rho / alpha / iteration counts reach the oracle's result; a run followed by the
+    hot path's objective matches the oracle's objective of the oracle's codes."""
+    import torch
+    import paper_1909_00145_b200 as pkg
+    N, K, s, H, W = 2, 12, 7, 60, 52
+    x, d, z = random_problem(41, N, K, s, H, W, code_density=0.2)
+    ctx = pkg.Context(N, K, s, H, W, device=0)
+    xt, dt = _t(x, torch_dev), _t(d, torch_dev)
+    for rho, alpha, na, nc in [(0.5, 1.0, 3, 2), (4.0, 1.5, 7, 8), (0.0, 1.8, 1, 1)]:
+        zt = _t(z, torch_dev)
+        ctx.invalidate()
+        ctx.code_step_admm(xt, dt, zt, 0.3, 0.4, 9, 2, rho=rho, alpha=alpha, n_admm=na, n_cg=nc)
+        zo = oracle.admm_code_step(x, d, z, 0.3, 0.4, 9, 2, rho=(rho or None), alpha=alpha, n_admm=na, n_cg=nc,
+                                   dtype=np.float64)
+        torch.cuda.synchronize()
+        err = rel_err(zt.cpu().numpy(), zo)
+        print(f"admm rho={rho} alpha={alpha} {na}x{nc}: rel err {err:.3e}")
+        assert err < TOL_ADMM, err
+    F = ctx.objective(xt, dt, zt, 0.3)
+    Fo = oracle.objective(x, d, zo, 0.3, dtype=np.float64)
+    assert abs(F[0] - Fo[0]) <= TOL_ADMM * Fo[0]
+    ctx.close()
+
+
+def test_admm_argument_errors(torch_dev):
+    import paper_1909_00145_b200 as pkg
+    N, K, s, H, W = 1, 2, 3, 8, 8
+    x, d, z = random_problem(1, N, K, s, H, W)
+    ctx = pkg.Context(N, K, s, H, W, device=0)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    for kw in [dict(lam=0.0), dict(alpha=2.0), dict(alpha=0.0), dict(n_admm=0), dict(n_cg=0), dict(p=0.0),
+               dict(rho=-1.0)]:
+        args = dict(lam=0.1, p=0.5, alpha=1.8, n_admm=10, n_cg=5, rho=0.0)
+        args.update(kw)
+        with pytest.raises(pkg.CSCError):
+            ctx.code_step_admm(xt, dt, zt, args["lam"], args["p"], 1, 1, rho=args["rho"], alpha=args["alpha"],
+                               n_admm=args["n_admm"], n_cg=args["n_cg"])
+    assert np.array_equal(zt.cpu().numpy(), z)
+    ctx.close()
