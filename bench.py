@@ -67,7 +67,7 @@ def _traffic():
         return {}
 
 
-def kernel_rooflines(prof, cfg, nl, steps, variants):
+def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox"):
     """Per kernel class: algorithmic work per launch / measured average launch time vs its roofs.
     Algorithmic units: dense pass / filter gradient 2*N*K*s^2*H*W FLOP and a read of
     all codes (4*N*K*Hc*Wc B); masked code step: sector-model bytes.  Tensor peaks: the measured
@@ -117,6 +117,27 @@ def kernel_rooflines(prof, cfg, nl, steps, variants):
             out[name] = {"kernel": "wgrad_kernel (SIMT FP32)", "bound": "alu",
                          "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
                          "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
+        elif name == "code_step" and solver == "admm":
+            # ADMM mode: code_h_kernel in plain mode writes the dense correlation D^T e
+            out[name] = two_roofs("code_h_kernel plain mode (dense D^T e for the ADMM operator)", avg,
+                                  bf16_tflops / 3.0, f"{kind} bf16/fp16 {bf16_tflops:.0f} TF/s / 3 products")
+            for rr_ in (out[name], out[name]["other_roof"]):
+                if rr_["bound"] == "hbm":
+                    rr_["bytes_model"] = "4 N K Hc Wc (dense correlation written once)"
+        elif name == "admm":
+            # vector / gather / expansion kernels of one ADMM step (10 x 5 CG), bytes per step:
+            # 50 expansions (4C dense write + 12 Mc), 51 gathers (sector-model read of C + 8 Mc),
+            # 50 CG steps (24 Mc), 10 updates (28 Mc), init + final scatter (2 x (sector C + 8 Mc))
+            mcn = cfg.p * codes
+            sect = 4.0 * (1.0 - (1.0 - cfg.p) ** 8) * codes
+            step_bytes = (50 * (4.0 * codes + 12 * mcn) + 51 * (sect + 8 * mcn) + 50 * 24 * mcn + 10 * 28 * mcn
+                          + 2 * (sect + 8 * mcn))
+            per_step_ms = ms / steps
+            out[name] = {"kernel": "ADMM vector kernels (expand, gather, cg_step, update; csc_admm.cu)",
+                         "bound": "hbm", "achieved": step_bytes / (per_step_ms / 1e3) / 1e9, "peak": hbm_gbs,
+                         "unit": "GB/s", "peak_note": f"{kind} copy bandwidth (MEASURED_PEAKS.json)",
+                         "bytes_model": "per step: 50(4C+12Mc) + 51(4C(1-(1-p)^8)+8Mc) + 1200Mc + 280Mc + 2(...)"
+                                        ", C = N K Hc Wc, Mc = p C; achieved = model bytes / class time per step"}
         elif name == "code_step":
             sector_bytes = 8.0 * (1.0 - (1.0 - cfg.p) ** 8) * codes + 12.0 * nl * cfg.H * cfg.W
             out[name] = {"kernel": ("code_h_kernel (tcgen05 kind::f16 3-term split, dense-then-mask, TMA code slices)" if variants & 32 else "code_tc_kernel (tcgen05 3xTF32 dense-then-mask)") if variants & 4
@@ -300,10 +321,24 @@ def run_ours(args):
         if ws > 1:
             dist.barrier(device_ids=[local])
 
+    admm = args.code_solver == "admm"
+
+    def step(it, x_host=None):
+        """One outer iteration: csc_iterate (prox code step), or with --code-solver admm the paper's
+        ADMM code update (csc_code_step_admm) followed by the filter step and the objective."""
+        if not admm:
+            return ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it, x_host=x_host)
+        if x_host is not None:
+            x.copy_(x_host, non_blocking=True)
+            ctx.invalidate()
+        ctx.code_step_admm(x, d, z, cfg.lam, cfg.p, seed, it)
+        ctx.filter_step(x, d, z)
+        return ctx.objective(x, d, z, cfg.lam), None
+
     it = 0
     for _ in range(args.warmup):
         it += 1
-        ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it)
+        step(it)
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident inputs
@@ -322,7 +357,7 @@ def run_ours(args):
         if l2_flush is not None:
             l2_flush.fill_(float(it))
         ev0.record(stream)
-        obj, taus = ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it)
+        obj, taus = step(it)
         ev1.record(stream)
         ev1.synchronize()
         t_total += ev0.elapsed_time(ev1)
@@ -350,7 +385,7 @@ def run_ours(args):
             l2_flush.fill_(float(it))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it, x_host=x_host)
+        step(it, x_host=x_host)
         e2e_ms += (time.perf_counter() - t0) * 1e3
     te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -359,7 +394,7 @@ def run_ours(args):
 
     if rank == 0:
         step_ms = t_ms / args.steps
-        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.variants)
+        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.variants, args.code_solver)
         dom = max(rl, key=lambda k: rl[k]["ms_per_step"])
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                        "share": v[0] / max(t_total, 1e-9)} for k, v in prof.items()}
@@ -367,7 +402,7 @@ def run_ours(args):
             "metric": "csc_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": _config_dict(cfg, ws),
+            "config": dict(_config_dict(cfg, ws), code_solver=args.code_solver),
             "roofline": dict(rl[dom], dominant_class=dom),
             "kernel_rooflines": rl,
             "kernels": kernels,
@@ -396,6 +431,9 @@ def main():
     ap.add_argument("--ref-images", type=int, default=1)
     ap.add_argument("--cpu-images", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--code-solver", default="prox", choices=["prox", "admm"],
+                    help="prox: the north_star masked prox-gradient step (default); admm: the paper's ADMM "
+                         "code update (SURVEY.md §8f NEXT-1), 10 x 5 CG iterations")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -13,12 +13,14 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 using csc::Geom;
@@ -112,11 +114,22 @@ struct csc_ctx {
   uint32_t* mwords = nullptr;  // selection-word mask [4*nkg][Hc*Wc]
   uint32_t* rmax = nullptr;    // max|r| (float bits) for the fp16-split code step
   // ADMM code solver scratch (csc_admm.cu), allocated by the first csc_code_step_admm
-  float* adm = nullptr;        // 7 code-sized buffers W Y U R PV Q ATB
-  float* adm_e = nullptr;      // image-sized operator output
-  uint32_t* adm_bits = nullptr;
-  double* adm_part = nullptr;  // [N][blocks]
-  double* adm_s = nullptr;     // rr, rr_new, pq  [3][N]
+  float* adm_zd = nullptr;      // [N][K][Hc][Wc] scatter target of the operator (0 off the mask)
+  float* adm_e = nullptr;       // [N][H][W] operator output
+  float* adm_cd = nullptr;      // [N][K][Hc][Wc] dense D^T e of the tensor-core correlation
+  uint32_t* adm_bits = nullptr; // canonical mask bits
+  uint32_t* adm_idx = nullptr;  // selected positions [K*Hc*Wc]
+  uint32_t* adm_woff = nullptr; // set bits before each mask word
+  uint32_t* adm_cnt = nullptr;
+  uint64_t* adm_off = nullptr;
+  uint64_t* adm_row = nullptr;  // row offsets [K*Hc + 1]
+  uint64_t* adm_mc = nullptr;   // device count + pinned host mirror
+  uint64_t* h_adm_mc = nullptr;
+  uint32_t* adm_bound = nullptr;
+  double* adm_part = nullptr;   // [2][N][blocks]
+  double* adm_s = nullptr;      // per-image CG scalars [2][N]
+  float* adm_vec = nullptr;     // 7 compact vectors W Y U R PV Q ATB [N][cap]
+  int64_t adm_cap = 0;
   ncclComm_t comm = nullptr;
   uint64_t launches = 0;
   std::string err;
@@ -200,6 +213,7 @@ cudaError_t conv_tc_any(csc_ctx* c, const float* z, const float* filt, double* l
     if (!c->zmax_known || c->zmax_ptr != z) {
       cudaError_t e = csc::launch_absmax(z, static_cast<int64_t>(c->g.N) * c->g.K * c->g.Hc * c->g.Wc, c->smax, c->st);
       if (e != cudaSuccess) return e;
+      c->launches += 1;
       c->zmax_known = true;
       c->zmax_ptr = z;
     }
@@ -261,18 +275,20 @@ uint32_t* zbound(csc_ctx* c, const float* z) {
 
 // out = D v - x (plain D v when x == nullptr) for a code-shaped v: the dense pass of
 // dense_residual into a caller buffer, without touching the residual cache.
-csc_status dense_apply(csc_ctx* c, const float* x, const float* d, const float* v, float* out, int cls) {
+csc_status dense_apply(csc_ctx* c, const float* x, const float* d, const float* v, float* out) {
   const Geom& g = c->g;
   if (c->tc_on) {
-    CSC_LAUNCH_C(c, cls, 1 + c->tc.nks, conv_tc_any(c, v, d, nullptr));
-    CSC_LAUNCH_C(c, cls, 1, csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, x, out, csc::kConvResidual, c->sq_part, c->st));
+    CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, v, d, nullptr));
+    CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
+                 csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, x, out, csc::kConvResidual, c->sq_part, c->st));
     return CSC_OK;
   }
   int nb = 0;
-  CSC_LAUNCH_C(c, cls, 1, csc::launch_conv_fwd(g, v, d, x, out, c->part, c->ksplit, csc::kConvResidual, c->sq_part,
-                                               nullptr, c->st, &nb));
+  CSC_LAUNCH_C(c, CSC_K_CONV, 1, csc::launch_conv_fwd(g, v, d, x, out, c->part, c->ksplit, csc::kConvResidual,
+                                                      c->sq_part, nullptr, c->st, &nb));
   if (c->ksplit > 1)
-    CSC_LAUNCH_C(c, cls, 1, csc::launch_conv_finalize(g, c->part, c->ksplit, x, out, csc::kConvResidual, c->sq_part, c->st));
+    CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
+                 csc::launch_conv_finalize(g, c->part, c->ksplit, x, out, csc::kConvResidual, c->sq_part, c->st));
   return CSC_OK;
 }
 
@@ -549,11 +565,21 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->colw);
   cudaFree(c->mwords);
   cudaFree(c->rmax);
-  cudaFree(c->adm);
+  cudaFree(c->adm_zd);
   cudaFree(c->adm_e);
+  cudaFree(c->adm_cd);
   cudaFree(c->adm_bits);
+  cudaFree(c->adm_idx);
+  cudaFree(c->adm_woff);
+  cudaFree(c->adm_cnt);
+  cudaFree(c->adm_off);
+  cudaFree(c->adm_mc);
+  cudaFree(c->adm_row);
+  cudaFreeHost(c->h_adm_mc);
+  cudaFree(c->adm_bound);
   cudaFree(c->adm_part);
   cudaFree(c->adm_s);
+  cudaFree(c->adm_vec);
   cudaFree(c->lip_part);
   cudaFree(c->tc_part);
   cudaFree(c->tc_bimg);
@@ -658,63 +684,164 @@ csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float*
   CSC_CUDA(c, cudaSetDevice(c->device));
   const Geom& g = c->g;
   if (g.N == 0) return CSC_OK;
-  const int64_t ncode = static_cast<int64_t>(g.N) * g.K * g.Hc * g.Wc;
   const int64_t nper = static_cast<int64_t>(g.K) * g.Hc * g.Wc;
-  const int nb = csc::admm_blocks_per_image(g);
-  if (c->adm == nullptr) {
-    bool ok = cudaMalloc(reinterpret_cast<void**>(&c->adm), sizeof(float) * 7 * ncode) == cudaSuccess;
-    ok = ok && cudaMalloc(reinterpret_cast<void**>(&c->adm_e), sizeof(float) * n_pix(g)) == cudaSuccess;
-    ok = ok && cudaMalloc(reinterpret_cast<void**>(&c->adm_bits), sizeof(uint32_t) * ((nper + 31) / 32)) == cudaSuccess;
-    ok = ok && cudaMalloc(reinterpret_cast<void**>(&c->adm_part), sizeof(double) * g.N * nb) == cudaSuccess;
-    ok = ok && cudaMalloc(reinterpret_cast<void**>(&c->adm_s), sizeof(double) * 3 * g.N) == cudaSuccess;
+  const int64_t ncode = static_cast<int64_t>(g.N) * nper;
+  const int nbmax = std::max(csc::admm_blocks(g, (nper + 3) / 4 * 4), csc::admm_dtr_blocks(g));
+  if (c->adm_zd == nullptr) {
+    auto al = [](void** q, size_t bytes) { return cudaMalloc(q, bytes < 16 ? 16 : bytes) == cudaSuccess; };
+    bool ok = al(reinterpret_cast<void**>(&c->adm_zd), sizeof(float) * ncode);
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_e), sizeof(float) * n_pix(g));
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_bits), sizeof(uint32_t) * ((nper + 31) / 32));
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_idx), sizeof(uint32_t) * nper);
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_woff), sizeof(uint32_t) * ((nper + 31) / 32));
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_cnt), sizeof(uint32_t) * csc::admm_idx_blocks(g));
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_off), sizeof(uint64_t) * csc::admm_idx_blocks(g));
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_mc), sizeof(uint64_t));
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_row), sizeof(uint64_t) * (static_cast<int64_t>(g.K) * g.Hc + 1));
+    ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_adm_mc), sizeof(uint64_t)) == cudaSuccess;
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_bound), sizeof(uint32_t) * 4);
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_part), sizeof(double) * 2 * g.N * nbmax);
+    ok = ok && al(reinterpret_cast<void**>(&c->adm_s), sizeof(double) * 2 * g.N);
     if (!ok) {
-      cudaFree(c->adm); cudaFree(c->adm_e); cudaFree(c->adm_bits); cudaFree(c->adm_part); cudaFree(c->adm_s);
-      c->adm = c->adm_e = nullptr;
-      c->adm_bits = nullptr;
-      c->adm_part = c->adm_s = nullptr;
       cudaGetLastError();
       return fail(c, CSC_ERR_OOM, "ADMM scratch allocation failed");
     }
   }
-  float* W = c->adm;
-  float* Y = W + ncode;
-  float* U = Y + ncode;
-  float* R = U + ncode;
-  float* PV = R + ncode;
-  float* Q = PV + ncode;
-  float* ATB = Q + ncode;
-  double* rr = c->adm_s;
-  double* rr_new = rr + g.N;
-  double* pq = rr_new + g.N;
+  // the selected positions of M^t (shared by every image), compacted; their count sizes the vectors
+  const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
+  CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_bits(g, seed, iter, thr, c->adm_bits, c->st));
+  CSC_LAUNCH_C(c, CSC_K_ADMM, 3, csc::launch_admm_index(g, c->adm_bits, c->adm_cnt, c->adm_off, c->adm_mc,
+                                                        c->adm_idx, c->adm_woff, c->st));
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_adm_mc, c->adm_mc, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  const int64_t mc = static_cast<int64_t>(*c->h_adm_mc);
+  if (mc == 0) return CSC_OK;
+  const int64_t ms = (mc + 3) / 4 * 4;
+  if (ms > c->adm_cap) {
+    cudaFree(c->adm_vec);
+    c->adm_vec = nullptr;
+    c->adm_cap = 0;
+    int64_t cap = (ms + ms / 8 + 3) / 4 * 4;
+    if (cap > (nper + 3) / 4 * 4) cap = (nper + 3) / 4 * 4;
+    if (cudaMalloc(reinterpret_cast<void**>(&c->adm_vec), sizeof(float) * 7 * g.N * cap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, CSC_ERR_OOM, "ADMM vector allocation failed");
+    }
+    c->adm_cap = cap;
+  }
+  CSC_LAUNCH_C(c, CSC_K_ADMM, 1, csc::launch_admm_row_off(g, c->adm_idx, mc, c->adm_row, c->st));
+  // r = D z - x (the hot path's residual cache when it is valid)
+  const bool zero_ok = c->cache_valid && c->cd == nullptr && c->cx == x && c->cz == z;
+  if (!zero_ok && !cache_ok(c, x, d, z)) {
+    s = dense_residual(c, x, d, z, false);
+    if (s != CSC_OK) return s;
+  }
+  const int64_t cv = static_cast<int64_t>(g.N) * ms;
+  float* W = c->adm_vec;
+  float* Y = W + cv;
+  float* U = Y + cv;
+  float* R = U + cv;
+  float* PV = R + cv;
+  float* Q = PV + cv;
+  float* ATB = Q + cv;  // explicit-residual mode only
+  double* part_a = c->adm_part;  // <PV, Q> partials [N][admm_dtr_blocks] (masked_dtr blocks)
+  double* part_b = part_a + static_cast<int64_t>(g.N) * nbmax;
+  double* rr_cur = c->adm_s;
+  double* rr_oth = rr_cur + g.N;
   const float rh = rho > 0.f ? rho : 10.f * lambda;
   const float kappa = lambda / rh;
   const int A = CSC_K_ADMM;
-  const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
-  CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_bits(g, seed, iter, thr, c->adm_bits, c->st));
-  // W = Y = z[M], U = 0, Q <- z off M;  ATB = M D^T (x - D z_off)
-  CSC_LAUNCH_C(c, A, 1, csc::launch_admm_init(g, z, c->adm_bits, W, Y, U, Q, c->st));
-  s = dense_apply(c, x, d, Q, c->adm_e, A);
-  if (s != CSC_OK) return s;
-  CSC_LAUNCH_C(c, A, 1, csc::launch_masked_dtr(g, c->adm_e, d, c->adm_bits, nullptr, 0.f, -1.f, ATB, nullptr, c->st));
-  for (int it = 0; it < n_admm; ++it) {
-    // R = ATB + rho (Y - U) - (A^T A + rho I) W,  PV = R,  rr = |R|^2
-    s = dense_apply(c, nullptr, d, W, c->adm_e, A);
-    if (s != CSC_OK) return s;
-    CSC_LAUNCH_C(c, A, 1, csc::launch_masked_dtr(g, c->adm_e, d, c->adm_bits, W, rh, 1.f, Q, nullptr, c->st));
-    CSC_LAUNCH_C(c, A, 2, csc::launch_cg_start(g, ATB, Y, U, Q, rh, R, PV, c->adm_part, rr, c->st));
-    for (int j = 0; j < n_cg; ++j) {
-      s = dense_apply(c, nullptr, d, PV, c->adm_e, A);
-      if (s != CSC_OK) return s;
-      CSC_LAUNCH_C(c, A, 1, csc::launch_masked_dtr(g, c->adm_e, d, c->adm_bits, PV, rh, 1.f, Q, c->adm_part, c->st));
-      CSC_LAUNCH_C(c, A, 1, csc::launch_image_sum(g, c->adm_part, pq, c->st));
-      CSC_LAUNCH_C(c, A, 2, csc::launch_cg_step(g, rr, pq, W, R, PV, Q, c->adm_part, rr_new, c->st));
-      CSC_LAUNCH_C(c, A, 2, csc::launch_cg_dir(g, rr, rr_new, R, PV, c->st));
+  bool first_conv = true;
+  // A^T on the tensor cores (code_h in plain mode: dense D^T e, then a gather of the selected
+  // codes) when the fp16-split code step is planned; else the SIMT masked gather-correlation.
+  const char* dev = std::getenv("CSC_ADMM_DTR");
+  const bool tc_dtr = c->ct_on && c->ct.half && !(dev != nullptr && std::string(dev) == "simt");
+  if (tc_dtr && c->adm_cd == nullptr) {
+    if (cudaMalloc(reinterpret_cast<void**>(&c->adm_cd), sizeof(float) * ncode) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, CSC_ERR_OOM, "ADMM correlation buffer allocation failed");
     }
-    CSC_LAUNCH_C(c, A, 1, csc::launch_admm_update(g, c->adm_bits, W, Y, U, alpha, kappa, c->st));
   }
-  CSC_LAUNCH_C(c, A, 1, csc::launch_admm_finish(g, c->adm_bits, Y, z, nullptr, c->st));
+  const int nb_pq = tc_dtr ? csc::admm_blocks(g, ms) : csc::admm_dtr_blocks(g);
+  float* E = c->adm_e;
+  // all vectors (and their pads) start at 0: U = 0, and the pads stay 0 throughout
+  CSC_CUDA(c, cudaMemsetAsync(c->adm_vec, 0, sizeof(float) * 7 * cv, c->st));
+  // E = A v for the vector just expanded into Zd (max|v| in adm_bound[0] for the fp16 split)
+  auto apply = [&]() -> csc_status {
+    if (c->tc_on && c->tc.half) {
+      CSC_LAUNCH_C(c, CSC_K_CONV, (first_conv ? 1 : 0) + c->tc.nks,
+                   csc::launch_conv_h(g, c->tc, c->adm_zd, d, c->tc_bimg, c->adm_bound, c->smax + 1, c->tc_part,
+                                      nullptr, c->st, first_conv));
+      CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
+                   csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, E, csc::kConvResidual, c->sq_part, c->st));
+      first_conv = false;
+      return CSC_OK;
+    }
+    return dense_apply(c, nullptr, d, c->adm_zd, E);
+  };
+  // out = M D^T e (+ rho v and the <v, out> partials when v != null)
+  auto dtr = [&](const float* e, const float* v, float* out, double* part, float sign) -> csc_status {
+    if (tc_dtr) {
+      CSC_LAUNCH(c, 1, csc::launch_absmax(e, n_pix(g), c->adm_bound + 1, c->st));
+      CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
+                   csc::launch_code_h(g, c->ct, e, d, c->adm_cd, nullptr, nullptr, 0.f, c->adm_bound + 1, nullptr,
+                                      c->st, true));
+      CSC_LAUNCH_C(c, CSC_K_ADMM, 1, csc::launch_admm_gather(g, c->adm_idx, mc, ms, c->adm_cd, v, rh, sign, out, part,
+                                                             c->st));
+      return CSC_OK;
+    }
+    CSC_LAUNCH_C(c, CSC_K_ADMM, 1, csc::launch_masked_dtr(g, c->adm_idx, c->adm_row, ms, e, d, v, rh, sign, out,
+                                                          part, c->st));
+    return CSC_OK;
+  };
+  CSC_LAUNCH_C(c, A, 1, csc::launch_admm_init(g, c->adm_idx, mc, ms, z, W, Y, c->st));
+  // CG residual of the first right-hand side, R = ATB + rho (Y - U) - (A^T A + rho I) W with
+  // W = Y = w0, U = 0:  R = A^T (b - A w0) = -M D^T r  (b - A w0 = x - D z = -r; A4)
+  s = dtr(c->r, nullptr, R, nullptr, -1.f);
+  if (s != CSC_OK) return s;
+  CSC_LAUNCH_C(c, A, 2, csc::launch_sumsq(g, ms, R, part_b, rr_cur, c->st));
+  // CSC_ADMM_RESID=explicit: recompute R = ATB + rho (Y - U) - (A^T A + rho I) W at every outer
+  // iteration as the oracle does (one more operator application each), instead of carrying it.
+  const char* rev = std::getenv("CSC_ADMM_RESID");
+  const bool explicit_r = rev != nullptr && std::string(rev) == "explicit";
+  auto q_of_w = [&]() -> csc_status {  // Q = (A^T A + rho I) W
+    CSC_CUDA(c, cudaMemsetAsync(c->adm_bound, 0, sizeof(uint32_t), c->st));
+    CSC_LAUNCH_C(c, A, 1, csc::launch_admm_expand(g, c->adm_bits, c->adm_woff, ms, W, nullptr, nullptr, nullptr,
+                                                  c->adm_zd, c->adm_bound, c->st));
+    csc_status s2 = apply();
+    if (s2 != CSC_OK) return s2;
+    return dtr(E, W, Q, nullptr, 1.f);
+  };
+  if (explicit_r) {
+    s = q_of_w();
+    if (s != CSC_OK) return s;
+    CSC_LAUNCH_C(c, A, 2, csc::launch_cg_resid(g, ms, ATB, Y, U, Q, rh, R, part_b, rr_cur, true, c->st));
+  }
+  for (int it = 0; it < n_admm; ++it) {
+    if (explicit_r && it > 0) {
+      s = q_of_w();
+      if (s != CSC_OK) return s;
+      CSC_LAUNCH_C(c, A, 2, csc::launch_cg_resid(g, ms, ATB, Y, U, Q, rh, R, part_b, rr_cur, false, c->st));
+    }
+    for (int j = 0; j < n_cg; ++j) {
+      // PV = R + (rr / rr_prev) PV  (PV = R first), expanded into Zd
+      CSC_CUDA(c, cudaMemsetAsync(c->adm_bound, 0, sizeof(uint32_t), c->st));
+      CSC_LAUNCH_C(c, A, 1, csc::launch_admm_expand(g, c->adm_bits, c->adm_woff, ms, R, PV, j == 0 ? nullptr : rr_oth,
+                                                    rr_cur, c->adm_zd, c->adm_bound, c->st));
+      s = apply();
+      if (s != CSC_OK) return s;
+      // Q = (A^T A + rho I) PV, part_a = <PV, Q>;  alpha_cg = rr / <PV,Q>;  W, R update; rr_new
+      s = dtr(E, PV, Q, part_a, 1.f);
+      if (s != CSC_OK) return s;
+      CSC_LAUNCH_C(c, A, 2, csc::launch_cg_step(g, ms, rr_cur, part_a, nb_pq, W, R, PV, Q, part_b, rr_oth, c->st));
+      std::swap(rr_cur, rr_oth);  // rr_cur = new |R|^2, rr_oth = previous
+    }
+    // y, u update; R carried to the next right-hand side, rr_cur = |R|^2
+    CSC_LAUNCH_C(c, A, 2, csc::launch_admm_update(g, ms, W, Y, U, R, alpha, kappa, rh, part_b, rr_cur, c->st));
+  }
+  // z[M] = y; off-mask codes untouched.  The max|z| bound of the fp16 dense pass is raised.
+  CSC_LAUNCH_C(c, A, 1, csc::launch_admm_scatter(g, c->adm_idx, mc, ms, Y, z, zbound(c, z), c->st));
   c->cache_valid = false;  // r no longer matches z
-  c->zmax_known = false;   // the fp16 dense pass re-derives max|z| (T6)
   return CSC_OK;
 }
 

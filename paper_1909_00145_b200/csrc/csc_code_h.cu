@@ -77,6 +77,7 @@ struct ChArgs {
   int L, nseg, nitems;
   int pitch, rs_rows, rs_floats;
   int b_bytes;           // one of hi / lo: 2 K-atoms x Npad rows x 128 B
+  int plain;             // 1: z <- c at every position (no z read, no step / shrinkage / mask)
 };
 
 struct ChItem {
@@ -286,7 +287,8 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
     const int q = warp & 3;
     const int cb = ew >> 2;            // filter block of NC
     const uint32_t tq = (static_cast<uint32_t>(32 * q) << 16);
-    const float tau = *A.tau;
+    const bool plain = A.plain != 0;
+    const float tau = plain ? 0.f : *A.tau;
     const float kappa = tau * A.lam;
     const float inv = exp2i_h(-(er + ed));
     const size_t plane = static_cast<size_t>(A.Hc) * A.Wc;
@@ -303,7 +305,7 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
       }
     };
     auto issue = [&](int item, int tl, int b) {  // TMA {32 positions, NC planes} of tile (item, tl)
-      if (item >= A.nitems || lane != 0) return;
+      if (plain || item >= A.nitems || lane != 0) return;
       const ChItem it = ch_item(A, item);
       const int pw = it.p0 + tl * kChTile + 32 * q;
       mbar_arrive_expect_tx(&z_full[ew][b], zbytes);
@@ -327,7 +329,7 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
                                              : (pok ? __ldg(A.mask + static_cast<size_t>(kg * 4 + cb) * plane + p) : 0u);
       float* zb = A.z + (static_cast<size_t>(it.n) * A.K + k0) * plane + p;
       const float* zs = zs0 + buf * kChEpiWarps * NC * 32;
-      mbar_wait_sleep(&z_full[ew][buf], use & 1u);
+      if (!plain) mbar_wait_sleep(&z_full[ew][buf], use & 1u);
       mbar_wait_sleep(&acc_full[buf], use & 1u);
       tc_after();
       const uint32_t colb = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
@@ -336,6 +338,14 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
         float c4[4];
         tmem_ld4_nowait(tq + colb + 4u * j4, c4);
         tmem_ld_wait();
+        if (plain) {
+#pragma unroll
+          for (int i4 = 0; i4 < 4; ++i4) {
+            const int i = 4 * j4 + i4;
+            if (pok && (k0 + i) < kend) zb[static_cast<size_t>(i) * plane] = c4[i4] * inv;
+          }
+          continue;
+        }
 #pragma unroll
         for (int i4 = 0; i4 < 4; ++i4) {
           const int i = 4 * j4 + i4;
@@ -455,7 +465,7 @@ CodeTcPlan code_h_plan(const Geom& g, int num_sms) {
 
 cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                           const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
-                          uint32_t* zmax, cudaStream_t st) {
+                          uint32_t* zmax, cudaStream_t st, bool plain) {
   static const float* cached_z = nullptr;
   static Geom cached_g{};
   static int cached_nc = 0;
@@ -482,6 +492,11 @@ cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, co
   a.KC = p.KC; a.Npad = p.Npad; a.nkg = p.nkg; a.G = p.G;
   a.L = p.L; a.nseg = p.nseg; a.nitems = p.nitems;
   a.pitch = p.pitch; a.rs_rows = p.rs_rows; a.rs_floats = p.rs_floats; a.b_bytes = p.b_bytes;
+  a.plain = plain ? 1 : 0;
+  if (plain) {
+    a.mask = nullptr;
+    a.zmax = nullptr;
+  }
   switch (g.S) {
     case 3: return run_code_h_nc<3>(tm, a, p.grid, p.smem, st);
     case 5: return run_code_h_nc<5>(tm, a, p.grid, p.smem, st);

@@ -465,7 +465,8 @@ cudaError_t launch_absmax(const float* x, int64_t n, uint32_t* out, cudaStream_t
 }
 
 cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const float* filt, float* bimg_f,
-                          const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part, cudaStream_t st) {
+                          const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part, cudaStream_t st,
+                          bool build_b) {
   static const float* cached_z = nullptr;
   static Geom cached_g{};
   static CUtensorMap tm;
@@ -484,7 +485,7 @@ cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const 
     cached_g = g;
   }
   uint16_t* bimg = reinterpret_cast<uint16_t*>(bimg_f);
-  bimg_h_kernel<<<1, 1024, 0, st>>>(filt, g.K, g.S * g.S, p.KC, p.nks, bimg, fmax);
+  if (build_b) bimg_h_kernel<<<1, 1024, 0, st>>>(filt, g.K, g.S * g.S, p.KC, p.nks, bimg, fmax);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   HArgs a{};

@@ -115,8 +115,10 @@ cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, const float* z, const
 // (float bits, device); fmax: written with max|filt| (float bits, device).
 bool conv_h_supported(const Geom& g);
 bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p);
+// build_b = false reuses the fp16 filter image (and fmax) of the previous call with the same filt.
 cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const float* filt, float* bimg,
-                          const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part, cudaStream_t st);
+                          const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part, cudaStream_t st,
+                          bool build_b = true);
 // *out = bits of max |x[i]| (atomicMax over non-negative float bits; resets *out first)
 cudaError_t launch_absmax(const float* x, int64_t n, uint32_t* out, cudaStream_t st);
 bool conv_tc_supported(const Geom& g);
@@ -160,28 +162,56 @@ bool code_h_supported(const Geom& g);
 CodeTcPlan code_h_plan(const Geom& g, int num_sms);
 cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                           const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
-                          uint32_t* zmax, cudaStream_t st);
+                          uint32_t* zmax, cudaStream_t st,
+                          bool plain = false);
 // words == nullptr: every code selected (p = 1).
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                            const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st);
 
-// ADMM masked-LASSO code solver (csc_admm.cu): grid (admm_blocks_per_image, N); `part` holds
-// N * admm_blocks_per_image doubles; per-image scalars rr / rr_new / pq are N doubles.
-int admm_blocks_per_image(const Geom& g);
-cudaError_t launch_masked_dtr(const Geom& g, const float* e, const float* d, const uint32_t* bits, const float* v,
-                              float rho, float sign, float* out, double* part, cudaStream_t st);
-cudaError_t launch_admm_init(const Geom& g, const float* z, const uint32_t* bits, float* W, float* Y, float* U,
-                             float* Zf, cudaStream_t st);
-cudaError_t launch_cg_start(const Geom& g, const float* ATB, const float* Y, const float* U, const float* Q,
-                            float rho, float* R, float* PV, double* part, double* rr, cudaStream_t st);
-cudaError_t launch_image_sum(const Geom& g, const double* part, double* out, cudaStream_t st);
-cudaError_t launch_cg_step(const Geom& g, const double* rr, const double* pq, float* W, float* R, const float* PV,
-                           const float* Q, double* part, double* rr_new, cudaStream_t st);
-cudaError_t launch_cg_dir(const Geom& g, double* rr, const double* rr_new, const float* R, float* PV,
-                          cudaStream_t st);
-cudaError_t launch_admm_update(const Geom& g, const uint32_t* bits, const float* W, float* Y, float* U, float alpha,
-                               float kappa, cudaStream_t st);
-cudaError_t launch_admm_finish(const Geom& g, const uint32_t* bits, const float* Y, float* z, uint32_t* zmax,
+// ADMM masked-LASSO code solver (csc_admm.cu).  Vectors are compact [N][ms] (ms = mc rounded up
+// to 4, pads 0) over the selected positions idx[0..mc) of the (image-shared) mask; per-block
+// partials `part` hold N * max(admm_blocks(g, ms), admm_dtr_blocks(g)) doubles; per-image scalars
+// are N doubles.
+int admm_blocks(const Geom& g, int64_t ms);
+int admm_dtr_blocks(const Geom& g);
+int admm_idx_blocks(const Geom& g);
+// bits (canonical layout) -> idx (ascending positions), woff[w] = set bits before word w,
+// *mc (device) = popcount; cnt/off: admm_idx_blocks entries
+cudaError_t launch_admm_index(const Geom& g, const uint32_t* bits, uint32_t* cnt, uint64_t* off, uint64_t* mc,
+                              uint32_t* idx, uint32_t* woff, cudaStream_t st);
+// row_off[r] (r in [0, K*Hc]) = first compact index of code row r = k*Hc + u
+cudaError_t launch_admm_row_off(const Geom& g, const uint32_t* idx, int64_t mc, uint64_t* row_off,
+                                cudaStream_t st);
+// SIMT masked correlation: out = sign * M D^T e (+ rho v, and part[N][admm_dtr_blocks] = per-block
+// sum v*out, when v != null)
+cudaError_t launch_masked_dtr(const Geom& g, const uint32_t* idx, const uint64_t* row_off, int64_t ms, const float* e,
+                              const float* d, const float* v, float rho, float sign, float* out, double* part,
+                              cudaStream_t st);
+// out = sign * Cd[idx] (+ rho v, part[N][admm_blocks] = per-block sum v*out, when v != null)
+cudaError_t launch_admm_gather(const Geom& g, const uint32_t* idx, int64_t mc, int64_t ms, const float* Cd,
+                               const float* v, float rho, float sign, float* out, double* part, cudaStream_t st);
+cudaError_t launch_admm_init(const Geom& g, const uint32_t* idx, int64_t mc, int64_t ms, const float* z, float* W,
+                             float* Y, cudaStream_t st);
+// Zd (dense, zeros off the mask) <- R, or with PV != null the CG direction PV = R + beta PV
+// (beta = rr_new/rr per image; PV = R when rr == null).  max|written| -> atomicMax(bound).
+cudaError_t launch_admm_expand(const Geom& g, const uint32_t* bits, const uint32_t* woff, int64_t ms, const float* R,
+                               float* PV, const double* rr, const double* rr_new, float* Zd, uint32_t* bound,
                                cudaStream_t st);
+// z[idx] = Y (selected positions only); max|written| -> atomicMax(bound) when bound != null
+cudaError_t launch_admm_scatter(const Geom& g, const uint32_t* idx, int64_t mc, int64_t ms, const float* Y, float* z,
+                                uint32_t* bound, cudaStream_t st);
+// rr[n] = |R_n|^2 (fixed-order fp64)
+cudaError_t launch_sumsq(const Geom& g, int64_t ms, const float* R, double* part, double* rr, cudaStream_t st);
+// Explicit CG residual R = ATB + rho (Y - U) - Q (init: ATB = R + Q - rho Y); rr[n] = |R_n|^2
+cudaError_t launch_cg_resid(const Geom& g, int64_t ms, float* ATB, const float* Y, const float* U, const float* Q,
+                            float rho, float* R, double* part, double* rr, bool init, cudaStream_t st);
+// part_pq: nb_pq partials per image (admm_dtr_blocks for masked_dtr, admm_blocks for gather)
+cudaError_t launch_cg_step(const Geom& g, int64_t ms, const double* rr, const double* part_pq, int nb_pq, float* W,
+                           float* R,
+                           const float* PV, const float* Q, double* part_rr, double* rr_new, cudaStream_t st);
+// ADMM update (over-relaxed, shrinkage, dual) carrying the CG residual R to the new right-hand
+// side; rr[n] = |R_n|^2 afterwards
+cudaError_t launch_admm_update(const Geom& g, int64_t ms, const float* W, float* Y, float* U, float* R, float alpha,
+                               float kappa, float rho, double* part, double* rr, cudaStream_t st);
 
 }  // namespace csc

@@ -1,11 +1,12 @@
 """GPU parity of the ADMM masked-LASSO code solver (
 include/csc.h csc_code_step_admm) against oracle.admm_code_step (pinned in tests/test_oracle_admm.py).
 
-Bar: codes within TOL_ADMM relative (norm-wise, reading R9) after one step of 10 ADMM x 5 CG
-iterations; codes off the mask bit-identical (R2).  TOL_ADMM is derived in DESIGN.md A7: the
-operator runs through the same dense pass as the hot path (relative ~1e-6 per application), and
-CG amplifies the per-application error by at most the condition number of A^T A + rho I over
-the 60 applications, which rho = 10 lambda keeps small.
+Bar: codes within TOL_ADMM relative (norm-wise, reading R9) of the fp64 oracle after one step of
+10 ADMM x 5 CG iterations; codes off the mask bit-identical (R2).  TOL_ADMM = 2e-5 is derived in
+DESIGN.md reading A7: one step applies the operator 50 times, and the output's relative error is
+~7-10x the per-application relative error (measured by perturbing an fp64 dense-matrix run,
+tests/test_admm_tolerance.py); the dense passes carry ~1e-6 per application after cancellation
+(fp16 / tf32 3-term splits, fp32 accumulation), so ~1e-5 is expected and 2e-5 is the bar.
 """
 import numpy as np
 import pytest
@@ -16,7 +17,7 @@ from tests.conftest import rel_err
 
 pytestmark = pytest.mark.gpu
 
-TOL_ADMM = 1e-5
+TOL_ADMM = 2e-5
 
 
 @pytest.fixture(scope="module")
@@ -35,16 +36,23 @@ def _t(a, dev):
 
 SHAPES = [((3, 5, 5, 70, 130), 0.1), ((2, 17, 11, 100, 100), 0.2), ((4, 8, 5, 32, 32), 1.0),
           ((1, 9, 3, 33, 47), 0.5), ((2, 4, 11, 11, 11), 0.05), ((2, 130, 7, 20, 300), 0.1),
-          ((1, 100, 11, 40, 11), 0.3)]
+          ((1, 100, 11, 40, 11), 0.3), ((2, 16, 7, 64, 64), 1.0), ((1, 32, 11, 50, 50), 1.0),
+          ((3, 24, 9, 40, 72), 0.5)]
 
 
-@pytest.mark.parametrize("dense", ["half", "simt"])
+@pytest.mark.parametrize("dense", ["half", "simt", "dtr_simt", "explicit"])
 @pytest.mark.parametrize("shape,p", SHAPES)
 def test_admm_code_step_parity(torch_dev, shape, p, dense, monkeypatch):
+    """dense: the operator A v on the fp16-split tensor-core pass ("half") or the SIMT pass; A^T e
+    on the tensor cores (code_h plain mode + gather) unless "dtr_simt" (SIMT masked correlation)."""
     import torch
     import paper_1909_00145_b200 as pkg
     if dense == "simt":
         monkeypatch.setenv("CSC_DENSE_PATH", "simt")
+    if dense == "dtr_simt":
+        monkeypatch.setenv("CSC_ADMM_DTR", "simt")
+    if dense == "explicit":
+        monkeypatch.setenv("CSC_ADMM_RESID", "explicit")
     N, K, s, H, W = shape
     x, d, z = random_problem(300 + K, N, K, s, H, W, code_density=0.3)
     seed, it, lam = 777, 5, 0.2
