@@ -60,7 +60,7 @@ def lib():
                 f.argtypes = [_c_i64, _c_i64, _vp]
                 f.restype = _c_dbl
                 getattr(L, f"oracle_code_step_{suf}").argtypes = (
-                    [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, _c_u64, _c_u32, _vp])
+                    [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, _c_u64, _c_u32, _vp, ctypes.c_int])
                 getattr(L, f"oracle_admm_code_step_{suf}").argtypes = (
                     [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, ctypes.c_int, ctypes.c_int, _c_dbl, _c_u64,
                                                 _c_u32])
@@ -161,18 +161,25 @@ def lipschitz(d, dtype=np.float32) -> float:
     return float(getattr(lib(), f"oracle_lipschitz_{_suf(dtype)}")(K, s, _p(d)))
 
 
-def code_step(x, d, z, lam, step_z, p, seed, t, dtype=np.float32):
-    """One masked prox-gradient code step.  Returns (z_new, tau_used)."""
+def code_step(x, d, z, lam, step_z, p, seed, t, dtype=np.float32, rule="lipschitz"):
+    """One masked prox-gradient code step.  Returns (z_new, tau_used).
+
+    rule (used when step_z == 0): "lipschitz" -> tau = 1/L_D (reading R8), tau_used a float;
+    "eso" -> tau_k = 1/(p L_D + (1-p)||d_k||^2) per filter (E1),
+    tau_used an array of K values."""
     x = _c(x, dtype); d = _c(d, dtype)
     z = np.array(z, dtype=dtype, copy=True, order="C")
     N, K, Hc, Wc = z.shape
     s = d.shape[-1]
     H, W = Hc - s + 1, Wc - s + 1
-    tau = np.zeros(1, dtype=np.float64)
+    eso = 1 if (rule == "eso" and not step_z > 0) else 0
+    if rule not in ("lipschitz", "eso"):
+        raise ValueError(rule)
+    tau = np.zeros(max(K, 1), dtype=np.float64)
     getattr(lib(), f"oracle_code_step_{_suf(dtype)}")(
         N, K, s, H, W, _p(x), _p(d), _p(z), float(lam), float(step_z), float(p),
-        int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(tau))
-    return z, float(tau[0])
+        int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(tau), eso)
+    return z, (tau.copy() if eso else float(tau[0]))
 
 
 ADMM_ITERS = 10      # P:317-318 "the ADMM iteration fixed to 10"

@@ -176,14 +176,36 @@ double lipschitz_dtft(const Dims& D, const T* d) {
 // One masked proximal-gradient step on the codes (reading R1): Eq.3
 // restricted by M^t (Eq.2) and upsampled in place (Eq.4, reading R2: unsampled
 // codes keep their values).
+//
+// Step rule (step_z == 0): eso == 0: tau = 1/L_D for every code (reading R8).  eso != 0: the
+// expected-separable-overapproximation step of parallel coordinate descent under independent
+// Bernoulli(p) sampling (P:620-623 cites the mini-batch coordinate
+// descent literature; reading E1): E ||A h_[S]||^2 = p^2 ||A h||^2 + p(1-p) sum_i
+// ||A_i||^2 h_i^2 <= p sum_i (p L + (1-p) ||A_i||^2) h_i^2, with ||A_i||^2 <= ||d_k||^2 for a code
+// of filter k, so  tau_k = 1 / (p L_D + (1-p) ||d_k||^2).  tau_used receives tau (eso == 0) or
+// tau_k for k = 0..K-1 (eso != 0).
 template <typename T>
 void code_step(const Dims& D, const T* x, const T* d, T* z, double lam, double step_z, double p,
-               uint64_t seed, uint32_t t, double* tau_used) {
+               uint64_t seed, uint32_t t, double* tau_used, int eso = 0) {
   std::vector<T> r((size_t)(D.N * D.H * D.W));
   residual<T>(D, x, d, z, r.data());
-  const T tau_t = step_z > 0.0 ? (T)step_z : (T)(1.0 / lipschitz_dtft<T>(D, d));
-  const double tau = (double)tau_t;
-  const double kappa = tau * lam;
+  const bool per_k = eso != 0 && !(step_z > 0.0);
+  std::vector<double> tauk((size_t)D.K);
+  if (per_k) {
+    const double L = lipschitz_dtft<T>(D, d);
+    for (int64_t k = 0; k < D.K; ++k) {
+      double dk2 = 0.0;
+      for (int64_t a = 0; a < D.s; ++a)
+        for (int64_t b = 0; b < D.s; ++b) {
+          const double v = (double)d[D.di(k, a, b)];
+          dk2 += v * v;
+        }
+      tauk[k] = (double)(T)(1.0 / (p * L + (1.0 - p) * dk2));
+    }
+  } else {
+    const T tau_t = step_z > 0.0 ? (T)step_z : (T)(1.0 / lipschitz_dtft<T>(D, d));
+    for (int64_t k = 0; k < D.K; ++k) tauk[k] = (double)tau_t;
+  }
   const uint64_t thr = mask_threshold(p);
   std::vector<double> rd(r.size());
   for (size_t q = 0; q < r.size(); ++q) rd[q] = (double)r[q];
@@ -198,10 +220,15 @@ void code_step(const Dims& D, const T* x, const T* d, T* z, double lam, double s
           if (!mask_bit(seed, t, l, thr)) continue;
           const double c = dtr_at(D, &dd[k * D.s * D.s], &rd[n * D.H * D.W], u, v);
           const int64_t zi = D.zi(n, k, u, v);
-          const double w = (double)z[zi] - tau * c;
-          z[zi] = (T)soft_threshold(w, kappa);
+          const double w = (double)z[zi] - tauk[k] * c;
+          z[zi] = (T)soft_threshold(w, tauk[k] * lam);
         }
-  if (tau_used) *tau_used = tau;
+  if (tau_used) {
+    if (per_k)
+      for (int64_t k = 0; k < D.K; ++k) tau_used[k] = tauk[k];
+    else
+      *tau_used = tauk[0];
+  }
 }
 
 // ADMM code step (§3.2): Eq.3, the LASSO for the codes
@@ -477,8 +504,8 @@ double oracle_soft_threshold(double w, double kappa) { return soft_threshold(w, 
   }                                                                                              \
   void oracle_code_step_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W, const T* x, \
                               const T* d, T* z, double lam, double step_z, double p,             \
-                              uint64_t seed, uint32_t t, double* tau_used) {                     \
-    code_step<T>(Dims(N, K, s, H, W), x, d, z, lam, step_z, p, seed, t, tau_used);              \
+                              uint64_t seed, uint32_t t, double* tau_used, int eso) {            \
+    code_step<T>(Dims(N, K, s, H, W), x, d, z, lam, step_z, p, seed, t, tau_used, eso);         \
   }                                                                                              \
   void oracle_admm_code_step_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,          \
                                    const T* x, const T* d, T* z, double lam, double rho,           \
