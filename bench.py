@@ -313,6 +313,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     ctx = pkg.Context(nl, cfg.K, cfg.s, cfg.H, cfg.W, world=ws, rank=rank, device=local, stream=stream,
                       nccl_id=nccl_id)
+    if args.step_rule != "lipschitz":
+        ctx.set_step_rule(args.step_rule)
     l2_flush = None
     if 4 * cfg.N * cfg.K * cfg.Hc * cfg.Wc <= 2 * 126e6:
         l2_flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)
@@ -402,7 +404,7 @@ def run_ours(args):
             "metric": "csc_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": dict(_config_dict(cfg, ws), code_solver=args.code_solver),
+            "config": dict(_config_dict(cfg, ws), code_solver=args.code_solver, step_rule=args.step_rule),
             "roofline": dict(rl[dom], dominant_class=dom),
             "kernel_rooflines": rl,
             "kernels": kernels,
@@ -431,6 +433,8 @@ def main():
     ap.add_argument("--ref-images", type=int, default=1)
     ap.add_argument("--cpu-images", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--step-rule", default="lipschitz", choices=["lipschitz", "eso"],
+                    help="built-in tau_z rule of the prox code step (eso: SURVEY.md §8f NEXT-4 (i))")
     ap.add_argument("--code-solver", default="prox", choices=["prox", "admm"],
                     help="prox: the north_star masked prox-gradient step (default); admm: the paper's ADMM "
                          "code update (SURVEY.md §8f NEXT-1), 10 x 5 CG iterations")

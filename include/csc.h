@@ -130,6 +130,20 @@ csc_status csc_code_step_admm(csc_ctx* ctx, const float* x, const float* d, floa
                               float rho, float alpha, int n_admm, int n_cg, double p, uint64_t seed,
                               uint32_t iter);
 
+/* Built-in code step-size rule, used by csc_code_step / csc_iterate when step_z == 0:
+ *   CSC_STEP_LIPSCHITZ (default): tau = 1/L_D for every code (reading R8);
+ *   CSC_STEP_ESO: tau_k = 1/(p L_D + (1-p) ||d_k||^2) for the codes of filter k -- the
+ *     parallel-coordinate-descent step whose expected separable overapproximation holds for
+ *     independent Bernoulli(p) sampling (E1).
+ *     Equal to the Lipschitz rule at p = 1.  step_used then receives tau_0.
+ * Per context; CSC_ERR_ARG for an unknown rule. */
+typedef enum { CSC_STEP_LIPSCHITZ = 0, CSC_STEP_ESO = 1 } csc_step_rule;
+csc_status csc_set_step_rule(csc_ctx* ctx, int rule);
+
+/* Test hook: the K step sizes tau_z of the last code step (DEVICE fp32 [K]; the same value K
+ * times unless that step used the ESO rule). */
+csc_status csc_read_step_z(csc_ctx* ctx, float* tau_dev);
+
 /* Forget the residual cache (caller changed x, d or z outside the API). */
 csc_status csc_invalidate(csc_ctx* ctx);
 

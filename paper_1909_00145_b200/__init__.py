@@ -29,6 +29,7 @@ ABI_SYMBOLS = (
     "csc_zero_codes", "csc_destroy", "csc_last_error", "csc_nccl_unique_id", "csc_abi_version",
     "csc_mask_bits", "csc_read_residual", "csc_read_grad", "csc_lipschitz", "csc_launch_count",
     "csc_profile_enable", "csc_profile_read", "csc_kernel_variants", "csc_code_step_admm",
+    "csc_set_step_rule", "csc_read_step_z",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -67,6 +68,8 @@ def load_library(path: Optional[str] = None):
         L.csc_init.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(vp)]
         L.csc_code_step.argtypes = [vp, vp, vp, vp, f32, f32, f64, u64, u32, vp]
         L.csc_filter_step.argtypes = [vp, vp, vp, vp, f32, vp]
+        L.csc_set_step_rule.argtypes = [vp, ctypes.c_int]
+        L.csc_read_step_z.argtypes = [vp, vp]
         L.csc_code_step_admm.argtypes = [vp, vp, vp, vp, f32, f32, f32, ctypes.c_int, ctypes.c_int, f64, u64, u32]
         L.csc_objective.argtypes = [vp, vp, vp, vp, f32, vp]
         L.csc_iterate.argtypes = [vp, vp, vp, vp, vp, f32, f32, f32, f64, u64, u32, vp, vp]
@@ -160,6 +163,17 @@ class Context:
                                           int(seed) & (2**64 - 1), int(it) & 0xffffffff,
                                           ctypes.byref(out) if want_step else None))
         return float(out.value) if want_step else None
+
+    STEP_RULES = {"lipschitz": 0, "eso": 1}
+
+    def set_step_rule(self, rule: str) -> None:
+        """Built-in tau_z rule when step_z == 0: "lipschitz" (1/L_D) or "eso" (per filter,
+        include/csc.h csc_set_step_rule)."""
+        self._check(self._L.csc_set_step_rule(self._h, self.STEP_RULES[rule]))
+
+    def read_step_z(self, out) -> None:
+        """K step sizes of the last code step into the float32 CUDA tensor out."""
+        self._check(self._L.csc_read_step_z(self._h, _ptr(out, "out", self.K)))
 
     def code_step_admm(self, x, d, z, lam: float, p: float, seed: int, it: int, rho: float = 0.0,
                        alpha: float = 1.8, n_admm: int = 10, n_cg: int = 5) -> None:

@@ -113,6 +113,9 @@ struct csc_ctx {
   csc::CodeTcPlan ct{};
   uint32_t* mwords = nullptr;  // selection-word mask [4*nkg][Hc*Wc]
   uint32_t* rmax = nullptr;    // max|r| (float bits) for the fp16-split code step
+  int step_rule = CSC_STEP_LIPSCHITZ;  // built-in tau_z rule (csc_set_step_rule)
+  bool last_eso = false;       // the last code step used per-filter taus
+  float* tauk = nullptr;       // [K] per-filter tau_z of the ESO rule
   // ADMM code solver scratch (csc_admm.cu), allocated by the first csc_code_step_admm
   float* adm_zd = nullptr;      // [N][K][Hc][Wc] scatter target of the operator (0 off the mask)
   float* adm_e = nullptr;       // [N][H][W] operator output
@@ -446,6 +449,7 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   ok = ok && alloc(reinterpret_cast<void**>(&c->gpart), sizeof(double) * static_cast<size_t>(gpart_groups) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->gsum), sizeof(double) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->g32), sizeof(float) * g.K * M);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->tauk), sizeof(float) * g.K);
   ok = ok && alloc(reinterpret_cast<void**>(&c->colw), sizeof(uint32_t) * static_cast<size_t>(g.K) * NB * g.Wc);
   ok = ok && alloc(reinterpret_cast<void**>(&c->lip_part), sizeof(double) * 64 * 64 * csc::ceil_div(g.K, 2));
   ok = ok && alloc(reinterpret_cast<void**>(&c->dscal), sizeof(double) * kNumD);
@@ -565,6 +569,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->colw);
   cudaFree(c->mwords);
   cudaFree(c->rmax);
+  cudaFree(c->tauk);
   cudaFree(c->adm_zd);
   cudaFree(c->adm_e);
   cudaFree(c->adm_cd);
@@ -635,11 +640,17 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
     s = dense_residual(c, x, d, z, false);
     if (s != CSC_OK) return s;
   }
+  const bool eso = step_z == 0.f && c->step_rule == CSC_STEP_ESO;
   if (step_z > 0.f) {
     CSC_CUDA(c, cudaMemcpyAsync(c->fscal + kTauZ, &step_z, sizeof(float), cudaMemcpyHostToDevice, c->st));
   } else {
     CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 2, csc::launch_lipschitz(g, d, c->lip_part, c->dscal + kLhat, c->fscal + kTauZ, c->st));
+    if (eso) CSC_LAUNCH(c, 1, csc::launch_eso_tau(g, d, p, c->dscal + kLhat, c->tauk, c->st));
   }
+  c->last_eso = eso;
+  // tau per filter (ESO) or one tau for all codes
+  const float* tau_dev = eso ? c->tauk : c->fscal + kTauZ;
+  const int tau_stride = eso ? 1 : 0;
   const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
   const int all_selected = thr >= (uint64_t(1) << 32) ? 1 : 0;
   if (g.N > 0) {
@@ -649,25 +660,44 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
       if (c->ct.half) {
         CSC_LAUNCH(c, 1, csc::launch_absmax(c->r, n_pix(g), c->rmax, c->st));
         CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
-                     csc::launch_code_h(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, c->fscal + kTauZ,
-                                        lambda, c->rmax, zbound(c, z), c->st));
+                     csc::launch_code_h(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, tau_dev,
+                                        lambda, c->rmax, zbound(c, z), c->st, false, tau_stride));
       } else {
         CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
-                     csc::launch_code_tc(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, c->fscal + kTauZ,
-                                         lambda, zbound(c, z), c->st));
+                     csc::launch_code_tc(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, tau_dev,
+                                         lambda, zbound(c, z), c->st, tau_stride));
       }
     } else {
       if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st));
-      CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, c->fscal + kTauZ, lambda,
-                                                                zbound(c, z), c->st));
+      CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, tau_dev, lambda,
+                                                                zbound(c, z), c->st, tau_stride));
     }
   }
   c->cache_valid = false;  // r no longer matches z
   if (step_used) {
-    CSC_CUDA(c, cudaMemcpyAsync(c->h_fscal + kTauZ, c->fscal + kTauZ, sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    CSC_CUDA(c, cudaMemcpyAsync(c->h_fscal + kTauZ, tau_dev, sizeof(float), cudaMemcpyDeviceToHost, c->st));
     CSC_CUDA(c, cudaStreamSynchronize(c->st));
     *step_used = c->h_fscal[kTauZ];
     if (!std::isfinite(*step_used)) return fail(c, CSC_ERR_NONFINITE, "tau_z is not finite");
+  }
+  return CSC_OK;
+}
+
+csc_status csc_set_step_rule(csc_ctx* c, int rule) {
+  if (!c) return CSC_ERR_ARG;
+  if (rule != CSC_STEP_LIPSCHITZ && rule != CSC_STEP_ESO) return fail(c, CSC_ERR_ARG, "unknown step rule");
+  c->step_rule = rule;
+  return CSC_OK;
+}
+
+csc_status csc_read_step_z(csc_ctx* c, float* tau_dev) {
+  if (!c || !aligned4(tau_dev)) return fail(c, CSC_ERR_ARG, "tau_dev must be a device pointer");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  if (c->last_eso) {
+    CSC_CUDA(c, cudaMemcpyAsync(tau_dev, c->tauk, sizeof(float) * c->g.K, cudaMemcpyDeviceToDevice, c->st));
+  } else {
+    for (int k = 0; k < c->g.K; ++k)
+      CSC_CUDA(c, cudaMemcpyAsync(tau_dev + k, c->fscal + kTauZ, sizeof(float), cudaMemcpyDeviceToDevice, c->st));
   }
   return CSC_OK;
 }

@@ -78,6 +78,7 @@ struct ChArgs {
   int pitch, rs_rows, rs_floats;
   int b_bytes;           // one of hi / lo: 2 K-atoms x Npad rows x 128 B
   int plain;             // 1: z <- c at every position (no z read, no step / shrinkage / mask)
+  int tau_stride;        // 0: tau[0] for every filter; 1: tau[k] per filter (ESO rule)
 };
 
 struct ChItem {
@@ -333,31 +334,40 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
       mbar_wait_sleep(&acc_full[buf], use & 1u);
       tc_after();
       const uint32_t colb = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
+      // per-filter step sizes (ESO rule) in a separate instantiation of the loop, so the
+      // scalar-tau hot path carries no extra loads
+      auto epi = [&](auto per_k) {
+        constexpr bool PK = decltype(per_k)::value;
 #pragma unroll
-      for (int j4 = 0; j4 < NC / 4; ++j4) {
-        float c4[4];
-        tmem_ld4_nowait(tq + colb + 4u * j4, c4);
-        tmem_ld_wait();
-        if (plain) {
+        for (int j4 = 0; j4 < NC / 4; ++j4) {
+          float c4[4];
+          tmem_ld4_nowait(tq + colb + 4u * j4, c4);
+          tmem_ld_wait();
+          if (plain) {
+#pragma unroll
+            for (int i4 = 0; i4 < 4; ++i4) {
+              const int i = 4 * j4 + i4;
+              if (pok && (k0 + i) < kend) zb[static_cast<size_t>(i) * plane] = c4[i4] * inv;
+            }
+            continue;
+          }
 #pragma unroll
           for (int i4 = 0; i4 < 4; ++i4) {
             const int i = 4 * j4 + i4;
-            if (pok && (k0 + i) < kend) zb[static_cast<size_t>(i) * plane] = c4[i4] * inv;
-          }
-          continue;
-        }
-#pragma unroll
-        for (int i4 = 0; i4 < 4; ++i4) {
-          const int i = 4 * j4 + i4;
-          const float zv = zs[i * 32 + lane];
-          const float w = fmaf(-tau, c4[i4] * inv, zv);
-          const float nz = (w > kappa) ? (w - kappa) : ((w < -kappa) ? (w + kappa) : 0.f);
-          if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv) {
-            zb[static_cast<size_t>(i) * plane] = nz;
-            wmax = fmaxf(wmax, fabsf(nz));
+            const float zv = zs[i * 32 + lane];
+            const float tk = PK ? __ldg(A.tau + min(k0 + i, A.K - 1)) : tau;
+            const float kk = PK ? tk * A.lam : kappa;
+            const float w = fmaf(-tk, c4[i4] * inv, zv);
+            const float nz = (w > kk) ? (w - kk) : ((w < -kk) ? (w + kk) : 0.f);
+            if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv) {
+              zb[static_cast<size_t>(i) * plane] = nz;
+              wmax = fmaxf(wmax, fabsf(nz));
+            }
           }
         }
-      }
+      };
+      if (A.tau_stride) epi(std::true_type{});
+      else epi(std::false_type{});
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
@@ -465,7 +475,7 @@ CodeTcPlan code_h_plan(const Geom& g, int num_sms) {
 
 cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                           const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
-                          uint32_t* zmax, cudaStream_t st, bool plain) {
+                          uint32_t* zmax, cudaStream_t st, bool plain, int tau_stride) {
   static const float* cached_z = nullptr;
   static Geom cached_g{};
   static int cached_nc = 0;
@@ -493,6 +503,7 @@ cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, co
   a.L = p.L; a.nseg = p.nseg; a.nitems = p.nitems;
   a.pitch = p.pitch; a.rs_rows = p.rs_rows; a.rs_floats = p.rs_floats; a.b_bytes = p.b_bytes;
   a.plain = plain ? 1 : 0;
+  a.tau_stride = tau_stride;
   if (plain) {
     a.mask = nullptr;
     a.zmax = nullptr;

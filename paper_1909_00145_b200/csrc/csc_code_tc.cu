@@ -56,6 +56,7 @@ struct CtArgs {
   int L, nseg, nitems;   // item = (image, segment of L flattened positions, L % 128 == 0)
   int pitch, rs_rows, rs_floats;
   int b_bytes;           // one of hi / lo: 4 K-atoms x Npad rows x 128 B
+  int tau_stride;        // 0: tau[0] for every filter; 1: tau[k] per filter (ESO rule)
 };
 
 struct CtItem {
@@ -267,22 +268,29 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
         mbar_wait_sleep(&acc_full[buf], use & 1u);
         tc_after();
         const uint32_t colb = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
+        auto epi = [&](auto per_k) {
+          constexpr bool PK = decltype(per_k)::value;
 #pragma unroll
-        for (int j4 = 0; j4 < NC / 4; ++j4) {
-          float c4[4];
-          tmem_ld4_nowait(tq + colb + 4u * j4, c4);
-          tmem_ld_wait();
+          for (int j4 = 0; j4 < NC / 4; ++j4) {
+            float c4[4];
+            tmem_ld4_nowait(tq + colb + 4u * j4, c4);
+            tmem_ld_wait();
 #pragma unroll
-          for (int i4 = 0; i4 < 4; ++i4) {
-            const int i = 4 * j4 + i4;
-            const float w = fmaf(-tau, c4[i4], zv[i]);
-            const float nz = (w > kappa) ? (w - kappa) : ((w < -kappa) ? (w + kappa) : 0.f);
-            if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv[i]) {
-              zb[static_cast<size_t>(i) * plane] = nz;
-              wmax = fmaxf(wmax, fabsf(nz));
+            for (int i4 = 0; i4 < 4; ++i4) {
+              const int i = 4 * j4 + i4;
+              const float tk = PK ? __ldg(A.tau + min(k0 + i, A.K - 1)) : tau;
+              const float kk = PK ? tk * A.lam : kappa;
+              const float w = fmaf(-tk, c4[i4], zv[i]);
+              const float nz = (w > kk) ? (w - kk) : ((w < -kk) ? (w + kk) : 0.f);
+              if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv[i]) {
+                zb[static_cast<size_t>(i) * plane] = nz;
+                wmax = fmaxf(wmax, fabsf(nz));
+              }
             }
           }
-        }
+        };
+        if (A.tau_stride) epi(std::true_type{});
+        else epi(std::false_type{});
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
@@ -430,9 +438,11 @@ cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t se
 }
 
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
-                           const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st) {
+                           const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st,
+                           int tau_stride) {
   CtArgs a{};
   a.r = r; a.d = d; a.z = z; a.mask = words; a.tau = tau_dev; a.lam = lam; a.zmax = zmax;
+  a.tau_stride = tau_stride;
   a.N = g.N; a.K = g.K; a.S = g.S; a.H = g.H; a.W = g.W; a.Hc = g.Hc; a.Wc = g.Wc; a.P = g.P;
   a.KC = p.KC; a.Npad = p.Npad; a.nkg = p.nkg; a.G = p.G;
   a.L = p.L; a.nseg = p.nseg; a.nitems = p.nitems;

@@ -36,6 +36,7 @@ inline bool filter_size_supported(int s) {
 }
 
 // All launchers return cudaGetLastError() of their launch.
+// Code-step launchers: tau_stride 0 -> tau_dev[0] for every filter; 1 -> tau_dev[k] (ESO rule).
 // kConvResidual: out = y - x (plain y when x == nullptr); kConvSumSq: only sum y^2.
 enum ConvMode : int { kConvResidual = 0, kConvSumSq = 1 };
 
@@ -75,9 +76,12 @@ cudaError_t launch_mask_bits(const Geom& g, uint64_t seed, uint32_t iter, uint64
 
 // Masked proximal-gradient code step.
 // zmax (may be null): raised (atomicMax of float bits) to >= |z| of every code written.
+// ESO step rule: tauk[k] = fp32(1 / (p * lhat + (1-p) ||d_k||^2))
+cudaError_t launch_eso_tau(const Geom& g, const float* d, double p, const double* lhat, float* tauk, cudaStream_t st);
 cudaError_t launch_code_step(const Geom& g, const float* r, const float* d, float* z,
                              const uint32_t* colw, int all_selected, const float* tau_dev,
-                             float lam, uint32_t* zmax, cudaStream_t st);
+                             float lam, uint32_t* zmax, cudaStream_t st,
+                             int tau_stride = 0);
 
 // L_D(d) = max over 64x64 DFT grid of sum_k |d^_k|^2 -> lhat (fp64), and
 // tau_out = (float)(1/L) if tau_out != nullptr.  part: >= 64 doubles scratch.
@@ -163,10 +167,11 @@ CodeTcPlan code_h_plan(const Geom& g, int num_sms);
 cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                           const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
                           uint32_t* zmax, cudaStream_t st,
-                          bool plain = false);
+                          bool plain = false, int tau_stride = 0);
 // words == nullptr: every code selected (p = 1).
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
-                           const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st);
+                           const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st,
+                             int tau_stride = 0);
 
 // ADMM masked-LASSO code solver (csc_admm.cu).  Vectors are compact [N][ms] (ms = mc rounded up
 // to 4, pads 0) over the selected positions idx[0..mc) of the (image-shared) mask; per-block

@@ -480,7 +480,7 @@ template <int S>
 __global__ void __launch_bounds__(kCodeThreads, 3)
 code_step_kernel(const float* __restrict__ r, const float* __restrict__ d, float* __restrict__ z,
                  const uint32_t* __restrict__ colw, int all_selected, const float* __restrict__ tau_dev,
-                 float lam, Geom g, int TH, int kgroups, int NB, uint32_t* __restrict__ zmax) {
+                 int tau_stride, float lam, Geom g, int TH, int kgroups, int NB, uint32_t* __restrict__ zmax) {
   constexpr int P = S - 1;
   extern __shared__ __align__(16) float rs[];
   const int v0 = blockIdx.x * 32;
@@ -505,13 +505,13 @@ code_step_kernel(const float* __restrict__ r, const float* __restrict__ d, float
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = v0 + lane;
   const bool col_ok = v < g.Wc;
-  const float tau = *tau_dev;
-  const float kappa = tau * lam;
   const int nblk = TH / 32;
   const int ub0 = u0 / 32;
   float wmax = 0.f;
 
   for (int k = kb + warp; k < ke; k += kCodeWarps) {
+    const float tau = tau_dev[k * tau_stride];
+    const float kappa = tau * lam;
     float dk[S * S];
 #pragma unroll
     for (int i = 0; i < S * S; ++i) dk[i] = __ldg(d + static_cast<int64_t>(k) * S * S + i);
@@ -743,7 +743,8 @@ inline int code_tile_rows(int Hc) {
 template <int S>
 struct CodeRun {
   static cudaError_t run(const Geom& g, const float* r, const float* d, float* z, const uint32_t* colw,
-                         int all_selected, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st) {
+                         int all_selected, const float* tau_dev, int tau_stride, float lam, uint32_t* zmax,
+                         cudaStream_t st) {
     const int TH = code_tile_rows(g.Hc);
     const int strips = ceil_div(g.Wc, 32), bands = ceil_div(g.Hc, TH);
     const int base = strips * bands * g.N;
@@ -759,8 +760,8 @@ struct CodeRun {
     }
     const int NB = ceil_div(g.Hc, 32);
     dim3 grid(strips, bands, g.N * kgroups);
-    code_step_kernel<S><<<grid, kCodeThreads, smem, st>>>(r, d, z, colw, all_selected, tau_dev, lam, g, TH, kgroups, NB,
-                                                          zmax);
+    code_step_kernel<S><<<grid, kCodeThreads, smem, st>>>(r, d, z, colw, all_selected, tau_dev, tau_stride, lam, g,
+                                                          TH, kgroups, NB, zmax);
     return cudaGetLastError();
   }
 };
@@ -825,8 +826,28 @@ cudaError_t launch_mask_bits(const Geom& g, uint64_t seed, uint32_t iter, uint64
 }
 
 cudaError_t launch_code_step(const Geom& g, const float* r, const float* d, float* z, const uint32_t* colw,
-                             int all_selected, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st) {
-  return dispatch_s<CodeRun>(g.S, g, r, d, z, colw, all_selected, tau_dev, lam, zmax, st);
+                             int all_selected, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st,
+                             int tau_stride) {
+  return dispatch_s<CodeRun>(g.S, g, r, d, z, colw, all_selected, tau_dev, tau_stride, lam, zmax, st);
+}
+
+// ESO step rule (E1): tau_k = fp32(1 / (p L + (1-p) ||d_k||^2)), ||d_k||^2 summed in fp64
+// over (a, b) in order; one thread per filter
+__global__ void eso_tau_kernel(const float* __restrict__ d, int K, int S2, double p, const double* __restrict__ lhat,
+                               float* __restrict__ tauk) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double dk2 = 0.0;
+  for (int i = 0; i < S2; ++i) {
+    const double v = static_cast<double>(d[static_cast<int64_t>(k) * S2 + i]);
+    dk2 += v * v;
+  }
+  tauk[k] = static_cast<float>(1.0 / (p * *lhat + (1.0 - p) * dk2));
+}
+
+cudaError_t launch_eso_tau(const Geom& g, const float* d, double p, const double* lhat, float* tauk, cudaStream_t st) {
+  eso_tau_kernel<<<ceil_div(g.K, 128), 128, 0, st>>>(d, g.K, g.S * g.S, p, lhat, tauk);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_lipschitz(const Geom& g, const float* d, double* part, double* lhat, float* tau_out,
