@@ -14,17 +14,19 @@
 // at <= 2^14, so no value overflows fp16 and values below 2^-24 of the maximum lose nothing that
 // survives the fp32 sum.
 //
-// Stage = 16 filter planes of one tile: 4 TMA boxes {32 positions, 16 planes} (fp32, no swizzle,
-// 8 KB), converted by one converter warp into fp16 hi/lo tiles in the canonical MN-major
-// SWIZZLE_128B layout (2 atoms of 64 positions x 16 rows of 128 B, 16-B chunks XOR row).
-// CTA (persistent, 26 warps): warp 0 MMA, warp 1 TMA, warps 2..17 converters (a pair per stage slot),
-// warps 18..25 epilogue.
+// Stage = 16 filter planes of one tile: one TMA box {128 positions, 16 planes} (fp32, no swizzle,
+// 8 KB: one request per stage keeps the TMA issue rate off the critical path), converted by a pair
+// of converter warps into fp16 hi/lo tiles in the canonical MN-major SWIZZLE_128B layout (2 atoms
+// of 64 positions x 16 rows of 128 B, 16-B chunks XOR row).
+// CTA (persistent, 30 warps, <= 64 registers): warp 0 MMA, warp 1 TMA, warps 2..17 converters (a pair
+// per stage slot), warps 18..29 epilogue (4 TMEM lane quarters x 3 groups of tap rows).
 #include "csc_internal.cuh"
 #include "csc_tc_ptx.cuh"
 
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
@@ -36,11 +38,11 @@ using namespace tcx;
 
 constexpr int kHNS = 8;             // stages (16 filters of one tile each)
 constexpr int kHConvWarps = 16;  // 2 per stage slot (kHNS slots): a slot is always converted by the same pair
-constexpr int kHEpiWarps = 8;
+constexpr int kHEpiWarps = 12;   // 4 lane quarters x 3 groups of tap rows
 constexpr int kHConvBase = 2, kHEpiBase = kHConvBase + kHConvWarps;
 constexpr int kHWarps = kHEpiBase + kHEpiWarps;
 constexpr int kHThreads = 32 * kHWarps;
-constexpr int kHRawBytes = 8192;    // 4 boxes x 16 rows x 128 B (fp32)
+constexpr int kHRawBytes = 8192;    // one TMA box: 16 planes x 128 positions (fp32, rows of 512 B)
 constexpr int kHHalfBytes = 4096;   // 2 atoms x 16 rows x 128 B (fp16), one of hi / lo
 constexpr int kHStageBytes = kHRawBytes + 2 * kHHalfBytes;
 constexpr int kHSmemMax = 220 * 1024;
@@ -77,6 +79,7 @@ struct HArgs {
   int N, K, S, H, W, Hc, Wc, P;
   int KC, NCH, NT, ks;       // NCH = KC / 16
   int BR, nbands, nitems, WL;
+  unsigned long long* tdbg;  // CSC_CH_TIMING: per-CTA role cycle counters [grid][16] or nullptr
 };
 
 struct HItem {
@@ -147,6 +150,8 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
 
   if (warp == 0) {
     // ================================ MMA issuer
+    const unsigned long long t_beg = clock64();
+    unsigned long long w_acc = 0, w_rdy = 0;
     const uint32_t idesc = idesc_f16_mn(128, A.NT);
     const uint32_t lbo_b = static_cast<uint32_t>(A.KC) * 128u;  // N atom (64 taps) stride
     const uint32_t sbh = su32(bsm), sbl = su32(bsm + bbytes), sst = su32(stg);
@@ -155,12 +160,16 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        const unsigned long long tw0 = clock64();
         mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
+        w_acc += clock64() - tw0;
         tc_after();
         const uint32_t d = tbase + buf * 128u;
         for (int c = 0; c < A.NCH; ++c, ++g) {
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+          const unsigned long long tw1 = clock64();
           mbar_wait(&ready[slot], ph);
+          w_rdy += clock64() - tw1;
           tc_after();
           const uint32_t ah = sst + slot * kHStageBytes + kHRawBytes;
           // A: MN-major SW128, 2 atoms of 64 positions at LBO = 16 rows x 128 B, 8-row K groups at SBO
@@ -186,9 +195,15 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       }
     }
     __syncwarp();
+    if (A.tdbg != nullptr && lane == 0) {
+      A.tdbg[blockIdx.x * 16 + 0] = clock64() - t_beg;
+      A.tdbg[blockIdx.x * 16 + 1] = w_acc;
+      A.tdbg[blockIdx.x * 16 + 2] = w_rdy;
+    }
   } else if (warp == 1) {
-    // ================================ TMA producer: 4 boxes {32 positions, 16 planes} per stage
+    // ================================ TMA producer: one box {128 positions, 16 planes} per stage
     if (lane == 0) {
+      unsigned long long w_emp = 0;
       uint32_t g = 0;
       for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
         const HItem it = h_item(A, item);
@@ -197,22 +212,25 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           const int pt = it.p0 + 128 * t;  // multiple of 4 floats (BR % 4 == 0): 16-B aligned box start
           for (int c = 0; c < A.NCH; ++c, ++g) {
             const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+            const unsigned long long tw2 = clock64();
             mbar_wait(&empty[slot], ph ^ 1u);
+            w_emp += clock64() - tw2;
             mbar_arrive_expect_tx(&full[slot], kHRawBytes);
             const uint32_t dst = su32(stg + slot * kHStageBytes);
-#pragma unroll
-            for (int at = 0; at < 4; ++at)
-              tma_load_2d(dst + at * 2048u, &tmap_z, pt + 32 * at, plane0 + 16 * c, &full[slot]);
+            tma_load_2d(dst, &tmap_z, pt, plane0 + 16 * c, &full[slot]);  // {128 positions, 16 planes}
           }
         }
       }
+      if (A.tdbg != nullptr) A.tdbg[blockIdx.x * 16 + 3] = w_emp;
     }
     __syncwarp();
   } else if (warp < kHEpiBase) {
-    // ================================ converters: one warp per stage (stages g = cw mod 4)
-    // thread job (row k, 8 positions 8j..8j+7): raw = box j/4, floats 8(j%4).. of row k;
+    // ================================ converters: a pair of warps per stage slot (g mod kHNS = cw / 2)
+    // thread job (row k, 8 positions 8j..8j+7): raw floats 8j..8j+7 of row k (row pitch 512 B);
     // fp16 chunk j%8 of atom j/8, row k, at 16-B chunk (j%8) ^ (k%8)
     const int cw = warp - kHConvBase;
+    const unsigned long long t_cv = clock64();
+    unsigned long long w_full = 0;
     const bool want_l1 = A.l1_part != nullptr;
     const float sz = exp2i(ez);
     double l1 = 0.0;
@@ -224,7 +242,9 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         for (int c = 0; c < A.NCH; ++c, ++g) {
           if (static_cast<int>(g % kHNS) != (cw >> 1)) continue;
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+          const unsigned long long tw3 = clock64();
           mbar_wait(&full[slot], ph);
+          w_full += clock64() - tw3;
           const uint8_t* rawp = stg + slot * kHStageBytes;
           uint8_t* hip = stg + slot * kHStageBytes + kHRawBytes;
           uint8_t* lop = hip + kHHalfBytes;
@@ -233,7 +253,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           for (int rep = 0; rep < 4; ++rep) {
             const int job = lane + 32 * (2 * rep + (cw & 1));   // 0..255, the pair splits the stage
             const int k = job >> 4, j = job & 15;
-            const float4* src = reinterpret_cast<const float4*>(rawp + (j >> 2) * 2048 + k * 128 + (j & 3) * 32);
+            const float4* src = reinterpret_cast<const float4*>(rawp + k * 512 + j * 32);
             const float4 x0 = src[0], x1 = src[1];
             float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
             uint32_t hv[4], lv[4];
@@ -264,22 +284,30 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         }
       }
     }
+    if (A.tdbg != nullptr && cw == 0 && lane == 0) {
+      A.tdbg[blockIdx.x * 16 + 4] = w_full;
+      A.tdbg[blockIdx.x * 16 + 5] = clock64() - t_cv;
+    }
     const double tsum = warp_sum_d(l1);
     if (lane == 0) l1_warp[cw] = tsum;
   } else {
     // ================================ epilogue (as csc_conv_ss.cu: one band window, Wc >= 128)
-    const int q = warp & 3;
-    const int h = (warp - kHEpiBase) >> 2;
-    constexpr int AH = (S + 1) / 2;
-    const int a_beg = h == 0 ? 0 : AH;
-    const int na = h == 0 ? AH : S - AH;
+    const int q = warp & 3;                 // TMEM lane quarter of this warp
+    const int h = (warp - kHEpiBase) >> 2;  // group of tap rows
+    constexpr int AH = (S + 2) / 3;
+    const int a_beg = h * AH;
+    const int na = min(AH, S - a_beg);      // may be <= 0 for small S
     const float inv = exp2i(-(ez + ef));
+    const unsigned long long t_ep = clock64();
+    unsigned long long w_af = 0, w_fl = 0;
     uint32_t tcount = 0;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        const unsigned long long tw4 = clock64();
         mbar_wait_sleep(&acc_full[buf], use & 1u);
+        w_af += clock64() - tw4;
         tc_after();
         const int pq = 128 * t + 32 * q;
         const bool pvalid = it.p0 + pq + lane < it.pend;
@@ -297,12 +325,15 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
 #pragma unroll
           for (int b = 0; b < S; ++b) {
+            // one rotation serves both parts: lanes >= b get position lane-b of this quarter, lanes < b
+            // get position lane-b+32, the halo that belongs to the next quarter's first lanes
             const float yv = pvalid ? y[b] : 0.f;
-            const float up = __shfl_up_sync(kFullMask, yv, b);
-            const float dn = __shfl_down_sync(kFullMask, yv, 32 - b);
-            const float uv = lane >= b ? up : 0.f;
-            const float dv = (b > 0 && lane < b) ? dn : 0.f;
-            if (b & 1) { u1s += uv; d1s += dv; } else { u0s += uv; d0s += dv; }
+            const float rot = b == 0 ? yv : __shfl_sync(kFullMask, yv, (lane - b) & 31);
+            if (lane >= b) {
+              if (b & 1) u1s += rot; else u0s += rot;
+            } else {
+              if (b & 1) d1s += rot; else d0s += rot;
+            }
           }
           rowb[i * A.Wc] += u0s + u1s;
           dnv[i] = d0s + d1s;
@@ -318,6 +349,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         }
         named_sync(1, 32 * kHEpiWarps);
       }
+      const unsigned long long tw5 = clock64();
       float* dst = A.part + (static_cast<size_t>(it.n) * A.nbands + (it.u0 / A.BR)) *
                                 static_cast<size_t>(A.BR + P) * A.W;
       const int rows = A.BR + P;
@@ -330,6 +362,12 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       named_sync(1, 32 * kHEpiWarps);
       for (int e = et; e < A.WL; e += 32 * kHEpiWarps) win[e] = 0.f;
       named_sync(1, 32 * kHEpiWarps);
+      w_fl += clock64() - tw5;
+    }
+    if (A.tdbg != nullptr && warp == kHEpiBase && lane == 0) {
+      A.tdbg[blockIdx.x * 16 + 6] = w_af;
+      A.tdbg[blockIdx.x * 16 + 7] = w_fl;
+      A.tdbg[blockIdx.x * 16 + 8] = clock64() - t_ep;
     }
   }
 
@@ -475,7 +513,7 @@ cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const 
     if (!enc) return cudaErrorNotSupported;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Hc) * g.Wc, static_cast<cuuint64_t>(g.N) * g.K};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Hc) * g.Wc * 4};
-    const cuuint32_t box[2] = {32u, 16u};
+    const cuuint32_t box[2] = {128u, 16u};
     const cuuint32_t estr[2] = {1u, 1u};
     CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(z), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -489,6 +527,29 @@ cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   HArgs a{};
+  {
+    static int tmode = -1;
+    static unsigned long long* tbuf = nullptr;
+    static int ncalls = 0;
+    if (tmode < 0) {
+      const char* ev = std::getenv("CSC_CH_TIMING");
+      tmode = ev ? std::atoi(ev) : 0;
+      if (tmode) cudaMalloc(&tbuf, sizeof(unsigned long long) * 16 * 2048);
+    }
+    a.tdbg = tmode ? tbuf : nullptr;
+    if (tmode && ++ncalls == 12) {
+      cudaStreamSynchronize(st);
+      static unsigned long long h[16 * 2048];
+      cudaMemcpy(h, tbuf, sizeof(unsigned long long) * 16 * p.grid, cudaMemcpyDeviceToHost);
+      double tot[16] = {0};
+      for (int b = 0; b < p.grid; ++b)
+        for (int r = 0; r < 9; ++r) tot[r] += static_cast<double>(h[b * 16 + r]);
+      for (int r = 0; r < 9; ++r) tot[r] /= p.grid;
+      fprintf(stderr, "[conv_h] per CTA cycles: mma total %.0f wait acc_empty %.0f wait ready %.0f | tma wait empty %.0f | "
+                      "conv0 wait full %.0f of %.0f | epi0 wait acc_full %.0f band flush %.0f of %.0f\n",
+              tot[0], tot[1], tot[2], tot[3], tot[4], tot[5], tot[6], tot[7], tot[8]);
+    }
+  }
   a.bimg = bimg;
   a.zmax = zmax;
   a.fmax = fmax;
