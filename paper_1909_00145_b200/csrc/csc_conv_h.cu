@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace csc {
@@ -314,30 +315,37 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         const uint32_t tacc = tbase + buf * 128u + (static_cast<uint32_t>(32 * q) << 16);
         float* rowb = win + pq + lane + a_beg * A.Wc;
         float dnv[AH];
+        // positions past the item's end only occur in its last tile: the common full tile runs
+        // without the per-value select
+        auto reduce_rows = [&](auto partial) {
+          constexpr bool PART = decltype(partial)::value;
 #pragma unroll
-        for (int i = 0; i < AH; ++i) {
-          dnv[i] = 0.f;
-          if (i >= na) continue;
-          const int a = a_beg + i;
-          float y[16];
-          tmem_ld16_nowait(tacc + a * S, y);
-          tmem_ld_wait();
-          float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
+          for (int i = 0; i < AH; ++i) {
+            dnv[i] = 0.f;
+            if (i >= na) continue;
+            const int a = a_beg + i;
+            float y[16];
+            tmem_ld16_nowait(tacc + a * S, y);
+            tmem_ld_wait();
+            float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
 #pragma unroll
-          for (int b = 0; b < S; ++b) {
-            // one rotation serves both parts: lanes >= b get position lane-b of this quarter, lanes < b
-            // get position lane-b+32, the halo that belongs to the next quarter's first lanes
-            const float yv = pvalid ? y[b] : 0.f;
-            const float rot = b == 0 ? yv : __shfl_sync(kFullMask, yv, (lane - b) & 31);
-            if (lane >= b) {
-              if (b & 1) u1s += rot; else u0s += rot;
-            } else {
-              if (b & 1) d1s += rot; else d0s += rot;
+            for (int b = 0; b < S; ++b) {
+              // one rotation serves both parts: lanes >= b get position lane-b of this quarter, lanes < b
+              // get position lane-b+32, the halo that belongs to the next quarter's first lanes
+              const float yv = PART ? (pvalid ? y[b] : 0.f) : y[b];
+              const float rot = b == 0 ? yv : __shfl_sync(kFullMask, yv, (lane - b) & 31);
+              if (lane >= b) {
+                if (b & 1) u1s += rot; else u0s += rot;
+              } else {
+                if (b & 1) d1s += rot; else d0s += rot;
+              }
             }
+            rowb[i * A.Wc] += u0s + u1s;
+            dnv[i] = d0s + d1s;
           }
-          rowb[i * A.Wc] += u0s + u1s;
-          dnv[i] = d0s + d1s;
-        }
+        };
+        if (__all_sync(kFullMask, pvalid)) reduce_rows(std::false_type{});
+        else reduce_rows(std::true_type{});
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
