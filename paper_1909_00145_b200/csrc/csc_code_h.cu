@@ -326,8 +326,10 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
       const int pw = it.p0 + tl * kChTile + 32 * q;
       const int p = pw + lane;
       const bool pok = p < it.p1;
-      const uint32_t sel = A.mask == nullptr ? (pok ? 0xffffffffu : 0u)
-                                             : (pok ? __ldg(A.mask + static_cast<size_t>(kg * 4 + cb) * plane + p) : 0u);
+      const int nvk = kend - k0;  // filters of this warp's block that exist (the rest is padding)
+      const uint32_t kbits = nvk >= 32 ? 0xffffffffu : (nvk <= 0 ? 0u : ((1u << nvk) - 1u));
+      const uint32_t sel = kbits & (A.mask == nullptr ? (pok ? 0xffffffffu : 0u)
+                                                      : (pok ? __ldg(A.mask + static_cast<size_t>(kg * 4 + cb) * plane + p) : 0u));
       float* zb = A.z + (static_cast<size_t>(it.n) * A.K + k0) * plane + p;
       const float* zs = zs0 + buf * kChEpiWarps * NC * 32;
       if (!plain) mbar_wait_sleep(&z_full[ew][buf], use & 1u);
@@ -336,6 +338,7 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
       const uint32_t colb = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
       // per-filter step sizes (ESO rule) in a separate instantiation of the loop, so the
       // scalar-tau hot path carries no extra loads
+      const float ntinv = -tau * inv;
       auto epi = [&](auto per_k) {
         constexpr bool PK = decltype(per_k)::value;
 #pragma unroll
@@ -357,9 +360,10 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
             const float zv = zs[i * 32 + lane];
             const float tk = PK ? __ldg(A.tau + min(k0 + i, A.K - 1)) : tau;
             const float kk = PK ? tk * A.lam : kappa;
-            const float w = fmaf(-tk, c4[i4] * inv, zv);
-            const float nz = (w > kk) ? (w - kk) : ((w < -kk) ? (w + kk) : 0.f);
-            if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv) {
+            // -tau * (c * 2^-(er+ed)) with one multiply: scaling by a power of two is exact
+            const float w = fmaf(PK ? -tk * inv : ntinv, c4[i4], zv);
+            const float nz = w - fminf(fmaxf(w, -kk), kk);  // S_kk(w): w -/+ kk outside [-kk, kk], +0 inside
+            if (((sel >> i) & 1u) && nz != zv) {
               zb[static_cast<size_t>(i) * plane] = nz;
               wmax = fmaxf(wmax, fabsf(nz));
             }

@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
               const float tk = PK ? __ldg(A.tau + min(k0 + i, A.K - 1)) : tau;
               const float kk = PK ? tk * A.lam : kappa;
               const float w = fmaf(-tk, c4[i4], zv[i]);
-              const float nz = (w > kk) ? (w - kk) : ((w < -kk) ? (w + kk) : 0.f);
+              const float nz = w - fminf(fmaxf(w, -kk), kk);  // S_kk(w): w -/+ kk outside [-kk, kk], +0 inside
               if (((sel >> i) & 1u) && (k0 + i) < kend && nz != zv[i]) {
                 zb[static_cast<size_t>(i) * plane] = nz;
                 wmax = fmaxf(wmax, fabsf(nz));
