@@ -270,10 +270,10 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
           for (int e = ctg; e < n4; e += 128) {
             const float4 x = hi4[e];
             float4 h, l;
-            tf32_split_rn(x.x, h.x, l.x);
-            tf32_split_rn(x.y, h.y, l.y);
-            tf32_split_rn(x.z, h.z, l.z);
-            tf32_split_rn(x.w, h.w, l.w);
+            tf32_split_rn_hi(x.x, h.x, l.x);
+            tf32_split_rn_hi(x.y, h.y, l.y);
+            tf32_split_rn_hi(x.z, h.z, l.z);
+            tf32_split_rn_hi(x.w, h.w, l.w);
             hi4[e] = h;
             lo4[e] = l;
           }
