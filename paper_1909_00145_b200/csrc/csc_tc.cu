@@ -570,6 +570,54 @@ __global__ void tc_fixup_kernel(const float* __restrict__ part, int N, int H, in
   }
 }
 
+// Same as tc_fixup_kernel for W % 4 == 0 with 16-B aligned buffers: a thread takes 4 consecutive
+// columns (float4) and the block covers 256 / (W/4) rows at once, so each thread has its loads of
+// several rows in flight instead of one dependent chain per element.
+__global__ void tc_fixup4_kernel(const float* __restrict__ part, int N, int H, int W, int P, int BR, int nbands,
+                                 const float4* __restrict__ x, float4* __restrict__ r, int mode,
+                                 double* __restrict__ sq_part) {
+  const size_t win = static_cast<size_t>(BR + P) * W;
+  const int W4 = W / 4;
+  const int rpb = blockDim.x / W4 > 0 ? blockDim.x / W4 : 1;  // rows per block step
+  const int rr = threadIdx.x / W4, j4 = threadIdx.x - rr * W4;
+  double sq = 0.0;
+  if (rr < rpb && j4 < W4) {
+    for (int row = blockIdx.x * rpb + rr; row < N * H; row += gridDim.x * rpb) {
+      const int n = row / H, i = row - n * H;
+      const int b0 = i / BR;
+      int b1 = (i + P) / BR;
+      if (b1 > nbands - 1) b1 = nbands - 1;
+      const float* pk = part + static_cast<size_t>(n) * nbands * win;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int b = b0; b <= b1; ++b) {
+        const float4 t = reinterpret_cast<const float4*>(pk + b * win + static_cast<size_t>(i - b * BR + P) * W)[j4];
+        v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
+      }
+      const size_t o4 = static_cast<size_t>(row) * W4 + j4;
+      if (mode == kConvResidual) {
+        if (x != nullptr) {
+          const float4 xv = x[o4];
+          v.x -= xv.x; v.y -= xv.y; v.z -= xv.z; v.w -= xv.w;
+        }
+        r[o4] = v;
+      }
+      sq += static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y + static_cast<double>(v.z) * v.z +
+            static_cast<double>(v.w) * v.w;
+    }
+  }
+  __shared__ double red[32];
+  double t = sq;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFullMask, t, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    sq_part[blockIdx.x] = s;
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- host side
@@ -691,8 +739,16 @@ cudaError_t launch_tc_bimg(const Geom& g, const TcPlan& p, const float* filt, fl
 
 cudaError_t launch_conv_tc_fixup(const Geom& g, const TcPlan& p, const float* part, const float* x, float* r,
                                  int mode, double* sq_part, cudaStream_t st) {
-  tc_fixup_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, g.N, g.H, g.W, g.P, p.BR, p.nbands, p.nks, x, r, mode,
-                                                    sq_part);
+  if (g.W % 4 == 0 && g.W <= 1024 && (reinterpret_cast<uintptr_t>(part) & 15u) == 0 &&
+      (x == nullptr || (reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
+      (r == nullptr || (reinterpret_cast<uintptr_t>(r) & 15u) == 0)) {
+    tc_fixup4_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, g.N, g.H, g.W, g.P, p.BR, p.nbands,
+                                                       reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(r),
+                                                       mode, sq_part);
+  } else {
+    tc_fixup_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, g.N, g.H, g.W, g.P, p.BR, p.nbands, p.nks, x, r, mode,
+                                                      sq_part);
+  }
   return cudaGetLastError();
 }
 
