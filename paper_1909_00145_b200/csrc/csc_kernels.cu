@@ -605,7 +605,9 @@ __global__ void __launch_bounds__(kLipThreads) lipschitz_partial_kernel(const fl
     rim[kk][a][m2] = im;
   }
   __syncthreads();
-  for (int pt = threadIdx.x; pt < kLipG * kLipG; pt += kLipThreads) {
+  // grid.y splits the 64x64 grid points so that K/2 filter chunks still fill the GPU
+  const int npt = kLipG * kLipG / gridDim.y;
+  for (int pt = blockIdx.y * npt + threadIdx.x; pt < (blockIdx.y + 1) * npt; pt += kLipThreads) {
     const int m1 = pt / kLipG, m2 = pt % kLipG;
     double tot = 0.0;
     for (int kk = 0; kk < k1 - k0; ++kk) {
@@ -628,6 +630,7 @@ __global__ void __launch_bounds__(1024) lipschitz_final_kernel(const double* __r
   double best = 0.0;
   for (int e = threadIdx.x; e < kLipG * kLipG; e += blockDim.x) {
     double s = 0.0;
+#pragma unroll 8
     for (int kc = 0; kc < nkc; ++kc) s += part[static_cast<int64_t>(kc) * kLipG * kLipG + e];
     best = fmax(best, s);
   }
@@ -853,7 +856,7 @@ cudaError_t launch_eso_tau(const Geom& g, const float* d, double p, const double
 cudaError_t launch_lipschitz(const Geom& g, const float* d, double* part, double* lhat, float* tau_out,
                              cudaStream_t st) {
   const int nkc = ceil_div(g.K, kLipKChunk);
-  lipschitz_partial_kernel<<<nkc, kLipThreads, 0, st>>>(d, g, part);
+  lipschitz_partial_kernel<<<dim3(nkc, 4), kLipThreads, 0, st>>>(d, g, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   lipschitz_final_kernel<<<1, 1024, 0, st>>>(part, nkc, lhat, tau_out);
