@@ -451,7 +451,7 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   ok = ok && alloc(reinterpret_cast<void**>(&c->g32), sizeof(float) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->tauk), sizeof(float) * g.K);
   ok = ok && alloc(reinterpret_cast<void**>(&c->colw), sizeof(uint32_t) * static_cast<size_t>(g.K) * NB * g.Wc);
-  ok = ok && alloc(reinterpret_cast<void**>(&c->lip_part), sizeof(double) * 64 * 64 * csc::ceil_div(g.K, 2));
+  ok = ok && alloc(reinterpret_cast<void**>(&c->lip_part), sizeof(double) * (64 * 64 * csc::ceil_div(g.K, 2) + 64));
   ok = ok && alloc(reinterpret_cast<void**>(&c->dscal), sizeof(double) * kNumD);
   ok = ok && alloc(reinterpret_cast<void**>(&c->fscal), sizeof(float) * kNumF);
   ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_dscal), sizeof(double) * kNumD) == cudaSuccess;
@@ -644,7 +644,7 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   if (step_z > 0.f) {
     CSC_CUDA(c, cudaMemcpyAsync(c->fscal + kTauZ, &step_z, sizeof(float), cudaMemcpyHostToDevice, c->st));
   } else {
-    CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 2, csc::launch_lipschitz(g, d, c->lip_part, c->dscal + kLhat, c->fscal + kTauZ, c->st));
+    CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 3, csc::launch_lipschitz(g, d, c->lip_part, c->dscal + kLhat, c->fscal + kTauZ, c->st));
     if (eso) CSC_LAUNCH(c, 1, csc::launch_eso_tau(g, d, p, c->dscal + kLhat, c->tauk, c->st));
   }
   c->last_eso = eso;
@@ -1023,7 +1023,7 @@ csc_status csc_read_grad(csc_ctx* c, double* g_dev) {
 csc_status csc_lipschitz(csc_ctx* c, const float* d, double* out) {
   if (!c || !aligned4(d) || !out) return fail(c, CSC_ERR_ARG, "d (device) and out (host) required");
   CSC_CUDA(c, cudaSetDevice(c->device));
-  CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 2, csc::launch_lipschitz(c->g, d, c->lip_part, c->dscal + kLhat, nullptr, c->st));
+  CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 3, csc::launch_lipschitz(c->g, d, c->lip_part, c->dscal + kLhat, nullptr, c->st));
   CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal + kLhat, c->dscal + kLhat, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CSC_CUDA(c, cudaStreamSynchronize(c->st));
   *out = c->h_dscal[kLhat];

@@ -390,7 +390,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
   }
 }
 
-// B image (one block): max |f| -> fmax (float bits); then, with 2^ef, the fp16 hi/lo image
+// B image (16 blocks, each computing the same max |f| -> fmax, float bits); then, with 2^ef, the fp16 hi/lo image
 // bimg[ks][hl][atom][k][64 taps] in the MN-major SW128 layout (16-B chunk (t%64)/8 XOR (k%8)).
 __global__ void __launch_bounds__(1024) bimg_h_kernel(const float* __restrict__ f, int K, int S2, int KC, int nks,
                                                       uint16_t* __restrict__ bimg, uint32_t* __restrict__ fmax) {
@@ -404,10 +404,11 @@ __global__ void __launch_bounds__(1024) bimg_h_kernel(const float* __restrict__ 
   if ((threadIdx.x & 31) == 0) atomicMax(&mx, m);
   __syncthreads();
   const uint32_t mbits = mx;
-  if (threadIdx.x == 0) *fmax = mbits;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *fmax = mbits;
   const float sf = exp2i(scale_exp(mbits));
   const int total = nks * KC * 128;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+  // every block finds the (same) max over the small filter tensor, then writes its share
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int t = e & 127;
     const int k = (e >> 7) % KC, ks = (e >> 7) / KC;
     const int kg = ks * KC + k;
@@ -531,7 +532,7 @@ cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const 
     cached_g = g;
   }
   uint16_t* bimg = reinterpret_cast<uint16_t*>(bimg_f);
-  if (build_b) bimg_h_kernel<<<1, 1024, 0, st>>>(filt, g.K, g.S * g.S, p.KC, p.nks, bimg, fmax);
+  if (build_b) bimg_h_kernel<<<16, 1024, 0, st>>>(filt, g.K, g.S * g.S, p.KC, p.nks, bimg, fmax);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   HArgs a{};

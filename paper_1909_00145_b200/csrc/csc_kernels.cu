@@ -625,20 +625,29 @@ __global__ void __launch_bounds__(kLipThreads) lipschitz_partial_kernel(const fl
   }
 }
 
-__global__ void __launch_bounds__(1024) lipschitz_final_kernel(const double* __restrict__ part, int nkc,
-                                                              double* __restrict__ lhat, float* __restrict__ tau_out) {
+// Per grid point: sum of the filter-chunk partials (fixed order); per block: the max over its
+// points -> bmax[blockIdx.x].  Then lipschitz_max_kernel takes the max over the blocks.
+constexpr int kLipFinalBlocks = 16;
+__global__ void __launch_bounds__(256) lipschitz_final_kernel(const double* __restrict__ part, int nkc,
+                                                             double* __restrict__ bmax) {
   double best = 0.0;
-  for (int e = threadIdx.x; e < kLipG * kLipG; e += blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kLipG * kLipG; e += gridDim.x * blockDim.x) {
     double s = 0.0;
-#pragma unroll 8
+#pragma unroll 10
     for (int kc = 0; kc < nkc; ++kc) s += part[static_cast<int64_t>(kc) * kLipG * kLipG + e];
     best = fmax(best, s);
   }
   const double m = block_max_d(best);
-  if (threadIdx.x == 0) {
-    *lhat = m;
-    if (tau_out != nullptr) *tau_out = m > 0.0 ? static_cast<float>(1.0 / m) : 0.f;
-  }
+  if (threadIdx.x == 0) bmax[blockIdx.x] = m;
+}
+
+__global__ void lipschitz_max_kernel(const double* __restrict__ bmax, double* __restrict__ lhat,
+                                     float* __restrict__ tau_out) {
+  if (threadIdx.x != 0) return;
+  double m = 0.0;
+  for (int b = 0; b < kLipFinalBlocks; ++b) m = fmax(m, bmax[b]);
+  *lhat = m;
+  if (tau_out != nullptr) *tau_out = m > 0.0 ? static_cast<float>(1.0 / m) : 0.f;
 }
 
 // ------------------------------------------------------------------ filter update
@@ -859,7 +868,9 @@ cudaError_t launch_lipschitz(const Geom& g, const float* d, double* part, double
   lipschitz_partial_kernel<<<dim3(nkc, 4), kLipThreads, 0, st>>>(d, g, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  lipschitz_final_kernel<<<1, 1024, 0, st>>>(part, nkc, lhat, tau_out);
+  double* bmax = part + static_cast<int64_t>(nkc) * kLipG * kLipG;  // lip_part has room (see csc_init)
+  lipschitz_final_kernel<<<kLipFinalBlocks, 256, 0, st>>>(part, nkc, bmax);
+  lipschitz_max_kernel<<<1, 32, 0, st>>>(bmax, lhat, tau_out);
   return cudaGetLastError();
 }
 
