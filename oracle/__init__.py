@@ -67,6 +67,8 @@ def lib():
                 getattr(L, f"oracle_filter_step_{suf}").argtypes = (
                     [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _vp, _vp, _vp])
                 getattr(L, f"oracle_objective_{suf}").argtypes = [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _vp]
+                getattr(L, f"oracle_filter_step_bcd_{suf}").argtypes = (
+                    [_c_i64] * 5 + [_vp] * 3 + [ctypes.c_int, _vp])
             _lib = L
     return _lib
 
@@ -216,6 +218,24 @@ def filter_step(x, d, z, step_d=0.0, dtype=np.float32):
     getattr(lib(), f"oracle_filter_step_{_suf(dtype)}")(
         N, K, s, H, W, _p(x), _p(d), _p(z), float(step_d), _p(tau), _p(g), _p(zg2))
     return d, float(tau[0]), g, float(zg2[0])
+
+
+BCD_RIDGE = 1e-10  # reading B2: ridge eps * tr(C_kk) / M in the block solve
+
+
+def filter_step_bcd(x, d, z, sweeps=1, dtype=np.float32):
+    """Projected block-coordinate descent on the filters: per filter
+    k in order, the exact minimiser of the Eq.5 quadratic in d_k (others fixed), projected on the unit
+    ball.  Returns (d_new, flags) with flags[k] = 1 for a filter left unchanged (no nonzero code)."""
+    x = _c(x, dtype); z = _c(z, dtype)
+    d = np.array(d, dtype=dtype, copy=True, order="C")
+    N, K, Hc, Wc = z.shape
+    s = d.shape[-1]
+    H, W = Hc - s + 1, Wc - s + 1
+    flags = np.zeros(K, dtype=np.uint8)
+    getattr(lib(), f"oracle_filter_step_bcd_{_suf(dtype)}")(
+        N, K, s, H, W, _p(x), _p(d), _p(z), int(sweeps), _p(flags))
+    return d, flags
 
 
 def objective(x, d, z, lam, dtype=np.float32):

@@ -412,6 +412,124 @@ void filter_step(const Dims& D, const T* x, T* d, const T* z, double step_d, dou
   if (zg2_out) *zg2_out = zg2;
 }
 
+// Projected block-coordinate descent on the filters ("solved
+// by projected block coordinate decent ... a single iteration is enough with f computed in previous
+// iteration as a warm start"; readings B1-B4).  Blocks = filters, ascending k.  Per block,
+// with the other filters fixed, the Eq.5 quadratic in d_k is minimised exactly:
+//   C_kk = sum_n Z_nk^T Z_nk (M x M),  g_k = sum_n Z_nk^T r_n (r = Z d - x, current),
+//   delta = -(C_kk + eps tr(C_kk)/M I)^{-1} g_k   (Cholesky; eps = BCD_RIDGE, reading B2),
+// then d_k <- P_ball(d_k + delta) (R7) and r <- r + Z_k (d_k,new - d_k,old).  tr(C_kk) = 0 (filter k
+// has no nonzero code): d_k unchanged, flags[k] = 1.  C, g, r in fp64; d stored in T.
+static const double BCD_RIDGE = 1e-10;
+
+// Cholesky factor of the SPD matrix A (n x n, row-major) in place (lower triangle); false if a pivot
+// is not positive.
+static bool cholesky(std::vector<double>& A, int64_t n) {
+  for (int64_t j = 0; j < n; ++j) {
+    double s = A[j * n + j];
+    for (int64_t q = 0; q < j; ++q) s -= A[j * n + q] * A[j * n + q];
+    if (!(s > 0.0)) return false;
+    const double ljj = std::sqrt(s);
+    A[j * n + j] = ljj;
+    for (int64_t i = j + 1; i < n; ++i) {
+      double t = A[i * n + j];
+      for (int64_t q = 0; q < j; ++q) t -= A[i * n + q] * A[j * n + q];
+      A[i * n + j] = t / ljj;
+    }
+  }
+  return true;
+}
+
+template <typename T>
+void filter_step_bcd(const Dims& D, const T* x, T* d, const T* z, int sweeps, uint8_t* flags) {
+  const int64_t M = D.s * D.s;
+  const size_t npx = (size_t)(D.N * D.H * D.W);
+  std::vector<double> r(npx);
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < D.N; ++n)
+    for (int64_t i = 0; i < D.H; ++i)
+      for (int64_t j = 0; j < D.W; ++j) {
+        double acc = 0.0;
+        for (int64_t k = 0; k < D.K; ++k)
+          for (int64_t a = 0; a < D.s; ++a)
+            for (int64_t b = 0; b < D.s; ++b)
+              acc += (double)d[D.di(k, a, b)] * (double)z[D.zi(n, k, i + D.P - a, j + D.P - b)];
+        r[D.xi(n, i, j)] = acc - (double)x[D.xi(n, i, j)];
+      }
+  if (flags)
+    for (int64_t k = 0; k < D.K; ++k) flags[k] = 0;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int64_t k = 0; k < D.K; ++k) {
+      std::vector<double> C((size_t)(M * M), 0.0), g((size_t)M, 0.0);
+#pragma omp parallel for schedule(static)
+      for (int64_t t1 = 0; t1 < M; ++t1) {
+        const int64_t a1 = t1 / D.s, b1 = t1 % D.s;
+        for (int64_t t2 = 0; t2 < M; ++t2) {
+          const int64_t a2 = t2 / D.s, b2 = t2 % D.s;
+          double acc = 0.0;
+          for (int64_t n = 0; n < D.N; ++n)
+            for (int64_t i = 0; i < D.H; ++i)
+              for (int64_t j = 0; j < D.W; ++j)
+                acc += (double)z[D.zi(n, k, i + D.P - a1, j + D.P - b1)] *
+                       (double)z[D.zi(n, k, i + D.P - a2, j + D.P - b2)];
+          C[t1 * M + t2] = acc;
+        }
+        double acc = 0.0;
+        for (int64_t n = 0; n < D.N; ++n)
+          for (int64_t i = 0; i < D.H; ++i)
+            for (int64_t j = 0; j < D.W; ++j)
+              acc += r[D.xi(n, i, j)] * (double)z[D.zi(n, k, i + D.P - a1, j + D.P - b1)];
+        g[t1] = acc;
+      }
+      double tr = 0.0;
+      for (int64_t m = 0; m < M; ++m) tr += C[m * M + m];
+      if (!(tr > 0.0)) {
+        if (flags) flags[k] = 1;
+        continue;
+      }
+      const double ridge = BCD_RIDGE * tr / (double)M;
+      for (int64_t m = 0; m < M; ++m) C[m * M + m] += ridge;
+      if (!cholesky(C, M)) {
+        if (flags) flags[k] = 1;
+        continue;
+      }
+      // solve L L^T delta = -g
+      std::vector<double> y((size_t)M), e((size_t)M);
+      for (int64_t i = 0; i < M; ++i) {
+        double t = -g[i];
+        for (int64_t q = 0; q < i; ++q) t -= C[i * M + q] * y[q];
+        y[i] = t / C[i * M + i];
+      }
+      for (int64_t i = M - 1; i >= 0; --i) {
+        double t = y[i];
+        for (int64_t q = i + 1; q < M; ++q) t -= C[q * M + i] * e[q];
+        e[i] = t / C[i * M + i];
+      }
+      double nrm2 = 0.0;
+      for (int64_t m = 0; m < M; ++m) {
+        e[m] += (double)d[k * M + m];
+        nrm2 += e[m] * e[m];
+      }
+      const double scale = std::max(1.0, std::sqrt(nrm2));
+      std::vector<double> dl((size_t)M);
+      for (int64_t m = 0; m < M; ++m) {
+        const T dn = (T)(e[m] / scale);
+        dl[m] = (double)dn - (double)d[k * M + m];
+        d[k * M + m] = dn;
+      }
+#pragma omp parallel for schedule(static)
+      for (int64_t n = 0; n < D.N; ++n)
+        for (int64_t i = 0; i < D.H; ++i)
+          for (int64_t j = 0; j < D.W; ++j) {
+            double acc = 0.0;
+            for (int64_t a = 0; a < D.s; ++a)
+              for (int64_t b = 0; b < D.s; ++b)
+                acc += dl[a * D.s + b] * (double)z[D.zi(n, k, i + D.P - a, j + D.P - b)];
+            r[D.xi(n, i, j)] += acc;
+          }
+    }
+}
+
 // Eq.1 objective: F = sum_n 1/2||x_n - sum_k d_k * z_{n,k}||^2 + lam sum ||z||_1.
 template <typename T>
 void objective(const Dims& D, const T* x, const T* d, const T* z, double lam, double out[3]) {
@@ -517,6 +635,10 @@ double oracle_soft_threshold(double w, double kappa) { return soft_threshold(w, 
                                 const T* x, T* d, const T* z, double step_d, double* tau_used,   \
                                 double* g_out, double* zg2_out) {                                \
     filter_step<T>(Dims(N, K, s, H, W), x, d, z, step_d, tau_used, g_out, zg2_out);             \
+  }                                                                                              \
+  void oracle_filter_step_bcd_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,       \
+                                    const T* x, T* d, const T* z, int sweeps, uint8_t* flags) {    \
+    filter_step_bcd<T>(Dims(N, K, s, H, W), x, d, z, sweeps, flags);                             \
   }                                                                                              \
   void oracle_objective_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W, const T* x, \
                               const T* d, const T* z, double lam, double out[3]) {               \
