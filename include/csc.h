@@ -144,6 +144,19 @@ csc_status csc_set_step_rule(csc_ctx* ctx, int rule);
  * times unless that step used the ESO rule). */
 csc_status csc_read_step_z(csc_ctx* ctx, float* tau_dev);
 
+/* Projected block-coordinate descent on the filters (§3.2; SURVEY.md §8f NEXT-3;
+ * DESIGN.md §11, readings B1-B4), in place of the one-step csc_filter_step.  Per sweep, for
+ * k = 0..K-1 in order, with the other filters fixed, the Eq.5 quadratic in d_k is minimised exactly
+ *   C_kk = sum_n Z_nk^T Z_nk,  g_k = sum_n Z_nk^T (Z_n d - x_n)  (all ranks),
+ *   d_k <- P_ball(d_k - (C_kk + 1e-10 tr(C_kk)/M I)^-1 g_k),  P_ball(e) = e / max(1, ||e||)
+ * and the residual is updated with the change.  A filter whose codes are all zero is left
+ * unchanged (flags_out[k] = 1; flags_out is a HOST array of K bytes or NULL).  sweeps >= 1 (the
+ * paper uses one, warm-started).  Requires s*s <= 128.  Collective (one all-reduce of the Gram
+ * blocks per sweep and one of g_k per filter).  Scratch (K*(splits+1)*M*M doubles) is allocated on
+ * the first call. */
+csc_status csc_filter_step_bcd(csc_ctx* ctx, const float* x, float* d, const float* z, int sweeps,
+                               uint8_t* flags_out);
+
 /* Forget the residual cache (caller changed x, d or z outside the API). */
 csc_status csc_invalidate(csc_ctx* ctx);
 
@@ -190,7 +203,8 @@ typedef enum {
   CSC_K_LIPSCHITZ = 5,     /* DTFT bound */
   CSC_K_SMALL = 6,         /* reductions, step size, update/projection */
   CSC_K_ADMM = 7,          /* ADMM solver: masked D^T and CG / ADMM vector kernels */
-  CSC_K_NCLASS = 8
+  CSC_K_BCD = 8,           /* block-coordinate filter update: Gram, inverse, per-filter kernels */
+  CSC_K_NCLASS = 9
 } csc_kernel_class;
 
 /* Enable (1) / disable (0) per-launch event timing; enabling resets the totals. */

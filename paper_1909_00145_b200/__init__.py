@@ -29,11 +29,11 @@ ABI_SYMBOLS = (
     "csc_zero_codes", "csc_destroy", "csc_last_error", "csc_nccl_unique_id", "csc_abi_version",
     "csc_mask_bits", "csc_read_residual", "csc_read_grad", "csc_lipschitz", "csc_launch_count",
     "csc_profile_enable", "csc_profile_read", "csc_kernel_variants", "csc_code_step_admm",
-    "csc_set_step_rule", "csc_read_step_z",
+    "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd",
 )
 
 # csc_kernel_class (include/csc.h)
-KERNEL_CLASSES = ("conv", "conv_finalize", "wgrad", "code_step", "mask", "lipschitz", "small", "admm")
+KERNEL_CLASSES = ("conv", "conv_finalize", "wgrad", "code_step", "mask", "lipschitz", "small", "admm", "bcd")
 
 
 class CSCError(RuntimeError):
@@ -69,6 +69,7 @@ def load_library(path: Optional[str] = None):
         L.csc_code_step.argtypes = [vp, vp, vp, vp, f32, f32, f64, u64, u32, vp]
         L.csc_filter_step.argtypes = [vp, vp, vp, vp, f32, vp]
         L.csc_set_step_rule.argtypes = [vp, ctypes.c_int]
+        L.csc_filter_step_bcd.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
         L.csc_read_step_z.argtypes = [vp, vp]
         L.csc_code_step_admm.argtypes = [vp, vp, vp, vp, f32, f32, f32, ctypes.c_int, ctypes.c_int, f64, u64, u32]
         L.csc_objective.argtypes = [vp, vp, vp, vp, f32, vp]
@@ -163,6 +164,15 @@ class Context:
                                           int(seed) & (2**64 - 1), int(it) & 0xffffffff,
                                           ctypes.byref(out) if want_step else None))
         return float(out.value) if want_step else None
+
+    def filter_step_bcd(self, x, d, z, sweeps: int = 1, want_flags: bool = False):
+        """Projected block-coordinate filter update (include/csc.h csc_filter_step_bcd).
+        Returns the K per-filter flags (1 = left unchanged) when want_flags."""
+        px, pd, pz = self._xdz(x, d, z)
+        flags = (ctypes.c_uint8 * max(self.K, 1))()
+        self._check(self._L.csc_filter_step_bcd(self._h, px, pd, pz, int(sweeps),
+                                                ctypes.cast(flags, ctypes.c_void_p) if want_flags else None))
+        return list(flags)[:self.K] if want_flags else None
 
     STEP_RULES = {"lipschitz": 0, "eso": 1}
 

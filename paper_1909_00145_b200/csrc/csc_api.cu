@@ -64,6 +64,8 @@ struct NcclApi {
 NcclApi g_nccl;
 std::mutex g_nccl_mu;
 
+constexpr double kBcdRidge = 1e-10;  // DESIGN.md reading B2
+
 // device scalar slots
 enum DSlot { kSqR = 0, kL1 = 1, kZg2 = 2, kGG = 3, kLhat = 4, kNumD = 8 };
 enum FSlot { kTauZ = 0, kTauD = 1, kNumF = 4 };
@@ -114,6 +116,12 @@ struct csc_ctx {
   uint32_t* mwords = nullptr;  // selection-word mask [4*nkg][Hc*Wc]
   uint32_t* rmax = nullptr;    // max|r| (float bits) for the fp16-split code step
   int step_rule = CSC_STEP_LIPSCHITZ;  // built-in tau_z rule (csc_set_step_rule)
+  // projected block-coordinate filter update scratch (csc_bcd.cu), allocated on first use
+  double* bcd_gpart = nullptr;  // [K][splits][M][M]
+  double* bcd_ainv = nullptr;   // [K][M][M]
+  uint8_t* bcd_flags = nullptr; // [K]
+  double* bcd_part = nullptr;   // [gk blocks][M]
+  double* bcd_vec = nullptr;    // gk[M], dl[M]
   bool last_eso = false;       // the last code step used per-filter taus
   float* tauk = nullptr;       // [K] per-filter tau_z of the ESO rule
   // ADMM code solver scratch (csc_admm.cu), allocated by the first csc_code_step_admm
@@ -570,6 +578,11 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->mwords);
   cudaFree(c->rmax);
   cudaFree(c->tauk);
+  cudaFree(c->bcd_gpart);
+  cudaFree(c->bcd_ainv);
+  cudaFree(c->bcd_flags);
+  cudaFree(c->bcd_part);
+  cudaFree(c->bcd_vec);
   cudaFree(c->adm_zd);
   cudaFree(c->adm_e);
   cudaFree(c->adm_cd);
@@ -872,6 +885,67 @@ csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float*
   // z[M] = y; off-mask codes untouched.  The max|z| bound of the fp16 dense pass is raised.
   CSC_LAUNCH_C(c, A, 1, csc::launch_admm_scatter(g, c->adm_idx, mc, ms, Y, z, zbound(c, z), c->st));
   c->cache_valid = false;  // r no longer matches z
+  return CSC_OK;
+}
+
+csc_status csc_filter_step_bcd(csc_ctx* c, const float* x, float* d, const float* z, int sweeps,
+                               uint8_t* flags_out) {
+  csc_status s = check_ptrs(c, x, d, z);
+  if (s != CSC_OK) return s;
+  if (sweeps < 1) return fail(c, CSC_ERR_ARG, "sweeps must be >= 1");
+  if (c->g.S * c->g.S > 128) return fail(c, CSC_ERR_SHAPE, "block solve supports s*s <= 128");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  const int M = g.S * g.S;
+  const int ns = csc::bcd_gram_splits(g);
+  const int nb = csc::bcd_gk_blocks(g);
+  if (c->bcd_gpart == nullptr) {
+    auto al = [](void** q, size_t bytes) { return cudaMalloc(q, bytes < 16 ? 16 : bytes) == cudaSuccess; };
+    bool ok = al(reinterpret_cast<void**>(&c->bcd_gpart), sizeof(double) * g.K * ns * M * M);
+    ok = ok && al(reinterpret_cast<void**>(&c->bcd_ainv), sizeof(double) * g.K * M * M);
+    ok = ok && al(reinterpret_cast<void**>(&c->bcd_flags), static_cast<size_t>(g.K));
+    ok = ok && al(reinterpret_cast<void**>(&c->bcd_part), sizeof(double) * (nb > 0 ? nb : 1) * M);
+    ok = ok && al(reinterpret_cast<void**>(&c->bcd_vec), sizeof(double) * 2 * M);
+    if (!ok) {
+      cudaGetLastError();
+      return fail(c, CSC_ERR_OOM, "BCD scratch allocation failed");
+    }
+  }
+  // r = D z - x (the residual cache when it is valid); the sweep keeps it current
+  if (!cache_ok(c, x, d, z)) {
+    s = dense_residual(c, x, d, z, false);
+    if (s != CSC_OK) return s;
+  }
+  double* gk = c->bcd_vec;
+  double* dl = c->bcd_vec + M;
+  for (int sw = 0; sw < sweeps; ++sw) {
+    // C_kk for all k on this rank's images, summed over ranks, then (C_kk + ridge)^-1
+    if (g.N > 0) {
+      CSC_LAUNCH_C(c, CSC_K_BCD, 1, csc::launch_bcd_gram(g, z, c->bcd_gpart, c->st));
+    } else {
+      CSC_CUDA(c, cudaMemsetAsync(c->bcd_gpart, 0, sizeof(double) * g.K * ns * M * M, c->st));
+    }
+    s = allreduce_d(c, c->bcd_gpart, static_cast<size_t>(g.K) * ns * M * M);
+    if (s != CSC_OK) return s;
+    CSC_LAUNCH_C(c, CSC_K_BCD, 1, csc::launch_bcd_inverse(g, c->bcd_gpart, kBcdRidge, c->bcd_ainv, c->bcd_flags,
+                                                          c->st));
+    for (int k = 0; k < g.K; ++k) {
+      CSC_LAUNCH_C(c, CSC_K_BCD, nb > 0 ? 2 : 1, csc::launch_bcd_gk(g, k, z, c->r, c->bcd_part, gk, c->st));
+      s = allreduce_d(c, gk, static_cast<size_t>(M));
+      if (s != CSC_OK) return s;
+      CSC_LAUNCH_C(c, CSC_K_BCD, g.N > 0 ? 2 : 1, csc::launch_bcd_update(g, k, gk, c->bcd_ainv, c->bcd_flags, d, dl, z,
+                                                                         c->r, c->st));
+    }
+  }
+  // the residual cache now belongs to the updated filters
+  c->cache_valid = true;
+  c->cx = x;
+  c->cd = d;
+  c->cz = z;
+  if (flags_out) {
+    CSC_CUDA(c, cudaMemcpyAsync(flags_out, c->bcd_flags, static_cast<size_t>(g.K), cudaMemcpyDeviceToHost, c->st));
+    CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  }
   return CSC_OK;
 }
 

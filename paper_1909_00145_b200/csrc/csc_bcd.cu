@@ -1,0 +1,364 @@
+// csc_bcd.cu -- projected block-coordinate descent on the filters (PAPER.md
+// P:313-317 "solved by projected block coordinate decent ... a single iteration is enough with f
+// computed in previous iteration as a warm start", readings B1-B4).  The sweep itself
+// is driven by csc_api.cu (csc_filter_step_bcd):
+//   once per sweep:  C_kk = sum_n Z_nk^T Z_nk for every k (bcd_gram_kernel, fp64), then
+//                    A_k^-1 = (C_kk + eps tr(C_kk)/M I)^-1 via Cholesky (bcd_inverse_kernel)
+//   per filter k:    g_k = sum_n Z_nk^T r_n (bcd_gk_kernel, fp64, current residual)
+//                    d_k <- P_ball(d_k - A_k^-1 g_k), delta = d_k,new - d_k,old (bcd_update_kernel)
+//                    r <- r + Z_k delta (bcd_resid_kernel)
+// All sums in fp64 in a fixed order (deterministic).  The products of fp32 codes are exact in fp64.
+#include "csc_internal.cuh"
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace csc {
+namespace {
+
+constexpr unsigned kFullB = 0xffffffffu;
+constexpr int kGramThreads = 256;
+constexpr int kGramBR = 8;  // output rows per staged band
+
+// ---- Gram blocks: block (split, k) accumulates sum over its images n and all positions of
+// X[p][t] X[p][t'] for the 4x4 tap tiles (T1 <= T2) its threads own; X[p][t] = z[n,k,i+P-a,j+P-b].
+__global__ void __launch_bounds__(kGramThreads) bcd_gram_kernel(Geom g, const float* __restrict__ z, int nsplit,
+                                                                double* __restrict__ gpart) {
+  extern __shared__ float zs[];  // [kGramBR + P][Wc] + 1 zero
+  const int k = blockIdx.y, sp = blockIdx.x;
+  const int M = g.S * g.S;
+  const int NT = (M + 3) / 4;                // tap tiles per dimension
+  const int ntiles = NT * (NT + 1) / 2;      // upper-triangular tile pairs
+  const int rows = kGramBR + g.P;
+  const int zero_at = rows * g.Wc;
+  // this thread's (up to 2) tile pairs and their smem tap offsets
+  int off1[2][4], off2[2][4];
+  bool own[2];
+  for (int q = 0; q < 2; ++q) {
+    int id = threadIdx.x + q * kGramThreads;
+    own[q] = id < ntiles;
+    int T1 = 0;
+    if (own[q]) {
+      while (id >= NT - T1) {
+        id -= NT - T1;
+        ++T1;
+      }
+    }
+    const int T2 = T1 + (own[q] ? id : 0);
+    for (int e = 0; e < 4; ++e) {
+      const int t1 = 4 * T1 + e, t2 = 4 * T2 + e;
+      off1[q][e] = t1 < M ? (g.P - t1 / g.S) * g.Wc + (g.P - t1 % g.S) : -1;
+      off2[q][e] = t2 < M ? (g.P - t2 / g.S) * g.Wc + (g.P - t2 % g.S) : -1;
+    }
+  }
+  double acc[2][4][4];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[q][a][b] = 0.0;
+  const int n0 = static_cast<int>((static_cast<int64_t>(sp) * g.N) / nsplit);
+  const int n1 = static_cast<int>((static_cast<int64_t>(sp + 1) * g.N) / nsplit);
+  const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
+  if (threadIdx.x == 0) zs[zero_at] = 0.f;
+  for (int n = n0; n < n1; ++n) {
+    const float* zk = z + (static_cast<int64_t>(n) * g.K + k) * plane;
+    for (int i0 = 0; i0 < g.H; i0 += kGramBR) {
+      __syncthreads();
+      const int nr = min(rows, g.Hc - i0);
+      for (int e = threadIdx.x; e < rows * g.Wc; e += kGramThreads) {
+        const int rr = e / g.Wc;
+        zs[e] = rr < nr ? __ldg(zk + static_cast<int64_t>(i0) * g.Wc + e) : 0.f;
+      }
+      __syncthreads();
+      const int ib = min(kGramBR, g.H - i0);
+      for (int ii = 0; ii < ib; ++ii)
+        for (int j = 0; j < g.W; ++j) {
+          const int base = ii * g.Wc + j;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (!own[q]) continue;
+            double x1[4], x2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              x1[e] = static_cast<double>(zs[off1[q][e] >= 0 ? base + off1[q][e] : zero_at]);
+              x2[e] = static_cast<double>(zs[off2[q][e] >= 0 ? base + off2[q][e] : zero_at]);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[q][a][b] = fma(x1[a], x2[b], acc[q][a][b]);
+          }
+        }
+    }
+  }
+  // partial [k][sp][M][M] (the owned upper tiles; bcd_inverse_kernel mirrors them)
+  double* out = gpart + (static_cast<int64_t>(k) * nsplit + sp) * M * M;
+  for (int q = 0; q < 2; ++q) {
+    if (!own[q]) continue;
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        if (off1[q][a] < 0 || off2[q][b] < 0) continue;
+        // recover t1, t2 from the offsets' tile ids
+        int id = threadIdx.x + q * kGramThreads, T1 = 0;
+        while (id >= NT - T1) {
+          id -= NT - T1;
+          ++T1;
+        }
+        const int t1 = 4 * T1 + a, t2 = 4 * (T1 + id) + b;
+        out[static_cast<int64_t>(t1) * M + t2] = acc[q][a][b];
+      }
+  }
+}
+
+// ---- one block per k: C = sum of the partials (fixed order, upper tiles mirrored), tr, ridge,
+// Cholesky, and the inverse A^-1 (column by column); flags[k] = 1 when tr(C) == 0 or a pivot fails.
+__global__ void bcd_inverse_kernel(Geom g, const double* __restrict__ gpart, int nsplit, double ridge_rel,
+                                   double* __restrict__ ainv, uint8_t* __restrict__ flags) {
+  extern __shared__ double A[];  // [M][M]
+  __shared__ int bad;
+  const int k = blockIdx.x;
+  const int M = g.S * g.S;
+  const int NT = (M + 3) / 4;
+  for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
+    const int t1 = e / M, t2 = e - t1 * M;
+    // the owned entry is the one in the upper tile (T1 <= T2); within a diagonal tile both halves exist
+    const int T1 = t1 / 4, T2 = t2 / 4;
+    const int r1 = T1 <= T2 ? t1 : t2, r2 = T1 <= T2 ? t2 : t1;
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) s += gpart[(static_cast<int64_t>(k) * nsplit + sp) * M * M + static_cast<int64_t>(r1) * M + r2];
+    A[e] = s;
+  }
+  (void)NT;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int m = 0; m < M; ++m) tr += A[m * M + m];
+    if (!(tr > 0.0)) bad = 1;
+    else {
+      const double rd = ridge_rel * tr / static_cast<double>(M);
+      for (int m = 0; m < M; ++m) A[m * M + m] += rd;
+    }
+  }
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) flags[k] = 1;
+    return;
+  }
+  // Cholesky in place (lower triangle), column by column
+  for (int j = 0; j < M; ++j) {
+    if (threadIdx.x == 0) {
+      double s = A[j * M + j];
+      for (int q = 0; q < j; ++q) s -= A[j * M + q] * A[j * M + q];
+      if (!(s > 0.0)) bad = 1;
+      A[j * M + j] = s > 0.0 ? sqrt(s) : 1.0;
+    }
+    __syncthreads();
+    const double ljj = A[j * M + j];
+    for (int i = j + 1 + threadIdx.x; i < M; i += blockDim.x) {
+      double t = A[i * M + j];
+      for (int q = 0; q < j; ++q) t -= A[i * M + q] * A[j * M + q];
+      A[i * M + j] = t / ljj;
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (threadIdx.x == 0) flags[k] = 1;
+    return;
+  }
+  if (threadIdx.x == 0) flags[k] = 0;
+  // A^-1 column c: L y = e_c, L^T x = y (one thread per column)
+  double* out = ainv + static_cast<int64_t>(k) * M * M;
+  for (int c = threadIdx.x; c < M; c += blockDim.x) {
+    double y[128];
+    for (int i = 0; i < M; ++i) {
+      double t = i == c ? 1.0 : 0.0;
+      for (int q = 0; q < i; ++q) t -= A[i * M + q] * y[q];
+      y[i] = t / A[i * M + i];
+    }
+    for (int i = M - 1; i >= 0; --i) {
+      double t = y[i];
+      for (int q = i + 1; q < M; ++q) t -= A[q * M + i] * y[q];
+      y[i] = t / A[i * M + i];
+    }
+    for (int i = 0; i < M; ++i) out[static_cast<int64_t>(i) * M + c] = y[i];
+  }
+}
+
+// ---- g_k partials: block (n, row band) computes sum over its positions of r[p] X[p][t], t = tap
+// (thread t < M), in fp64 -> part[blk][M]
+constexpr int kGkBR = 16;
+__global__ void bcd_gk_kernel(Geom g, int k, const float* __restrict__ z, const float* __restrict__ r,
+                              double* __restrict__ part) {
+  extern __shared__ float sm[];  // z rows [kGkBR + P][Wc], r rows [kGkBR][W]
+  const int nbands = (g.H + kGkBR - 1) / kGkBR;
+  const int n = blockIdx.x / nbands, band = blockIdx.x - n * nbands;
+  const int i0 = band * kGkBR;
+  const int ib = min(kGkBR, g.H - i0);
+  const int rows = kGkBR + g.P;
+  float* zs = sm;
+  float* rsm = sm + rows * g.Wc;
+  const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
+  const float* zk = z + (static_cast<int64_t>(n) * g.K + k) * plane;
+  for (int e = threadIdx.x; e < rows * g.Wc; e += blockDim.x) {
+    const int rr = e / g.Wc;
+    zs[e] = (i0 + rr < g.Hc) ? __ldg(zk + static_cast<int64_t>(i0) * g.Wc + e) : 0.f;
+  }
+  for (int e = threadIdx.x; e < ib * g.W; e += blockDim.x)
+    rsm[e] = r[(static_cast<int64_t>(n) * g.H + i0) * g.W + e];
+  __syncthreads();
+  const int M = g.S * g.S;
+  const int t = threadIdx.x;
+  if (t < M) {
+    const int a = t / g.S, b = t - a * g.S;
+    double acc = 0.0;
+    for (int ii = 0; ii < ib; ++ii) {
+      const float* zrow = zs + (ii + g.P - a) * g.Wc + (g.P - b);
+      const float* rrow = rsm + ii * g.W;
+      double s = 0.0;
+      for (int j = 0; j < g.W; ++j) s = fma(static_cast<double>(rrow[j]), static_cast<double>(zrow[j]), s);
+      acc += s;
+    }
+    part[static_cast<int64_t>(blockIdx.x) * M + t] = acc;
+  }
+}
+
+// ---- gk[t] = sum of the g_k partials (fixed order)
+__global__ void bcd_gsum_kernel(int M, const double* __restrict__ part, int nparts, double* __restrict__ gk) {
+  const int t = threadIdx.x;
+  if (t >= M) return;
+  double s = 0.0;
+  for (int b = 0; b < nparts; ++b) s += part[static_cast<int64_t>(b) * M + t];
+  gk[t] = s;
+}
+
+// ---- one block: delta = -A^-1 g_k, e = d_k + delta, d_k <- e / max(1, ||e||) (fp32),
+// dl = d_k,new - d_k,old (fp64).  Flagged filters: dl = 0, d_k unchanged.
+__global__ void bcd_update_kernel(Geom g, int k, const double* __restrict__ gk, const double* __restrict__ ainv,
+                                  const uint8_t* __restrict__ flags, float* __restrict__ d, double* __restrict__ dl) {
+  __shared__ double gs[128], es[128], red[32];
+  const int M = g.S * g.S;
+  const int t = threadIdx.x;
+  if (flags[k]) {
+    if (t < M) dl[t] = 0.0;
+    return;
+  }
+  if (t < M) gs[t] = gk[t];
+  __syncthreads();
+  double e = 0.0;
+  if (t < M) {
+    const double* row = ainv + (static_cast<int64_t>(k) * M + t) * M;
+    double s = 0.0;
+    for (int q = 0; q < M; ++q) s = fma(row[q], gs[q], s);
+    e = static_cast<double>(d[static_cast<int64_t>(k) * M + t]) - s;
+    es[t] = e;
+  }
+  double v = t < M ? e * e : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullB, v, o);
+  if ((t & 31) == 0) red[t >> 5] = v;
+  __syncthreads();
+  if (t == 0) {
+    double nrm2 = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) nrm2 += red[w];
+    red[0] = fmax(1.0, sqrt(nrm2));
+  }
+  __syncthreads();
+  if (t < M) {
+    const float dn = static_cast<float>(es[t] / red[0]);
+    const int64_t di = static_cast<int64_t>(k) * M + t;
+    dl[t] = static_cast<double>(dn) - static_cast<double>(d[di]);
+    d[di] = dn;
+  }
+}
+
+// ---- r[n,i,j] += sum_ab dl[a,b] z[n,k,i+P-a,j+P-b]
+__global__ void bcd_resid_kernel(Geom g, int k, const float* __restrict__ z, const double* __restrict__ dl,
+                                 float* __restrict__ r) {
+  __shared__ double dls[128];
+  const int M = g.S * g.S;
+  if (threadIdx.x < M) dls[threadIdx.x] = dl[threadIdx.x];
+  __syncthreads();
+  const int64_t npx = static_cast<int64_t>(g.N) * g.H * g.W;
+  const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < npx;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = q / (static_cast<int64_t>(g.H) * g.W);
+    const int64_t rem = q - n * g.H * g.W;
+    const int i = static_cast<int>(rem / g.W), j = static_cast<int>(rem - static_cast<int64_t>(i) * g.W);
+    const float* zk = z + (n * g.K + k) * plane;
+    double s = 0.0;
+    for (int a = 0; a < g.S; ++a)
+      for (int b = 0; b < g.S; ++b)
+        s = fma(dls[a * g.S + b], static_cast<double>(__ldg(zk + static_cast<int64_t>(i + g.P - a) * g.Wc + j + g.P - b)),
+                s);
+    r[q] = static_cast<float>(static_cast<double>(r[q]) + s);
+  }
+}
+
+}  // namespace
+
+int bcd_gram_splits(const Geom& g) {
+  int ns = (148 * 2 + g.K - 1) / g.K;  // independent of the local image count (same on every rank)
+  if (ns < 1) ns = 1;
+  return ns;
+}
+int bcd_gk_blocks(const Geom& g) { return g.N * ((g.H + kGkBR - 1) / kGkBR); }
+
+cudaError_t launch_bcd_gram(const Geom& g, const float* z, double* gpart, cudaStream_t st) {
+  const int ns = bcd_gram_splits(g);
+  const size_t smem = sizeof(float) * ((kGramBR + g.P) * g.Wc + 1);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(bcd_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  bcd_gram_kernel<<<dim3(ns, g.K), kGramThreads, smem, st>>>(g, z, ns, gpart);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_inverse(const Geom& g, const double* gpart, double ridge_rel, double* ainv, uint8_t* flags,
+                               cudaStream_t st) {
+  const int M = g.S * g.S;
+  const size_t smem2 = sizeof(double) * M * M;
+  if (smem2 > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(bcd_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem2));
+    if (e != cudaSuccess) return e;
+  }
+  bcd_inverse_kernel<<<g.K, 128, smem2, st>>>(g, gpart, bcd_gram_splits(g), ridge_rel, ainv, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_gk(const Geom& g, int k, const float* z, const float* r, double* part, double* gk,
+                          cudaStream_t st) {
+  const int M = g.S * g.S;
+  const int nb = bcd_gk_blocks(g);
+  if (nb > 0) {
+    const size_t smem = sizeof(float) * ((kGkBR + g.P) * g.Wc + kGkBR * g.W);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(bcd_gk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    bcd_gk_kernel<<<nb, 128, smem, st>>>(g, k, z, r, part);
+  }
+  bcd_gsum_kernel<<<1, 128, 0, st>>>(M, part, nb, gk);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_update(const Geom& g, int k, const double* gk, const double* ainv, const uint8_t* flags,
+                              float* d, double* dl, const float* z, float* r, cudaStream_t st) {
+  bcd_update_kernel<<<1, 128, 0, st>>>(g, k, gk, ainv, flags, d, dl);
+  const int64_t npx = static_cast<int64_t>(g.N) * g.H * g.W;
+  if (npx > 0) {
+    int64_t rb = (npx + 255) / 256;
+    if (rb > 148 * 8) rb = 148 * 8;
+    bcd_resid_kernel<<<static_cast<unsigned>(rb), 256, 0, st>>>(g, k, z, dl, r);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace csc

@@ -219,4 +219,17 @@ cudaError_t launch_cg_step(const Geom& g, int64_t ms, const double* rr, const do
 cudaError_t launch_admm_update(const Geom& g, int64_t ms, const float* W, float* Y, float* U, float* R, float alpha,
                                float kappa, float rho, double* part, double* rr, cudaStream_t st);
 
+// Projected block-coordinate filter update (csc_bcd.cu).  gpart: K * bcd_gram_splits * M * M
+// doubles (the per-rank Gram partials; all-reduce them for world > 1), ainv: K * M * M doubles,
+// flags: K bytes (1 = filter left unchanged), part: bcd_gk_blocks * M doubles, gk / dl: M doubles.
+int bcd_gram_splits(const Geom& g);
+int bcd_gk_blocks(const Geom& g);
+cudaError_t launch_bcd_gram(const Geom& g, const float* z, double* gpart, cudaStream_t st);
+cudaError_t launch_bcd_inverse(const Geom& g, const double* gpart, double ridge_rel, double* ainv, uint8_t* flags,
+                               cudaStream_t st);
+cudaError_t launch_bcd_gk(const Geom& g, int k, const float* z, const float* r, double* part, double* gk,
+                          cudaStream_t st);
+cudaError_t launch_bcd_update(const Geom& g, int k, const double* gk, const double* ainv, const uint8_t* flags,
+                              float* d, double* dl, const float* z, float* r, cudaStream_t st);
+
 }  // namespace csc
