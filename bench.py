@@ -117,6 +117,17 @@ def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox"):
             out[name] = {"kernel": "wgrad_kernel (SIMT FP32)", "bound": "alu",
                          "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
                          "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
+        elif name == "bcd":
+            # Gram blocks C_kk = sum_n Z_nk^T Z_nk in fp64 dominate: N K H W (M^2/2 + M/2) fp64 FMA per sweep
+            # (upper triangle incl. the diagonal tiles), against the fp64 FMA rate
+            M = cfg.s * cfg.s
+            nt = (M + 3) // 4
+            fma = nl * cfg.K * cfg.H * cfg.W * 16.0 * nt * (nt + 1) / 2
+            fp64_peak = SMS * 64 * 2 * sm_max_mhz * 1e6 / 1e12
+            out[name] = {"kernel": "bcd_gram_kernel + per-filter kernels (fp64, csc_bcd.cu)", "bound": "alu",
+                         "achieved": 2.0 * fma / (ms / steps / 1e3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "peak_note": f"148 SMs x 64 FP64 lanes x 2 x {sm_max_mhz:.0f} MHz (derived, DESIGN.md §11)",
+                         "flop_model": "2 * N K H W * 16 * (ceil(M/4)(ceil(M/4)+1)/2) per sweep (whole class time)"}
         elif name == "code_step" and solver == "admm":
             # ADMM mode: code_h_kernel in plain mode writes the dense correlation D^T e
             out[name] = two_roofs("code_h_kernel plain mode (dense D^T e for the ADMM operator)", avg,
@@ -324,17 +335,25 @@ def run_ours(args):
             dist.barrier(device_ids=[local])
 
     admm = args.code_solver == "admm"
+    bcd = args.filter_solver == "bcd"
 
     def step(it, x_host=None):
-        """One outer iteration: csc_iterate (prox code step), or with --code-solver admm the paper's
-        ADMM code update (csc_code_step_admm) followed by the filter step and the objective."""
-        if not admm:
+        """One outer iteration: csc_iterate (prox code step + projected-gradient filter step), or with
+        --code-solver admm / --filter-solver bcd the paper's ADMM code update (csc_code_step_admm) /
+        projected block-coordinate filter update (csc_filter_step_bcd), then the objective."""
+        if not admm and not bcd:
             return ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it, x_host=x_host)
         if x_host is not None:
             x.copy_(x_host, non_blocking=True)
             ctx.invalidate()
-        ctx.code_step_admm(x, d, z, cfg.lam, cfg.p, seed, it)
-        ctx.filter_step(x, d, z)
+        if admm:
+            ctx.code_step_admm(x, d, z, cfg.lam, cfg.p, seed, it)
+        else:
+            ctx.code_step(x, d, z, cfg.lam, cfg.p, seed, it)
+        if bcd:
+            ctx.filter_step_bcd(x, d, z)
+        else:
+            ctx.filter_step(x, d, z)
         return ctx.objective(x, d, z, cfg.lam), None
 
     it = 0
@@ -404,7 +423,8 @@ def run_ours(args):
             "metric": "csc_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": dict(_config_dict(cfg, ws), code_solver=args.code_solver, step_rule=args.step_rule),
+            "config": dict(_config_dict(cfg, ws), code_solver=args.code_solver, filter_solver=args.filter_solver,
+                           step_rule=args.step_rule),
             "roofline": dict(rl[dom], dominant_class=dom),
             "kernel_rooflines": rl,
             "kernels": kernels,
@@ -433,6 +453,9 @@ def main():
     ap.add_argument("--ref-images", type=int, default=1)
     ap.add_argument("--cpu-images", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--filter-solver", default="pg", choices=["pg", "bcd"],
+                    help="pg: the north_star projected-gradient filter step (default); bcd: the paper's "
+                         "projected block-coordinate update, one warm-started sweep (SURVEY.md §8f NEXT-3)")
     ap.add_argument("--step-rule", default="lipschitz", choices=["lipschitz", "eso"],
                     help="built-in tau_z rule of the prox code step (eso: SURVEY.md §8f NEXT-4 (i))")
     ap.add_argument("--code-solver", default="prox", choices=["prox", "admm"],
