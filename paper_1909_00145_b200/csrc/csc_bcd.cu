@@ -24,7 +24,7 @@ constexpr int kGramBR = 8;  // output rows per staged band
 // X[p][t] X[p][t'] for the 4x4 tap tiles (T1 <= T2) its threads own; X[p][t] = z[n,k,i+P-a,j+P-b].
 __global__ void __launch_bounds__(kGramThreads) bcd_gram_kernel(Geom g, const float* __restrict__ z, int nsplit,
                                                                 double* __restrict__ gpart) {
-  extern __shared__ float zs[];  // [kGramBR + P][Wc] + 1 zero
+  extern __shared__ double zs[];  // [kGramBR + P][Wc] + 1 zero, staged as fp64 (exact)
   const int k = blockIdx.y, sp = blockIdx.x;
   const int M = g.S * g.S;
   const int NT = (M + 3) / 4;                // tap tiles per dimension
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kGramThreads) bcd_gram_kernel(Geom g, const fl
   const int n0 = static_cast<int>((static_cast<int64_t>(sp) * g.N) / nsplit);
   const int n1 = static_cast<int>((static_cast<int64_t>(sp + 1) * g.N) / nsplit);
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
-  if (threadIdx.x == 0) zs[zero_at] = 0.f;
+  if (threadIdx.x == 0) zs[zero_at] = 0.0;
   for (int n = n0; n < n1; ++n) {
     const float* zk = z + (static_cast<int64_t>(n) * g.K + k) * plane;
     for (int i0 = 0; i0 < g.H; i0 += kGramBR) {
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kGramThreads) bcd_gram_kernel(Geom g, const fl
       const int nr = min(rows, g.Hc - i0);
       for (int e = threadIdx.x; e < rows * g.Wc; e += kGramThreads) {
         const int rr = e / g.Wc;
-        zs[e] = rr < nr ? __ldg(zk + static_cast<int64_t>(i0) * g.Wc + e) : 0.f;
+        zs[e] = rr < nr ? static_cast<double>(__ldg(zk + static_cast<int64_t>(i0) * g.Wc + e)) : 0.0;
       }
       __syncthreads();
       const int ib = min(kGramBR, g.H - i0);
@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(kGramThreads) bcd_gram_kernel(Geom g, const fl
             double x1[4], x2[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              x1[e] = static_cast<double>(zs[off1[q][e] >= 0 ? base + off1[q][e] : zero_at]);
-              x2[e] = static_cast<double>(zs[off2[q][e] >= 0 ? base + off2[q][e] : zero_at]);
+              x1[e] = zs[off1[q][e] >= 0 ? base + off1[q][e] : zero_at];
+              x2[e] = zs[off2[q][e] >= 0 ? base + off2[q][e] : zero_at];
             }
 #pragma unroll
             for (int a = 0; a < 4; ++a)
@@ -309,7 +309,7 @@ int bcd_gk_blocks(const Geom& g) { return g.N * ((g.H + kGkBR - 1) / kGkBR); }
 
 cudaError_t launch_bcd_gram(const Geom& g, const float* z, double* gpart, cudaStream_t st) {
   const int ns = bcd_gram_splits(g);
-  const size_t smem = sizeof(float) * ((kGramBR + g.P) * g.Wc + 1);
+  const size_t smem = sizeof(double) * ((kGramBR + g.P) * g.Wc + 1);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(bcd_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
