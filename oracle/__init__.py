@@ -69,6 +69,9 @@ def lib():
                 getattr(L, f"oracle_objective_{suf}").argtypes = [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _vp]
                 getattr(L, f"oracle_filter_step_bcd_{suf}").argtypes = (
                     [_c_i64] * 5 + [_vp] * 3 + [ctypes.c_int, _vp])
+                getattr(L, f"oracle_surrogate_update_{suf}").argtypes = [_c_i64] * 5 + [_vp] * 4 + [_c_i64]
+                getattr(L, f"oracle_filter_step_surrogate_{suf}").argtypes = [_c_i64] * 2 + [_vp] * 3 + [
+                    ctypes.c_int, _vp]
             _lib = L
     return _lib
 
@@ -235,6 +238,29 @@ def filter_step_bcd(x, d, z, sweeps=1, dtype=np.float32):
     flags = np.zeros(K, dtype=np.uint8)
     getattr(lib(), f"oracle_filter_step_bcd_{_suf(dtype)}")(
         N, K, s, H, W, _p(x), _p(d), _p(z), int(sweeps), _p(flags))
+    return d, flags
+
+
+def surrogate_update(x, z, C, B, t, dtype=np.float32):
+    """Eq.7 in place on C [K][K][M][M] and B [K][M] (fp64, block-major): t is the count
+    after this mini-batch (t >= 1).  SURVEY.md §8f NEXT-2."""
+    x = _c(x, dtype); z = _c(z, dtype)
+    N, K, Hc, Wc = z.shape
+    s = int(round(np.sqrt(C.shape[-1])))
+    H, W = Hc - s + 1, Wc - s + 1
+    assert C.dtype == np.float64 and B.dtype == np.float64 and C.flags.c_contiguous and B.flags.c_contiguous
+    getattr(lib(), f"oracle_surrogate_update_{_suf(dtype)}")(N, K, s, H, W, _p(x), _p(z), _p(C), _p(B), int(t))
+
+
+def filter_step_surrogate(C, B, d, sweeps=1, dtype=np.float32):
+    """Eq.8: projected block-coordinate sweep(s) on 1/2 d^T C d - d^T B, ||d_k|| <= 1.
+    Returns (d_new, flags)."""
+    d = np.array(d, dtype=dtype, copy=True, order="C")
+    K, s = d.shape[0], d.shape[-1]
+    flags = np.zeros(K, dtype=np.uint8)
+    getattr(lib(), f"oracle_filter_step_surrogate_{_suf(dtype)}")(K, s, _p(np.ascontiguousarray(C)),
+                                                                  _p(np.ascontiguousarray(B)), _p(d),
+                                                                  int(sweeps), _p(flags))
     return d, flags
 
 

@@ -530,6 +530,92 @@ void filter_step_bcd(const Dims& D, const T* x, T* d, const T* z, int sweeps, ui
     }
 }
 
+// Online surrogates (§3.3, Eq.7): after the t-th
+// mini-batch (codes z, images x),
+//   C^t = ((t-1)/t) C^{t-1} + (1/t) sum_n Z_n^T Z_n,   B^t = ((t-1)/t) B^{t-1} + (1/t) sum_n Z_n^T x_n,
+// C stored block-major [K][K][M][M] (block (k1,k2), entry (t1,t2) = sum z_k1[p-t1] z_k2[p-t2]),
+// B [K][M].  t is the count after the update (t >= 1).  fp64 throughout.
+template <typename T>
+void surrogate_update(const Dims& D, const T* x, const T* z, double* C, double* B, int64_t t) {
+  const int64_t M = D.s * D.s, K = D.K;
+  const double wo = (double)(t - 1) / (double)t, wn = 1.0 / (double)t;
+#pragma omp parallel for collapse(2) schedule(dynamic)
+  for (int64_t k1 = 0; k1 < K; ++k1)
+    for (int64_t t1 = 0; t1 < M; ++t1) {
+      const int64_t a1 = t1 / D.s, b1 = t1 % D.s;
+      for (int64_t k2 = 0; k2 < K; ++k2)
+        for (int64_t t2 = 0; t2 < M; ++t2) {
+          const int64_t a2 = t2 / D.s, b2 = t2 % D.s;
+          double acc = 0.0;
+          for (int64_t n = 0; n < D.N; ++n)
+            for (int64_t i = 0; i < D.H; ++i)
+              for (int64_t j = 0; j < D.W; ++j)
+                acc += (double)z[D.zi(n, k1, i + D.P - a1, j + D.P - b1)] *
+                       (double)z[D.zi(n, k2, i + D.P - a2, j + D.P - b2)];
+          double& c = C[((k1 * K + k2) * M + t1) * M + t2];
+          c = wo * c + wn * acc;
+        }
+      double acc = 0.0;
+      for (int64_t n = 0; n < D.N; ++n)
+        for (int64_t i = 0; i < D.H; ++i)
+          for (int64_t j = 0; j < D.W; ++j)
+            acc += (double)x[D.xi(n, i, j)] * (double)z[D.zi(n, k1, i + D.P - a1, j + D.P - b1)];
+      B[k1 * M + t1] = wo * B[k1 * M + t1] + wn * acc;
+    }
+}
+
+// Eq.8: min_d 1/2 d^T C d - d^T B  s.t. ||d_k|| <= 1, by the projected block-coordinate
+// sweep of filter_step_bcd with the surrogate in place of the data: per k in order,
+//   g_k = sum_k' C_kk' d_k' - B_k,  d_k <- P_ball(d_k - (C_kk + eps tr(C_kk)/M I)^-1 g_k).
+// tr(C_kk) = 0: unchanged, flags[k] = 1.
+template <typename T>
+void filter_step_surrogate(int64_t K, int64_t s, const double* C, const double* B, T* d, int sweeps,
+                           uint8_t* flags) {
+  const int64_t M = s * s;
+  if (flags)
+    for (int64_t k = 0; k < K; ++k) flags[k] = 0;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int64_t k = 0; k < K; ++k) {
+      std::vector<double> A((size_t)(M * M)), g((size_t)M);
+      for (int64_t t1 = 0; t1 < M; ++t1) {
+        double acc = -B[k * M + t1];
+        for (int64_t k2 = 0; k2 < K; ++k2)
+          for (int64_t t2 = 0; t2 < M; ++t2) acc += C[((k * K + k2) * M + t1) * M + t2] * (double)d[k2 * M + t2];
+        g[t1] = acc;
+        for (int64_t t2 = 0; t2 < M; ++t2) A[t1 * M + t2] = C[((k * K + k) * M + t1) * M + t2];
+      }
+      double tr = 0.0;
+      for (int64_t m = 0; m < M; ++m) tr += A[m * M + m];
+      if (!(tr > 0.0)) {
+        if (flags) flags[k] = 1;
+        continue;
+      }
+      for (int64_t m = 0; m < M; ++m) A[m * M + m] += BCD_RIDGE * tr / (double)M;
+      if (!cholesky(A, M)) {
+        if (flags) flags[k] = 1;
+        continue;
+      }
+      std::vector<double> y((size_t)M), e((size_t)M);
+      for (int64_t i = 0; i < M; ++i) {
+        double tt = -g[i];
+        for (int64_t q = 0; q < i; ++q) tt -= A[i * M + q] * y[q];
+        y[i] = tt / A[i * M + i];
+      }
+      for (int64_t i = M - 1; i >= 0; --i) {
+        double tt = y[i];
+        for (int64_t q = i + 1; q < M; ++q) tt -= A[q * M + i] * e[q];
+        e[i] = tt / A[i * M + i];
+      }
+      double nrm2 = 0.0;
+      for (int64_t m = 0; m < M; ++m) {
+        e[m] += (double)d[k * M + m];
+        nrm2 += e[m] * e[m];
+      }
+      const double scale = std::max(1.0, std::sqrt(nrm2));
+      for (int64_t m = 0; m < M; ++m) d[k * M + m] = (T)(e[m] / scale);
+    }
+}
+
 // Eq.1 objective: F = sum_n 1/2||x_n - sum_k d_k * z_{n,k}||^2 + lam sum ||z||_1.
 template <typename T>
 void objective(const Dims& D, const T* x, const T* d, const T* z, double lam, double out[3]) {
@@ -639,6 +725,14 @@ double oracle_soft_threshold(double w, double kappa) { return soft_threshold(w, 
   void oracle_filter_step_bcd_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,       \
                                     const T* x, T* d, const T* z, int sweeps, uint8_t* flags) {    \
     filter_step_bcd<T>(Dims(N, K, s, H, W), x, d, z, sweeps, flags);                             \
+  }                                                                                              \
+  void oracle_surrogate_update_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,      \
+                                     const T* x, const T* z, double* C, double* B, int64_t t) {    \
+    surrogate_update<T>(Dims(N, K, s, H, W), x, z, C, B, t);                                     \
+  }                                                                                              \
+  void oracle_filter_step_surrogate_##SUF(int64_t K, int64_t s, const double* C, const double* B,  \
+                                          T* d, int sweeps, uint8_t* flags) {                    \
+    filter_step_surrogate<T>(K, s, C, B, d, sweeps, flags);                                      \
   }                                                                                              \
   void oracle_objective_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W, const T* x, \
                               const T* d, const T* z, double lam, double out[3]) {               \
