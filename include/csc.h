@@ -157,6 +157,22 @@ csc_status csc_read_step_z(csc_ctx* ctx, float* tau_dev);
 csc_status csc_filter_step_bcd(csc_ctx* ctx, const float* x, float* d, const float* z, int sweeps,
                                uint8_t* flags_out);
 
+/* Online dictionary learning surrogates (§3.3, Eq.7-8; SURVEY.md §8f NEXT-2;
+ * DESIGN.md §12).  The context keeps C (K x K blocks of M x M, fp64, 8 K^2 M^2 bytes -- 18.7 GB at
+ * K = 400, s = 11) and B (K x M, fp64) and the count t:
+ *   csc_surrogate_reset:   C = 0, B = 0, t = 0 (allocates on first use).
+ *   csc_surrogate_update:  with the current mini-batch (x, z of this rank; all ranks together),
+ *       t <- t + 1,  C <- ((t-1)/t) C + (1/t) sum_n Z_n^T Z_n,  B <- ((t-1)/t) B + (1/t) sum_n Z_n^T x_n.
+ *       Collective.
+ *   csc_filter_step_surrogate:  Eq.8, min 1/2 d^T C d - d^T B s.t. ||d_k|| <= 1, by projected
+ *       block-coordinate sweeps (as csc_filter_step_bcd with the surrogate in place of the data).
+ *       Rank-local (C, B are identical on every rank); flags_out as csc_filter_step_bcd.
+ *   csc_read_surrogate:  test hook, copies C / B (DEVICE, nullable) and returns t (HOST, nullable). */
+csc_status csc_surrogate_reset(csc_ctx* ctx);
+csc_status csc_surrogate_update(csc_ctx* ctx, const float* x, const float* z);
+csc_status csc_filter_step_surrogate(csc_ctx* ctx, float* d, int sweeps, uint8_t* flags_out);
+csc_status csc_read_surrogate(csc_ctx* ctx, double* C_dev, double* B_dev, int64_t* t_out);
+
 /* Forget the residual cache (caller changed x, d or z outside the API). */
 csc_status csc_invalidate(csc_ctx* ctx);
 

@@ -29,7 +29,8 @@ ABI_SYMBOLS = (
     "csc_zero_codes", "csc_destroy", "csc_last_error", "csc_nccl_unique_id", "csc_abi_version",
     "csc_mask_bits", "csc_read_residual", "csc_read_grad", "csc_lipschitz", "csc_launch_count",
     "csc_profile_enable", "csc_profile_read", "csc_kernel_variants", "csc_code_step_admm",
-    "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd",
+    "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd", "csc_surrogate_reset",
+    "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -70,6 +71,10 @@ def load_library(path: Optional[str] = None):
         L.csc_filter_step.argtypes = [vp, vp, vp, vp, f32, vp]
         L.csc_set_step_rule.argtypes = [vp, ctypes.c_int]
         L.csc_filter_step_bcd.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
+        L.csc_surrogate_reset.argtypes = [vp]
+        L.csc_surrogate_update.argtypes = [vp, vp, vp]
+        L.csc_filter_step_surrogate.argtypes = [vp, vp, ctypes.c_int, vp]
+        L.csc_read_surrogate.argtypes = [vp, vp, vp, ctypes.POINTER(ctypes.c_int64)]
         L.csc_read_step_z.argtypes = [vp, vp]
         L.csc_code_step_admm.argtypes = [vp, vp, vp, vp, f32, f32, f32, ctypes.c_int, ctypes.c_int, f64, u64, u32]
         L.csc_objective.argtypes = [vp, vp, vp, vp, f32, vp]
@@ -173,6 +178,35 @@ class Context:
         self._check(self._L.csc_filter_step_bcd(self._h, px, pd, pz, int(sweeps),
                                                 ctypes.cast(flags, ctypes.c_void_p) if want_flags else None))
         return list(flags)[:self.K] if want_flags else None
+
+    def surrogate_reset(self) -> None:
+        """Online surrogates C = 0, B = 0, t = 0 (include/csc.h csc_surrogate_reset; Eq.7)."""
+        self._check(self._L.csc_surrogate_reset(self._h))
+
+    def surrogate_update(self, x, z) -> None:
+        """Fold the mini-batch (x, z) into C, B (Eq.7)."""
+        nx = self.n_local * self.H * self.W
+        nz = self.n_local * self.K * self.Hc * self.Wc
+        self._check(self._L.csc_surrogate_update(self._h, _ptr(x, "x", nx) if self.n_local else 0,
+                                                 _ptr(z, "z", nz) if self.n_local else 0))
+
+    def filter_step_surrogate(self, d, sweeps: int = 1, want_flags: bool = False):
+        """Eq.8 projected block-coordinate filter update on the surrogates."""
+        flags = (ctypes.c_uint8 * max(self.K, 1))()
+        self._check(self._L.csc_filter_step_surrogate(self._h, _ptr(d, "d", self.K * self.s * self.s), int(sweeps),
+                                                      ctypes.cast(flags, ctypes.c_void_p) if want_flags else None))
+        return list(flags)[:self.K] if want_flags else None
+
+    def read_surrogate(self, C, B) -> int:
+        """Copy C [K][K][M][M] and B [K][M] (float64 CUDA tensors) and return t."""
+        import torch
+        M = self.s * self.s
+        for t_, n_, nm in ((C, self.K * self.K * M * M, "C"), (B, self.K * M, "B")):
+            if not (t_.is_cuda and t_.dtype == torch.float64 and t_.is_contiguous() and t_.numel() == n_):
+                raise ValueError(f"{nm} must be a contiguous float64 CUDA tensor with {n_} elements")
+        t = ctypes.c_int64(0)
+        self._check(self._L.csc_read_surrogate(self._h, C.data_ptr(), B.data_ptr(), ctypes.byref(t)))
+        return int(t.value)
 
     STEP_RULES = {"lipschitz": 0, "eso": 1}
 

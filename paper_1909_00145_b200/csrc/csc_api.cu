@@ -122,6 +122,12 @@ struct csc_ctx {
   uint8_t* bcd_flags = nullptr; // [K]
   double* bcd_part = nullptr;   // [gk blocks][M]
   double* bcd_vec = nullptr;    // gk[M], dl[M]
+  // online surrogates (Eq.7), allocated by the first csc_surrogate_reset / update
+  double* sur_C = nullptr;      // [K][K][M][M]
+  double* sur_B = nullptr;      // [K][M]
+  double* sur_pp = nullptr;     // batch Gram partials
+  double* sur_diag = nullptr;   // [K][M][M]
+  int64_t sur_t = 0;
   bool last_eso = false;       // the last code step used per-filter taus
   float* tauk = nullptr;       // [K] per-filter tau_z of the ESO rule
   // ADMM code solver scratch (csc_admm.cu), allocated by the first csc_code_step_admm
@@ -301,6 +307,27 @@ csc_status dense_apply(csc_ctx* c, const float* x, const float* d, const float* 
     CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
                  csc::launch_conv_finalize(g, c->part, c->ksplit, x, out, csc::kConvResidual, c->sq_part, c->st));
   return CSC_OK;
+}
+
+// scratch of the block-coordinate filter updates (csc_filter_step_bcd, csc_filter_step_surrogate)
+bool bcd_scratch(csc_ctx* c) {
+  if (c->bcd_gpart != nullptr) return true;
+  const Geom& g = c->g;
+  const int M = g.S * g.S;
+  const int ns = csc::bcd_gram_splits(g);
+  const int nb = csc::bcd_gk_blocks(g);
+  auto al = [](void** q, size_t bytes) { return cudaMalloc(q, bytes < 16 ? 16 : bytes) == cudaSuccess; };
+  bool ok = al(reinterpret_cast<void**>(&c->bcd_gpart), sizeof(double) * g.K * ns * M * M);
+  ok = ok && al(reinterpret_cast<void**>(&c->bcd_ainv), sizeof(double) * g.K * M * M);
+  ok = ok && al(reinterpret_cast<void**>(&c->bcd_flags), static_cast<size_t>(g.K));
+  ok = ok && al(reinterpret_cast<void**>(&c->bcd_part), sizeof(double) * (nb > 0 ? nb : 1) * M);
+  ok = ok && al(reinterpret_cast<void**>(&c->bcd_vec), sizeof(double) * 2 * M);
+  if (!ok) {
+    cudaFree(c->bcd_gpart);
+    c->bcd_gpart = nullptr;
+    cudaGetLastError();
+  }
+  return ok;
 }
 
 bool cache_ok(const csc_ctx* c, const float* x, const float* d, const float* z) {
@@ -583,6 +610,10 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->bcd_flags);
   cudaFree(c->bcd_part);
   cudaFree(c->bcd_vec);
+  cudaFree(c->sur_C);
+  cudaFree(c->sur_B);
+  cudaFree(c->sur_pp);
+  cudaFree(c->sur_diag);
   cudaFree(c->adm_zd);
   cudaFree(c->adm_e);
   cudaFree(c->adm_cd);
@@ -899,18 +930,8 @@ csc_status csc_filter_step_bcd(csc_ctx* c, const float* x, float* d, const float
   const int M = g.S * g.S;
   const int ns = csc::bcd_gram_splits(g);
   const int nb = csc::bcd_gk_blocks(g);
-  if (c->bcd_gpart == nullptr) {
-    auto al = [](void** q, size_t bytes) { return cudaMalloc(q, bytes < 16 ? 16 : bytes) == cudaSuccess; };
-    bool ok = al(reinterpret_cast<void**>(&c->bcd_gpart), sizeof(double) * g.K * ns * M * M);
-    ok = ok && al(reinterpret_cast<void**>(&c->bcd_ainv), sizeof(double) * g.K * M * M);
-    ok = ok && al(reinterpret_cast<void**>(&c->bcd_flags), static_cast<size_t>(g.K));
-    ok = ok && al(reinterpret_cast<void**>(&c->bcd_part), sizeof(double) * (nb > 0 ? nb : 1) * M);
-    ok = ok && al(reinterpret_cast<void**>(&c->bcd_vec), sizeof(double) * 2 * M);
-    if (!ok) {
-      cudaGetLastError();
-      return fail(c, CSC_ERR_OOM, "BCD scratch allocation failed");
-    }
-  }
+  if (!bcd_scratch(c)) return fail(c, CSC_ERR_OOM, "BCD scratch allocation failed");
+  (void)nb;
   // r = D z - x (the residual cache when it is valid); the sweep keeps it current
   if (!cache_ok(c, x, d, z)) {
     s = dense_residual(c, x, d, z, false);
@@ -946,6 +967,92 @@ csc_status csc_filter_step_bcd(csc_ctx* c, const float* x, float* d, const float
     CSC_CUDA(c, cudaMemcpyAsync(flags_out, c->bcd_flags, static_cast<size_t>(g.K), cudaMemcpyDeviceToHost, c->st));
     CSC_CUDA(c, cudaStreamSynchronize(c->st));
   }
+  return CSC_OK;
+}
+
+csc_status csc_surrogate_reset(csc_ctx* c) {
+  if (!c) return CSC_ERR_ARG;
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  const int M = g.S * g.S;
+  if (g.S * g.S > 128) return fail(c, CSC_ERR_SHAPE, "block solve supports s*s <= 128");
+  if (c->sur_C == nullptr) {
+    const int64_t np = static_cast<int64_t>(g.K) * (g.K + 1) / 2;
+    auto al = [](void** q, size_t bytes) { return cudaMalloc(q, bytes < 16 ? 16 : bytes) == cudaSuccess; };
+    bool ok = al(reinterpret_cast<void**>(&c->sur_C), sizeof(double) * g.K * g.K * M * M);
+    ok = ok && al(reinterpret_cast<void**>(&c->sur_B), sizeof(double) * g.K * M);
+    ok = ok && al(reinterpret_cast<void**>(&c->sur_pp), sizeof(double) * np * csc::sur_gram_splits(g) * M * M);
+    ok = ok && al(reinterpret_cast<void**>(&c->sur_diag), sizeof(double) * g.K * M * M);
+    if (!ok) {
+      cudaFree(c->sur_C); cudaFree(c->sur_B); cudaFree(c->sur_pp); cudaFree(c->sur_diag);
+      c->sur_C = c->sur_B = c->sur_pp = c->sur_diag = nullptr;
+      cudaGetLastError();
+      return fail(c, CSC_ERR_OOM, "surrogate allocation failed (K^2 M^2 doubles)");
+    }
+  }
+  if (!bcd_scratch(c)) return fail(c, CSC_ERR_OOM, "BCD scratch allocation failed");
+  CSC_CUDA(c, cudaMemsetAsync(c->sur_C, 0, sizeof(double) * g.K * g.K * M * M, c->st));
+  CSC_CUDA(c, cudaMemsetAsync(c->sur_B, 0, sizeof(double) * g.K * M, c->st));
+  c->sur_t = 0;
+  return CSC_OK;
+}
+
+csc_status csc_surrogate_update(csc_ctx* c, const float* x, const float* z) {
+  if (!c) return CSC_ERR_ARG;
+  if (c->g.N > 0 && (!aligned4(x) || !aligned4(z))) return fail(c, CSC_ERR_ARG, "x, z must be device pointers");
+  if (c->sur_C == nullptr) {
+    csc_status s0 = csc_surrogate_reset(c);
+    if (s0 != CSC_OK) return s0;
+  }
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  const int M = g.S * g.S;
+  const int64_t t = c->sur_t + 1;
+  // Eq.7 with the batch sums of all ranks: each rank folds (wo / world) C + wn (its batch) and the
+  // all-reduce adds the ranks (C is identical on every rank)
+  const double wo = static_cast<double>(t - 1) / static_cast<double>(t) / static_cast<double>(c->world);
+  const double wn = 1.0 / static_cast<double>(t);
+  CSC_LAUNCH_C(c, CSC_K_BCD, 2 + 3 * g.K, csc::launch_sur_update(g, x, z, c->sur_pp, c->bcd_part, c->bcd_vec, wo, wn,
+                                                                c->sur_C, c->sur_B, c->st));
+  csc_status s = allreduce_d(c, c->sur_C, static_cast<size_t>(g.K) * g.K * M * M);
+  if (s != CSC_OK) return s;
+  s = allreduce_d(c, c->sur_B, static_cast<size_t>(g.K) * M);
+  if (s != CSC_OK) return s;
+  c->sur_t = t;
+  return CSC_OK;
+}
+
+csc_status csc_filter_step_surrogate(csc_ctx* c, float* d, int sweeps, uint8_t* flags_out) {
+  if (!c || !aligned4(d)) return fail(c, CSC_ERR_ARG, "d must be a device pointer");
+  if (sweeps < 1) return fail(c, CSC_ERR_ARG, "sweeps must be >= 1");
+  if (c->sur_C == nullptr || c->sur_t < 1) return fail(c, CSC_ERR_ARG, "no surrogate: call csc_surrogate_update first");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  const int M = g.S * g.S;
+  CSC_LAUNCH_C(c, CSC_K_BCD, 2, csc::launch_sur_prepare(g, c->sur_C, c->sur_diag, kBcdRidge, c->bcd_ainv,
+                                                        c->bcd_flags, c->st));
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int k = 0; k < g.K; ++k)
+      CSC_LAUNCH_C(c, CSC_K_BCD, 2, csc::launch_sur_filter(g, k, c->sur_C, c->sur_B, c->bcd_ainv, c->bcd_flags, d,
+                                                           c->bcd_vec, c->bcd_vec + M, c->st));
+  c->cache_valid = false;  // d changed
+  if (flags_out) {
+    CSC_CUDA(c, cudaMemcpyAsync(flags_out, c->bcd_flags, static_cast<size_t>(g.K), cudaMemcpyDeviceToHost, c->st));
+    CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  }
+  return CSC_OK;
+}
+
+csc_status csc_read_surrogate(csc_ctx* c, double* C_dev, double* B_dev, int64_t* t_out) {
+  if (!c) return CSC_ERR_ARG;
+  if (c->sur_C == nullptr) return fail(c, CSC_ERR_ARG, "no surrogate state");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  const int M = g.S * g.S;
+  if (C_dev)
+    CSC_CUDA(c, cudaMemcpyAsync(C_dev, c->sur_C, sizeof(double) * g.K * g.K * M * M, cudaMemcpyDeviceToDevice, c->st));
+  if (B_dev) CSC_CUDA(c, cudaMemcpyAsync(B_dev, c->sur_B, sizeof(double) * g.K * M, cudaMemcpyDeviceToDevice, c->st));
+  if (t_out) *t_out = c->sur_t;
   return CSC_OK;
 }
 

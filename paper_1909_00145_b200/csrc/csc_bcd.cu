@@ -298,6 +298,165 @@ __global__ void bcd_resid_kernel(Geom g, int k, const float* __restrict__ z, con
   }
 }
 
+
+// ================================================================ online surrogates (Eq.7 / Eq.8)
+// SURVEY.md §8f NEXT-2; DESIGN.md §12.  C block-major [K][K][M][M], B [K][M].
+
+// Batch Gram block (k1, k2), k1 <= k2 (pair index q in the upper triangle, row by row): partial over
+// the images of split sp, all M x M entries, 4x4 tiles, processed in passes of 2 tiles per thread.
+__global__ void __launch_bounds__(kGramThreads) sur_gram_kernel(Geom g, const float* __restrict__ z, int nsplit,
+                                                                double* __restrict__ pp) {
+  extern __shared__ double zz[];  // [2][kGramBR + P][Wc] + 1 zero
+  const int q = blockIdx.y, sp = blockIdx.x;
+  int k1 = 0, rem = q;
+  while (rem >= g.K - k1) {
+    rem -= g.K - k1;
+    ++k1;
+  }
+  const int k2 = k1 + rem;
+  const int M = g.S * g.S;
+  const int NT = (M + 3) / 4;
+  const int rows = kGramBR + g.P;
+  const int half = rows * g.Wc;
+  const int zero_at = 2 * half;
+  double* z1s = zz;
+  double* z2s = zz + half;
+  const int n0 = static_cast<int>((static_cast<int64_t>(sp) * g.N) / nsplit);
+  const int n1 = static_cast<int>((static_cast<int64_t>(sp + 1) * g.N) / nsplit);
+  const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
+  double* out = pp + (static_cast<int64_t>(q) * nsplit + sp) * M * M;
+  if (threadIdx.x == 0) zz[zero_at] = 0.0;
+  for (int pass = 0; pass * 2 * kGramThreads < NT * NT; ++pass) {
+    int off1[2][4], off2[2][4], T1v[2], T2v[2];
+    bool own[2];
+    for (int h = 0; h < 2; ++h) {
+      const int id = pass * 2 * kGramThreads + h * kGramThreads + threadIdx.x;
+      own[h] = id < NT * NT;
+      T1v[h] = own[h] ? id / NT : 0;
+      T2v[h] = own[h] ? id % NT : 0;
+      for (int e = 0; e < 4; ++e) {
+        const int t1 = 4 * T1v[h] + e, t2 = 4 * T2v[h] + e;
+        off1[h][e] = t1 < M ? (g.P - t1 / g.S) * g.Wc + (g.P - t1 % g.S) : -1;
+        off2[h][e] = t2 < M ? half + (g.P - t2 / g.S) * g.Wc + (g.P - t2 % g.S) : -1;
+      }
+    }
+    double acc[2][4][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[h][a][b] = 0.0;
+    for (int n = n0; n < n1; ++n) {
+      const float* za = z + (static_cast<int64_t>(n) * g.K + k1) * plane;
+      const float* zb = z + (static_cast<int64_t>(n) * g.K + k2) * plane;
+      for (int i0 = 0; i0 < g.H; i0 += kGramBR) {
+        __syncthreads();
+        const int nr = min(rows, g.Hc - i0);
+        for (int e = threadIdx.x; e < half; e += kGramThreads) {
+          const int rr = e / g.Wc;
+          const bool in = rr < nr;
+          z1s[e] = in ? static_cast<double>(__ldg(za + static_cast<int64_t>(i0) * g.Wc + e)) : 0.0;
+          z2s[e] = in ? static_cast<double>(__ldg(zb + static_cast<int64_t>(i0) * g.Wc + e)) : 0.0;
+        }
+        __syncthreads();
+        const int ib = min(kGramBR, g.H - i0);
+        for (int ii = 0; ii < ib; ++ii)
+          for (int j = 0; j < g.W; ++j) {
+            const int base = ii * g.Wc + j;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (!own[h]) continue;
+              double x1[4], x2[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                x1[e] = zz[off1[h][e] >= 0 ? base + off1[h][e] : zero_at];
+                x2[e] = zz[off2[h][e] >= 0 ? base + off2[h][e] : zero_at];
+              }
+#pragma unroll
+              for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[h][a][b] = fma(x1[a], x2[b], acc[h][a][b]);
+            }
+          }
+      }
+    }
+    for (int h = 0; h < 2; ++h) {
+      if (!own[h]) continue;
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+          const int t1 = 4 * T1v[h] + a, t2 = 4 * T2v[h] + b;
+          if (t1 < M && t2 < M) out[static_cast<int64_t>(t1) * M + t2] = acc[h][a][b];
+        }
+    }
+  }
+}
+
+// C[k1][k2] = wo C + wn sum_sp pp, mirrored into C[k2][k1] (fixed order over the splits)
+__global__ void sur_fold_kernel(Geom g, const double* __restrict__ pp, int nsplit, double wo, double wn,
+                                double* __restrict__ C) {
+  const int M = g.S * g.S;
+  const int64_t npairs = static_cast<int64_t>(g.K) * (g.K + 1) / 2;
+  const int64_t total = npairs * M * M;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t q = e / (M * M);
+    const int rem2 = static_cast<int>(e - q * M * M);
+    const int t1 = rem2 / M, t2 = rem2 - t1 * M;
+    int k1 = 0;
+    int64_t rem = q;
+    while (rem >= g.K - k1) {
+      rem -= g.K - k1;
+      ++k1;
+    }
+    const int k2 = k1 + static_cast<int>(rem);
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) s += pp[(q * nsplit + sp) * M * M + rem2];
+    double& c = C[((static_cast<int64_t>(k1) * g.K + k2) * M + t1) * M + t2];
+    c = wo * c + wn * s;
+    if (k1 != k2) C[((static_cast<int64_t>(k2) * g.K + k1) * M + t2) * M + t1] = c;
+  }
+}
+
+// B[k] = wo B[k] + wn gk (gk = sum_n Z_nk^T x_n from bcd_gk_kernel with r := x)
+__global__ void sur_bfold_kernel(int M, int k, const double* __restrict__ gk, double wo, double wn,
+                                 double* __restrict__ B) {
+  const int t = threadIdx.x;
+  if (t < M) B[static_cast<int64_t>(k) * M + t] = wo * B[static_cast<int64_t>(k) * M + t] + wn * gk[t];
+}
+
+// diag[k] = C[k][k] (contiguous [K][M][M] for bcd_inverse_kernel)
+__global__ void sur_diag_kernel(Geom g, const double* __restrict__ C, double* __restrict__ diag) {
+  const int M = g.S * g.S;
+  const int k = blockIdx.x;
+  for (int e = threadIdx.x; e < M * M; e += blockDim.x)
+    diag[static_cast<int64_t>(k) * M * M + e] = C[(static_cast<int64_t>(k) * g.K + k) * M * M + e];
+}
+
+// g[t] = sum_k2 sum_t2 C[k][k2][t][t2] d[k2][t2] - B[k][t]: block t (fixed-order tree reduction)
+__global__ void sur_grad_kernel(Geom g, int k, const double* __restrict__ C, const double* __restrict__ B,
+                                const float* __restrict__ d, double* __restrict__ gk) {
+  __shared__ double red[32];
+  const int M = g.S * g.S;
+  const int t = blockIdx.x;
+  const int64_t KM = static_cast<int64_t>(g.K) * M;
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < KM; e += blockDim.x) {
+    const int64_t k2 = e / M;
+    const int t2 = static_cast<int>(e - k2 * M);
+    s = fma(C[((static_cast<int64_t>(k) * g.K + k2) * M + t) * M + t2], static_cast<double>(d[e]), s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFullB, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+    gk[t] = tot - B[static_cast<int64_t>(k) * M + t];
+  }
+}
+
 }  // namespace
 
 int bcd_gram_splits(const Geom& g) {
@@ -358,6 +517,62 @@ cudaError_t launch_bcd_update(const Geom& g, int k, const double* gk, const doub
     if (rb > 148 * 8) rb = 148 * 8;
     bcd_resid_kernel<<<static_cast<unsigned>(rb), 256, 0, st>>>(g, k, z, dl, r);
   }
+  return cudaGetLastError();
+}
+
+int sur_gram_splits(const Geom& g) {
+  const int64_t np = static_cast<int64_t>(g.K) * (g.K + 1) / 2;
+  int ns = static_cast<int>((148 * 2 + np - 1) / np);
+  if (ns < 1) ns = 1;
+  return ns;
+}
+
+cudaError_t launch_sur_update(const Geom& g, const float* x, const float* z, double* pp, double* part, double* gk,
+                              double wo, double wn, double* C, double* B, cudaStream_t st) {
+  const int ns = sur_gram_splits(g);
+  const int64_t np = static_cast<int64_t>(g.K) * (g.K + 1) / 2;
+  const int M = g.S * g.S;
+  if (g.N > 0) {
+    const size_t smem = sizeof(double) * (2 * (kGramBR + g.P) * g.Wc + 1);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(sur_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    sur_gram_kernel<<<dim3(ns, static_cast<unsigned>(np)), kGramThreads, smem, st>>>(g, z, ns, pp);
+  } else {
+    cudaMemsetAsync(pp, 0, sizeof(double) * np * ns * M * M, st);
+  }
+  int64_t fb = (np * M * M + 255) / 256;
+  if (fb > 148 * 16) fb = 148 * 16;
+  sur_fold_kernel<<<static_cast<unsigned>(fb), 256, 0, st>>>(g, pp, ns, wo, wn, C);
+  for (int k = 0; k < g.K; ++k) {
+    cudaError_t e = launch_bcd_gk(g, k, z, x, part, gk, st);
+    if (e != cudaSuccess) return e;
+    sur_bfold_kernel<<<1, 128, 0, st>>>(M, k, gk, wo, wn, B);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sur_prepare(const Geom& g, const double* C, double* diag, double ridge_rel, double* ainv,
+                               uint8_t* flags, cudaStream_t st) {
+  sur_diag_kernel<<<g.K, 256, 0, st>>>(g, C, diag);
+  const int M = g.S * g.S;
+  const size_t smem2 = sizeof(double) * M * M;
+  if (smem2 > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(bcd_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem2));
+    if (e != cudaSuccess) return e;
+  }
+  bcd_inverse_kernel<<<g.K, 128, smem2, st>>>(g, diag, 1, ridge_rel, ainv, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sur_filter(const Geom& g, int k, const double* C, const double* B, const double* ainv,
+                              const uint8_t* flags, float* d, double* gk, double* dl, cudaStream_t st) {
+  const int M = g.S * g.S;
+  sur_grad_kernel<<<M, 256, 0, st>>>(g, k, C, B, d, gk);
+  bcd_update_kernel<<<1, 128, 0, st>>>(g, k, gk, ainv, flags, d, dl);
   return cudaGetLastError();
 }
 

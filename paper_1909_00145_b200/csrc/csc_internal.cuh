@@ -232,4 +232,16 @@ cudaError_t launch_bcd_gk(const Geom& g, int k, const float* z, const float* r, 
 cudaError_t launch_bcd_update(const Geom& g, int k, const double* gk, const double* ainv, const uint8_t* flags,
                               float* d, double* dl, const float* z, float* r, cudaStream_t st);
 
+// Online surrogates (csc_bcd.cu): C block-major [K][K][M][M], B [K][M] (fp64).  pp: K(K+1)/2 *
+// sur_gram_splits * M * M doubles; C <- wo C + wn (batch Gram), B <- wo B + wn (batch Z^T x).
+int sur_gram_splits(const Geom& g);
+cudaError_t launch_sur_update(const Geom& g, const float* x, const float* z, double* pp, double* part, double* gk,
+                              double wo, double wn, double* C, double* B, cudaStream_t st);
+// diag (K M M doubles) <- the diagonal blocks; ainv / flags as launch_bcd_inverse
+cudaError_t launch_sur_prepare(const Geom& g, const double* C, double* diag, double ridge_rel, double* ainv,
+                               uint8_t* flags, cudaStream_t st);
+// one Eq.8 block step for filter k (gk, dl: M doubles)
+cudaError_t launch_sur_filter(const Geom& g, int k, const double* C, const double* B, const double* ainv,
+                              const uint8_t* flags, float* d, double* gk, double* dl, cudaStream_t st);
+
 }  // namespace csc
