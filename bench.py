@@ -67,7 +67,7 @@ def _traffic():
         return {}
 
 
-def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox"):
+def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox", filter_solver="pg"):
     """Per kernel class: algorithmic work per launch / measured average launch time vs its roofs.
     Algorithmic units: dense pass / filter gradient 2*N*K*s^2*H*W FLOP and a read of
     all codes (4*N*K*Hc*Wc B); masked code step: sector-model bytes.  Tensor peaks: the measured
@@ -122,7 +122,10 @@ def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox"):
             # (upper triangle incl. the diagonal tiles), against the fp64 FMA rate
             M = cfg.s * cfg.s
             nt = (M + 3) // 4
-            fma = nl * cfg.K * cfg.H * cfg.W * 16.0 * nt * (nt + 1) / 2
+            if filter_solver == "surrogate":  # batch Gram over all filter pairs, full 4x4 tiles
+                fma = nl * cfg.H * cfg.W * (cfg.K * (cfg.K + 1) / 2) * 16.0 * nt * nt
+            else:
+                fma = nl * cfg.K * cfg.H * cfg.W * 16.0 * nt * (nt + 1) / 2
             fp64_peak = SMS * 64 * 2 * sm_max_mhz * 1e6 / 1e12
             out[name] = {"kernel": "bcd_gram_kernel + per-filter kernels (fp64, csc_bcd.cu)", "bound": "alu",
                          "achieved": 2.0 * fma / (ms / steps / 1e3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
@@ -336,12 +339,15 @@ def run_ours(args):
 
     admm = args.code_solver == "admm"
     bcd = args.filter_solver == "bcd"
+    sur = args.filter_solver == "surrogate"
+    if sur:
+        ctx.surrogate_reset()
 
     def step(it, x_host=None):
         """One outer iteration: csc_iterate (prox code step + projected-gradient filter step), or with
         --code-solver admm / --filter-solver bcd the paper's ADMM code update (csc_code_step_admm) /
         projected block-coordinate filter update (csc_filter_step_bcd), then the objective."""
-        if not admm and not bcd:
+        if not admm and not bcd and not sur:
             return ctx.iterate(x, d, z, cfg.lam, cfg.p, seed, it, x_host=x_host)
         if x_host is not None:
             x.copy_(x_host, non_blocking=True)
@@ -352,6 +358,9 @@ def run_ours(args):
             ctx.code_step(x, d, z, cfg.lam, cfg.p, seed, it)
         if bcd:
             ctx.filter_step_bcd(x, d, z)
+        elif sur:
+            ctx.surrogate_update(x, z)
+            ctx.filter_step_surrogate(d)
         else:
             ctx.filter_step(x, d, z)
         return ctx.objective(x, d, z, cfg.lam), None
@@ -415,7 +424,7 @@ def run_ours(args):
 
     if rank == 0:
         step_ms = t_ms / args.steps
-        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.variants, args.code_solver)
+        rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.variants, args.code_solver, args.filter_solver)
         dom = max(rl, key=lambda k: rl[k]["ms_per_step"])
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                        "share": v[0] / max(t_total, 1e-9)} for k, v in prof.items()}
@@ -453,9 +462,10 @@ def main():
     ap.add_argument("--ref-images", type=int, default=1)
     ap.add_argument("--cpu-images", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--filter-solver", default="pg", choices=["pg", "bcd"],
+    ap.add_argument("--filter-solver", default="pg", choices=["pg", "bcd", "surrogate"],
                     help="pg: the north_star projected-gradient filter step (default); bcd: the paper's "
-                         "projected block-coordinate update, one warm-started sweep (SURVEY.md §8f NEXT-3)")
+                         "projected block-coordinate update, one warm-started sweep (SURVEY.md §8f NEXT-3); "
+                         "surrogate: Eq.7 surrogate update + Eq.8 sweep per step (NEXT-2)")
     ap.add_argument("--step-rule", default="lipschitz", choices=["lipschitz", "eso"],
                     help="built-in tau_z rule of the prox code step (eso: SURVEY.md §8f NEXT-4 (i))")
     ap.add_argument("--code-solver", default="prox", choices=["prox", "admm"],
