@@ -50,6 +50,7 @@ def lib():
             L.oracle_mask_threshold.argtypes = [_c_dbl]
             L.oracle_mask_threshold.restype = _c_u64
             L.oracle_mask_bits.argtypes = [_c_i64, _c_i64, _c_i64, _c_dbl, _c_u64, _c_u32, _vp]
+            L.oracle_mask_bits_mode.argtypes = [_c_i64, _c_i64, _c_i64, _c_dbl, _c_u64, _c_u32, _vp, ctypes.c_int]
             L.oracle_soft_threshold.argtypes = [_c_dbl, _c_dbl]
             L.oracle_soft_threshold.restype = _c_dbl
             for suf in ("f32", "f64"):
@@ -60,7 +61,8 @@ def lib():
                 f.argtypes = [_c_i64, _c_i64, _vp]
                 f.restype = _c_dbl
                 getattr(L, f"oracle_code_step_{suf}").argtypes = (
-                    [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, _c_u64, _c_u32, _vp, ctypes.c_int])
+                    [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, _c_u64, _c_u32, _vp, ctypes.c_int,
+                                                ctypes.c_int])
                 getattr(L, f"oracle_admm_code_step_{suf}").argtypes = (
                     [_c_i64] * 5 + [_vp] * 3 + [_c_dbl, _c_dbl, _c_dbl, ctypes.c_int, ctypes.c_int, _c_dbl, _c_u64,
                                                 _c_u32])
@@ -109,10 +111,18 @@ def mask_threshold(p: float) -> int:
     return int(lib().oracle_mask_threshold(float(p)))
 
 
-def mask_bits(K: int, Hc: int, Wc: int, p: float, seed: int, t: int) -> np.ndarray:
+MASK_MODES = {"entry": 0, "sector8": 1}
+
+
+def mask_bits(K: int, Hc: int, Wc: int, p: float, seed: int, t: int, mode: str = "entry") -> np.ndarray:
+    """Canonical mask bits; mode "sector8": one draw per aligned block of 8 coordinates (E5)."""
     total = K * Hc * Wc
     out = np.zeros((total + 31) // 32, dtype=np.uint32)
-    lib().oracle_mask_bits(K, Hc, Wc, float(p), int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(out))
+    if mode == "entry":
+        lib().oracle_mask_bits(K, Hc, Wc, float(p), int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(out))
+    else:
+        lib().oracle_mask_bits_mode(K, Hc, Wc, float(p), int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(out),
+                                    MASK_MODES[mode])
     return out
 
 
@@ -166,7 +176,7 @@ def lipschitz(d, dtype=np.float32) -> float:
     return float(getattr(lib(), f"oracle_lipschitz_{_suf(dtype)}")(K, s, _p(d)))
 
 
-def code_step(x, d, z, lam, step_z, p, seed, t, dtype=np.float32, rule="lipschitz"):
+def code_step(x, d, z, lam, step_z, p, seed, t, dtype=np.float32, rule="lipschitz", mask="entry"):
     """One masked prox-gradient code step.  Returns (z_new, tau_used).
 
     rule (used when step_z == 0): "lipschitz" -> tau = 1/L_D (reading R8), tau_used a float;
@@ -183,7 +193,7 @@ def code_step(x, d, z, lam, step_z, p, seed, t, dtype=np.float32, rule="lipschit
     tau = np.zeros(max(K, 1), dtype=np.float64)
     getattr(lib(), f"oracle_code_step_{_suf(dtype)}")(
         N, K, s, H, W, _p(x), _p(d), _p(z), float(lam), float(step_z), float(p),
-        int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(tau), eso)
+        int(seed) & (2**64 - 1), int(t) & 0xffffffff, _p(tau), eso, MASK_MODES[mask])
     return z, (tau.copy() if eso else float(tau[0]))
 
 

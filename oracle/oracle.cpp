@@ -84,6 +84,23 @@ bool mask_bit(uint64_t seed, uint32_t t, uint64_t l, uint64_t thr) {
   return (uint64_t)w[l & 3] < thr;
 }
 
+// Block-structured variant (a labelled deviation from the per-entry
+// Bernoulli sampling of Eq.2; reading E5): one Bernoulli(p) draw per aligned
+// block of 8 consecutive coordinates b = l >> 3 (one 32-B sector of fp32 codes), word b & 3 of
+// Philox(ctr = {q lo, q hi, t, kSectorTag}, q = b >> 2).
+const uint32_t kSectorTag = 0x43534253u;  // "CSBS"
+bool mask_bit_sector8(uint64_t seed, uint32_t t, uint64_t l, uint64_t thr) {
+  const uint64_t b = l >> 3, q = b >> 2;
+  const uint32_t ctr[4] = {(uint32_t)(q & 0xffffffffu), (uint32_t)(q >> 32), t, kSectorTag};
+  const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+  uint32_t w[4];
+  philox4x32_10(ctr, key, w);
+  return (uint64_t)w[b & 3] < thr;
+}
+inline bool mask_bit_mode(int mode, uint64_t seed, uint32_t t, uint64_t l, uint64_t thr) {
+  return mode == 1 ? mask_bit_sector8(seed, t, l, thr) : mask_bit(seed, t, l, thr);
+}
+
 // Dz - x  (Sec.3.1 P:191-197 "D z = sum_k d_k * z_k", fit term of Eq.1):
 //   r[n,i,j] = sum_k sum_{a,b} d[k,a,b] z[n,k,i+P-a,j+P-b] - x[n,i,j]
 // a "valid" true convolution: every tap lands inside the code map.
@@ -186,7 +203,7 @@ double lipschitz_dtft(const Dims& D, const T* d) {
 // tau_k for k = 0..K-1 (eso != 0).
 template <typename T>
 void code_step(const Dims& D, const T* x, const T* d, T* z, double lam, double step_z, double p,
-               uint64_t seed, uint32_t t, double* tau_used, int eso = 0) {
+               uint64_t seed, uint32_t t, double* tau_used, int eso = 0, int mask_mode = 0) {
   std::vector<T> r((size_t)(D.N * D.H * D.W));
   residual<T>(D, x, d, z, r.data());
   const bool per_k = eso != 0 && !(step_z > 0.0);
@@ -217,7 +234,7 @@ void code_step(const Dims& D, const T* x, const T* d, T* z, double lam, double s
       for (int64_t u = 0; u < D.Hc; ++u)
         for (int64_t v = 0; v < D.Wc; ++v) {
           const uint64_t l = (uint64_t)((k * D.Hc + u) * D.Wc + v);
-          if (!mask_bit(seed, t, l, thr)) continue;
+          if (!mask_bit_mode(mask_mode, seed, t, l, thr)) continue;
           const double c = dtr_at(D, &dd[k * D.s * D.s], &rd[n * D.H * D.W], u, v);
           const int64_t zi = D.zi(n, k, u, v);
           const double w = (double)z[zi] - tauk[k] * c;
@@ -668,6 +685,22 @@ void oracle_philox_batch(int64_t count, const uint32_t* ctr, const uint32_t* key
 uint64_t oracle_mask_threshold(double p) { return mask_threshold(p); }
 
 // Mask bits in the ABI layout: bit l of word l>>5 (LSB first).
+void oracle_mask_bits_mode(int64_t K, int64_t Hc, int64_t Wc, double p, uint64_t seed, uint32_t t,
+                           uint32_t* bits, int mode) {
+  const uint64_t total = (uint64_t)(K * Hc * Wc);
+  const uint64_t nwords = (total + 31) / 32;
+  const uint64_t thr = mask_threshold(p);
+#pragma omp parallel for schedule(static)
+  for (int64_t wi = 0; wi < (int64_t)nwords; ++wi) {
+    uint32_t word = 0;
+    for (uint64_t bit = 0; bit < 32; ++bit) {
+      const uint64_t l = (uint64_t)wi * 32 + bit;
+      if (l < total && mask_bit_mode(mode, seed, t, l, thr)) word |= (1u << bit);
+    }
+    bits[wi] = word;
+  }
+}
+
 void oracle_mask_bits(int64_t K, int64_t Hc, int64_t Wc, double p, uint64_t seed, uint32_t t,
                       uint32_t* bits) {
   const uint64_t total = (uint64_t)(K * Hc * Wc);
@@ -708,8 +741,8 @@ double oracle_soft_threshold(double w, double kappa) { return soft_threshold(w, 
   }                                                                                              \
   void oracle_code_step_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W, const T* x, \
                               const T* d, T* z, double lam, double step_z, double p,             \
-                              uint64_t seed, uint32_t t, double* tau_used, int eso) {            \
-    code_step<T>(Dims(N, K, s, H, W), x, d, z, lam, step_z, p, seed, t, tau_used, eso);         \
+                              uint64_t seed, uint32_t t, double* tau_used, int eso, int mmode) { \
+    code_step<T>(Dims(N, K, s, H, W), x, d, z, lam, step_z, p, seed, t, tau_used, eso, mmode);  \
   }                                                                                              \
   void oracle_admm_code_step_##SUF(int64_t N, int64_t K, int64_t s, int64_t H, int64_t W,          \
                                    const T* x, const T* d, T* z, double lam, double rho,           \

@@ -131,3 +131,22 @@ def test_eso_small_p_is_exact_coordinate_minimiser():
         assert abs(zo.ravel()[i] - wstar) <= 2 * rel * max(1.0, abs(wstar - zf[i])) + 1e-9
         checked += 1
     assert checked >= 1
+
+
+def test_sector8_code_step_is_masked_ista_on_the_sector_mask():
+    """NEXT-4 (ii): the code step under block-structured masks is the textbook ISTA update on the
+    coordinates the sector mask selects (dense matrix), the other codes untouched."""
+    K, s, H, W = 2, 3, 10, 9
+    x, d, z = random_problem(41, 1, K, s, H, W, code_density=0.3)
+    x = x.astype(np.float64); d = d.astype(np.float64); z = z.astype(np.float64)
+    lam, p, seed, t = 0.1, 0.3, 9, 2
+    zo, tau = oracle.code_step(x, d, z, lam, 0.0, p, seed, t, dtype=np.float64, mask="sector8")
+    Hc, Wc = H + s - 1, W + s - 1
+    m = oracle.unpack_mask(oracle.mask_bits(K, Hc, Wc, p, seed, t, mode="sector8"), K, Hc, Wc).ravel()
+    assert m.any() and (~m).any()
+    A = dense_D(d, H, W)
+    zf = z.ravel()
+    w = zf - tau * (A.T @ (A @ zf - x.ravel()))
+    ista = np.sign(w) * np.maximum(np.abs(w) - tau * lam, 0.0)
+    expect = np.where(m, ista, zf)
+    assert np.allclose(zo.ravel(), expect, rtol=0, atol=1e-12 * max(1.0, np.abs(expect).max()))

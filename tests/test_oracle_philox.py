@@ -103,3 +103,38 @@ def test_mask_threshold_rounding():
     assert oracle.mask_threshold(0.5) == 2 ** 31
     assert oracle.mask_threshold(0.1) == int(np.floor(0.1 * 2.0 ** 32))
     assert oracle.mask_threshold(2.0 ** -32) == 1
+
+
+# ---- block-structured masks (reading E5)
+SECTOR_TAG = 0x43534253
+
+
+def test_sector8_mask_layout_against_curand(curand_ref):
+    """Bit l is curand(ctr={q lo, q hi, t, tag'}, key=seed)[b & 3] < thr with b = l >> 3, q = b >> 2:
+    one draw per aligned block of 8 coordinates, blocks running across plane boundaries."""
+    K, Hc, Wc, p, seed, t = 3, 7, 9, 0.37, 0x0123456789ABCDEF, 5
+    m = oracle.unpack_mask(oracle.mask_bits(K, Hc, Wc, p, seed, t, mode="sector8"), K, Hc, Wc).ravel()
+    L = K * Hc * Wc
+    nb = (L + 7) // 8
+    q = np.arange((nb + 3) // 4, dtype=np.uint64)
+    ctr = np.stack([q & 0xFFFFFFFF, q >> 32, np.full_like(q, t), np.full_like(q, SECTOR_TAG)],
+                   axis=1).astype(np.uint32)
+    key = np.tile(np.array([seed & 0xFFFFFFFF, seed >> 32], dtype=np.uint64), (len(q), 1)).astype(np.uint32)
+    w = _run_curand(curand_ref, ctr, key).ravel()[:nb]
+    thr = int(np.floor(p * 2.0 ** 32))
+    expect = np.repeat(w.astype(np.uint64) < thr, 8)[:L]
+    assert np.array_equal(m, expect)
+
+
+@pytest.mark.parametrize("p", [0.1, 0.5])
+def test_sector8_mask_blocks_and_statistics(p):
+    K, Hc, Wc = 8, 64, 64
+    n = K * Hc * Wc
+    m = oracle.unpack_mask(oracle.mask_bits(K, Hc, Wc, p, 77, 3, mode="sector8"), K, Hc, Wc).ravel()
+    blocks = m.reshape(-1, 8)
+    assert (blocks.all(axis=1) | ~blocks.any(axis=1)).all()  # constant on every aligned block
+    nbk = n // 8
+    sd = np.sqrt(nbk * p * (1 - p))
+    assert abs(int(blocks[:, 0].sum()) - nbk * p) < 6 * sd
+    full = oracle.unpack_mask(oracle.mask_bits(K, Hc, Wc, 1.0, 77, 3, mode="sector8"), K, Hc, Wc)
+    assert full.all()
