@@ -140,6 +140,15 @@ csc_status csc_code_step_admm(csc_ctx* ctx, const float* x, const float* d, floa
 typedef enum { CSC_STEP_LIPSCHITZ = 0, CSC_STEP_ESO = 1 } csc_step_rule;
 csc_status csc_set_step_rule(csc_ctx* ctx, int rule);
 
+/* Mask sampling (reading R4 / DESIGN.md E5):
+ *   CSC_MASK_ENTRY (default): i.i.d. Bernoulli(p) per code coordinate (Eq.2);
+ *   CSC_MASK_SECTOR8: one Bernoulli(p) draw per aligned block of 8 consecutive coordinates
+ *     l = (k*Hc+u)*Wc+v (one 32-B sector of fp32 codes) -- SURVEY.md §8f NEXT-4 (ii), a labelled
+ *     DEVIATION from the per-entry sampling of the paper.
+ * Applies to csc_code_step / csc_iterate and csc_mask_bits; csc_code_step_admm requires ENTRY. */
+typedef enum { CSC_MASK_ENTRY = 0, CSC_MASK_SECTOR8 = 1 } csc_mask_mode;
+csc_status csc_set_mask_mode(csc_ctx* ctx, int mode);
+
 /* Test hook: the K step sizes tau_z of the last code step (DEVICE fp32 [K]; the same value K
  * times unless that step used the ESO rule). */
 csc_status csc_read_step_z(csc_ctx* ctx, float* tau_dev);

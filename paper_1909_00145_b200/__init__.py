@@ -30,7 +30,7 @@ ABI_SYMBOLS = (
     "csc_mask_bits", "csc_read_residual", "csc_read_grad", "csc_lipschitz", "csc_launch_count",
     "csc_profile_enable", "csc_profile_read", "csc_kernel_variants", "csc_code_step_admm",
     "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd", "csc_surrogate_reset",
-    "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate",
+    "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate", "csc_set_mask_mode",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -70,6 +70,7 @@ def load_library(path: Optional[str] = None):
         L.csc_code_step.argtypes = [vp, vp, vp, vp, f32, f32, f64, u64, u32, vp]
         L.csc_filter_step.argtypes = [vp, vp, vp, vp, f32, vp]
         L.csc_set_step_rule.argtypes = [vp, ctypes.c_int]
+        L.csc_set_mask_mode.argtypes = [vp, ctypes.c_int]
         L.csc_filter_step_bcd.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
         L.csc_surrogate_reset.argtypes = [vp]
         L.csc_surrogate_update.argtypes = [vp, vp, vp]
@@ -207,6 +208,13 @@ class Context:
         t = ctypes.c_int64(0)
         self._check(self._L.csc_read_surrogate(self._h, C.data_ptr(), B.data_ptr(), ctypes.byref(t)))
         return int(t.value)
+
+    MASK_MODES = {"entry": 0, "sector8": 1}
+
+    def set_mask_mode(self, mode: str) -> None:
+        """Mask sampling: "entry" (Eq.2, default) or "sector8" (one draw per 8-code block; a labelled
+        deviation, include/csc.h csc_set_mask_mode)."""
+        self._check(self._L.csc_set_mask_mode(self._h, self.MASK_MODES[mode]))
 
     STEP_RULES = {"lipschitz": 0, "eso": 1}
 

@@ -129,6 +129,7 @@ struct csc_ctx {
   double* sur_diag = nullptr;   // [K][M][M]
   int64_t sur_t = 0;
   bool last_eso = false;       // the last code step used per-filter taus
+  int mask_mode = CSC_MASK_ENTRY;  // csc_set_mask_mode
   float* tauk = nullptr;       // [K] per-filter tau_z of the ESO rule
   // ADMM code solver scratch (csc_admm.cu), allocated by the first csc_code_step_admm
   float* adm_zd = nullptr;      // [N][K][Hc][Wc] scatter target of the operator (0 off the mask)
@@ -700,7 +701,7 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   if (g.N > 0) {
     if (c->ct_on) {
       if (!all_selected)
-        CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(g, c->ct, seed, iter, thr, c->mwords, c->st));
+        CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(g, c->ct, seed, iter, thr, c->mwords, c->st, c->mask_mode));
       if (c->ct.half) {
         CSC_LAUNCH(c, 1, csc::launch_absmax(c->r, n_pix(g), c->rmax, c->st));
         CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
@@ -712,7 +713,7 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
                                          lambda, zbound(c, z), c->st, tau_stride));
       }
     } else {
-      if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st));
+      if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st, c->mask_mode));
       CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, tau_dev, lambda,
                                                                 zbound(c, z), c->st, tau_stride));
     }
@@ -731,6 +732,13 @@ csc_status csc_set_step_rule(csc_ctx* c, int rule) {
   if (!c) return CSC_ERR_ARG;
   if (rule != CSC_STEP_LIPSCHITZ && rule != CSC_STEP_ESO) return fail(c, CSC_ERR_ARG, "unknown step rule");
   c->step_rule = rule;
+  return CSC_OK;
+}
+
+csc_status csc_set_mask_mode(csc_ctx* c, int mode) {
+  if (!c) return CSC_ERR_ARG;
+  if (mode != CSC_MASK_ENTRY && mode != CSC_MASK_SECTOR8) return fail(c, CSC_ERR_ARG, "unknown mask mode");
+  c->mask_mode = mode;
   return CSC_OK;
 }
 
@@ -754,6 +762,7 @@ csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float*
   if (!(rho >= 0.f) || !std::isfinite(rho)) return fail(c, CSC_ERR_ARG, "rho must be finite and >= 0");
   if (!(alpha > 0.f && alpha < 2.f)) return fail(c, CSC_ERR_ARG, "alpha must be in (0, 2)");
   if (n_admm < 1 || n_cg < 1) return fail(c, CSC_ERR_ARG, "n_admm and n_cg must be >= 1");
+  if (c->mask_mode != CSC_MASK_ENTRY) return fail(c, CSC_ERR_ARG, "the ADMM solver uses per-entry masks only");
   if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
   CSC_CUDA(c, cudaSetDevice(c->device));
   const Geom& g = c->g;
@@ -1181,7 +1190,7 @@ csc_status csc_mask_bits(csc_ctx* c, uint32_t iter, double p, uint64_t seed, uin
   if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
   CSC_CUDA(c, cudaSetDevice(c->device));
   const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
-  CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_bits(c->g, seed, iter, thr, bits_dev, c->st));
+  CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_bits(c->g, seed, iter, thr, bits_dev, c->st, c->mask_mode));
   return CSC_OK;
 }
 

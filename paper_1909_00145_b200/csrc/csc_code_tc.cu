@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) code_tc_kernel(const CtArgs A) 
 // (#13).  A thread makes 4 consecutive positions of one block: each Philox call of a
 // filter yields the 4 positions' words when l is 4-aligned.
 constexpr uint32_t kMaskTag = 0x4353434Du;
+constexpr uint32_t kSectorTag = 0x43534253u;  // block-structured masks (E5)
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
@@ -330,7 +331,7 @@ __device__ __forceinline__ uint32_t word_of(const uint4& b, int i) {
   return i == 0 ? b.x : (i == 1 ? b.y : (i == 2 ? b.z : b.w));
 }
 __global__ void mask_selwords_kernel(int K, int KC, int NC, int nblk, int64_t plane, uint64_t seed, uint32_t iter,
-                                     uint64_t thr, uint32_t* __restrict__ sw) {
+                                     uint64_t thr, int mode, uint32_t* __restrict__ sw) {
   const int64_t nq = (plane + 3) / 4;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= static_cast<int64_t>(nblk) * nq) return;
@@ -344,6 +345,21 @@ __global__ void mask_selwords_kernel(int K, int KC, int NC, int nblk, int64_t pl
     const int k = kg * KC + kl;
     if (kl >= KC || k >= K) break;
     const uint64_t l0 = static_cast<uint64_t>(k) * plane + p0;
+    if (mode == 1) {
+      // block-structured masks (E5): one draw per aligned 8-coordinate block b = l >> 3
+      const uint64_t qa = (l0 >> 3) >> 2, qb = ((l0 + 3) >> 3) >> 2;
+      const uint4 ba = philox4x32_10(make_uint4(static_cast<uint32_t>(qa), static_cast<uint32_t>(qa >> 32), iter, kSectorTag), key);
+      const uint4 bb = qb != qa ? philox4x32_10(make_uint4(static_cast<uint32_t>(qb), static_cast<uint32_t>(qb >> 32), iter,
+                                                           kSectorTag), key)
+                                : ba;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t b = (l0 + j) >> 3;
+        const uint32_t rnd = word_of((b >> 2) == qa ? ba : bb, static_cast<int>(b & 3));
+        if (static_cast<uint64_t>(rnd) < thr) out[j] |= 1u << i;
+      }
+      continue;
+    }
     const uint64_t qa = l0 >> 2;
     const uint4 ba = philox4x32_10(make_uint4(static_cast<uint32_t>(qa), static_cast<uint32_t>(qa >> 32), iter, kMaskTag), key);
     uint4 bb = ba;
@@ -428,12 +444,12 @@ CodeTcPlan code_tc_plan(const Geom& g, int num_sms) {
 }
 
 cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
-                                 uint32_t* words, cudaStream_t st) {
+                                 uint32_t* words, cudaStream_t st, int mode) {
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
   const int nblk = 4 * p.nkg;
   const int64_t total = static_cast<int64_t>(nblk) * ((plane + 3) / 4);
   mask_selwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g.K, p.KC, p.Npad / 4, nblk, plane,
-                                                                                 seed, iter, thr, words);
+                                                                                 seed, iter, thr, mode, words);
   return cudaGetLastError();
 }
 

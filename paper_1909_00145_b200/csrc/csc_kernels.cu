@@ -96,9 +96,37 @@ __device__ __forceinline__ uint4 mask_block(uint64_t seed, uint32_t iter, uint64
 __device__ __forceinline__ uint32_t pick(const uint4& w, int i) {
   return i == 0 ? w.x : (i == 1 ? w.y : (i == 2 ? w.z : w.w));
 }
+// Block-structured masks (E5): one draw per aligned block b = l >> 3 of 8 coordinates,
+// word b & 3 of Philox(ctr = {q lo, q hi, t, kSectorTag}, q = b >> 2).  r[j] = draw of l0 + j.
+constexpr uint32_t kSectorTag = 0x43534253u;  // "CSBS"
+__device__ __forceinline__ uint4 sector_block(uint64_t seed, uint32_t iter, uint64_t q) {
+  return philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), iter, kSectorTag),
+                       make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)));
+}
+__device__ __forceinline__ void mask_rnd4(int mode, uint64_t seed, uint32_t iter, uint64_t l0, uint32_t r[4]) {
+  if (mode == 1) {
+    const uint64_t qa = (l0 >> 3) >> 2, qb = ((l0 + 3) >> 3) >> 2;
+    const uint4 wa = sector_block(seed, iter, qa);
+    const uint4 wb = qb != qa ? sector_block(seed, iter, qb) : wa;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t b = (l0 + j) >> 3;
+      r[j] = pick((b >> 2) == qa ? wa : wb, static_cast<int>(b & 3));
+    }
+  } else {
+    const uint64_t qa = l0 >> 2;
+    const uint4 wa = mask_block(seed, iter, qa);
+    const uint4 wb = (l0 & 3) != 0 ? mask_block(seed, iter, qa + 1) : wa;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t l = l0 + j;
+      r[j] = pick((l >> 2) == qa ? wa : wb, static_cast<int>(l & 3));
+    }
+  }
+}
 
 // Canonical layout: one 32-bit word per thread, bit l = (k*Hc+u)*Wc+v.
-__global__ void mask_bits_kernel(uint64_t total, uint64_t seed, uint32_t iter, uint64_t thr,
+__global__ void mask_bits_kernel(uint64_t total, uint64_t seed, uint32_t iter, uint64_t thr, int mode,
                                  uint32_t* __restrict__ bits) {
   const uint64_t wi = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t nwords = (total + 31) / 32;
@@ -108,8 +136,8 @@ __global__ void mask_bits_kernel(uint64_t total, uint64_t seed, uint32_t iter, u
   for (int qq = 0; qq < 8; ++qq) {
     const uint64_t q = wi * 8 + qq;
     if (q * 4 >= total) break;
-    const uint4 w = mask_block(seed, iter, q);
-    const uint32_t v[4] = {w.x, w.y, w.z, w.w};
+    uint32_t v[4];
+    mask_rnd4(mode, seed, iter, q * 4, v);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint64_t l = q * 4 + j;
@@ -121,7 +149,7 @@ __global__ void mask_bits_kernel(uint64_t total, uint64_t seed, uint32_t iter, u
 
 // Column-word layout for the code step: thread per (k, ub, quad of 4 columns);
 // colw[(k*NB+ub)*Wc+v] bit r = mask(k, 32*ub+r, v).  Rows >= Hc are 0.
-__global__ void mask_colwords_kernel(Geom g, int NB, uint64_t seed, uint32_t iter, uint64_t thr,
+__global__ void mask_colwords_kernel(Geom g, int NB, uint64_t seed, uint32_t iter, uint64_t thr, int mode,
                                      uint32_t* __restrict__ colw) {
   const int nq = (g.Wc + 3) / 4;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -138,16 +166,12 @@ __global__ void mask_colwords_kernel(Geom g, int NB, uint64_t seed, uint32_t ite
     const int u = ub * 32 + r;
     if (u >= g.Hc) break;
     const uint64_t l0 = (static_cast<uint64_t>(k) * g.Hc + u) * g.Wc + v0;
-    const uint64_t qa = l0 >> 2;
-    const uint4 wa = mask_block(seed, iter, qa);
-    uint4 wb = wa;
-    if ((l0 & 3) != 0) wb = mask_block(seed, iter, qa + 1);
+    uint32_t w4[4];
+    mask_rnd4(mode, seed, iter, l0, w4);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       if (v0 + c >= g.Wc) break;
-      const uint64_t l = l0 + c;
-      const uint32_t w = ((l >> 2) == qa) ? pick(wa, static_cast<int>(l & 3)) : pick(wb, static_cast<int>(l & 3));
-      if (static_cast<uint64_t>(w) < thr) out[c] |= 1u << r;
+      if (static_cast<uint64_t>(w4[c]) < thr) out[c] |= 1u << r;
     }
   }
   uint32_t* dst = colw + (static_cast<int64_t>(k) * NB + ub) * g.Wc + v0;
@@ -822,18 +846,19 @@ cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, do
 }
 
 cudaError_t launch_mask_colwords(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr, uint32_t* colw,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int mode) {
   const int NB = ceil_div(g.Hc, 32);
   const int64_t total = static_cast<int64_t>(g.K) * NB * ceil_div(g.Wc, 4);
-  mask_colwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g, NB, seed, iter, thr, colw);
+  mask_colwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g, NB, seed, iter, thr, mode,
+                                                                                    colw);
   return cudaGetLastError();
 }
 
 cudaError_t launch_mask_bits(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr, uint32_t* bits,
-                             cudaStream_t st) {
+                             cudaStream_t st, int mode) {
   const uint64_t total = static_cast<uint64_t>(g.K) * g.Hc * g.Wc;
   const uint64_t nwords = (total + 31) / 32;
-  mask_bits_kernel<<<static_cast<unsigned>((nwords + 255) / 256), 256, 0, st>>>(total, seed, iter, thr, bits);
+  mask_bits_kernel<<<static_cast<unsigned>((nwords + 255) / 256), 256, 0, st>>>(total, seed, iter, thr, mode, bits);
   return cudaGetLastError();
 }
 

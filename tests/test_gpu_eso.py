@@ -100,3 +100,47 @@ def test_step_rule_argument_error(torch_dev):
     with pytest.raises(pkg.CSCError):
         ctx._check(ctx._L.csc_set_step_rule(ctx._h, 7))
     ctx.close()
+
+
+# ---- NEXT-4 (ii): block-structured masks (a labelled deviation, E5)
+@pytest.mark.parametrize("K,Hc,Wc", [(8, 36, 36), (3, 7, 9), (5, 41, 67), (100, 110, 110)])
+@pytest.mark.parametrize("p", [0.1, 0.5, 1.0])
+def test_sector8_mask_bits_bit_exact(torch_dev, K, Hc, Wc, p):
+    import torch
+    import paper_1909_00145_b200 as pkg
+    s = 3
+    ctx = pkg.Context(1, K, s, Hc - s + 1, Wc - s + 1, device=0)
+    ctx.set_mask_mode("sector8")
+    out = torch.zeros((K * Hc * Wc + 31) // 32, dtype=torch.int32, device=torch_dev)
+    for seed, it in [(0, 0), (0x0123456789ABCDEF, 7)]:
+        ctx.mask_bits(it, p, seed, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle.mask_bits(K, Hc, Wc, p, seed, it, "sector8"))
+    ctx.close()
+
+
+@pytest.mark.parametrize("path", ["half", "tc", "simt"])
+@pytest.mark.parametrize("shape,p", [((3, 5, 5, 70, 130), 0.1), ((2, 17, 11, 100, 100), 0.2),
+                                     ((1, 9, 3, 33, 47), 0.5), ((2, 130, 7, 20, 300), 0.1)])
+def test_sector8_code_step_parity(torch_dev, shape, p, path, monkeypatch):
+    import torch
+    import paper_1909_00145_b200 as pkg
+    monkeypatch.setenv("CSC_CODE_PATH", path)
+    N, K, s, H, W = shape
+    x, d, z = random_problem(700 + K, N, K, s, H, W, code_density=0.3)
+    seed, it, lam = 31337, 4, 0.2
+    ctx = pkg.Context(N, K, s, H, W, device=0)
+    ctx.set_mask_mode("sector8")
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    ctx.code_step(xt, dt, zt, lam, p, seed, it)
+    zo, _ = oracle.code_step(x, d, z, lam, 0.0, p, seed, it, mask="sector8")
+    torch.cuda.synchronize()
+    zg = zt.cpu().numpy()
+    assert rel_err(zg, zo) < TOL
+    Hc, Wc = H + s - 1, W + s - 1
+    m = oracle.unpack_mask(oracle.mask_bits(K, Hc, Wc, p, seed, it, "sector8"), K, Hc, Wc)
+    for n in range(N):
+        assert np.array_equal(zg[n][~m], z[n][~m])
+    with pytest.raises(pkg.CSCError):
+        ctx.code_step_admm(xt, dt, zt, lam, p, seed, it)  # ADMM keeps the per-entry masks of Eq.2
+    ctx.close()
