@@ -329,6 +329,8 @@ def run_ours(args):
                       nccl_id=nccl_id)
     if args.step_rule != "lipschitz":
         ctx.set_step_rule(args.step_rule)
+    if args.mask != "entry":
+        ctx.set_mask_mode(args.mask)
     l2_flush = None
     if 4 * cfg.N * cfg.K * cfg.Hc * cfg.Wc <= 2 * 126e6:
         l2_flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)
@@ -433,7 +435,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(_config_dict(cfg, ws), code_solver=args.code_solver, filter_solver=args.filter_solver,
-                           step_rule=args.step_rule),
+                           step_rule=args.step_rule, mask=args.mask),
             "roofline": dict(rl[dom], dominant_class=dom),
             "kernel_rooflines": rl,
             "kernels": kernels,
@@ -466,6 +468,9 @@ def main():
                     help="pg: the north_star projected-gradient filter step (default); bcd: the paper's "
                          "projected block-coordinate update, one warm-started sweep (SURVEY.md §8f NEXT-3); "
                          "surrogate: Eq.7 surrogate update + Eq.8 sweep per step (NEXT-2)")
+    ap.add_argument("--mask", default="entry", choices=["entry", "sector8"],
+                    help="entry: per-code Bernoulli (Eq.2, default); sector8: one draw per 8-code sector "
+                         "(SURVEY.md §8f NEXT-4 (ii), a labelled deviation)")
     ap.add_argument("--step-rule", default="lipschitz", choices=["lipschitz", "eso"],
                     help="built-in tau_z rule of the prox code step (eso: SURVEY.md §8f NEXT-4 (i))")
     ap.add_argument("--code-solver", default="prox", choices=["prox", "admm"],
