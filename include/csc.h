@@ -106,7 +106,9 @@ csc_status csc_objective(csc_ctx* ctx, const float* x, const float* d, const flo
                          float lambda, double out[3]);
 
 /* One SBCSC outer iteration (Alg.1): [x_host -> x upload] ->
- * csc_code_step(iter) -> csc_filter_step -> csc_objective.  x_host (HOST,
+ * csc_code_step(iter) -> csc_filter_step -> csc_objective.  When the residual cache
+ * holds D z - x for the same (x, d, z) pointers, the upload moves it to the new images
+ * elementwise (r <- r + x_old - x_new) instead of recomputing it.  x_host (HOST,
  * nullable, ideally pinned) is copied into the device buffer x first (the step's
  * input for the end-to-end measurement); obj_out[3] (HOST) as csc_objective;
  * taus_out[2] (HOST, nullable) = {tau_z, tau_d}.  Collective. */

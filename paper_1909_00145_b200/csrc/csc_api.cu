@@ -1168,8 +1168,17 @@ csc_status csc_iterate(csc_ctx* c, const float* x_host, float* x, float* d, floa
   if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
   CSC_CUDA(c, cudaSetDevice(c->device));
   if (x_host && c->g.N > 0) {
+    // new images into x.  When the residual cache holds r = D z - x_old for these (d, z) -- the
+    // previous iteration's objective pass, or z = 0 -- move it to the new images without a dense
+    // pass: r <- (r + x_old) - x_new (a3', linearity)
+    const bool shift = c->cache_valid && c->cx == x && c->cz == z && (c->cd == d || c->cd == nullptr);
+    if (shift) CSC_LAUNCH(c, 1, csc::launch_resid_shift(x, c->r, n_pix(c->g), 1.f, c->st));
     CSC_CUDA(c, cudaMemcpyAsync(x, x_host, sizeof(float) * n_pix(c->g), cudaMemcpyHostToDevice, c->st));
-    c->cache_valid = false;
+    if (shift) {
+      CSC_LAUNCH(c, 1, csc::launch_resid_shift(x, c->r, n_pix(c->g), -1.f, c->st));
+    } else {
+      c->cache_valid = false;
+    }
   }
   s = csc_code_step(c, x, d, z, lambda, step_z, p, seed, iter, nullptr);
   if (s != CSC_OK) return s;

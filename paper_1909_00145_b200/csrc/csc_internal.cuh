@@ -98,6 +98,8 @@ cudaError_t launch_filter_update(const Geom& g, float* d, const double* gsum, co
 
 // r = -x (zero codes).
 cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st);
+// r += sign * x
+cudaError_t launch_resid_shift(const float* x, float* r, int64_t n, float sign, cudaStream_t st);
 
 // ---- tensor-core (tcgen05, 3xTF32) dense pass, csc_tc.cu
 constexpr int kTcMaxKC = 104;  // filters per k-split held resident in shared memory

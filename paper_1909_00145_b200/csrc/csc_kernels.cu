@@ -910,6 +910,18 @@ cudaError_t launch_filter_update(const Geom& g, float* d, const double* gsum, co
   return cudaGetLastError();
 }
 
+// r += sign * x (the residual moved to new images without a dense pass, csc_iterate)
+__global__ void axpy_sign_kernel(const float* __restrict__ x, float* __restrict__ r, int64_t n, float sign) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    r[i] = fmaf(sign, x[i], r[i]);
+}
+
+cudaError_t launch_resid_shift(const float* x, float* r, int64_t n, float sign, cudaStream_t st) {
+  axpy_sign_kernel<<<kFinalizeBlocks, 256, 0, st>>>(x, r, n, sign);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st) {
   neg_copy_kernel<<<kFinalizeBlocks, 256, 0, st>>>(x, r, n);
   return cudaGetLastError();

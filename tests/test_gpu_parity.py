@@ -361,3 +361,28 @@ def test_full_size_large_config_sampled():
         F_prev = F[0]
     del zt
     ctx.close()
+
+
+def test_iterate_with_new_images_each_step(torch_dev):
+    """csc_iterate with x_host: the residual cache is moved to the new images elementwise
+    (r + x_old - x_new); 6 iterations on a different seeded batch each step match the oracle."""
+    import torch
+    cfg = CONFIGS["tiny"]
+    p, lam = 0.5, cfg.lam
+    d = make_filters(cfg)
+    z = make_codes(cfg)
+    seed = mask_seed(cfg)
+    ctx = _ctx(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W)
+    x0 = make_images(cfg)
+    xt, dt, zt = _t(x0, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    for t in range(1, 7):
+        xb = np.ascontiguousarray(make_images(cfg.with_(N=cfg.N), 0, cfg.N) * (1.0 + 0.1 * t)).astype(np.float32)
+        xh = torch.from_numpy(xb).pin_memory()
+        F, _ = ctx.iterate(xt, dt, zt, lam, p, seed, t, x_host=xh)
+        it = oracle.iteration(xb, d, z, lam, p, seed, t)
+        z, d = it["z"], it["d"]
+        torch.cuda.synchronize()
+        assert rel_err(zt.cpu().numpy(), z) < TOL, t
+        assert rel_err(dt.cpu().numpy(), d) < TOL, t
+        assert abs(F[0] - it["F"][0]) <= TOL * abs(it["F"][0]), t
+    ctx.close()
