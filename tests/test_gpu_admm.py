@@ -112,3 +112,27 @@ def test_admm_argument_errors(torch_dev):
                                n_admm=args["n_admm"], n_cg=args["n_cg"])
     assert np.array_equal(zt.cpu().numpy(), z)
     ctx.close()
+
+
+def test_admm_full_size_batch_config_image0(torch_dev):
+    """BASELINE.json configs[1] at full size (10 images 100x100, K = 100, s = 11, p = 0.1): the ADMM
+    step is per image (A2), so the oracle solves image 0 alone and its codes are compared with the
+    GPU's image 0 from the full 10-image launch (the launch configuration bench.py uses)."""
+    import torch
+    import paper_1909_00145_b200 as pkg
+    from synth import CONFIGS, make_codes, make_filters, make_images, mask_seed
+    cfg = CONFIGS["batch"]
+    x, d = make_images(cfg), make_filters(cfg)
+    rng = np.random.default_rng(5)
+    z = make_codes(cfg)
+    z[:] = (rng.standard_normal(z.shape) * (rng.random(z.shape) < 0.05)).astype(np.float32) * 0.1
+    seed = mask_seed(cfg)
+    ctx = pkg.Context(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W, device=0)
+    xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    ctx.code_step_admm(xt, dt, zt, cfg.lam, cfg.p, seed, 3)
+    torch.cuda.synchronize()
+    zo = oracle.admm_code_step(x[:1], d, z[:1], cfg.lam, cfg.p, seed, 3, dtype=np.float64)
+    err = rel_err(zt.cpu().numpy()[:1], zo)
+    print(f"admm full-size batch image 0: rel err {err:.3e}")
+    assert err < TOL_ADMM, err
+    ctx.close()
