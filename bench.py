@@ -406,19 +406,28 @@ def run_ours(args):
     t_ms = float(tt.item())
     value = args.steps / (t_ms / 1e3)
 
-    # ---- e2e: same iteration through the C ABI with the step's images uploaded from pinned host memory
+    # ---- e2e: same iteration through the C ABI with the step's images uploaded from pinned host memory.
+    # Hot path: double-buffered -- step i+1's images are staged (async H2D on the library's copy stream)
+    # before step i runs, so every step's transfer is inside the timed region but overlaps compute.
     x_host = torch.from_numpy(x_np).pin_memory()
     barrier()
     torch.cuda.synchronize()
-    e2e_ms = 0.0
-    for _ in range(args.steps):
+    staged = not (admm or bcd or sur)
+    t0 = time.perf_counter()
+    if staged:
+        ctx.stage_images(x_host, 0)
+    for i in range(args.steps):
         it += 1
         if l2_flush is not None:
             l2_flush.fill_(float(it))
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        step(it, x_host=x_host)
-        e2e_ms += (time.perf_counter() - t0) * 1e3
+        if staged:
+            if i + 1 < args.steps:
+                ctx.stage_images(x_host, (i + 1) % 2)
+            ctx.iterate_staged(x, d, z, cfg.lam, cfg.p, seed, it, i % 2)
+        else:
+            step(it, x_host=x_host)
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
     te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)

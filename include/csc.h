@@ -184,6 +184,18 @@ csc_status csc_surrogate_update(csc_ctx* ctx, const float* x, const float* z);
 csc_status csc_filter_step_surrogate(csc_ctx* ctx, float* d, int sweeps, uint8_t* flags_out);
 csc_status csc_read_surrogate(csc_ctx* ctx, double* C_dev, double* B_dev, int64_t* t_out);
 
+/* Double-buffered image input for streaming use.  csc_stage_images starts an asynchronous copy
+ * of x_host (HOST, pinned, n_local*H*W floats) into the library's staging slot (0 or 1) on an
+ * internal copy stream and returns at once; csc_iterate_staged(slot, ...) is csc_iterate with the
+ * images taken from that slot (waiting for its copy on the device, then a device-to-device copy
+ * into x).  Staging the next batch before calling csc_iterate_staged on the current one overlaps
+ * the host-to-device transfer with the iteration.  A slot is reusable once the iteration that
+ * consumed it has been enqueued.  CSC_ERR_ARG for an unstaged slot. */
+csc_status csc_stage_images(csc_ctx* ctx, const float* x_host, int slot);
+csc_status csc_iterate_staged(csc_ctx* ctx, int slot, float* x, float* d, float* z, float lambda,
+                              float step_z, float step_d, double p, uint64_t seed, uint32_t iter,
+                              double obj_out[3], float taus_out[2]);
+
 /* Forget the residual cache (caller changed x, d or z outside the API). */
 csc_status csc_invalidate(csc_ctx* ctx);
 

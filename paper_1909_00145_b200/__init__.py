@@ -31,6 +31,7 @@ ABI_SYMBOLS = (
     "csc_profile_enable", "csc_profile_read", "csc_kernel_variants", "csc_code_step_admm",
     "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd", "csc_surrogate_reset",
     "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate", "csc_set_mask_mode",
+    "csc_stage_images", "csc_iterate_staged",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -71,6 +72,8 @@ def load_library(path: Optional[str] = None):
         L.csc_filter_step.argtypes = [vp, vp, vp, vp, f32, vp]
         L.csc_set_step_rule.argtypes = [vp, ctypes.c_int]
         L.csc_set_mask_mode.argtypes = [vp, ctypes.c_int]
+        L.csc_stage_images.argtypes = [vp, vp, ctypes.c_int]
+        L.csc_iterate_staged.argtypes = [vp, ctypes.c_int, vp, vp, vp, f32, f32, f32, f64, u64, u32, vp, vp]
         L.csc_filter_step_bcd.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
         L.csc_surrogate_reset.argtypes = [vp]
         L.csc_surrogate_update.argtypes = [vp, vp, vp]
@@ -264,6 +267,26 @@ class Context:
         taus = (ctypes.c_float * 2)()
         self._check(self._L.csc_iterate(self._h, ph, px, pd, pz, float(lam), float(step_z), float(step_d),
                                         float(p), int(seed) & (2**64 - 1), int(it) & 0xffffffff, obj, taus))
+        return (float(obj[0]), float(obj[1]), float(obj[2])), (float(taus[0]), float(taus[1]))
+
+    def stage_images(self, x_host, slot: int) -> None:
+        """Asynchronous copy of the pinned CPU float32 tensor x_host into staging slot 0/1
+        (include/csc.h csc_stage_images); x_host must stay alive until the copy has run."""
+        if x_host.is_cuda or x_host.dtype.itemsize != 4 or not x_host.is_contiguous():
+            raise ValueError("x_host must be a contiguous float32 CPU tensor")
+        if x_host.numel() != self.n_local * self.H * self.W:
+            raise ValueError("x_host has the wrong size")
+        self._check(self._L.csc_stage_images(self._h, x_host.data_ptr(), int(slot)))
+
+    def iterate_staged(self, x, d, z, lam: float, p: float, seed: int, it: int, slot: int, *, step_z: float = 0.0,
+                       step_d: float = 0.0):
+        """csc_iterate with the images of a staged slot (include/csc.h csc_iterate_staged)."""
+        px, pd, pz = self._xdz(x, d, z)
+        obj = (ctypes.c_double * 3)()
+        taus = (ctypes.c_float * 2)()
+        self._check(self._L.csc_iterate_staged(self._h, int(slot), px, pd, pz, float(lam), float(step_z),
+                                               float(step_d), float(p), int(seed) & (2**64 - 1),
+                                               int(it) & 0xffffffff, obj, taus))
         return (float(obj[0]), float(obj[1]), float(obj[2])), (float(taus[0]), float(taus[1]))
 
     def invalidate(self):

@@ -130,6 +130,13 @@ struct csc_ctx {
   int64_t sur_t = 0;
   bool last_eso = false;       // the last code step used per-filter taus
   int mask_mode = CSC_MASK_ENTRY;  // csc_set_mask_mode
+  // double-buffered image staging (csc_stage_images / csc_iterate_staged)
+  cudaStream_t cp_st = nullptr;
+  float* stage[2] = {nullptr, nullptr};
+  cudaEvent_t st_ready[2] = {nullptr, nullptr};
+  cudaEvent_t st_free[2] = {nullptr, nullptr};
+  bool staged[2] = {false, false};
+  bool st_used[2] = {false, false};
   float* tauk = nullptr;       // [K] per-filter tau_z of the ESO rule
   // ADMM code solver scratch (csc_admm.cu), allocated by the first csc_code_step_admm
   float* adm_zd = nullptr;      // [N][K][Hc][Wc] scatter target of the operator (0 off the mask)
@@ -611,6 +618,12 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->bcd_flags);
   cudaFree(c->bcd_part);
   cudaFree(c->bcd_vec);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c->stage[i]);
+    if (c->st_ready[i]) cudaEventDestroy(c->st_ready[i]);
+    if (c->st_free[i]) cudaEventDestroy(c->st_free[i]);
+  }
+  if (c->cp_st) cudaStreamDestroy(c->cp_st);
   cudaFree(c->sur_C);
   cudaFree(c->sur_B);
   cudaFree(c->sur_pp);
@@ -1157,8 +1170,44 @@ csc_status csc_objective(csc_ctx* c, const float* x, const float* d, const float
   return objective_finish(c, lambda, out);
 }
 
+csc_status csc_stage_images(csc_ctx* c, const float* x_host, int slot) {
+  if (!c || !x_host || slot < 0 || slot > 1) return fail(c, CSC_ERR_ARG, "x_host (host) and slot 0/1 required");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const size_t bytes = sizeof(float) * static_cast<size_t>(n_pix(c->g));
+  if (c->cp_st == nullptr) {
+    CSC_CUDA(c, cudaStreamCreateWithFlags(&c->cp_st, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CSC_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->stage[i]), bytes < 16 ? 16 : bytes));
+      CSC_CUDA(c, cudaEventCreateWithFlags(&c->st_ready[i], cudaEventDisableTiming));
+      CSC_CUDA(c, cudaEventCreateWithFlags(&c->st_free[i], cudaEventDisableTiming));
+    }
+  }
+  if (c->st_used[slot]) CSC_CUDA(c, cudaStreamWaitEvent(c->cp_st, c->st_free[slot], 0));  // slot consumed
+  if (bytes > 0) CSC_CUDA(c, cudaMemcpyAsync(c->stage[slot], x_host, bytes, cudaMemcpyHostToDevice, c->cp_st));
+  CSC_CUDA(c, cudaEventRecord(c->st_ready[slot], c->cp_st));
+  c->staged[slot] = true;
+  return CSC_OK;
+}
+
+static csc_status iterate_impl(csc_ctx* c, const float* x_host, int slot, float* x, float* d, float* z, float lambda,
+                               float step_z, float step_d, double p, uint64_t seed, uint32_t iter, double obj_out[3],
+                               float taus_out[2]);
+
+csc_status csc_iterate_staged(csc_ctx* c, int slot, float* x, float* d, float* z, float lambda, float step_z,
+                              float step_d, double p, uint64_t seed, uint32_t iter, double obj_out[3],
+                              float taus_out[2]) {
+  if (!c || slot < 0 || slot > 1 || !c->staged[slot]) return fail(c, CSC_ERR_ARG, "slot not staged");
+  return iterate_impl(c, nullptr, slot, x, d, z, lambda, step_z, step_d, p, seed, iter, obj_out, taus_out);
+}
+
 csc_status csc_iterate(csc_ctx* c, const float* x_host, float* x, float* d, float* z, float lambda, float step_z,
                        float step_d, double p, uint64_t seed, uint32_t iter, double obj_out[3], float taus_out[2]) {
+  return iterate_impl(c, x_host, -1, x, d, z, lambda, step_z, step_d, p, seed, iter, obj_out, taus_out);
+}
+
+static csc_status iterate_impl(csc_ctx* c, const float* x_host, int slot, float* x, float* d, float* z, float lambda,
+                               float step_z, float step_d, double p, uint64_t seed, uint32_t iter, double obj_out[3],
+                               float taus_out[2]) {
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
   if (!obj_out) return fail(c, CSC_ERR_ARG, "obj_out must be a host pointer to 3 doubles");
@@ -1167,13 +1216,23 @@ csc_status csc_iterate(csc_ctx* c, const float* x_host, float* x, float* d, floa
     return fail(c, CSC_ERR_ARG, "steps must be finite and >= 0");
   if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
   CSC_CUDA(c, cudaSetDevice(c->device));
-  if (x_host && c->g.N > 0) {
+  if ((x_host || slot >= 0) && c->g.N > 0) {
     // new images into x.  When the residual cache holds r = D z - x_old for these (d, z) -- the
     // previous iteration's objective pass, or z = 0 -- move it to the new images without a dense
     // pass: r <- (r + x_old) - x_new (a3', linearity)
     const bool shift = c->cache_valid && c->cx == x && c->cz == z && (c->cd == d || c->cd == nullptr);
     if (shift) CSC_LAUNCH(c, 1, csc::launch_resid_shift(x, c->r, n_pix(c->g), 1.f, c->st));
-    CSC_CUDA(c, cudaMemcpyAsync(x, x_host, sizeof(float) * n_pix(c->g), cudaMemcpyHostToDevice, c->st));
+    if (slot >= 0) {
+      // staged images (csc_stage_images): the H2D copy ran on the copy stream, overlapped with the
+      // previous iteration; wait for it and copy device to device
+      CSC_CUDA(c, cudaStreamWaitEvent(c->st, c->st_ready[slot], 0));
+      CSC_CUDA(c, cudaMemcpyAsync(x, c->stage[slot], sizeof(float) * n_pix(c->g), cudaMemcpyDeviceToDevice, c->st));
+      CSC_CUDA(c, cudaEventRecord(c->st_free[slot], c->st));
+      c->st_used[slot] = true;
+      c->staged[slot] = false;
+    } else {
+      CSC_CUDA(c, cudaMemcpyAsync(x, x_host, sizeof(float) * n_pix(c->g), cudaMemcpyHostToDevice, c->st));
+    }
     if (shift) {
       CSC_LAUNCH(c, 1, csc::launch_resid_shift(x, c->r, n_pix(c->g), -1.f, c->st));
     } else {

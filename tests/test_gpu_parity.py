@@ -386,3 +386,33 @@ def test_iterate_with_new_images_each_step(torch_dev):
         assert rel_err(dt.cpu().numpy(), d) < TOL, t
         assert abs(F[0] - it["F"][0]) <= TOL * abs(it["F"][0]), t
     ctx.close()
+
+
+def test_iterate_staged_double_buffered(torch_dev):
+    """csc_stage_images + csc_iterate_staged: the next batch is staged on the copy stream while the
+    current iteration runs; 5 iterations on different batches match the oracle, and an unstaged
+    slot is refused."""
+    import torch
+    import paper_1909_00145_b200 as pkg
+    cfg = CONFIGS["tiny"]
+    p, lam = 0.5, cfg.lam
+    d, z = make_filters(cfg), make_codes(cfg)
+    seed = mask_seed(cfg)
+    ctx = _ctx(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W)
+    xt, dt, zt = _t(make_images(cfg), torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    batches = [np.ascontiguousarray(make_images(cfg) * (1.0 + 0.2 * t)).astype(np.float32) for t in range(5)]
+    hosts = [torch.from_numpy(b).pin_memory() for b in batches]
+    with pytest.raises(pkg.CSCError):
+        ctx.iterate_staged(xt, dt, zt, lam, p, seed, 1, 1)
+    ctx.stage_images(hosts[0], 0)
+    for t in range(5):
+        if t + 1 < 5:
+            ctx.stage_images(hosts[t + 1], (t + 1) % 2)
+        F, _ = ctx.iterate_staged(xt, dt, zt, lam, p, seed, t + 1, t % 2)
+        it = oracle.iteration(batches[t], d, z, lam, p, seed, t + 1)
+        z, d = it["z"], it["d"]
+        torch.cuda.synchronize()
+        assert rel_err(zt.cpu().numpy(), z) < TOL, t
+        assert rel_err(dt.cpu().numpy(), d) < TOL, t
+        assert abs(F[0] - it["F"][0]) <= TOL * abs(it["F"][0]), t
+    ctx.close()
