@@ -124,13 +124,17 @@ def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox", filter_solve
             nt = (M + 3) // 4
             if filter_solver == "surrogate":  # batch Gram over all filter pairs, full 4x4 tiles
                 fma = nl * cfg.H * cfg.W * (cfg.K * (cfg.K + 1) / 2) * 16.0 * nt * nt
+            elif cfg.H > cfg.s - 1 and cfg.W > cfg.s - 1:  # lag-structured Gram: (2s-1)^2 lags x Hc x Wc
+                fma = nl * cfg.K * (2 * cfg.s - 1) ** 2 * cfg.Hc * cfg.Wc
             else:
                 fma = nl * cfg.K * cfg.H * cfg.W * 16.0 * nt * (nt + 1) / 2
             fp64_peak = SMS * 64 * 2 * sm_max_mhz * 1e6 / 1e12
-            out[name] = {"kernel": "bcd_gram_kernel + per-filter kernels (fp64, csc_bcd.cu)", "bound": "alu",
+            out[name] = {"kernel": "bcd_lag_kernel / bcd_gram_kernel + per-filter kernels (fp64, csc_bcd.cu)",
+                         "bound": "alu",
                          "achieved": 2.0 * fma / (ms / steps / 1e3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
                          "peak_note": f"148 SMs x 64 FP64 lanes x 2 x {sm_max_mhz:.0f} MHz (derived, DESIGN.md §11)",
-                         "flop_model": "2 * N K H W * 16 * (ceil(M/4)(ceil(M/4)+1)/2) per sweep (whole class time)"}
+                         "flop_model": "Gram FMAs x 2 per sweep: lag-structured N K (2s-1)^2 Hc Wc (H, W > s-1), else "
+                                       "N K H W 16 ceil(M/4)(ceil(M/4)+1)/2; whole class time"}
         elif name == "code_step" and solver == "admm":
             # ADMM mode: code_h_kernel in plain mode writes the dense correlation D^T e
             out[name] = two_roofs("code_h_kernel plain mode (dense D^T e for the ADMM operator)", avg,

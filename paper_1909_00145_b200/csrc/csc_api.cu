@@ -122,6 +122,8 @@ struct csc_ctx {
   uint8_t* bcd_flags = nullptr; // [K]
   double* bcd_part = nullptr;   // [gk blocks][M]
   double* bcd_vec = nullptr;    // gk[M], dl[M]
+  double* bcd_gq = nullptr;     // lag-structured Gram prefix sums
+  double* bcd_cfull = nullptr;  // [K][M][M]
   // online surrogates (Eq.7), allocated by the first csc_surrogate_reset / update
   double* sur_C = nullptr;      // [K][K][M][M]
   double* sur_B = nullptr;      // [K][M]
@@ -618,6 +620,8 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->bcd_flags);
   cudaFree(c->bcd_part);
   cudaFree(c->bcd_vec);
+  cudaFree(c->bcd_gq);
+  cudaFree(c->bcd_cfull);
   for (int i = 0; i < 2; ++i) {
     cudaFree(c->stage[i]);
     if (c->st_ready[i]) cudaEventDestroy(c->st_ready[i]);
@@ -962,16 +966,34 @@ csc_status csc_filter_step_bcd(csc_ctx* c, const float* x, float* d, const float
   double* gk = c->bcd_vec;
   double* dl = c->bcd_vec + M;
   for (int sw = 0; sw < sweeps; ++sw) {
-    // C_kk for all k on this rank's images, summed over ranks, then (C_kk + ridge)^-1
-    if (g.N > 0) {
-      CSC_LAUNCH_C(c, CSC_K_BCD, 1, csc::launch_bcd_gram(g, z, c->bcd_gpart, c->st));
+    // C_kk for all k on this rank's images, summed over ranks, then (C_kk + ridge)^-1.  Lag-structured
+    // Gram (plane autocorrelation windows) when H, W > P unless CSC_BCD_GRAM=direct.
+    const char* gev = std::getenv("CSC_BCD_GRAM");
+    const bool lag = csc::bcd_lag_supported(g) && !(gev != nullptr && std::string(gev) == "direct");
+    if (lag) {
+      if (c->bcd_gq == nullptr) {
+        if (cudaMalloc(reinterpret_cast<void**>(&c->bcd_gq), csc::bcd_lag_bytes(g)) != cudaSuccess ||
+            cudaMalloc(reinterpret_cast<void**>(&c->bcd_cfull), sizeof(double) * g.K * M * M) != cudaSuccess) {
+          cudaGetLastError();
+          return fail(c, CSC_ERR_OOM, "BCD lag-Gram scratch allocation failed");
+        }
+      }
+      CSC_LAUNCH_C(c, CSC_K_BCD, 2, csc::launch_bcd_lag_gram(g, z, c->bcd_gq, c->bcd_cfull, c->st));
+      s = allreduce_d(c, c->bcd_cfull, static_cast<size_t>(g.K) * M * M);
+      if (s != CSC_OK) return s;
+      CSC_LAUNCH_C(c, CSC_K_BCD, 1, csc::launch_bcd_inverse_full(g, c->bcd_cfull, kBcdRidge, c->bcd_ainv,
+                                                                 c->bcd_flags, c->st));
     } else {
-      CSC_CUDA(c, cudaMemsetAsync(c->bcd_gpart, 0, sizeof(double) * g.K * ns * M * M, c->st));
+      if (g.N > 0) {
+        CSC_LAUNCH_C(c, CSC_K_BCD, 1, csc::launch_bcd_gram(g, z, c->bcd_gpart, c->st));
+      } else {
+        CSC_CUDA(c, cudaMemsetAsync(c->bcd_gpart, 0, sizeof(double) * g.K * ns * M * M, c->st));
+      }
+      s = allreduce_d(c, c->bcd_gpart, static_cast<size_t>(g.K) * ns * M * M);
+      if (s != CSC_OK) return s;
+      CSC_LAUNCH_C(c, CSC_K_BCD, 1, csc::launch_bcd_inverse(g, c->bcd_gpart, kBcdRidge, c->bcd_ainv, c->bcd_flags,
+                                                            c->st));
     }
-    s = allreduce_d(c, c->bcd_gpart, static_cast<size_t>(g.K) * ns * M * M);
-    if (s != CSC_OK) return s;
-    CSC_LAUNCH_C(c, CSC_K_BCD, 1, csc::launch_bcd_inverse(g, c->bcd_gpart, kBcdRidge, c->bcd_ainv, c->bcd_flags,
-                                                          c->st));
     for (int k = 0; k < g.K; ++k) {
       CSC_LAUNCH_C(c, CSC_K_BCD, nb > 0 ? 2 : 1, csc::launch_bcd_gk(g, k, z, c->r, c->bcd_part, gk, c->st));
       s = allreduce_d(c, gk, static_cast<size_t>(M));

@@ -11,6 +11,7 @@
 #include "csc_internal.cuh"
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace csc {
@@ -299,6 +300,106 @@ __global__ void bcd_resid_kernel(Geom g, int k, const float* __restrict__ z, con
 }
 
 
+// ---- Lag-structured Gram (the default when H, W > P): C_kk[(a,b),(a',b')] is the sum of
+// Pi(u,v) = z[u,v] z[u+du, v+dv], du = a - a', dv = b - b', over the box [P-a, P-a+H) x
+// [P-b, P-b+W) of the code plane -- a window of the plane's autocorrelation at lag (du, dv).  One
+// thread per lag accumulates the 2D prefix sums Q(r, c) = sum_{u<r, v<c} Pi at the 2S row cuts
+// {0..P} u {H..H+P} and the 2S column cuts {0..P} u {W..W+P}; every entry is then a 4-corner box sum
+// (bcd_lag_assemble_kernel).  (2S-1)^2 lags x Hc x Wc products per plane instead of M^2/2 x H x W.
+constexpr int kLagRB = 16;  // code rows per staged band
+
+template <int S>
+__global__ void __launch_bounds__(((2 * S - 1) * (2 * S - 1) + 31) / 32 * 32, 1)
+bcd_lag_kernel(Geom g, const float* __restrict__ z, int nsplit, double* __restrict__ gq) {
+  constexpr int P = S - 1;
+  constexpr int NL = (2 * S - 1) * (2 * S - 1);
+  constexpr int NCUT = 2 * S;
+  extern __shared__ float zb[];  // rows [u0 - P, u0 + kLagRB + P) of the plane, zero outside
+  const int k = blockIdx.y, sp = blockIdx.x;
+  const int t = threadIdx.x;
+  const bool act = t < NL;
+  const int du = act ? t / (2 * S - 1) - P : 0, dv = act ? t % (2 * S - 1) - P : 0;
+  const int rows = kLagRB + 2 * P;
+  const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
+  // column cuts: c_j = j (j <= P), W + j - S (j > P); row cuts likewise with H
+  double Q[NCUT][NCUT];
+#pragma unroll
+  for (int i = 0; i < NCUT; ++i)
+#pragma unroll
+    for (int j = 0; j < NCUT; ++j) Q[i][j] = 0.0;
+  const int n0 = static_cast<int>((static_cast<int64_t>(sp) * g.N) / nsplit);
+  const int n1 = static_cast<int>((static_cast<int64_t>(sp + 1) * g.N) / nsplit);
+  for (int n = n0; n < n1; ++n) {
+    const float* zk = z + (static_cast<int64_t>(n) * g.K + k) * plane;
+    double colacc[NCUT];  // sum over rows u < current of the row prefixes at the column cuts
+#pragma unroll
+    for (int j = 0; j < NCUT; ++j) colacc[j] = 0.0;
+    int ri = 1;  // next row cut to capture (cut 0 is the empty prefix)
+    for (int u0 = 0; u0 < g.Hc; u0 += kLagRB) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < rows * g.Wc; e += blockDim.x) {
+        const int rr = e / g.Wc, c = e - rr * g.Wc;
+        const int u = u0 - P + rr;
+        zb[e] = (u >= 0 && u < g.Hc) ? __ldg(zk + static_cast<int64_t>(u) * g.Wc + c) : 0.f;
+      }
+      __syncthreads();
+      if (!act) continue;
+      const int ub = min(kLagRB, g.Hc - u0);
+      for (int uu = 0; uu < ub; ++uu) {
+        const float* r0 = zb + (uu + P) * g.Wc;       // row u
+        const float* r1 = zb + (uu + P + du) * g.Wc;  // row u + du (zero rows outside the plane)
+        double rp = 0.0;
+        int v = 0;
+#pragma unroll
+        for (int j = 1; j < NCUT; ++j) {
+          const int cj = j <= P ? j : g.W + j - S;
+          for (; v < cj; ++v) {
+            const int v2 = v + dv;
+            const float b = (v2 >= 0 && v2 < g.Wc) ? r1[v2] : 0.f;
+            rp = fma(static_cast<double>(r0[v]), static_cast<double>(b), rp);
+          }
+          colacc[j] += rp;
+        }
+        const int u = u0 + uu;
+        // after row u: rows < u + 1 are in colacc; capture at the row cuts
+        const int rcut = ri <= P ? ri : g.H + ri - S;
+        if (ri < NCUT && u + 1 == rcut) {
+#pragma unroll
+          for (int j = 0; j < NCUT; ++j) Q[ri][j] += colacc[j];
+          ++ri;
+        }
+      }
+    }
+  }
+  if (act) {
+    double* out = gq + ((static_cast<int64_t>(k) * nsplit + sp) * NL + t) * NCUT * NCUT;
+#pragma unroll
+    for (int i = 0; i < NCUT; ++i)
+#pragma unroll
+      for (int j = 0; j < NCUT; ++j) out[i * NCUT + j] = Q[i][j];
+  }
+}
+
+// C_kk entries from the prefix sums: E = Q(rh, ch) - Q(rl, ch) - Q(rh, cl) + Q(rl, cl) summed over the
+// splits (fixed order), rl = P - a (cut a' = P - a), rh = P - a + H (cut S + P - a), cl / ch likewise
+__global__ void bcd_lag_assemble_kernel(Geom g, const double* __restrict__ gq, int nsplit, double* __restrict__ cout) {
+  const int S = g.S, P = g.P, M = S * S;
+  const int NL = (2 * S - 1) * (2 * S - 1), NCUT = 2 * S;
+  const int k = blockIdx.x;
+  for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
+    const int t1 = e / M, t2 = e - t1 * M;
+    const int a = t1 / S, b = t1 % S, a2 = t2 / S, b2 = t2 % S;
+    const int lag = (a - a2 + P) * (2 * S - 1) + (b - b2 + P);
+    const int rl = P - a, rh = S + P - a, cl = P - b, ch = S + P - b;
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const double* q = gq + ((static_cast<int64_t>(k) * nsplit + sp) * NL + lag) * NCUT * NCUT;
+      s += (q[rh * NCUT + ch] - q[rl * NCUT + ch]) - (q[rh * NCUT + cl] - q[rl * NCUT + cl]);
+    }
+    cout[static_cast<int64_t>(k) * M * M + e] = s;
+  }
+}
+
 // ================================================================ online surrogates (Eq.7 / Eq.8)
 // SURVEY.md §8f NEXT-2; DESIGN.md §12.  C block-major [K][K][M][M], B [K][M].
 
@@ -517,6 +618,56 @@ cudaError_t launch_bcd_update(const Geom& g, int k, const double* gk, const doub
     if (rb > 148 * 8) rb = 148 * 8;
     bcd_resid_kernel<<<static_cast<unsigned>(rb), 256, 0, st>>>(g, k, z, dl, r);
   }
+  return cudaGetLastError();
+}
+
+bool bcd_lag_supported(const Geom& g) { return g.H > g.P && g.W > g.P && g.S >= 1 && g.S <= 11 && (g.S & 1); }
+
+cudaError_t launch_bcd_lag_gram(const Geom& g, const float* z, double* gq, double* cfull, cudaStream_t st) {
+  const int ns = bcd_gram_splits(g);
+  const size_t smem = sizeof(float) * (kLagRB + 2 * g.P) * g.Wc;
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto sz) -> cudaError_t {
+    constexpr int SS = decltype(sz)::value;
+    constexpr int NT = ((2 * SS - 1) * (2 * SS - 1) + 31) / 32 * 32;
+    if (smem > 48 * 1024) {
+      cudaError_t er = cudaFuncSetAttribute(bcd_lag_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem));
+      if (er != cudaSuccess) return er;
+    }
+    if (g.N > 0) bcd_lag_kernel<SS><<<dim3(ns, g.K), NT, smem, st>>>(g, z, ns, gq);
+    else cudaMemsetAsync(gq, 0, sizeof(double) * g.K * ns * (2 * SS - 1) * (2 * SS - 1) * 4 * SS * SS, st);
+    return cudaGetLastError();
+  };
+  switch (g.S) {
+    case 1: e = go(std::integral_constant<int, 1>{}); break;
+    case 3: e = go(std::integral_constant<int, 3>{}); break;
+    case 5: e = go(std::integral_constant<int, 5>{}); break;
+    case 7: e = go(std::integral_constant<int, 7>{}); break;
+    case 9: e = go(std::integral_constant<int, 9>{}); break;
+    case 11: e = go(std::integral_constant<int, 11>{}); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  bcd_lag_assemble_kernel<<<g.K, 256, 0, st>>>(g, gq, ns, cfull);
+  return cudaGetLastError();
+}
+
+size_t bcd_lag_bytes(const Geom& g) {
+  const int ns = bcd_gram_splits(g);
+  return sizeof(double) * static_cast<size_t>(g.K) * ns * (2 * g.S - 1) * (2 * g.S - 1) * 4 * g.S * g.S;
+}
+
+cudaError_t launch_bcd_inverse_full(const Geom& g, const double* cfull, double ridge_rel, double* ainv,
+                                    uint8_t* flags, cudaStream_t st) {
+  const int M = g.S * g.S;
+  const size_t smem2 = sizeof(double) * M * M;
+  if (smem2 > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(bcd_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem2));
+    if (e != cudaSuccess) return e;
+  }
+  bcd_inverse_kernel<<<g.K, 128, smem2, st>>>(g, cfull, 1, ridge_rel, ainv, flags);
   return cudaGetLastError();
 }
 

@@ -235,6 +235,13 @@ cudaError_t launch_bcd_gk(const Geom& g, int k, const float* z, const float* r, 
 cudaError_t launch_bcd_update(const Geom& g, int k, const double* gk, const double* ainv, const uint8_t* flags,
                               float* d, double* dl, const float* z, float* r, cudaStream_t st);
 
+// Lag-structured Gram blocks (csc_bcd.cu; needs H, W > P): gq = bcd_lag_bytes scratch, cfull =
+// K*M*M doubles (the full C_kk), then launch_bcd_inverse_full.
+bool bcd_lag_supported(const Geom& g);
+size_t bcd_lag_bytes(const Geom& g);
+cudaError_t launch_bcd_lag_gram(const Geom& g, const float* z, double* gq, double* cfull, cudaStream_t st);
+cudaError_t launch_bcd_inverse_full(const Geom& g, const double* cfull, double ridge_rel, double* ainv,
+                                    uint8_t* flags, cudaStream_t st);
 // Online surrogates (csc_bcd.cu): C block-major [K][K][M][M], B [K][M] (fp64).  pp: K(K+1)/2 *
 // sur_gram_splits * M * M doubles; C <- wo C + wn (batch Gram), B <- wo B + wn (batch Z^T x).
 int sur_gram_splits(const Geom& g);

@@ -30,12 +30,16 @@ def _t(a, dev):
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
 
+@pytest.mark.parametrize("gram", ["lag", "direct"])
 @pytest.mark.parametrize("sweeps", [1, 3])
 @pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 40, 44), (4, 8, 5, 32, 32), (1, 9, 3, 33, 47),
                                    (2, 4, 11, 11, 11), (1, 3, 1, 9, 12)])
-def test_bcd_filter_step_parity(torch_dev, shape, sweeps):
+def test_bcd_filter_step_parity(torch_dev, shape, sweeps, gram, monkeypatch):
+    """gram: the lag-structured Gram (default where H, W > P) or the direct per-tap-pair sum."""
     import torch
     import paper_1909_00145_b200 as pkg
+    if gram == "direct":
+        monkeypatch.setenv("CSC_BCD_GRAM", "direct")
     N, K, s, H, W = shape
     x, d, z = random_problem(500 + K, N, K, s, H, W, code_density=0.3)
     if K > 2:
@@ -46,7 +50,7 @@ def test_bcd_filter_step_parity(torch_dev, shape, sweeps):
     dn, fo = oracle.filter_step_bcd(x, d, z, sweeps=sweeps)
     torch.cuda.synchronize()
     err = rel_err(dt.cpu().numpy(), dn)
-    print(f"bcd {shape} sweeps={sweeps}: rel err {err:.3e}")
+    print(f"bcd {shape} sweeps={sweeps} {gram}: rel err {err:.3e}")
     assert err < TOL, err
     assert list(flags) == list(fo)
     F = ctx.objective(xt, dt, zt, 0.3)
