@@ -314,12 +314,13 @@ bcd_lag_kernel(Geom g, const float* __restrict__ z, int nsplit, double* __restri
   constexpr int P = S - 1;
   constexpr int NL = (2 * S - 1) * (2 * S - 1);
   constexpr int NCUT = 2 * S;
-  extern __shared__ float zb[];  // rows [u0 - P, u0 + kLagRB + P) of the plane, zero outside
+  extern __shared__ double zb[];  // rows [u0 - P, u0 + kLagRB + P) x columns [-P, Wc + P), fp64, zero outside
   const int k = blockIdx.y, sp = blockIdx.x;
   const int t = threadIdx.x;
   const bool act = t < NL;
   const int du = act ? t / (2 * S - 1) - P : 0, dv = act ? t % (2 * S - 1) - P : 0;
   const int rows = kLagRB + 2 * P;
+  const int pitch = g.Wc + 2 * P;
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
   // column cuts: c_j = j (j <= P), W + j - S (j > P); row cuts likewise with H
   double Q[NCUT][NCUT];
@@ -337,27 +338,24 @@ bcd_lag_kernel(Geom g, const float* __restrict__ z, int nsplit, double* __restri
     int ri = 1;  // next row cut to capture (cut 0 is the empty prefix)
     for (int u0 = 0; u0 < g.Hc; u0 += kLagRB) {
       __syncthreads();
-      for (int e = threadIdx.x; e < rows * g.Wc; e += blockDim.x) {
-        const int rr = e / g.Wc, c = e - rr * g.Wc;
+      for (int e = threadIdx.x; e < rows * pitch; e += blockDim.x) {
+        const int rr = e / pitch, c = e - rr * pitch - P;
         const int u = u0 - P + rr;
-        zb[e] = (u >= 0 && u < g.Hc) ? __ldg(zk + static_cast<int64_t>(u) * g.Wc + c) : 0.f;
+        zb[e] = (u >= 0 && u < g.Hc && c >= 0 && c < g.Wc)
+                    ? static_cast<double>(__ldg(zk + static_cast<int64_t>(u) * g.Wc + c)) : 0.0;
       }
       __syncthreads();
       if (!act) continue;
       const int ub = min(kLagRB, g.Hc - u0);
       for (int uu = 0; uu < ub; ++uu) {
-        const float* r0 = zb + (uu + P) * g.Wc;       // row u
-        const float* r1 = zb + (uu + P + du) * g.Wc;  // row u + du (zero rows outside the plane)
+        const double* r0 = zb + (uu + P) * pitch + P;            // row u, column 0
+        const double* r1 = zb + (uu + P + du) * pitch + P + dv;  // row u + du, column dv (zero padded)
         double rp = 0.0;
         int v = 0;
 #pragma unroll
         for (int j = 1; j < NCUT; ++j) {
           const int cj = j <= P ? j : g.W + j - S;
-          for (; v < cj; ++v) {
-            const int v2 = v + dv;
-            const float b = (v2 >= 0 && v2 < g.Wc) ? r1[v2] : 0.f;
-            rp = fma(static_cast<double>(r0[v]), static_cast<double>(b), rp);
-          }
+          for (; v < cj; ++v) rp = fma(r0[v], r1[v], rp);
           colacc[j] += rp;
         }
         const int u = u0 + uu;
@@ -625,7 +623,7 @@ bool bcd_lag_supported(const Geom& g) { return g.H > g.P && g.W > g.P && g.S >= 
 
 cudaError_t launch_bcd_lag_gram(const Geom& g, const float* z, double* gq, double* cfull, cudaStream_t st) {
   const int ns = bcd_gram_splits(g);
-  const size_t smem = sizeof(float) * (kLagRB + 2 * g.P) * g.Wc;
+  const size_t smem = sizeof(double) * (kLagRB + 2 * g.P) * (g.Wc + 2 * g.P);
   cudaError_t e = cudaSuccess;
   auto go = [&](auto sz) -> cudaError_t {
     constexpr int SS = decltype(sz)::value;
