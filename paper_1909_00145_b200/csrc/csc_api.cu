@@ -1056,8 +1056,12 @@ csc_status csc_surrogate_update(csc_ctx* c, const float* x, const float* z) {
   // all-reduce adds the ranks (C is identical on every rank)
   const double wo = static_cast<double>(t - 1) / static_cast<double>(t) / static_cast<double>(c->world);
   const double wn = 1.0 / static_cast<double>(t);
-  CSC_LAUNCH_C(c, CSC_K_BCD, 2 + 3 * g.K, csc::launch_sur_update(g, x, z, c->sur_pp, c->bcd_part, c->bcd_vec, wo, wn,
-                                                                c->sur_C, c->sur_B, c->st));
+  // lag-structured pair Grams when H, W > P (CSC_BCD_GRAM=direct keeps the direct tap-pair sums)
+  const char* gev = std::getenv("CSC_BCD_GRAM");
+  const bool lag = csc::bcd_lag_supported(g) && g.N > 0 && !(gev != nullptr && std::string(gev) == "direct");
+  CSC_LAUNCH_C(c, CSC_K_BCD, 1 + 3 * g.K + (lag ? 0 : 1),
+               csc::launch_sur_update(g, x, z, lag ? nullptr : c->sur_pp, c->bcd_part, c->bcd_vec, wo, wn, c->sur_C,
+                                      c->sur_B, c->st));
   csc_status s = allreduce_d(c, c->sur_C, static_cast<size_t>(g.K) * g.K * M * M);
   if (s != CSC_OK) return s;
   s = allreduce_d(c, c->sur_B, static_cast<size_t>(g.K) * M);

@@ -401,6 +401,94 @@ __global__ void bcd_lag_assemble_kernel(Geom g, const double* __restrict__ gq, i
 // ================================================================ online surrogates (Eq.7 / Eq.8)
 // SURVEY.md §8f NEXT-2; DESIGN.md §12.  C block-major [K][K][M][M], B [K][M].
 
+// Lag-structured batch Gram of one filter pair (k1 <= k2, block q) folded straight into C (Eq.7):
+// as bcd_lag_kernel with the products z_k1[u,v] z_k2[u+du, v+dv] of two planes, every thread (lag)
+// then assembles the entries of its lag from the 4-corner box sums and writes
+// C[k1][k2][t1][t2] = wo C + wn E (and the mirrored C[k2][k1][t2][t1]).
+template <int S>
+__global__ void __launch_bounds__(((2 * S - 1) * (2 * S - 1) + 31) / 32 * 32, 1)
+sur_lag_kernel(Geom g, const float* __restrict__ z, double wo, double wn, double* __restrict__ C) {
+  constexpr int P = S - 1;
+  constexpr int NL = (2 * S - 1) * (2 * S - 1);
+  constexpr int NCUT = 2 * S;
+  constexpr int M = S * S;
+  extern __shared__ double zb2[];  // [2][rows][pitch]: plane k1 rows u, plane k2 rows u+du (zero padded)
+  const int q = blockIdx.x;
+  int k1 = 0, rem = q;
+  while (rem >= g.K - k1) {
+    rem -= g.K - k1;
+    ++k1;
+  }
+  const int k2 = k1 + rem;
+  const int t = threadIdx.x;
+  const bool act = t < NL;
+  const int du = act ? t / (2 * S - 1) - P : 0, dv = act ? t % (2 * S - 1) - P : 0;
+  const int rows = kLagRB + 2 * P;
+  const int pitch = g.Wc + 2 * P;
+  double* za = zb2;
+  double* zc = zb2 + rows * pitch;
+  const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
+  double Q[NCUT][NCUT];
+#pragma unroll
+  for (int i = 0; i < NCUT; ++i)
+#pragma unroll
+    for (int j = 0; j < NCUT; ++j) Q[i][j] = 0.0;
+  for (int n = 0; n < g.N; ++n) {
+    const float* z1 = z + (static_cast<int64_t>(n) * g.K + k1) * plane;
+    const float* z2 = z + (static_cast<int64_t>(n) * g.K + k2) * plane;
+    double colacc[NCUT];
+#pragma unroll
+    for (int j = 0; j < NCUT; ++j) colacc[j] = 0.0;
+    int ri = 1;
+    for (int u0 = 0; u0 < g.Hc; u0 += kLagRB) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < rows * pitch; e += blockDim.x) {
+        const int rr = e / pitch, c = e - rr * pitch - P;
+        const int u = u0 - P + rr;
+        const bool in = u >= 0 && u < g.Hc && c >= 0 && c < g.Wc;
+        const int64_t off = static_cast<int64_t>(u) * g.Wc + c;
+        za[e] = in ? static_cast<double>(__ldg(z1 + off)) : 0.0;
+        zc[e] = in ? static_cast<double>(__ldg(z2 + off)) : 0.0;
+      }
+      __syncthreads();
+      if (!act) continue;
+      const int ub = min(kLagRB, g.Hc - u0);
+      for (int uu = 0; uu < ub; ++uu) {
+        const double* r0 = za + (uu + P) * pitch + P;
+        const double* r1 = zc + (uu + P + du) * pitch + P + dv;
+        double rp = 0.0;
+        int v = 0;
+#pragma unroll
+        for (int j = 1; j < NCUT; ++j) {
+          const int cj = j <= P ? j : g.W + j - S;
+          for (; v < cj; ++v) rp = fma(r0[v], r1[v], rp);
+          colacc[j] += rp;
+        }
+        const int u = u0 + uu;
+        const int rcut = ri <= P ? ri : g.H + ri - S;
+        if (ri < NCUT && u + 1 == rcut) {
+#pragma unroll
+          for (int j = 0; j < NCUT; ++j) Q[ri][j] += colacc[j];
+          ++ri;
+        }
+      }
+    }
+  }
+  if (!act) return;
+  // the entries of this lag: (a, b) with a' = a - du, b' = b - dv inside [0, S)
+  for (int a = max(0, du); a < min(S, S + du); ++a)
+    for (int b = max(0, dv); b < min(S, S + dv); ++b) {
+      const int a2 = a - du, b2 = b - dv;
+      const int rl = P - a, rh = S + P - a, cl = P - b, ch = S + P - b;
+      const double E = (Q[rh][ch] - Q[rl][ch]) - (Q[rh][cl] - Q[rl][cl]);
+      const int t1 = a * S + b, t2 = a2 * S + b2;
+      double& c12 = C[((static_cast<int64_t>(k1) * g.K + k2) * M + t1) * M + t2];
+      const double nv = wo * c12 + wn * E;
+      c12 = nv;
+      if (k1 != k2) C[((static_cast<int64_t>(k2) * g.K + k1) * M + t2) * M + t1] = nv;
+    }
+}
+
 // Batch Gram block (k1, k2), k1 <= k2 (pair index q in the upper triangle, row by row): partial over
 // the images of split sp, all M x M entries, 4x4 tiles, processed in passes of 2 tiles per thread.
 __global__ void __launch_bounds__(kGramThreads) sur_gram_kernel(Geom g, const float* __restrict__ z, int nsplit,
@@ -681,6 +769,38 @@ cudaError_t launch_sur_update(const Geom& g, const float* x, const float* z, dou
   const int ns = sur_gram_splits(g);
   const int64_t np = static_cast<int64_t>(g.K) * (g.K + 1) / 2;
   const int M = g.S * g.S;
+  if (pp == nullptr) {
+    // lag-structured path (bcd_lag_supported): one block per filter pair, folded in place
+    const size_t smem = sizeof(double) * 2 * (kLagRB + 2 * g.P) * (g.Wc + 2 * g.P);
+    auto go = [&](auto sz) -> cudaError_t {
+      constexpr int SS = decltype(sz)::value;
+      constexpr int NT = ((2 * SS - 1) * (2 * SS - 1) + 31) / 32 * 32;
+      if (smem > 48 * 1024) {
+        cudaError_t er = cudaFuncSetAttribute(sur_lag_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem));
+        if (er != cudaSuccess) return er;
+      }
+      sur_lag_kernel<SS><<<static_cast<unsigned>(np), NT, smem, st>>>(g, z, wo, wn, C);
+      return cudaGetLastError();
+    };
+    cudaError_t e = cudaSuccess;
+    switch (g.S) {
+      case 1: e = go(std::integral_constant<int, 1>{}); break;
+      case 3: e = go(std::integral_constant<int, 3>{}); break;
+      case 5: e = go(std::integral_constant<int, 5>{}); break;
+      case 7: e = go(std::integral_constant<int, 7>{}); break;
+      case 9: e = go(std::integral_constant<int, 9>{}); break;
+      case 11: e = go(std::integral_constant<int, 11>{}); break;
+      default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    for (int k = 0; k < g.K; ++k) {
+      e = launch_bcd_gk(g, k, z, x, part, gk, st);
+      if (e != cudaSuccess) return e;
+      sur_bfold_kernel<<<1, 128, 0, st>>>(M, k, gk, wo, wn, B);
+    }
+    return cudaGetLastError();
+  }
   if (g.N > 0) {
     const size_t smem = sizeof(double) * (2 * (kGramBR + g.P) * g.Wc + 1);
     if (smem > 48 * 1024) {

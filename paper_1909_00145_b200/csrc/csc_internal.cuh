@@ -244,6 +244,7 @@ cudaError_t launch_bcd_inverse_full(const Geom& g, const double* cfull, double r
                                     uint8_t* flags, cudaStream_t st);
 // Online surrogates (csc_bcd.cu): C block-major [K][K][M][M], B [K][M] (fp64).  pp: K(K+1)/2 *
 // sur_gram_splits * M * M doubles; C <- wo C + wn (batch Gram), B <- wo B + wn (batch Z^T x).
+// pp == nullptr selects the lag-structured pair kernel (needs bcd_lag_supported), folded in place.
 int sur_gram_splits(const Geom& g);
 cudaError_t launch_sur_update(const Geom& g, const float* x, const float* z, double* pp, double* part, double* gk,
                               double wo, double wn, double* C, double* B, cudaStream_t st);

@@ -29,10 +29,13 @@ def _t(a, dev):
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
 
+@pytest.mark.parametrize("gram", ["lag", "direct"])
 @pytest.mark.parametrize("shape", [(2, 5, 5, 20, 24), (3, 3, 3, 10, 12), (1, 8, 7, 16, 16), (2, 4, 11, 12, 12)])
-def test_surrogate_update_and_filter_step_parity(torch_dev, shape):
+def test_surrogate_update_and_filter_step_parity(torch_dev, shape, gram, monkeypatch):
     import torch
     import paper_1909_00145_b200 as pkg
+    if gram == "direct":
+        monkeypatch.setenv("CSC_BCD_GRAM", "direct")
     N, K, s, H, W = shape
     M = s * s
     ctx = pkg.Context(N, K, s, H, W, device=0)
