@@ -122,9 +122,12 @@ def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox", filter_solve
             # (upper triangle incl. the diagonal tiles), against the fp64 FMA rate
             M = cfg.s * cfg.s
             nt = (M + 3) // 4
-            if filter_solver == "surrogate":  # batch Gram over all filter pairs, full 4x4 tiles
+            lagged = cfg.H > cfg.s - 1 and cfg.W > cfg.s - 1
+            if filter_solver == "surrogate" and lagged:  # lag-structured pair Grams
+                fma = nl * (cfg.K * (cfg.K + 1) / 2) * (2 * cfg.s - 1) ** 2 * cfg.Hc * cfg.Wc
+            elif filter_solver == "surrogate":  # direct pair Grams, full 4x4 tiles
                 fma = nl * cfg.H * cfg.W * (cfg.K * (cfg.K + 1) / 2) * 16.0 * nt * nt
-            elif cfg.H > cfg.s - 1 and cfg.W > cfg.s - 1:  # lag-structured Gram: (2s-1)^2 lags x Hc x Wc
+            elif lagged:  # lag-structured Gram: (2s-1)^2 lags x Hc x Wc
                 fma = nl * cfg.K * (2 * cfg.s - 1) ** 2 * cfg.Hc * cfg.Wc
             else:
                 fma = nl * cfg.K * cfg.H * cfg.W * 16.0 * nt * (nt + 1) / 2
