@@ -226,13 +226,17 @@ __global__ void bcd_gk_kernel(Geom g, int k, const float* __restrict__ z, const 
   }
 }
 
-// ---- gk[t] = sum of the g_k partials (fixed order)
+// ---- gk[t] = sum of the g_k partials: one warp per tap, lane-strided partial sums then a fixed
+// butterfly (deterministic)
 __global__ void bcd_gsum_kernel(int M, const double* __restrict__ part, int nparts, double* __restrict__ gk) {
-  const int t = threadIdx.x;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (t >= M) return;
   double s = 0.0;
-  for (int b = 0; b < nparts; ++b) s += part[static_cast<int64_t>(b) * M + t];
-  gk[t] = s;
+  for (int b = lane; b < nparts; b += 32) s += part[static_cast<int64_t>(b) * M + t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFullB, s, o);
+  if (lane == 0) gk[t] = s;
 }
 
 // ---- one block: delta = -A^-1 g_k, e = d_k + delta, d_k <- e / max(1, ||e||) (fp32),
@@ -275,12 +279,12 @@ __global__ void bcd_update_kernel(Geom g, int k, const double* __restrict__ gk, 
   }
 }
 
-// ---- r[n,i,j] += sum_ab dl[a,b] z[n,k,i+P-a,j+P-b]
+// ---- r[n,i,j] += sum_ab dl[a,b] z[n,k,i+P-a,j+P-b]  (fp32: r is fp32 and the update is small)
 __global__ void bcd_resid_kernel(Geom g, int k, const float* __restrict__ z, const double* __restrict__ dl,
                                  float* __restrict__ r) {
-  __shared__ double dls[128];
+  __shared__ float dls[128];
   const int M = g.S * g.S;
-  if (threadIdx.x < M) dls[threadIdx.x] = dl[threadIdx.x];
+  if (threadIdx.x < M) dls[threadIdx.x] = static_cast<float>(dl[threadIdx.x]);
   __syncthreads();
   const int64_t npx = static_cast<int64_t>(g.N) * g.H * g.W;
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
@@ -290,15 +294,13 @@ __global__ void bcd_resid_kernel(Geom g, int k, const float* __restrict__ z, con
     const int64_t rem = q - n * g.H * g.W;
     const int i = static_cast<int>(rem / g.W), j = static_cast<int>(rem - static_cast<int64_t>(i) * g.W);
     const float* zk = z + (n * g.K + k) * plane;
-    double s = 0.0;
+    float s = 0.f;
     for (int a = 0; a < g.S; ++a)
       for (int b = 0; b < g.S; ++b)
-        s = fma(dls[a * g.S + b], static_cast<double>(__ldg(zk + static_cast<int64_t>(i + g.P - a) * g.Wc + j + g.P - b)),
-                s);
-    r[q] = static_cast<float>(static_cast<double>(r[q]) + s);
+        s = fmaf(dls[a * g.S + b], __ldg(zk + static_cast<int64_t>(i + g.P - a) * g.Wc + j + g.P - b), s);
+    r[q] += s;
   }
 }
-
 
 // ---- Lag-structured Gram (the default when H, W > P): C_kk[(a,b),(a',b')] is the sum of
 // Pi(u,v) = z[u,v] z[u+du, v+dv], du = a - a', dv = b - b', over the box [P-a, P-a+H) x
@@ -691,7 +693,7 @@ cudaError_t launch_bcd_gk(const Geom& g, int k, const float* z, const float* r, 
     }
     bcd_gk_kernel<<<nb, 128, smem, st>>>(g, k, z, r, part);
   }
-  bcd_gsum_kernel<<<1, 128, 0, st>>>(M, part, nb, gk);
+  bcd_gsum_kernel<<<(M + 7) / 8, 256, 0, st>>>(M, part, nb, gk);
   return cudaGetLastError();
 }
 
