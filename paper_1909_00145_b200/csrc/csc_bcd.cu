@@ -310,33 +310,50 @@ __global__ void bcd_resid_kernel(Geom g, int k, const float* __restrict__ z, con
 // (bcd_lag_assemble_kernel).  (2S-1)^2 lags x Hc x Wc products per plane instead of M^2/2 x H x W.
 constexpr int kLagRB = 16;  // code rows per staged band
 
+// Three lags (du, dv0..dv0+2) per thread: the products share the row-u value and a sliding window
+// over row u+du, so a position costs two shared loads for three FMAs.
+constexpr int kLagPerThread = 3;
 template <int S>
-__global__ void __launch_bounds__(((2 * S - 1) * (2 * S - 1) + 31) / 32 * 32, 1)
+__host__ __device__ constexpr int lag_threads() {
+  return ((2 * S - 1) * ((2 * S - 1 + kLagPerThread - 1) / kLagPerThread) + 31) / 32 * 32;
+}
+
+template <int S>
+__global__ void __launch_bounds__(lag_threads<S>(), 1)
 bcd_lag_kernel(Geom g, const float* __restrict__ z, int nsplit, double* __restrict__ gq) {
   constexpr int P = S - 1;
-  constexpr int NL = (2 * S - 1) * (2 * S - 1);
+  constexpr int NDV = 2 * S - 1;
+  constexpr int NG = (NDV + kLagPerThread - 1) / kLagPerThread;
+  constexpr int NL = NDV * NDV;
   constexpr int NCUT = 2 * S;
-  extern __shared__ double zb[];  // rows [u0 - P, u0 + kLagRB + P) x columns [-P, Wc + P), fp64, zero outside
+  constexpr int L = kLagPerThread;
+  // rows [u0 - P, u0 + kLagRB + P) x columns [-P, Wc + P + L), fp64, zero outside the plane
+  extern __shared__ double zb[];
   const int k = blockIdx.y, sp = blockIdx.x;
   const int t = threadIdx.x;
-  const bool act = t < NL;
-  const int du = act ? t / (2 * S - 1) - P : 0, dv = act ? t % (2 * S - 1) - P : 0;
+  const bool act = t < NDV * NG;
+  const int du = act ? t / NG - P : 0;
+  const int dv0 = act ? (t % NG) * L - P : 0;
   const int rows = kLagRB + 2 * P;
-  const int pitch = g.Wc + 2 * P;
+  const int pitch = g.Wc + 2 * P + L;
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
   // column cuts: c_j = j (j <= P), W + j - S (j > P); row cuts likewise with H
-  double Q[NCUT][NCUT];
+  double Q[L][NCUT][NCUT];
 #pragma unroll
-  for (int i = 0; i < NCUT; ++i)
+  for (int l = 0; l < L; ++l)
 #pragma unroll
-    for (int j = 0; j < NCUT; ++j) Q[i][j] = 0.0;
+    for (int i = 0; i < NCUT; ++i)
+#pragma unroll
+      for (int j = 0; j < NCUT; ++j) Q[l][i][j] = 0.0;
   const int n0 = static_cast<int>((static_cast<int64_t>(sp) * g.N) / nsplit);
   const int n1 = static_cast<int>((static_cast<int64_t>(sp + 1) * g.N) / nsplit);
   for (int n = n0; n < n1; ++n) {
     const float* zk = z + (static_cast<int64_t>(n) * g.K + k) * plane;
-    double colacc[NCUT];  // sum over rows u < current of the row prefixes at the column cuts
+    double colacc[L][NCUT];  // sum over rows u < current of the row prefixes at the column cuts
 #pragma unroll
-    for (int j = 0; j < NCUT; ++j) colacc[j] = 0.0;
+    for (int l = 0; l < L; ++l)
+#pragma unroll
+      for (int j = 0; j < NCUT; ++j) colacc[l][j] = 0.0;
     int ri = 1;  // next row cut to capture (cut 0 is the empty prefix)
     for (int u0 = 0; u0 < g.Hc; u0 += kLagRB) {
       __syncthreads();
@@ -350,33 +367,53 @@ bcd_lag_kernel(Geom g, const float* __restrict__ z, int nsplit, double* __restri
       if (!act) continue;
       const int ub = min(kLagRB, g.Hc - u0);
       for (int uu = 0; uu < ub; ++uu) {
-        const double* r0 = zb + (uu + P) * pitch + P;            // row u, column 0
-        const double* r1 = zb + (uu + P + du) * pitch + P + dv;  // row u + du, column dv (zero padded)
-        double rp = 0.0;
+        const double* r0 = zb + (uu + P) * pitch + P;             // row u, column 0
+        const double* r1 = zb + (uu + P + du) * pitch + P + dv0;  // row u + du, column dv0 (zero padded)
+        double rp[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) rp[l] = 0.0;
+        double w0 = r1[0], w1 = r1[1], w2 = r1[2];
         int v = 0;
 #pragma unroll
         for (int j = 1; j < NCUT; ++j) {
           const int cj = j <= P ? j : g.W + j - S;
-          for (; v < cj; ++v) rp = fma(r0[v], r1[v], rp);
-          colacc[j] += rp;
+          for (; v < cj; ++v) {
+            const double x = r0[v];
+            rp[0] = fma(x, w0, rp[0]);
+            rp[1] = fma(x, w1, rp[1]);
+            rp[2] = fma(x, w2, rp[2]);
+            w0 = w1;
+            w1 = w2;
+            w2 = r1[v + 3];
+          }
+#pragma unroll
+          for (int l = 0; l < L; ++l) colacc[l][j] += rp[l];
         }
         const int u = u0 + uu;
         // after row u: rows < u + 1 are in colacc; capture at the row cuts
         const int rcut = ri <= P ? ri : g.H + ri - S;
         if (ri < NCUT && u + 1 == rcut) {
 #pragma unroll
-          for (int j = 0; j < NCUT; ++j) Q[ri][j] += colacc[j];
+          for (int l = 0; l < L; ++l)
+#pragma unroll
+            for (int j = 0; j < NCUT; ++j) Q[l][ri][j] += colacc[l][j];
           ++ri;
         }
       }
     }
   }
   if (act) {
-    double* out = gq + ((static_cast<int64_t>(k) * nsplit + sp) * NL + t) * NCUT * NCUT;
 #pragma unroll
-    for (int i = 0; i < NCUT; ++i)
+    for (int l = 0; l < L; ++l) {
+      const int dv = dv0 + l;
+      if (dv > P) continue;
+      const int lag = (du + P) * NDV + (dv + P);
+      double* out = gq + ((static_cast<int64_t>(k) * nsplit + sp) * NL + lag) * NCUT * NCUT;
 #pragma unroll
-      for (int j = 0; j < NCUT; ++j) out[i * NCUT + j] = Q[i][j];
+      for (int i = 0; i < NCUT; ++i)
+#pragma unroll
+        for (int j = 0; j < NCUT; ++j) out[i * NCUT + j] = Q[l][i][j];
+    }
   }
 }
 
@@ -713,11 +750,11 @@ bool bcd_lag_supported(const Geom& g) { return g.H > g.P && g.W > g.P && g.S >= 
 
 cudaError_t launch_bcd_lag_gram(const Geom& g, const float* z, double* gq, double* cfull, cudaStream_t st) {
   const int ns = bcd_gram_splits(g);
-  const size_t smem = sizeof(double) * (kLagRB + 2 * g.P) * (g.Wc + 2 * g.P);
+  const size_t smem = sizeof(double) * (kLagRB + 2 * g.P) * (g.Wc + 2 * g.P + kLagPerThread);
   cudaError_t e = cudaSuccess;
   auto go = [&](auto sz) -> cudaError_t {
     constexpr int SS = decltype(sz)::value;
-    constexpr int NT = ((2 * SS - 1) * (2 * SS - 1) + 31) / 32 * 32;
+    constexpr int NT = lag_threads<SS>();
     if (smem > 48 * 1024) {
       cudaError_t er = cudaFuncSetAttribute(bcd_lag_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem));
