@@ -445,12 +445,14 @@ __global__ void bcd_lag_assemble_kernel(Geom g, const double* __restrict__ gq, i
 // then assembles the entries of its lag from the 4-corner box sums and writes
 // C[k1][k2][t1][t2] = wo C + wn E (and the mirrored C[k2][k1][t2][t1]).
 template <int S>
-__global__ void __launch_bounds__(((2 * S - 1) * (2 * S - 1) + 31) / 32 * 32, 1)
+__global__ void __launch_bounds__(lag_threads<S>(), 1)
 sur_lag_kernel(Geom g, const float* __restrict__ z, double wo, double wn, double* __restrict__ C) {
   constexpr int P = S - 1;
-  constexpr int NL = (2 * S - 1) * (2 * S - 1);
+  constexpr int NDV = 2 * S - 1;
+  constexpr int NG = (NDV + kLagPerThread - 1) / kLagPerThread;
   constexpr int NCUT = 2 * S;
   constexpr int M = S * S;
+  constexpr int L = kLagPerThread;
   extern __shared__ double zb2[];  // [2][rows][pitch]: plane k1 rows u, plane k2 rows u+du (zero padded)
   const int q = blockIdx.x;
   int k1 = 0, rem = q;
@@ -460,24 +462,29 @@ sur_lag_kernel(Geom g, const float* __restrict__ z, double wo, double wn, double
   }
   const int k2 = k1 + rem;
   const int t = threadIdx.x;
-  const bool act = t < NL;
-  const int du = act ? t / (2 * S - 1) - P : 0, dv = act ? t % (2 * S - 1) - P : 0;
+  const bool act = t < NDV * NG;
+  const int du = act ? t / NG - P : 0;
+  const int dv0 = act ? (t % NG) * L - P : 0;
   const int rows = kLagRB + 2 * P;
-  const int pitch = g.Wc + 2 * P;
+  const int pitch = g.Wc + 2 * P + L;
   double* za = zb2;
   double* zc = zb2 + rows * pitch;
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
-  double Q[NCUT][NCUT];
+  double Q[L][NCUT][NCUT];
 #pragma unroll
-  for (int i = 0; i < NCUT; ++i)
+  for (int l = 0; l < L; ++l)
 #pragma unroll
-    for (int j = 0; j < NCUT; ++j) Q[i][j] = 0.0;
+    for (int i = 0; i < NCUT; ++i)
+#pragma unroll
+      for (int j = 0; j < NCUT; ++j) Q[l][i][j] = 0.0;
   for (int n = 0; n < g.N; ++n) {
     const float* z1 = z + (static_cast<int64_t>(n) * g.K + k1) * plane;
     const float* z2 = z + (static_cast<int64_t>(n) * g.K + k2) * plane;
-    double colacc[NCUT];
+    double colacc[L][NCUT];
 #pragma unroll
-    for (int j = 0; j < NCUT; ++j) colacc[j] = 0.0;
+    for (int l = 0; l < L; ++l)
+#pragma unroll
+      for (int j = 0; j < NCUT; ++j) colacc[l][j] = 0.0;
     int ri = 1;
     for (int u0 = 0; u0 < g.Hc; u0 += kLagRB) {
       __syncthreads();
@@ -494,38 +501,57 @@ sur_lag_kernel(Geom g, const float* __restrict__ z, double wo, double wn, double
       const int ub = min(kLagRB, g.Hc - u0);
       for (int uu = 0; uu < ub; ++uu) {
         const double* r0 = za + (uu + P) * pitch + P;
-        const double* r1 = zc + (uu + P + du) * pitch + P + dv;
-        double rp = 0.0;
+        const double* r1 = zc + (uu + P + du) * pitch + P + dv0;
+        double rp[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) rp[l] = 0.0;
+        double w0 = r1[0], w1 = r1[1], w2 = r1[2];
         int v = 0;
 #pragma unroll
         for (int j = 1; j < NCUT; ++j) {
           const int cj = j <= P ? j : g.W + j - S;
-          for (; v < cj; ++v) rp = fma(r0[v], r1[v], rp);
-          colacc[j] += rp;
+          for (; v < cj; ++v) {
+            const double x = r0[v];
+            rp[0] = fma(x, w0, rp[0]);
+            rp[1] = fma(x, w1, rp[1]);
+            rp[2] = fma(x, w2, rp[2]);
+            w0 = w1;
+            w1 = w2;
+            w2 = r1[v + 3];
+          }
+#pragma unroll
+          for (int l = 0; l < L; ++l) colacc[l][j] += rp[l];
         }
         const int u = u0 + uu;
         const int rcut = ri <= P ? ri : g.H + ri - S;
         if (ri < NCUT && u + 1 == rcut) {
 #pragma unroll
-          for (int j = 0; j < NCUT; ++j) Q[ri][j] += colacc[j];
+          for (int l = 0; l < L; ++l)
+#pragma unroll
+            for (int j = 0; j < NCUT; ++j) Q[l][ri][j] += colacc[l][j];
           ++ri;
         }
       }
     }
   }
   if (!act) return;
-  // the entries of this lag: (a, b) with a' = a - du, b' = b - dv inside [0, S)
-  for (int a = max(0, du); a < min(S, S + du); ++a)
-    for (int b = max(0, dv); b < min(S, S + dv); ++b) {
-      const int a2 = a - du, b2 = b - dv;
-      const int rl = P - a, rh = S + P - a, cl = P - b, ch = S + P - b;
-      const double E = (Q[rh][ch] - Q[rl][ch]) - (Q[rh][cl] - Q[rl][cl]);
-      const int t1 = a * S + b, t2 = a2 * S + b2;
-      double& c12 = C[((static_cast<int64_t>(k1) * g.K + k2) * M + t1) * M + t2];
-      const double nv = wo * c12 + wn * E;
-      c12 = nv;
-      if (k1 != k2) C[((static_cast<int64_t>(k2) * g.K + k1) * M + t2) * M + t1] = nv;
-    }
+  // the entries of this thread's lags: (a, b) with a' = a - du, b' = b - dv inside [0, S)
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const int dv = dv0 + l;
+    if (dv > P) continue;
+    for (int a = max(0, du); a < min(S, S + du); ++a)
+      for (int b = max(0, dv); b < min(S, S + dv); ++b) {
+        const int a2 = a - du, b2 = b - dv;
+        const int rl = P - a, rh = S + P - a, cl = P - b, ch = S + P - b;
+        const double E = (Q[l][rh][ch] - Q[l][rl][ch]) - (Q[l][rh][cl] - Q[l][rl][cl]);
+        const int t1 = a * S + b, t2 = a2 * S + b2;
+        double& c12 = C[((static_cast<int64_t>(k1) * g.K + k2) * M + t1) * M + t2];
+        const double nv = wo * c12 + wn * E;
+        c12 = nv;
+        if (k1 != k2) C[((static_cast<int64_t>(k2) * g.K + k1) * M + t2) * M + t1] = nv;
+      }
+  }
 }
 
 // Batch Gram block (k1, k2), k1 <= k2 (pair index q in the upper triangle, row by row): partial over
@@ -810,10 +836,10 @@ cudaError_t launch_sur_update(const Geom& g, const float* x, const float* z, dou
   const int M = g.S * g.S;
   if (pp == nullptr) {
     // lag-structured path (bcd_lag_supported): one block per filter pair, folded in place
-    const size_t smem = sizeof(double) * 2 * (kLagRB + 2 * g.P) * (g.Wc + 2 * g.P);
+    const size_t smem = sizeof(double) * 2 * (kLagRB + 2 * g.P) * (g.Wc + 2 * g.P + kLagPerThread);
     auto go = [&](auto sz) -> cudaError_t {
       constexpr int SS = decltype(sz)::value;
-      constexpr int NT = ((2 * SS - 1) * (2 * SS - 1) + 31) / 32 * 32;
+      constexpr int NT = lag_threads<SS>();
       if (smem > 48 * 1024) {
         cudaError_t er = cudaFuncSetAttribute(sur_lag_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem));
