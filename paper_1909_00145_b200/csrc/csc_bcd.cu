@@ -190,25 +190,25 @@ __global__ void bcd_inverse_kernel(Geom g, const double* __restrict__ gpart, int
 
 // ---- g_k partials: block (n, row band) computes sum over its positions of r[p] X[p][t], t = tap
 // (thread t < M), in fp64 -> part[blk][M]
-constexpr int kGkBR = 16;
+constexpr int kGkBR = 6;
 __global__ void bcd_gk_kernel(Geom g, int k, const float* __restrict__ z, const float* __restrict__ r,
                               double* __restrict__ part) {
-  extern __shared__ float sm[];  // z rows [kGkBR + P][Wc], r rows [kGkBR][W]
+  extern __shared__ double smd[];  // z rows [kGkBR + P][Wc], r rows [kGkBR][W], staged as fp64 (exact)
   const int nbands = (g.H + kGkBR - 1) / kGkBR;
   const int n = blockIdx.x / nbands, band = blockIdx.x - n * nbands;
   const int i0 = band * kGkBR;
   const int ib = min(kGkBR, g.H - i0);
   const int rows = kGkBR + g.P;
-  float* zs = sm;
-  float* rsm = sm + rows * g.Wc;
+  double* zs = smd;
+  double* rsm = smd + rows * g.Wc;
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
   const float* zk = z + (static_cast<int64_t>(n) * g.K + k) * plane;
   for (int e = threadIdx.x; e < rows * g.Wc; e += blockDim.x) {
     const int rr = e / g.Wc;
-    zs[e] = (i0 + rr < g.Hc) ? __ldg(zk + static_cast<int64_t>(i0) * g.Wc + e) : 0.f;
+    zs[e] = (i0 + rr < g.Hc) ? static_cast<double>(__ldg(zk + static_cast<int64_t>(i0) * g.Wc + e)) : 0.0;
   }
   for (int e = threadIdx.x; e < ib * g.W; e += blockDim.x)
-    rsm[e] = r[(static_cast<int64_t>(n) * g.H + i0) * g.W + e];
+    rsm[e] = static_cast<double>(r[(static_cast<int64_t>(n) * g.H + i0) * g.W + e]);
   __syncthreads();
   const int M = g.S * g.S;
   const int t = threadIdx.x;
@@ -216,11 +216,16 @@ __global__ void bcd_gk_kernel(Geom g, int k, const float* __restrict__ z, const 
     const int a = t / g.S, b = t - a * g.S;
     double acc = 0.0;
     for (int ii = 0; ii < ib; ++ii) {
-      const float* zrow = zs + (ii + g.P - a) * g.Wc + (g.P - b);
-      const float* rrow = rsm + ii * g.W;
-      double s = 0.0;
-      for (int j = 0; j < g.W; ++j) s = fma(static_cast<double>(rrow[j]), static_cast<double>(zrow[j]), s);
-      acc += s;
+      const double* zrow = zs + (ii + g.P - a) * g.Wc + (g.P - b);
+      const double* rrow = rsm + ii * g.W;
+      double s0 = 0.0, s1 = 0.0;  // two chains against the fp64 FMA latency
+      int j = 0;
+      for (; j + 1 < g.W; j += 2) {
+        s0 = fma(rrow[j], zrow[j], s0);
+        s1 = fma(rrow[j + 1], zrow[j + 1], s1);
+      }
+      if (j < g.W) s0 = fma(rrow[j], zrow[j], s0);
+      acc += s0 + s1;
     }
     part[static_cast<int64_t>(blockIdx.x) * M + t] = acc;
   }
@@ -748,7 +753,7 @@ cudaError_t launch_bcd_gk(const Geom& g, int k, const float* z, const float* r, 
   const int M = g.S * g.S;
   const int nb = bcd_gk_blocks(g);
   if (nb > 0) {
-    const size_t smem = sizeof(float) * ((kGkBR + g.P) * g.Wc + kGkBR * g.W);
+    const size_t smem = sizeof(double) * ((kGkBR + g.P) * g.Wc + kGkBR * g.W);
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(bcd_gk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));
