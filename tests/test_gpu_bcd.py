@@ -66,3 +66,27 @@ def test_bcd_argument_errors(torch_dev):
     with pytest.raises(pkg.CSCError):
         ctx.filter_step_bcd(_t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev), sweeps=0)
     ctx.close()
+
+
+def test_next_rows_with_an_empty_local_batch(torch_dev):
+    """n_local = 0 (a rank with no images): the ADMM step is a no-op, the BCD sweep leaves every
+    filter unchanged and flagged (no codes), and a surrogate update with no images keeps C = 0."""
+    import torch
+    import paper_1909_00145_b200 as pkg
+    from synth import CONFIGS, make_filters
+    K, s = 4, 3
+    ctx = pkg.Context(0, K, s, 8, 8, device=0)
+    d = _t(make_filters(CONFIGS["tiny"].with_(K=K, s=s)), torch_dev)
+    d0 = d.clone()
+    e = torch.zeros(0, device=torch_dev)
+    ctx.code_step_admm(e, d, e, 0.5, 0.5, 1, 1)
+    flags = ctx.filter_step_bcd(e, d, e, want_flags=True)
+    assert flags == [1] * K
+    ctx.surrogate_update(e, e)
+    C = torch.ones(K * K * s ** 4, dtype=torch.float64, device=torch_dev)
+    B = torch.ones(K * s * s, dtype=torch.float64, device=torch_dev)
+    assert ctx.read_surrogate(C, B) == 1
+    torch.cuda.synchronize()
+    assert torch.equal(d, d0)
+    assert float(C.abs().max()) == 0.0 and float(B.abs().max()) == 0.0
+    ctx.close()
