@@ -267,14 +267,15 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
           float4* hi4 = reinterpret_cast<float4*>(stages + slot * 2 * A.stage_bytes);
           float4* lo4 = reinterpret_cast<float4*>(stages + slot * 2 * A.stage_bytes + A.stage_bytes);
           const int n4 = A.KC * 8;  // KC rows x 32 floats / 4
+          // hi stays the fp32 z in place (the tensor core reads its tf32 truncation); lo = z - trunc(z)
+          // exactly, itself truncated to tf32 by the tensor core (reading T1'')
           for (int e = ctg; e < n4; e += 128) {
             const float4 x = hi4[e];
-            float4 h, l;
-            tf32_split_rn_hi(x.x, h.x, l.x);
-            tf32_split_rn_hi(x.y, h.y, l.y);
-            tf32_split_rn_hi(x.z, h.z, l.z);
-            tf32_split_rn_hi(x.w, h.w, l.w);
-            hi4[e] = h;
+            float4 l;
+            l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+            l.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+            l.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+            l.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
             lo4[e] = l;
           }
         }
