@@ -53,6 +53,19 @@ __device__ __forceinline__ double image_total(const double* __restrict__ part, i
   return *slot;
 }
 
+// max over the block of mx (every thread calls it), then one global atomicMax per block: per-warp
+// atomics on a single address serialise at L2 (~20k of them in a full expansion)
+__device__ __forceinline__ void block_atomic_max(uint32_t mx, uint32_t* bound) {
+  __shared__ uint32_t red;
+  if (threadIdx.x == 0) red = 0u;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFullA, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx != 0u) atomicMax(&red, mx);
+  __syncthreads();
+  if (threadIdx.x == 0 && bound != nullptr && red != 0u) atomicMax(bound, red);
+}
+
 // ---- index build: idx[m] = position of the m-th set bit of the canonical mask bits,
 // woff[w] = number of set bits in words [0, w)
 __global__ void idx_count_kernel(const uint32_t* __restrict__ bits, int64_t nwords, uint32_t* __restrict__ cnt) {
@@ -361,22 +374,26 @@ __global__ void __launch_bounds__(256) expand_kernel(int64_t nper, const uint32_
     const uint32_t myoff = wok ? __ldg(woff + w0 + lane) : 0u;
 #pragma unroll 1
     for (int i0 = 0; i0 < 32; i0 += 8) {
-      float val[8];
+      // all compact loads of the round before any PV store (the stores alias PV for the
+      // compiler, so interleaving them would serialise the loads)
+      float val[8], pv[8];
+      uint32_t mi[8];
+      bool on[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const uint32_t word = __shfl_sync(kFullA, myword, i0 + i);
         const uint32_t off = __shfl_sync(kFullA, myoff, i0 + i);
-        val[i] = 0.f;
-        if ((word >> lane) & 1u) {
-          const uint32_t m = off + __popc(word & lt);
-          float x = Rn[m];
-          if (PVn != nullptr) {
-            if (dir) x = fmaf(beta, PVn[m], x);
-            PVn[m] = x;
-          }
-          val[i] = x;
-          mx = max(mx, __float_as_uint(fabsf(x)));
-        }
+        on[i] = (word >> lane) & 1u;
+        mi[i] = off + __popc(word & lt);
+        val[i] = on[i] ? Rn[mi[i]] : 0.f;
+        pv[i] = (on[i] && dir) ? PVn[mi[i]] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (dir) val[i] = fmaf(beta, pv[i], val[i]);
+        if (on[i] && PVn != nullptr) PVn[mi[i]] = val[i];
+        if (!on[i]) val[i] = 0.f;
+        mx = max(mx, __float_as_uint(fabsf(val[i])));
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -385,24 +402,28 @@ __global__ void __launch_bounds__(256) expand_kernel(int64_t nper, const uint32_
       }
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFullA, mx, o));
-  if (lane == 0 && bound != nullptr && mx != 0u) atomicMax(bound, mx);
+  block_atomic_max(mx, bound);
 }
 
-// expand_kernel for nper % 4 == 0 (every image row of Zd 16-B aligned): the same result with one
-// float4 store per lane per 128 positions.  A warp takes 32 mask words (1024 positions); in round j
-// (0..7) lane L owns positions 128 j + 4 L .. +3, i.e. nibble L & 7 of word 4 j + (L >> 3), whose
-// compact index starts at woff + popc(lower bits).  All 8 rounds are unrolled, so a lane's compact
-// loads (3.2 expected at p = 0.1) are all in flight before its stores.
-__global__ void __launch_bounds__(256) expand4_kernel(int64_t nper, const uint32_t* __restrict__ bits,
-                                                      const uint32_t* __restrict__ woff, int64_t ms,
-                                                      const float* __restrict__ R, float* __restrict__ PV,
-                                                      const double* __restrict__ rr,
-                                                      const double* __restrict__ rr_new, float* __restrict__ Zd,
-                                                      uint32_t* __restrict__ bound) {
+// expand_kernel for nper % 4 == 0 (every image row of Zd 16-B aligned), staged through shared
+// memory.  A block takes a span of kExpWords = 256 mask words (8192 positions, one word per
+// thread); the span's selected codes are one contiguous compact segment [woff[w0], woff[w0] + cnt),
+// which the block reads with coalesced loads (forming PV on the way) into smem, then each warp
+// writes its 32 words (1024 positions) as float4 lines: in round j (0..7) lane L owns positions
+// 128 j + 4 L .. +3, nibble L & 7 of the warp's word 4 j + (L >> 3).  Every load of a span is
+// independent of the others, so a block keeps ~cnt / 256 loads per thread in flight instead of a
+// chain of dependent word -> value loads per warp.
+constexpr int kExpWords = 256;
+__global__ void __launch_bounds__(kExpWords) expand_seg_kernel(int64_t nper, const uint32_t* __restrict__ bits,
+                                                               const uint32_t* __restrict__ woff, int64_t ms,
+                                                               const float* __restrict__ R, float* __restrict__ PV,
+                                                               const double* __restrict__ rr,
+                                                               const double* __restrict__ rr_new,
+                                                               float* __restrict__ Zd, uint32_t* __restrict__ bound) {
+  __shared__ float seg[kExpWords * 32];
+  __shared__ uint32_t span[2];
   const int n = blockIdx.y;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool dir = rr != nullptr;
   float beta = 0.f;
   if (dir) {
@@ -416,48 +437,65 @@ __global__ void __launch_bounds__(256) expand4_kernel(int64_t nper, const uint32
   const uint32_t below = (1u << sh) - 1u;
   uint32_t mx = 0u;
   const int64_t nwords = (nper + 31) / 32;
-  const int64_t nchunk = (nwords + 31) / 32;
-  const int64_t wstride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunk;
-       ch += wstride) {
-    const int64_t w0 = ch * 32;
-    const bool wok = w0 + lane < nwords;
-    const uint32_t myword = wok ? __ldg(bits + w0 + lane) : 0u;
-    const uint32_t myoff = wok ? __ldg(woff + w0 + lane) : 0u;
-    float4 val[8];
+  const int64_t wstep = static_cast<int64_t>(gridDim.x) * kExpWords;
+  int64_t wn = static_cast<int64_t>(blockIdx.x) * kExpWords + threadIdx.x;
+  uint32_t nword = wn < nwords ? __ldg(bits + wn) : 0u;  // the next span's word / offset, one span ahead
+  uint32_t noff = wn < nwords ? __ldg(woff + wn) : 0u;
+  for (int64_t w0 = static_cast<int64_t>(blockIdx.x) * kExpWords; w0 < nwords; w0 += wstep) {
+    const int64_t w = w0 + threadIdx.x;
+    const uint32_t myword = nword, myoff = noff;
+    wn = w + wstep;
+    nword = wn < nwords ? __ldg(bits + wn) : 0u;
+    noff = wn < nwords ? __ldg(woff + wn) : 0u;
+    if (threadIdx.x == 0) span[0] = myoff;
+    // the last word of the span (or of the mask) closes the segment
+    if (w < nwords && (threadIdx.x == kExpWords - 1 || w == nwords - 1)) span[1] = myoff + __popc(myword);
+    __syncthreads();
+    const uint32_t mb = span[0];
+    const int cnt = static_cast<int>(span[1] - mb);
+    // batches of 4 per thread, every load of a batch before its PV stores (which alias PV for the
+    // compiler and would otherwise serialise the loads)
+    for (int i0 = threadIdx.x; i0 < cnt; i0 += 4 * kExpWords) {
+      float rv[4], pv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kExpWords;
+        rv[u] = i < cnt ? Rn[mb + i] : 0.f;
+        pv[u] = (i < cnt && dir) ? PVn[mb + i] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kExpWords;
+        if (i < cnt) {
+          float x = rv[u];
+          if (dir) x = fmaf(beta, pv[u], x);
+          if (PVn != nullptr) PVn[mb + i] = x;
+          seg[i] = x;
+          mx = max(mx, __float_as_uint(fabsf(x)));
+        }
+      }
+    }
+    __syncthreads();
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int src = 4 * j + (lane >> 3);
       const uint32_t word = __shfl_sync(kFullA, myword, src);
-      const uint32_t off = __shfl_sync(kFullA, myoff, src);
+      const uint32_t off = __shfl_sync(kFullA, myoff, src) - mb;
       const uint32_t nib = (word >> sh) & 0xFu;
       uint32_t m = off + __popc(word & below);
       float v[4];
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        v[b] = 0.f;
-        if ((nib >> b) & 1u) {
-          float x = Rn[m];
-          if (PVn != nullptr) {
-            if (dir) x = fmaf(beta, PVn[m], x);
-            PVn[m] = x;
-          }
-          v[b] = x;
-          mx = max(mx, __float_as_uint(fabsf(x)));
-          ++m;
-        }
+        const bool on = (nib >> b) & 1u;
+        v[b] = on ? seg[m] : 0.f;
+        m += on ? 1u : 0u;
       }
-      val[j] = make_float4(v[0], v[1], v[2], v[3]);
+      const int64_t pos = (w0 + 32 * warp) * 32 + 128 * j + 4 * lane;
+      if (pos < nper) Zn[pos / 4] = make_float4(v[0], v[1], v[2], v[3]);
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t pos = w0 * 32 + 128 * j + 4 * lane;
-      if (pos < nper) Zn[pos / 4] = val[j];
-    }
+    __syncthreads();
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFullA, mx, o));
-  if (lane == 0 && bound != nullptr && mx != 0u) atomicMax(bound, mx);
+  block_atomic_max(mx, bound);
 }
 
 // z[n][idx[m]] = Y[n][m] (selected positions only); max|written| -> atomicMax(bound)
@@ -472,9 +510,7 @@ __global__ void scatter_kernel(Geom g, const uint32_t* __restrict__ idx, int64_t
     z[static_cast<int64_t>(n) * nc + __ldg(idx + m)] = val;
     mx = max(mx, __float_as_uint(fabsf(val)));
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFullA, mx, o));
-  if ((threadIdx.x & 31) == 0 && bound != nullptr && mx != 0u) atomicMax(bound, mx);
+  block_atomic_max(mx, bound);
 }
 
 __device__ __forceinline__ double dot4(float4 a) {
@@ -690,10 +726,13 @@ cudaError_t launch_admm_expand(const Geom& g, const uint32_t* bits, const uint32
   if (nb > cap) nb = cap;
   const char* ev = std::getenv("CSC_ADMM_EXPAND");
   const bool scalar = ev != nullptr && std::strcmp(ev, "scalar") == 0;
-  if (nper % 4 == 0 && (reinterpret_cast<uintptr_t>(Zd) & 15u) == 0 && !scalar)
-    expand4_kernel<<<dim3(static_cast<unsigned>(nb), g.N), 256, 0, st>>>(nper, bits, woff, ms, R, PV, rr, rr_new, Zd,
-                                                                          bound);
-  else
+  if (nper % 4 == 0 && (reinterpret_cast<uintptr_t>(Zd) & 15u) == 0 && !scalar) {
+    int64_t nbs = ((nper + 31) / 32 + kExpWords - 1) / kExpWords;
+    const int64_t caps = (148 * 6 + g.N - 1) / g.N;  // ~6 resident blocks per SM (33 KB smem each)
+    if (nbs > caps) nbs = caps;
+    expand_seg_kernel<<<dim3(static_cast<unsigned>(nbs), g.N), kExpWords, 0, st>>>(nper, bits, woff, ms, R, PV, rr,
+                                                                                   rr_new, Zd, bound);
+  } else
     expand_kernel<<<dim3(static_cast<unsigned>(nb), g.N), 256, 0, st>>>(nper, bits, woff, ms, R, PV, rr, rr_new, Zd,
                                                                          bound);
   return cudaGetLastError();
