@@ -296,26 +296,39 @@ __global__ void gather_kernel(Geom g, const uint32_t* __restrict__ idx, int64_t 
   const float* Cn = Cd + static_cast<int64_t>(n) * nc;
   const int64_t m4 = ms / 4;
   double acc = 0.0;
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kAT + threadIdx.x; t < m4;
-       t += static_cast<int64_t>(gridDim.x) * kAT) {
-    const int64_t m = 4 * t;
-    float c[4];
-    if (m + 4 <= mc) {
-      const uint4 l4 = __ldg(reinterpret_cast<const uint4*>(idx) + t);
-      c[0] = Cn[l4.x]; c[1] = Cn[l4.y]; c[2] = Cn[l4.z]; c[3] = Cn[l4.w];
-    } else {
+  // 4 grid-stride steps per batch with all their index -> value loads issued first (one dependent
+  // latency per batch instead of per step); the dot partial keeps the per-thread ascending order
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kAT;
+  for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kAT + threadIdx.x; t0 < m4; t0 += 4 * stride) {
+    float c[4][4];
+    float4 vi[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) c[j] = m + j < mc ? Cn[__ldg(idx + m + j)] : 0.f;
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = t0 + u * stride;
+      const int64_t m = 4 * t;
+      if (m + 4 <= mc) {
+        const uint4 l4 = __ldg(reinterpret_cast<const uint4*>(idx) + t);
+        c[u][0] = Cn[l4.x]; c[u][1] = Cn[l4.y]; c[u][2] = Cn[l4.z]; c[u][3] = Cn[l4.w];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[u][j] = m + j < mc ? Cn[__ldg(idx + m + j)] : 0.f;
+      }
+      vi[u] = (v != nullptr && t < m4) ? v[static_cast<int64_t>(n) * m4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const int64_t gi = static_cast<int64_t>(n) * m4 + t;
-    float4 o = make_float4(sign * c[0], sign * c[1], sign * c[2], sign * c[3]);
-    if (v != nullptr) {
-      const float4 vi = v[gi];
-      o.x = fmaf(rho, vi.x, o.x); o.y = fmaf(rho, vi.y, o.y); o.z = fmaf(rho, vi.z, o.z); o.w = fmaf(rho, vi.w, o.w);
-      acc += static_cast<double>(vi.x) * o.x + static_cast<double>(vi.y) * o.y + static_cast<double>(vi.z) * o.z +
-             static_cast<double>(vi.w) * o.w;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = t0 + u * stride;
+      if (t >= m4) break;
+      const int64_t gi = static_cast<int64_t>(n) * m4 + t;
+      float4 o = make_float4(sign * c[u][0], sign * c[u][1], sign * c[u][2], sign * c[u][3]);
+      if (v != nullptr) {
+        o.x = fmaf(rho, vi[u].x, o.x); o.y = fmaf(rho, vi[u].y, o.y); o.z = fmaf(rho, vi[u].z, o.z);
+        o.w = fmaf(rho, vi[u].w, o.w);
+        acc += static_cast<double>(vi[u].x) * o.x + static_cast<double>(vi[u].y) * o.y +
+               static_cast<double>(vi[u].z) * o.z + static_cast<double>(vi[u].w) * o.w;
+      }
+      out[gi] = o;
     }
-    out[gi] = o;
   }
   if (part != nullptr) {
     const double t = block_sum_d(acc, red);

@@ -42,15 +42,17 @@ SHAPES = [((3, 5, 5, 70, 130), 0.1), ((2, 17, 11, 100, 100), 0.2), ((4, 8, 5, 32
 
 @pytest.mark.parametrize("shape,p", [((2, 17, 11, 100, 100), 0.2), ((1, 9, 3, 33, 47), 0.5),
                                      ((2, 16, 7, 64, 64), 1.0)])
-def test_admm_expand_float4_bit_identical(torch_dev, shape, p, monkeypatch):
-    """The float4 expansion (nper % 4 == 0) and the scalar one move the same values: identical z."""
+@pytest.mark.parametrize("var,modes", [("CSC_ADMM_EXPAND", ["float4", "scalar"])])
+def test_admm_data_movement_bit_identical(torch_dev, shape, p, var, modes, monkeypatch):
+    """Variants that only move the same values differently give identical z: the staged float4
+    expansion vs the scalar one."""
     import torch
     import paper_1909_00145_b200 as pkg
     N, K, s, H, W = shape
     x, d, z = random_problem(900 + K, N, K, s, H, W, code_density=0.3)
     out = []
-    for mode in ["float4", "scalar"]:
-        monkeypatch.setenv("CSC_ADMM_EXPAND", mode)
+    for mode in modes:
+        monkeypatch.setenv(var, mode)
         ctx = pkg.Context(N, K, s, H, W, device=0)
         zt = _t(z, torch_dev)
         ctx.code_step_admm(_t(x, torch_dev), _t(d, torch_dev), zt, 0.2, p, 99, 3)
