@@ -398,7 +398,18 @@ __global__ void __launch_bounds__(1024) bimg_h_kernel(const float* __restrict__ 
   if (threadIdx.x == 0) mx = 0u;
   __syncthreads();
   uint32_t m = 0u;
-  for (int e = threadIdx.x; e < K * S2; e += blockDim.x) m = max(m, __float_as_uint(fabsf(f[e])));
+  // 8 independent loads in flight per thread (the max over K*S2 values is latency-bound)
+  const int nf = K * S2;
+  for (int e0 = threadIdx.x; e0 < nf; e0 += 8 * blockDim.x) {
+    float fv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      fv[u] = e < nf ? __ldg(f + e) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m = max(m, __float_as_uint(fabsf(fv[u])));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFullMask, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(&mx, m);
