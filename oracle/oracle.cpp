@@ -106,7 +106,8 @@ inline bool mask_bit_mode(int mode, uint64_t seed, uint32_t t, uint64_t l, uint6
 // a "valid" true convolution: every tap lands inside the code map.
 template <typename T>
 void residual(const Dims& D, const T* x, const T* d, const T* z, T* r) {
-#pragma omp parallel for schedule(static)
+  // every output pixel is an independent fp64 sum: rows (n, i) are spread over the threads
+#pragma omp parallel for collapse(2) schedule(static)
   for (int64_t n = 0; n < D.N; ++n)
     for (int64_t i = 0; i < D.H; ++i)
       for (int64_t j = 0; j < D.W; ++j) {
@@ -368,11 +369,12 @@ void filter_grad(const Dims& D, const double* r, const double* zd, double* g) {
 
 // ||Z g||^2 with (Z g)[n,i,j] = sum_k sum_{a,b} g[k,a,b] z[n,k,i+P-a,j+P-b].
 double zg_sq(const Dims& D, const double* g, const double* zd) {
-  std::vector<double> part((size_t)D.N, 0.0);
-#pragma omp parallel for schedule(static)
-  for (int64_t n = 0; n < D.N; ++n) {
-    double s2 = 0.0;
-    for (int64_t i = 0; i < D.H; ++i)
+  // per-row fp64 partials (rows (n, i) spread over the threads), summed in row order
+  std::vector<double> part((size_t)(D.N * D.H), 0.0);
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t n = 0; n < D.N; ++n)
+    for (int64_t i = 0; i < D.H; ++i) {
+      double s2 = 0.0;
       for (int64_t j = 0; j < D.W; ++j) {
         double acc = 0.0;
         for (int64_t k = 0; k < D.K; ++k)
@@ -381,10 +383,10 @@ double zg_sq(const Dims& D, const double* g, const double* zd) {
               acc += g[D.di(k, a, b)] * zd[((n * D.K + k) * D.Hc + i + D.P - a) * D.Wc + j + D.P - b];
         s2 += acc * acc;
       }
-    part[n] = s2;
-  }
+      part[n * D.H + i] = s2;
+    }
   double tot = 0.0;
-  for (int64_t n = 0; n < D.N; ++n) tot += part[n];
+  for (size_t q = 0; q < part.size(); ++q) tot += part[q];
   return tot;
 }
 
@@ -636,11 +638,13 @@ void filter_step_surrogate(int64_t K, int64_t s, const double* C, const double* 
 // Eq.1 objective: F = sum_n 1/2||x_n - sum_k d_k * z_{n,k}||^2 + lam sum ||z||_1.
 template <typename T>
 void objective(const Dims& D, const T* x, const T* d, const T* z, double lam, double out[3]) {
-  std::vector<double> h((size_t)D.N, 0.0), l1((size_t)D.N, 0.0);
-#pragma omp parallel for schedule(static)
-  for (int64_t n = 0; n < D.N; ++n) {
-    double s2 = 0.0;
-    for (int64_t i = 0; i < D.H; ++i)
+  // per-row fp64 partials of the squared residual (rows (n, i) spread over the threads) and per-image
+  // partials of |z|, each summed in a fixed order
+  std::vector<double> h((size_t)(D.N * D.H), 0.0), l1((size_t)D.N, 0.0);
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t n = 0; n < D.N; ++n)
+    for (int64_t i = 0; i < D.H; ++i) {
+      double s2 = 0.0;
       for (int64_t j = 0; j < D.W; ++j) {
         double acc = 0.0;
         for (int64_t k = 0; k < D.K; ++k)
@@ -650,15 +654,20 @@ void objective(const Dims& D, const T* x, const T* d, const T* z, double lam, do
         const double rr = acc - (double)x[D.xi(n, i, j)];
         s2 += rr * rr;
       }
+      h[n * D.H + i] = s2;
+    }
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < D.N; ++n) {
     double a1 = 0.0;
     for (int64_t k = 0; k < D.K; ++k)
       for (int64_t u = 0; u < D.Hc; ++u)
         for (int64_t v = 0; v < D.Wc; ++v) a1 += std::fabs((double)z[D.zi(n, k, u, v)]);
-    h[n] = 0.5 * s2;
     l1[n] = a1;
   }
   double hs = 0.0, ls = 0.0;
-  for (int64_t n = 0; n < D.N; ++n) { hs += h[n]; ls += l1[n]; }
+  for (size_t q = 0; q < h.size(); ++q) hs += h[q];
+  hs *= 0.5;
+  for (int64_t n = 0; n < D.N; ++n) ls += l1[n];
   out[1] = hs;
   out[2] = lam * ls;
   out[0] = out[1] + out[2];
