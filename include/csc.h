@@ -220,6 +220,14 @@ int csc_abi_version(void);
  *       < floor(p*2^32), q = l>>2. */
 csc_status csc_mask_bits(csc_ctx* ctx, uint32_t iter, double p, uint64_t seed, uint32_t* bits_dev);
 
+/* The mask exactly as the tensor-core code step consumes it (selection words, the hot path's own
+ * mask kernel): info[4] (HOST) receives {nkg, wper, wnc, KC}; words_dev (DEVICE, NULL to query only)
+ * receives nkg*wper*Hc*Wc 32-bit words with bit i of word (kg*wper + b)*Hc*Wc + u*Wc + v equal to
+ * the canonical mask bit of filter k = kg*KC + b*wnc + i (zero for k >= min(K, (kg+1)*KC)).
+ * CSC_ERR_SHAPE when this context's code step does not run on the tensor cores. */
+csc_status csc_mask_selwords(csc_ctx* ctx, uint32_t iter, double p, uint64_t seed, uint32_t* words_dev,
+                             int32_t info[4]);
+
 /* Copy the cached residual [n_local][H][W] into r_dev (DEVICE). */
 csc_status csc_read_residual(csc_ctx* ctx, float* r_dev);
 

@@ -31,7 +31,7 @@ ABI_SYMBOLS = (
     "csc_profile_enable", "csc_profile_read", "csc_kernel_variants", "csc_code_step_admm",
     "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd", "csc_surrogate_reset",
     "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate", "csc_set_mask_mode",
-    "csc_stage_images", "csc_iterate_staged",
+    "csc_stage_images", "csc_iterate_staged", "csc_mask_selwords",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -91,6 +91,7 @@ def load_library(path: Optional[str] = None):
         L.csc_nccl_unique_id.argtypes = [vp]
         L.csc_abi_version.restype = ctypes.c_int
         L.csc_mask_bits.argtypes = [vp, u32, f64, u64, vp]
+        L.csc_mask_selwords.argtypes = [vp, u32, f64, u64, vp, vp]
         L.csc_read_residual.argtypes = [vp, vp]
         L.csc_read_grad.argtypes = [vp, vp]
         L.csc_lipschitz.argtypes = [vp, vp, vp]
@@ -304,6 +305,20 @@ class Context:
             raise ValueError(f"out must be a contiguous int32 CUDA tensor of {nwords} words")
         self._check(self._L.csc_mask_bits(self._h, int(it) & 0xffffffff, float(p), int(seed) & (2**64 - 1),
                                           out.data_ptr()))
+
+    def mask_selwords(self, it: int, p: float, seed: int, out=None):
+        """The selection words of the tensor-core code step (csc_mask_selwords); returns
+        (nkg, wper, wnc, KC).  out: contiguous int32 CUDA tensor of nkg*wper*Hc*Wc words, or None."""
+        info = (ctypes.c_int32 * 4)()
+        self._check(self._L.csc_mask_selwords(self._h, 0, 1.0, 0, None, info))
+        if out is not None:
+            import torch
+            n = info[0] * info[1] * self.Hc * self.Wc
+            if not (out.is_cuda and out.dtype == torch.int32 and out.numel() == n and out.is_contiguous()):
+                raise ValueError(f"out must be a contiguous int32 CUDA tensor of {n} words")
+            self._check(self._L.csc_mask_selwords(self._h, int(it) & 0xffffffff, float(p), int(seed) & (2**64 - 1),
+                                                  out.data_ptr(), info))
+        return tuple(info)
 
     def read_residual(self, out):
         self._check(self._L.csc_read_residual(self._h, _ptr(out, "out", self.n_local * self.H * self.W)

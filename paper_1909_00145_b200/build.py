@@ -65,8 +65,22 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in sources() + _headers())
 
 
+def _flags_changed(objdir: str) -> bool:
+    stamp = os.path.join(objdir, "extra_flags.txt")
+    want = os.environ.get("CSC_NVCC_EXTRA", "")
+    have = open(stamp).read() if os.path.exists(stamp) else ""
+    if have != want:
+        os.makedirs(objdir, exist_ok=True)
+        with open(stamp, "w") as f:
+            f.write(want)
+        return True
+    return False
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile every csrc/*.cu to an object (in parallel, only the stale ones) and link the .so."""
+    if _flags_changed(os.path.join(HERE, "build")):
+        force = True
     if not force and not _stale():
         return LIB
     nvcc = _nvcc()
@@ -76,6 +90,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     hdr_t = max(os.path.getmtime(p) for p in _headers())
     base = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-ccbin", host_cxx,
             "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
+    # tuning builds only (e.g. CSC_NVCC_EXTRA=-DCSC_ROLE_TIMING); the product build passes nothing
+    base += [f for f in os.environ.get("CSC_NVCC_EXTRA", "").split() if f]
     if verbose:
         base.insert(1, "-Xptxas=-v")
     jobs, objs = [], []

@@ -113,7 +113,10 @@ struct csc_ctx {
   // tensor-core dense-then-mask code step (csc_code_tc.cu)
   bool ct_on = false;
   csc::CodeTcPlan ct{};
-  uint32_t* mwords = nullptr;  // selection-word mask [4*nkg][Hc*Wc]
+  uint32_t* mwords = nullptr;  // selection-word mask [wper*nkg][Hc*Wc]
+  float* a3_part = nullptr;    // a3' band partials of the fp16-split code step [nkg][N][nbands][BR+P][W]
+  csc::TmapCache tm_code[2];   // code step: z, selection words
+  csc::TmapCache tm_adm[2];    // ADMM's D^T e pass through the code-step kernel (plain mode)
   uint32_t* rmax = nullptr;    // max|r| (float bits) for the fp16-split code step
   int step_rule = CSC_STEP_LIPSCHITZ;  // built-in tau_z rule (csc_set_step_rule)
   // projected block-coordinate filter update scratch (csc_bcd.cu), allocated on first use
@@ -486,6 +489,7 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
       if (c->ct.ok) {
         c->ct_on = true;
         ok = ok && alloc(reinterpret_cast<void**>(&c->mwords), sizeof(uint32_t) * c->ct.sw_words);
+        if (c->ct.half) ok = ok && alloc(reinterpret_cast<void**>(&c->a3_part), sizeof(float) * c->ct.a3_floats);
         ok = ok && alloc(reinterpret_cast<void**>(&c->rmax), sizeof(uint32_t) * 4);
       }
     }
@@ -613,6 +617,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->g32);
   cudaFree(c->colw);
   cudaFree(c->mwords);
+  cudaFree(c->a3_part);
   cudaFree(c->rmax);
   cudaFree(c->tauk);
   cudaFree(c->bcd_gpart);
@@ -715,15 +720,20 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   const int tau_stride = eso ? 1 : 0;
   const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
   const int all_selected = thr >= (uint64_t(1) << 32) ? 1 : 0;
+  bool a3_done = false;
   if (g.N > 0) {
     if (c->ct_on) {
       if (!all_selected)
         CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(g, c->ct, seed, iter, thr, c->mwords, c->st, c->mask_mode));
       if (c->ct.half) {
+        // masked step fused with the incremental residual r' = r + D dz (a3'): the cache then holds
+        // D z_new - x for (x, d, z) and the filter step needs no dense residual pass
         CSC_LAUNCH(c, 1, csc::launch_absmax(c->r, n_pix(g), c->rmax, c->st));
         CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
-                     csc::launch_code_h(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, tau_dev,
-                                        lambda, c->rmax, zbound(c, z), c->st, false, tau_stride));
+                     csc::launch_code_h(g, c->ct, c->tm_code, c->r, d, z, all_selected ? nullptr : c->mwords, tau_dev,
+                                        lambda, c->rmax, zbound(c, z), c->st, false, tau_stride, c->a3_part));
+        CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1, csc::launch_code_a3_fixup(g, c->ct, c->a3_part, c->r, c->st));
+        a3_done = true;
       } else {
         CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
                      csc::launch_code_tc(g, c->ct, c->r, d, z, all_selected ? nullptr : c->mwords, tau_dev,
@@ -735,7 +745,14 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
                                                                 zbound(c, z), c->st, tau_stride));
     }
   }
-  c->cache_valid = false;  // r no longer matches z
+  if (a3_done || g.N == 0) {
+    c->cache_valid = true;  // r' = r + D dz = D z_new - x  (a3')
+    c->cx = x;
+    c->cd = d;
+    c->cz = z;
+  } else {
+    c->cache_valid = false;  // r no longer matches z
+  }
   if (step_used) {
     CSC_CUDA(c, cudaMemcpyAsync(c->h_fscal + kTauZ, tau_dev, sizeof(float), cudaMemcpyDeviceToHost, c->st));
     CSC_CUDA(c, cudaStreamSynchronize(c->st));
@@ -884,7 +901,7 @@ csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float*
     if (tc_dtr) {
       CSC_LAUNCH(c, 1, csc::launch_absmax(e, n_pix(g), c->adm_bound + 1, c->st));
       CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1,
-                   csc::launch_code_h(g, c->ct, e, d, c->adm_cd, nullptr, nullptr, 0.f, c->adm_bound + 1, nullptr,
+                   csc::launch_code_h(g, c->ct, c->tm_adm, e, d, c->adm_cd, nullptr, nullptr, 0.f, c->adm_bound + 1, nullptr,
                                       c->st, true));
       CSC_LAUNCH_C(c, CSC_K_ADMM, 1, csc::launch_admm_gather(g, c->adm_idx, mc, ms, c->adm_cd, v, rh, sign, out, part,
                                                              c->st));
@@ -1285,6 +1302,23 @@ csc_status csc_mask_bits(csc_ctx* c, uint32_t iter, double p, uint64_t seed, uin
   CSC_CUDA(c, cudaSetDevice(c->device));
   const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
   CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_bits(c->g, seed, iter, thr, bits_dev, c->st, c->mask_mode));
+  return CSC_OK;
+}
+
+csc_status csc_mask_selwords(csc_ctx* c, uint32_t iter, double p, uint64_t seed, uint32_t* words_dev,
+                             int32_t info[4]) {
+  if (!c || !info) return fail(c, CSC_ERR_ARG, "info (host, 4 ints) required");
+  if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
+  if (!c->ct_on) return fail(c, CSC_ERR_SHAPE, "the code step of this context does not use selection words");
+  info[0] = c->ct.nkg;
+  info[1] = c->ct.wper;
+  info[2] = c->ct.wnc;
+  info[3] = c->ct.KC;
+  if (words_dev == nullptr) return CSC_OK;
+  if (!aligned4(words_dev)) return fail(c, CSC_ERR_ARG, "words_dev must be a device pointer");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
+  CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(c->g, c->ct, seed, iter, thr, words_dev, c->st, c->mask_mode));
   return CSC_OK;
 }
 

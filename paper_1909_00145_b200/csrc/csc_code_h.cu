@@ -1,30 +1,44 @@
 // csc_code_h.cu -- masked proximal-gradient code step, dense-then-mask on the sm_100a tensor cores
-// with the 3-term fp16 split (tcgen05.mma kind::f16) and TMA-fed code tiles in the epilogue.
+// with the 3-term fp16 split (tcgen05.mma kind::f16), fused with the incremental residual (a3').
 //
-// Same step as csc_code_tc.cu (Eq.3-4, §3.1, shrinkage P:311-312, R1/R2):
+// Code step (Eq.3-4, §3.1, shrinkage P:311-312, R1/R2):
 //   for every masked code (k, u, v) of image n:  c = sum_{a,b} d[k,a,b] r[n,u-P+a,v-P+b],
 //   z <- S_{tau lambda}(z - tau c);  unmasked codes are untouched.
-// GEMM per 128-position tile: C[p][k] = sum_t R[p][t] d[k][t], M = 128 flattened positions,
-// N = Npad filters, K = 128 taps in 8 steps of 16 (kind::f16).  Operands (reading T6):
-//   R_s = r * 2^er, d_s = d * 2^ed split as hi = rn11(x_s) (exact fp16), lo = fp16_rn(x_s - hi);
-//   C_s = R_hi d_hi + R_hi d_lo + R_lo d_hi (fp32 accumulate), c = C_s * 2^-(er+ed).
-//   er comes from max|r| (device scalar written with the residual, csc_api.cu), ed from max|d| over
-//   the CTA's filter group (computed in the prologue).
-//   A = im2col(r) in TMEM (lane = position, two fp16 taps per 32-bit column), written by the
-//       converter warps from the zero-padded residual tile (cp.async, as csc_code_tc.cu).
-//   B = the filters, K-major SWIZZLE_128B fp16 (2 K-atoms of 64 taps), resident: 57 KB for 112
-//       filters instead of 115 KB for tf32.
-// The freed shared memory holds the codes: each epilogue warp owns a {32 positions, NC filters}
-// slice and TMA-loads it two tiles ahead (double buffer, own mbarriers), so HBM latency is hidden
-// behind two MMA tiles; the warp applies mask / step / shrinkage from shared memory and stores only
-// the codes that change (and raises the max|z| bound with them).
-// CTA (persistent, 25 warps): warp 0 MMA; warps 1..8 converters; warps 9..24 epilogue.
+// Incremental residual (SURVEY.md §8(a) a3'; linearity of D):
+//   r' = r + sum_k d_k * (z_new - z_old)_k,  so the filter step needs no dense residual pass.
+//
+// Per 128-position tile of a band of BR code rows (flattened positions p = u*Wc + v):
+//   GEMM 1 (the correlation):  C[p][k] = sum_t R[p][t] d[k][t], M = 128 positions, N = Npad filters,
+//     K = 128 taps (8 K16-steps).  A = im2col(r) in TMEM (lane = position, two fp16 taps per column),
+//     written by the converter warps from the band's residual rows (cp.async staging); B = the filters,
+//     K-major SWIZZLE_128B fp16, resident.
+//   epilogue (16 warps = 4 TMEM lane quarters x 4): warp (q, j) owns the 16-filter groups (j + t) mod 4
+//     and +4 of tile t (rotated so the 7 groups of Npad = 112 spread evenly).  Only the codes the mask
+//     selects are read: each lane cp.async's the 4-byte codes whose selection bit is set, one tile
+//     ahead, so HBM moves the 32-B sectors that hold a selected code and nothing else (the cost falls
+//     with p).  It applies step / shrinkage, stores the codes that change, and writes
+//     dz = z_new - z_old (0 elsewhere) as fp16 hi/lo into the accumulator columns it has just read:
+//     K16-step g of the second GEMM takes hi from columns 16g..16g+7 and lo from 16g+8..16g+15, exactly
+//     the columns of C for filters 16g..16g+15, so no warp overwrites a column another warp still reads.
+//   GEMM 2 (the increment):  Y[p][t] = sum_k dz[p][k] d[k][t], M = 128, N = 128 taps, K = Npad filters;
+//     A = dz in TMEM, B = the same resident filter image read MN-major (taps contiguous).
+//   col2im (4 warps, one per lane quarter): as the dense pass (csc_conv_h.cu), one rotation shuffle per
+//     tap into the band window; the window is flushed per band to partials [kg][n][band][BR+P][W] that
+//     launch_code_a3_fixup adds to r in a fixed order.
+// Operands are split after exact power-of-two scalings (reading T6): x_s = x 2^e,
+// hi = rn11(x_s) (an exact fp16), lo = fp16_rn(x_s - hi); products hi*hi + hi*lo + lo*hi accumulate
+// in fp32.  e_r from max|r|, e_d from max|d| of the CTA's filter group, e_dz from the bound
+// |dz| <= tau (||d_k||_1 max|r| + lambda) (one step of the prox-gradient map, |S(w) - z| <= |w - z| +
+// kappa), which keeps every scaled value <= 2^14 with 2^17 of headroom below for full precision.
+// CTA (persistent, 25 warps): warp 0 MMA, warps 1..4 converters, 5..20 epilogue, 21..24 col2im.
+// TMEM (512 columns): C / dz double buffer [0, 2 Npad), im2col slots [256, 384), Y [384, 512).
 #include "csc_internal.cuh"
 #include "csc_tc_ptx.cuh"
 
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -35,17 +49,27 @@ namespace {
 
 using namespace tcx;
 
-constexpr int kChNS = 4;          // A slots (4 K16-steps = 64 taps each) in TMEM
-constexpr int kChConvWarps = 8;
-constexpr int kChEpiWarps = 16;
-constexpr int kChConvBase = 1, kChEpiBase = kChConvBase + kChConvWarps;
-constexpr int kChWarps = kChEpiBase + kChEpiWarps;
+constexpr int kChNS = 2;          // im2col slots (4 K16-steps = 64 taps each) in TMEM
+constexpr int kChConvWarps = 4;
+constexpr int kChEpiWarps = 12;  // 3 per TMEM lane quarter
+constexpr int kChColWarps = 8;   // 2 per TMEM lane quarter (tap rows split)
+constexpr int kChEpiPerQ = kChEpiWarps / 4;
+constexpr int kChChunks = (8 + kChEpiPerQ - 1) / kChEpiPerQ;  // 16-filter groups per warp per tile (Npad <= 128)
+constexpr int kChConvBase = 1, kChEpiBase = kChConvBase + kChConvWarps, kChColBase = kChEpiBase + kChEpiWarps;
+constexpr int kChWarps = kChColBase + kChColWarps;
 constexpr int kChThreads = 32 * kChWarps;
 constexpr int kChTile = 128;
-constexpr int kChSmemMax = 220 * 1024;
+constexpr int kChSmemMax = 226 * 1024;
+constexpr uint32_t kColA = 256, kColY = 384;
+constexpr int kZBuf = kChChunks * 16 * 32;  // floats per epilogue warp: chunks x 16 filters x 32 positions
+constexpr int kWBuf = kChChunks * 32;       // selection words per epilogue warp
 
 __host__ __device__ constexpr uint32_t idesc_f16_kk(int M, int N) {  // fp16 A/B K-major, fp32 D
   return (1u << 4) | (0u << 7) | (0u << 10) | (0u << 15) | (0u << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc_f16_kmn(int M, int N) {  // A K-major (TMEM), B MN-major
+  return (1u << 4) | (0u << 7) | (0u << 10) | (0u << 15) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 __device__ __forceinline__ int scale_exp_h(uint32_t mbits) {
@@ -62,61 +86,163 @@ __device__ __forceinline__ uint32_t pack_h2_h(float a, float b) {
   const __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+__device__ __forceinline__ void cp_async4_if(uint32_t smem_dst, const float* src, bool p) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(smem_dst),
+               "l"(src), "r"(p ? 1 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void st_global_if(float* ptr, float v, bool p) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.f32 [%0], %1;\n}\n" ::"l"(ptr), "f"(v),
+               "r"(p ? 1 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, float (&f)[8]) {
+  uint32_t v[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[i]);
+}
+
+// Per-role cycle counters for tuning (build with -DCSC_ROLE_TIMING; off in the product build).
+#ifdef CSC_ROLE_TIMING
+struct RoleClock {
+  unsigned long long v[7];
+  unsigned long long t0;
+  __device__ RoleClock() : t0(0) {
+#ifdef __CUDA_ARCH__
+    t0 = clock64();
+#endif
+    for (int i = 0; i < 7; ++i) v[i] = 0;
+  }
+};
+#define RT_WAIT(rc, slot, stmt)                      \
+  do {                                               \
+    const unsigned long long _a = clock64();         \
+    stmt;                                            \
+    (rc).v[slot] += clock64() - _a;                  \
+  } while (0)
+#define RT_DUMP(rc, dbg, role)                                                          \
+  do {                                                                              \
+    if ((dbg) != nullptr) {                                                         \
+      for (int _i = 0; _i < 7; ++_i) (dbg)[blockIdx.x * 32 + (role) * 8 + _i] = (rc).v[_i]; \
+      (dbg)[blockIdx.x * 32 + (role) * 8 + 7] = clock64() - (rc).t0;               \
+    }                                                                               \
+  } while (0)
+#else
+struct RoleClock {};
+#define RT_WAIT(rc, slot, stmt) stmt
+#define RT_DUMP(rc, dbg, role) \
+  do {                         \
+  } while (0)
+#endif
+
+// the S accumulator columns of one tap row (exact widths: no TMEM read bandwidth spent on padding)
+__device__ __forceinline__ void tmem_ld_x1(uint32_t taddr, float& f) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(v) : "r"(taddr) : "memory");
+  f = __uint_as_float(v);
+}
+__device__ __forceinline__ void tmem_ld_x2(uint32_t taddr, float& f0, float& f1) {
+  uint32_t v0, v1;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(v0), "=r"(v1) : "r"(taddr) : "memory");
+  f0 = __uint_as_float(v0);
+  f1 = __uint_as_float(v1);
+}
+template <int S>
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&y)[S]) {
+  int c = 0;
+  if constexpr (S >= 8) {
+    float t[8];
+    tmem_ld8_nowait(taddr, t);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) y[i] = t[i];
+    c = 8;
+  }
+  if constexpr ((S & 4) != 0) {
+    float t[4];
+    tmem_ld4_nowait(taddr + c, t);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) y[(S >= 8 ? 8 : 0) + i] = t[i];
+  }
+  constexpr int c2 = (S >= 8 ? 8 : 0) + ((S & 4) != 0 ? 4 : 0);
+  if constexpr ((S & 2) != 0) tmem_ld_x2(taddr + c2, y[c2], y[c2 + 1]);
+  constexpr int c1 = c2 + ((S & 2) != 0 ? 2 : 0);
+  if constexpr ((S & 1) != 0) tmem_ld_x1(taddr + c1, y[c1]);
+  (void)c;
+}
 
 struct ChArgs {
+  CUtensorMap tm_z;      // z as [N*K planes][Hc*Wc positions] fp32, box {32, 16}
+  CUtensorMap tm_w;      // selection words [nkg*ngroups][Hc*Wc] u32, box {32, 1}
   const float* r;        // [N][H][W]
   const float* d;        // [K][S][S]
   float* z;              // [N][K][Hc][Wc]
-  const uint32_t* mask;  // selection words [nkg*4][plane] or nullptr (all)
+  const uint32_t* mask;  // selection words [nkg][ngroups][plane] (bit i: filter kg*KC + 16 g + i) or nullptr (all)
   const float* tau;
   const uint32_t* rmax;  // max|r| (float bits)
   uint32_t* zmax;        // raised by every written code, or nullptr
+  float* part;           // a3' band partials [nkg][N][nbands][BR+P][W], or nullptr (no a3')
   float lam;
   int N, K, S, H, W, Hc, Wc, P;
-  int KC, Npad, nkg, G;
-  int L, nseg, nitems;
-  int pitch, rs_rows, rs_floats;
+  int KC, Npad, nkg, G, ngroups;
+  int BR, nbands, nitems, WL;
+  int pitch, rs_floats;
   int b_bytes;           // one of hi / lo: 2 K-atoms x Npad rows x 128 B
-  int plain;             // 1: z <- c at every position (no z read, no step / shrinkage / mask)
+  int plain;             // 1: z <- c at every position (no z read, no step / shrinkage / mask / a3')
   int tau_stride;        // 0: tau[0] for every filter; 1: tau[k] per filter (ESO rule)
+  unsigned long long* dbg;  // CSC_ROLE_TIMING: [grid][4 roles][8] cycle counters
 };
 
 struct ChItem {
-  int n, p0, p1, ntiles, u_first;
+  int n, u0, u1, p0, p1, ntiles, band;
 };
 __device__ __forceinline__ ChItem ch_item(const ChArgs& A, int item) {
   ChItem it;
-  it.n = item / A.nseg;
-  const int sg = item - it.n * A.nseg;
-  it.p0 = sg * A.L;
-  it.p1 = min(it.p0 + A.L, A.Hc * A.Wc);
+  it.n = item / A.nbands;
+  it.band = item - it.n * A.nbands;
+  it.u0 = it.band * A.BR;
+  it.u1 = min(it.u0 + A.BR, A.Hc);
+  it.p0 = it.u0 * A.Wc;
+  it.p1 = it.u1 * A.Wc;
   it.ntiles = (it.p1 - it.p0 + kChTile - 1) / kChTile;
-  it.u_first = it.p0 / A.Wc;
   return it;
 }
 
-template <int S, int NC>
-__global__ void __launch_bounds__(kChThreads, 1)
-code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
+template <int S>
+__global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_constant__ ChArgs A) {
   constexpr int S2 = S * S;
+  constexpr int P = S - 1;
   extern __shared__ uint8_t smraw[];
-  __shared__ __align__(8) uint64_t a_full[kChNS], a_empty[kChNS], acc_full[2], acc_empty[2];
-  __shared__ __align__(8) uint64_t z_full[kChEpiWarps][2];
+  __shared__ __align__(8) uint64_t a_full[kChNS], a_empty[kChNS], acc_full[2], acc_empty[2], dz_full[2];
+  __shared__ __align__(8) uint64_t y_full, y_empty;
+  __shared__ __align__(8) uint64_t zfull[kChEpiWarps][kChChunks];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ uint32_t dmax_sh;
+  __shared__ uint32_t dmax_sh, dl1_sh, tmax_sh;
 
   const int tid = threadIdx.x, warp = __shfl_sync(kFullMask, tid >> 5, 0), lane = tid & 31;
   const int gi = blockIdx.x % A.G, kg = blockIdx.x / A.G;
+  const bool plain = A.plain != 0;
+  const bool a3p = !plain && A.part != nullptr;
   const uint32_t raw = su32(smraw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* sm = smraw + (base - raw);
-  uint8_t* bh = sm;                                        // [2 K-atoms][Npad][128 B] fp16 hi
-  uint8_t* bl = sm + A.b_bytes;                            // lo
-  float* zsm = reinterpret_cast<float*>(sm + 2 * A.b_bytes);  // [2][16 warps][NC][32] (1 KB aligned)
-  float* rs = zsm + 2 * kChEpiWarps * NC * 32;             // [2][rs_rows][pitch]
+  uint8_t* bh = sm;                                              // [2 K-atoms][Npad][128 B] fp16 hi
+  uint8_t* bl = sm + A.b_bytes;                                  // lo
+  float* zsm = reinterpret_cast<float*>(sm + 2 * A.b_bytes);     // [16 warps][2][16][32]
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(zsm + kChEpiWarps * kZBuf);  // [epilogue warps][chunks][32]
+  float* rs = reinterpret_cast<float*>(wsm + kChEpiWarps * kWBuf);  // residual pairs hi | lo [BR+P][pitch]
+  float* win = rs + 2 * A.rs_floats;                             // [WL] band window of the a3' col2im
 
-  // ---- setup: max|d| of this filter group, then the fp16 hi/lo B image (K-major SW128)
-  if (tid == 0) dmax_sh = 0u;
+  // ---- setup: max|d|, max ||d_k||_1 and max tau of this filter group, then the fp16 hi/lo B image
+  if (tid == 0) {
+    dmax_sh = 0u;
+    dl1_sh = 0u;
+    tmax_sh = 0u;
+  }
+  for (int e = tid; e < A.WL; e += kChThreads) win[e] = 0.f;
   __syncthreads();
   {
     uint32_t m = 0u;
@@ -127,6 +253,16 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFullMask, m, o));
     if (lane == 0) atomicMax(&dmax_sh, m);
+    if (!plain) {
+      for (int k = tid; k < A.KC; k += kChThreads) {  // one thread per filter (fp32 sums: a bound only)
+        const int kk = kg * A.KC + k;
+        if (kk >= A.K) break;
+        float l1 = 0.f;
+        for (int t = 0; t < S2; ++t) l1 += fabsf(A.d[static_cast<size_t>(kk) * S2 + t]);
+        atomicMax(&dl1_sh, __float_as_uint(l1 * 1.0001f));
+        atomicMax(&tmax_sh, __float_as_uint(fabsf(A.tau[A.tau_stride ? kk : 0])));
+      }
+    }
   }
   __syncthreads();
   const int ed = scale_exp_h(dmax_sh), er = scale_exp_h(*A.rmax);
@@ -145,6 +281,11 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
       *reinterpret_cast<uint32_t*>(bl + off) = pack_h2_h(v0 - h0, v1 - h1);
     }
   }
+  // |dz| <= tau (|c| + lambda) with |c| <= ||d_k||_1 max|r|  (a bound; only its exponent is used)
+  const float dzb = plain ? 0.f
+                          : __uint_as_float(tmax_sh) *
+                                (__uint_as_float(dl1_sh) * __uint_as_float(*A.rmax) * 1.0001f + A.lam);
+  const int edz = scale_exp_h(__float_as_uint(dzb));
   fence_async_shared();
   if (tid == 0) {
     for (int i = 0; i < kChNS; ++i) {
@@ -153,39 +294,72 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], kChEpiWarps);
+      mbar_init(&acc_empty[i], a3p ? 1 : kChEpiWarps);  // a3': released by the GEMM 2 commit
+      mbar_init(&dz_full[i], kChEpiWarps);
     }
-    for (int w = 0; w < kChEpiWarps; ++w) {
-      mbar_init(&z_full[w][0], 1);
-      mbar_init(&z_full[w][1], 1);
-    }
+    mbar_init(&y_full, 1);
+    mbar_init(&y_empty, kChColWarps);
+    for (int w = 0; w < kChEpiWarps; ++w)
+      for (int c = 0; c < kChChunks; ++c) mbar_init(&zfull[w][c], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) tmem_alloc(&tmem_base_sh, 512);
-  if (warp == kChEpiBase && lane == 0) tma_prefetch_desc(&tmap_z);
+  if (warp == kChEpiBase && lane == 0 && !plain) {
+    tma_prefetch_desc(&A.tm_z);
+    if (A.mask != nullptr) tma_prefetch_desc(&A.tm_w);
+  }
   tc_before();
   __syncthreads();
   tc_after();
   const uint32_t tbase = __shfl_sync(kFullMask, tmem_base_sh, 0);
-  const uint32_t t_acc = tbase;         // 2 x Npad columns
-  const uint32_t t_a = tbase + 256u;    // kChNS slots x 64 columns
+  const uint32_t t_acc = tbase;          // 2 x Npad columns
+  const uint32_t t_a = tbase + kColA;    // kChNS slots x 64 columns
+  const uint32_t t_y = tbase + kColY;    // 128 columns
 
   if (warp == 0) {
     // ================================ MMA issuer
+    RoleClock rc;
     const uint32_t idesc = idesc_f16_kk(128, A.Npad);
+    const uint32_t idesc2 = idesc_f16_kmn(128, 128);
     const uint32_t sbh = su32(bh), sbl = su32(bl);
     const uint32_t katom = static_cast<uint32_t>(A.Npad) * 128u;
+    // GEMM 2 of tile u: Y = dz(u) x B (B read MN-major: taps contiguous, filters = K rows)
+    auto gemm2 = [&](uint32_t u) {
+      const uint32_t bu = u & 1u;
+      RT_WAIT(rc, 2, mbar_wait_backoff(&dz_full[bu], (u >> 1) & 1u, 32));
+      RT_WAIT(rc, 3, mbar_wait_backoff(&y_empty, (u & 1u) ^ 1u, 32));
+      tc_after();
+      const uint32_t acol = t_acc + bu * static_cast<uint32_t>(A.Npad);
+      for (int c = 0; c < A.ngroups; ++c) {
+        const uint64_t dbh = sdesc(sbh + static_cast<uint32_t>(c) * 2048u, katom, 1024u, kLayout128B);
+        const uint64_t dbl = sdesc(sbl + static_cast<uint32_t>(c) * 2048u, katom, 1024u, kLayout128B);
+        const uint32_t acc0 = c > 0 ? 1u : 0u;
+        const uint32_t ah = acol + 16u * c;
+        asm volatile(
+            "{\n.reg .pred e, p, t;\n"
+            "elect.sync _|e, 0xffffffff;\n"
+            "setp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 1, 1;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %4, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %6, %4, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %4, t;\n"
+            "}\n" ::"r"(t_y),
+            "r"(ah), "r"(ah + 8u), "l"(dbh), "r"(idesc2), "r"(acc0), "l"(dbl)
+            : "memory");
+      }
+      mma_commit_elect(&y_full);
+      mma_commit_elect(&acc_empty[bu]);
+    };
     uint32_t g = 0, tcount = 0;
     for (int item = gi; item < A.nitems; item += A.G) {
       const ChItem it = ch_item(A, item);
       for (int tl = 0; tl < it.ntiles; ++tl, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
-        mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
+        RT_WAIT(rc, 0, mbar_wait_backoff(&acc_empty[buf], (use & 1u) ^ 1u, 32));
         tc_after();
         const uint32_t dcol = t_acc + buf * static_cast<uint32_t>(A.Npad);
         for (int j = 0; j < 2; ++j, ++g) {  // 2 slots of 4 K16-steps (64 taps)
           const uint32_t slot = g % kChNS, ph = (g / kChNS) & 1u;
-          mbar_wait(&a_full[slot], ph);
+          RT_WAIT(rc, 1, mbar_wait_backoff(&a_full[slot], ph, 32));
           tc_after();
           const uint32_t ah = t_a + slot * 64u;
 #pragma unroll
@@ -208,63 +382,87 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
           mma_commit_elect(&a_empty[slot]);
         }
         mma_commit_elect(&acc_full[buf]);
+        if (a3p && tcount > 0) gemm2(tcount - 1);
       }
     }
+    if (a3p && tcount > 0) gemm2(tcount - 1);
     __syncwarp();
+    if (lane == 0) RT_DUMP(rc, A.dbg, 0);
   } else if (warp < kChEpiBase) {
     // ================================ converters: im2col(r) -> TMEM, two fp16 taps per column
     const int cw = warp - kChConvBase;  // 0..7
     const int q = warp & 3;
-    const int h = cw >> 2;              // K16-steps {2h, 2h+1} of every slot
     const uint32_t tq = (static_cast<uint32_t>(32 * q) << 16);
     const int ct = tid - 32 * kChConvBase;
     const float sr = exp2i_h(er);
-    auto stage_r = [&](int item, int buf) {
+    RoleClock rc;
+    // The band's residual rows u0-P .. u1-1 (columns -P .. Wc-1, zero outside the image), scaled by
+    // 2^er and split once per band into fp16 hi / lo PAIRS: hp[row][c] = (hi(r[row][c-P]), hi(r[row][c-P+1])),
+    // lp likewise.  A TMEM column of the im2col holds two consecutive taps (a, b), (a, b+1) of one
+    // position, which is then a single 32-bit shared load of each array (no per-tap arithmetic).
+    uint32_t* hp = reinterpret_cast<uint32_t*>(rs);
+    uint32_t* lp = hp + A.rs_floats;
+    auto fill = [&](int item) {
       const ChItem it = ch_item(A, item);
-      float* dst = rs + buf * A.rs_floats;
       const float* rn = A.r + static_cast<size_t>(it.n) * A.H * A.W;
       for (int e = ct; e < A.rs_floats; e += 32 * kChConvWarps) {
         const int rho = e / A.pitch, c = e - rho * A.pitch;
-        const int i = it.u_first - A.P + rho, jj = c - A.P;
-        const bool ok = i >= 0 && i < A.H && jj >= 0 && jj < A.W;
-        cp_async4(su32(dst + e), ok ? rn + static_cast<size_t>(i) * A.W + jj : rn, ok);
+        const int i = it.u0 - P + rho, jj = c - P;
+        const bool iok = i >= 0 && i < A.H;
+        const float* rr = rn + static_cast<size_t>(iok ? i : 0) * A.W;
+        const float x0 = (iok && jj >= 0 && jj < A.W) ? __ldg(rr + jj) * sr : 0.f;
+        const float x1 = (iok && jj + 1 >= 0 && jj + 1 < A.W) ? __ldg(rr + jj + 1) * sr : 0.f;
+        const float h0 = rn11_h(x0), h1 = rn11_h(x1);
+        hp[e] = pack_h2_h(h0, h1);
+        lp[e] = pack_h2_h(x0 - h0, x1 - h1);
       }
-      cp_async_commit();
     };
-    auto body = [&](auto hc) {
-      constexpr int H = decltype(hc)::value;
+    {
       uint32_t g = 0;
-      int ibuf = 0;
-      if (gi < A.nitems) stage_r(gi, 0);
-      for (int item = gi; item < A.nitems; item += A.G, ibuf ^= 1) {
+      for (int item = gi; item < A.nitems; item += A.G) {
         const ChItem it = ch_item(A, item);
-        if (item + A.G < A.nitems) stage_r(item + A.G, ibuf ^ 1);
-        else cp_async_commit();
-        cp_async_wait<1>();
-        named_sync(1, 32 * kChConvWarps);
-        const float* rtile = rs + ibuf * A.rs_floats;
+        RT_WAIT(rc, 2, named_sync(1, 32 * kChConvWarps));  // every converter is done with the last band
+        fill(item);
+        RT_WAIT(rc, 0, named_sync(1, 32 * kChConvWarps));
         for (int tl = 0; tl < it.ntiles; ++tl) {
           const int p = it.p0 + tl * kChTile + 32 * q + lane;
           const bool pok = p < it.p1;
           const int u = p / A.Wc, v = p - u * A.Wc;
-          const float* src = rtile + (pok ? (u - it.u_first) * A.pitch + v : 0);
+          const int o = pok ? (u - it.u0) * A.pitch + v : 0;
+          const uint32_t* sh = hp + o;
+          const uint32_t* sl = lp + o;
 #pragma unroll
           for (int j = 0; j < 2; ++j, ++g) {  // slot j: taps 64 j .. 64 j + 63
             const uint32_t slot = g % kChNS, ph = (g / kChNS) & 1u;
-            mbar_wait_sleep(&a_empty[slot], ph ^ 1u);
+            RT_WAIT(rc, 1, mbar_wait_backoff(&a_empty[slot], ph ^ 1u, 512));
             tc_after();
 #pragma unroll
-            for (int ee = 0; ee < 2; ++ee) {
-              const int e = 2 * H + ee;  // K16-step within the slot
+            for (int e = 0; e < 4; ++e) {  // K16-step within the slot
               uint32_t hv[8], lv[8];
 #pragma unroll
               for (int jj = 0; jj < 8; ++jj) {
                 const int t0 = 64 * j + 16 * e + 2 * jj, t1 = t0 + 1;
-                const float x0 = (t0 < S2 && pok) ? src[(t0 / S) * A.pitch + (t0 % S)] * sr : 0.f;
-                const float x1 = (t1 < S2 && pok) ? src[(t1 / S) * A.pitch + (t1 % S)] * sr : 0.f;
-                const float h0 = rn11_h(x0), h1 = rn11_h(x1);
-                hv[jj] = pack_h2_h(h0, h1);
-                lv[jj] = pack_h2_h(x0 - h0, x1 - h1);
+                const int a0 = t0 / S, b0 = t0 % S, a1 = t1 / S, b1 = t1 % S;
+                uint32_t xh = 0u, xl = 0u;
+                if (t0 < S2) {
+                  const int o0 = a0 * A.pitch + b0;
+                  if (t1 < S2 && a1 == a0) {  // both taps in one row: the stored pair
+                    xh = sh[o0];
+                    xl = sl[o0];
+                  } else {                     // the pair straddles two tap rows (or ends the taps)
+                    const uint32_t h0 = sh[o0], l0 = sl[o0];
+                    if (t1 < S2) {
+                      const int o1 = a1 * A.pitch + b1;
+                      xh = __byte_perm(h0, sh[o1], 0x5410);
+                      xl = __byte_perm(l0, sl[o1], 0x5410);
+                    } else {
+                      xh = h0 & 0xFFFFu;
+                      xl = l0 & 0xFFFFu;
+                    }
+                  }
+                }
+                hv[jj] = pok ? xh : 0u;
+                lv[jj] = pok ? xl : 0u;
               }
               const uint32_t col = t_a + slot * 64u + 8u * e;
               tmem_st8(tq + col, hv);
@@ -276,116 +474,254 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
             if (lane == 0) mbar_arrive(&a_full[slot]);
           }
         }
-        named_sync(1, 32 * kChConvWarps);
       }
-    };
-    if (h == 0) body(std::integral_constant<int, 0>{});
-    else body(std::integral_constant<int, 1>{});
-    cp_async_wait<0>();
-  } else {
-    // ================================ epilogue: z <- S(z - tau c) on masked codes
+    }
+    if (cw == 0 && lane == 0) RT_DUMP(rc, A.dbg, 1);
+  } else if (warp < kChColBase) {
+    // ================================ epilogue: z <- S(z - tau c) on masked codes, dz -> TMEM
     const int ew = warp - kChEpiBase;  // 0..15
     const int q = warp & 3;
-    const int cb = ew >> 2;            // filter block of NC
+    const int jq = ew >> 2;            // 0..kChEpiPerQ-1: group rotation slot
     const uint32_t tq = (static_cast<uint32_t>(32 * q) << 16);
-    const bool plain = A.plain != 0;
     const float tau = plain ? 0.f : *A.tau;
     const float kappa = tau * A.lam;
     const float inv = exp2i_h(-(er + ed));
+    const float ntinv = -tau * inv;
+    const float sdz = exp2i_h(edz);
     const size_t plane = static_cast<size_t>(A.Hc) * A.Wc;
-    const int k0 = kg * A.KC + cb * NC;
-    const int kend = min(kg * A.KC + A.KC, A.K);
-    float* zs0 = zsm + ew * NC * 32;                 // buffer b at zs0 + b * kChEpiWarps * NC * 32
-    const uint32_t zbytes = static_cast<uint32_t>(NC) * 128u;
-    // the sequence of (item, tile) this warp consumes, advanced by one per step
-    auto advance = [&](int& item, int& tl) {
-      const ChItem it = ch_item(A, item);
-      if (++tl >= it.ntiles) {
-        tl = 0;
-        item += A.G;
+    const int kbase = kg * A.KC;
+    const int kend = min(kbase + A.KC, A.K);
+    const bool masked = A.mask != nullptr;
+    float* zs0 = zsm + ew * kZBuf;     // [chunks][16 filters][32 positions]
+    uint32_t* ws0 = wsm + ew * kWBuf;  // [chunks][32 positions] selection words
+    // bits of the filters of group k0 .. k0+15 that exist (the rest of the group is padding)
+    auto kvalid = [&](int k0) -> uint32_t {
+      const int nv = kend - k0;
+      return nv >= 16 ? 0xFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+    };
+    // tile cursors: the current tile and the next (its slices are loaded one tile ahead)
+    int item = gi, tl = 0;
+    ChItem it = ch_item(A, item < A.nitems ? item : 0);
+    int ni = item, ntl = 0;
+    ChItem nit = it;
+    auto step = [&](int& itm, int& t, ChItem& c) {
+      if (++t >= c.ntiles) {
+        t = 0;
+        itm += A.G;
+        if (itm < A.nitems) c = ch_item(A, itm);
       }
     };
-    auto issue = [&](int item, int tl, int b) {  // TMA {32 positions, NC planes} of tile (item, tl)
-      if (plain || item >= A.nitems || lane != 0) return;
-      const ChItem it = ch_item(A, item);
-      const int pw = it.p0 + tl * kChTile + 32 * q;
-      mbar_arrive_expect_tx(&z_full[ew][b], zbytes);
-      tma_load_2d(su32(zs0 + b * kChEpiWarps * NC * 32), &tmap_z, pw, it.n * A.K + k0, &z_full[ew][b]);
+    // TMA of chunk s (group (jq + tc) mod E + E s, E = epilogue warps per quarter) of tile (itm, t): the {32 positions, 16 filters}
+    // code slice and the 32 selection words; an empty arrival when the group does not exist
+    auto issue = [&](int itm, int t, const ChItem& c, uint32_t tc, int s) {
+      if (plain || itm >= A.nitems) return;
+      const int g = static_cast<int>((jq + tc) % kChEpiPerQ) + kChEpiPerQ * s;
+      if (lane == 0) {
+        if (g < A.ngroups) {
+          const int pw = c.p0 + t * kChTile + 32 * q;
+          mbar_arrive_expect_tx(&zfull[ew][s], 2048u + (masked ? 128u : 0u));
+          tma_load_2d(su32(zs0 + s * 512), &A.tm_z, pw, c.n * A.K + kbase + 16 * g, &zfull[ew][s]);
+          if (masked) tma_load_2d(su32(ws0 + s * 32), &A.tm_w, pw, kg * A.ngroups + g, &zfull[ew][s]);
+        } else {
+          mbar_arrive(&zfull[ew][s]);
+        }
+      }
     };
     float wmax = 0.f;
-    int item = gi, tl = 0;
-    int pi = gi, ptl = 0;  // prefetch cursor: two tiles ahead
-    issue(pi, ptl, 0);
-    if (pi < A.nitems) advance(pi, ptl);
-    issue(pi, ptl, 1);
-    if (pi < A.nitems) advance(pi, ptl);
+    RoleClock rc;
     uint32_t tcount = 0;
+    for (int s0 = 0; s0 < kChChunks; ++s0) issue(item, tl, it, 0u, s0);
+    if (ni < A.nitems) step(ni, ntl, nit);
     while (item < A.nitems) {
-      const ChItem it = ch_item(A, item);
       const uint32_t buf = tcount & 1u, use = tcount >> 1;
-      const int pw = it.p0 + tl * kChTile + 32 * q;
-      const int p = pw + lane;
+      const int p = it.p0 + tl * kChTile + 32 * q + lane;
       const bool pok = p < it.p1;
-      const int nvk = kend - k0;  // filters of this warp's block that exist (the rest is padding)
-      const uint32_t kbits = nvk >= 32 ? 0xffffffffu : (nvk <= 0 ? 0u : ((1u << nvk) - 1u));
-      const uint32_t sel = kbits & (A.mask == nullptr ? (pok ? 0xffffffffu : 0u)
-                                                      : (pok ? __ldg(A.mask + static_cast<size_t>(kg * 4 + cb) * plane + p) : 0u));
-      float* zb = A.z + (static_cast<size_t>(it.n) * A.K + k0) * plane + p;
-      const float* zs = zs0 + buf * kChEpiWarps * NC * 32;
-      if (!plain) mbar_wait_sleep(&z_full[ew][buf], use & 1u);
-      mbar_wait_sleep(&acc_full[buf], use & 1u);
+      const int ga = static_cast<int>((jq + tcount) % kChEpiPerQ);
+      RT_WAIT(rc, 0, mbar_wait_backoff(&acc_full[buf], use & 1u, 64));
       tc_after();
-      const uint32_t colb = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
-      // per-filter step sizes (ESO rule) in a separate instantiation of the loop, so the
-      // scalar-tau hot path carries no extra loads
-      const float ntinv = -tau * inv;
-      auto epi = [&](auto per_k) {
-        constexpr bool PK = decltype(per_k)::value;
-#pragma unroll
-        for (int j4 = 0; j4 < NC / 4; ++j4) {
-          float c4[4];
-          tmem_ld4_nowait(tq + colb + 4u * j4, c4);
-          tmem_ld_wait();
-          if (plain) {
-#pragma unroll
-            for (int i4 = 0; i4 < 4; ++i4) {
-              const int i = 4 * j4 + i4;
-              if (pok && (k0 + i) < kend) zb[static_cast<size_t>(i) * plane] = c4[i4] * inv;
-            }
-            continue;
+      const uint32_t colb = t_acc + buf * static_cast<uint32_t>(A.Npad);
+      float* zrow = A.z + (static_cast<size_t>(it.n) * A.K + kbase) * plane + p;
+#pragma unroll 1
+      for (int s = 0; s < kChChunks; ++s) {
+        const int gg = ga + kChEpiPerQ * s;
+        if (gg >= A.ngroups) {
+          if (!plain) {
+            RT_WAIT(rc, 1, mbar_wait_backoff(&zfull[ew][s], tcount & 1u, 32));
+            __syncwarp();
+            issue(ni, ntl, nit, tcount + 1, s);
           }
-#pragma unroll
-          for (int i4 = 0; i4 < 4; ++i4) {
-            const int i = 4 * j4 + i4;
-            const float zv = zs[i * 32 + lane];
-            const float tk = PK ? __ldg(A.tau + min(k0 + i, A.K - 1)) : tau;
-            const float kk = PK ? tk * A.lam : kappa;
-            // -tau * (c * 2^-(er+ed)) with one multiply: scaling by a power of two is exact
-            const float w = fmaf(PK ? -tk * inv : ntinv, c4[i4], zv);
-            const float nz = w - fminf(fmaxf(w, -kk), kk);  // S_kk(w): w -/+ kk outside [-kk, kk], +0 inside
-            if (((sel >> i) & 1u) && nz != zv) {
-              zb[static_cast<size_t>(i) * plane] = nz;
-              wmax = fmaxf(wmax, fabsf(nz));
-            }
-          }
+          continue;
         }
-      };
-      if (A.tau_stride) epi(std::true_type{});
-      else epi(std::false_type{});
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
-      fence_async_shared();  // generic reads of the slice before the async-proxy refill
-      __syncwarp();
-      issue(pi, ptl, static_cast<int>(buf));
-      if (pi < A.nitems) advance(pi, ptl);
-      advance(item, tl);
+        const int k0 = kbase + 16 * gg;
+        const uint32_t kv = kvalid(k0);
+        float c[16];
+        {
+          float c8[8];
+          tmem_ld8_nowait(tq + colb + 16u * gg, c8);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) c[i] = c8[i];
+          tmem_ld8_nowait(tq + colb + 16u * gg + 8u, c8);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) c[8 + i] = c8[i];
+        }
+        float* zb = zrow + static_cast<size_t>(16 * gg) * plane;
+        if (plain) {
+          const uint32_t pv = pok ? kv : 0u;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) st_global_if(zb + static_cast<size_t>(i) * plane, c[i] * inv, (pv >> i) & 1u);
+          continue;
+        }
+        RT_WAIT(rc, 1, mbar_wait_backoff(&zfull[ew][s], tcount & 1u, 32));
+        const uint32_t wb = (masked ? ws0[s * 32 + lane] : 0xFFFFu) & (pok ? kv : 0u);
+        float zc[16];
+        const float* zr = zs0 + s * 512 + lane;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) zc[i] = zr[32 * i];
+        fence_async_shared();  // generic reads of the slice before the async-proxy refill
+        __syncwarp();
+        issue(ni, ntl, nit, tcount + 1, s);  // refill the chunk with the next tile's slice
+        uint32_t hv[8], lv[8];
+        auto body = [&](auto per_k) {
+          constexpr bool PK = decltype(per_k)::value;
+          float* zp = zb;
+#pragma unroll
+          for (int i2 = 0; i2 < 8; ++i2) {
+            float dzp[2];
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int i = 2 * i2 + h2;
+              const float tk = PK ? __ldg(A.tau + min(k0 + i, A.K - 1)) : tau;
+              const float kk = PK ? tk * A.lam : kappa;
+              // -tau * (c * 2^-(er+ed)) with one multiply: scaling by a power of two is exact
+              const float w = fmaf(PK ? -tk * inv : ntinv, c[i], zc[i]);
+              const float nz = w - fminf(fmaxf(w, -kk), kk);  // S_kk(w): w -/+ kk outside [-kk, kk], +0 inside
+              const bool ch = (wb & (1u << i)) != 0u && nz != zc[i];
+              if (ch) *zp = nz;
+              zp += plane;
+              // max |z| bound: every code of the slice was loaded, so |S(z - tau c)| over all of them bounds
+              // the changed codes and the unchanged ones keep the previous bound
+              wmax = fmaxf(wmax, fabsf(nz));
+              dzp[h2] = ch ? (nz - zc[i]) * sdz : 0.f;
+            }
+            const float h0 = rn11_h(dzp[0]), h1 = rn11_h(dzp[1]);
+            hv[i2] = pack_h2_h(h0, h1);
+            lv[i2] = pack_h2_h(dzp[0] - h0, dzp[1] - h1);
+          }
+        };
+        if (A.tau_stride) body(std::true_type{});
+        else body(std::false_type{});
+        if (a3p) {
+          tmem_st8(tq + colb + 16u * gg, hv);
+          tmem_st8(tq + colb + 16u * gg + 8u, lv);
+        }
+      }
+      if (a3p) {
+        tmem_st_wait();
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dz_full[buf]);
+      } else {
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      }
+      step(item, tl, it);
+      if (ni < A.nitems) step(ni, ntl, nit);
       ++tcount;
     }
-    uint32_t wb = __float_as_uint(wmax);
+    if (ew == 0 && lane == 0) RT_DUMP(rc, A.dbg, 2);
+    uint32_t wbm = __float_as_uint(wmax);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wb = max(wb, __shfl_xor_sync(kFullMask, wb, o));
-    if (lane == 0 && A.zmax != nullptr && wb != 0u) atomicMax(A.zmax, wb);
+    for (int o = 16; o > 0; o >>= 1) wbm = max(wbm, __shfl_xor_sync(kFullMask, wbm, o));
+    if (lane == 0 && A.zmax != nullptr && wbm != 0u) atomicMax(A.zmax, wbm);
+  } else if (a3p) {
+    // ================================ col2im of Y = D dz into the band window (a3')
+    const int q = warp & 3;
+    const int half = (warp - kChColBase) >> 2;  // tap rows [a0, a1) of this warp
+    constexpr int AH = (S + 1) / 2;
+    const int a0 = half * AH, a1 = half ? S : AH;
+    const float inv2 = exp2i_h(-(edz + ed));
+    // add phases: the quarters in order (and the two row halves of a quarter in order when their windows
+    // can overlap, Wc < 32 + P): deterministic fp32 sums
+    const bool split = A.Wc < 32 + P;
+    const int nph = split ? 8 : 4;
+    const int myph = split ? 2 * q + half : q;
+    uint32_t tcount = 0;
+    const int et = tid - 32 * kChColBase;
+    RoleClock rc;
+    for (int item = gi; item < A.nitems; item += A.G) {
+      const ChItem it = ch_item(A, item);
+      for (int t = 0; t < it.ntiles; ++t, ++tcount) {
+        RT_WAIT(rc, 0, mbar_wait_backoff(&y_full, tcount & 1u, 256));
+        tc_after();
+        const int pq = 128 * t + 32 * q;
+        const bool pvalid = it.p0 + pq + lane < it.p1;
+        const uint32_t tacc = t_y + (static_cast<uint32_t>(32 * q) << 16);
+        float* rowb = win + pq + lane;
+        float own[AH], dnv[AH];
+        auto rows = [&](auto partial) {
+          constexpr bool PART = decltype(partial)::value;
+#pragma unroll
+          for (int i = 0; i < AH; ++i) {
+            own[i] = 0.f;
+            dnv[i] = 0.f;
+            const int a = a0 + i;
+            if (a >= a1) continue;
+            float y[S];
+            tmem_ld_row<S>(tacc + a * S, y);
+            tmem_ld_wait();
+            float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
+#pragma unroll
+            for (int b = 0; b < S; ++b) {
+              // one rotation serves both parts: lanes >= b get position lane-b of this quarter, lanes < b
+              // get position lane-b+32, the halo that belongs to the next quarter's first lanes
+              const float yv = PART ? (pvalid ? y[b] : 0.f) : y[b];
+              const float rot = b == 0 ? yv : __shfl_sync(kFullMask, yv, (lane - b) & 31);
+              if (lane >= b) {
+                if (b & 1) u1s += rot; else u0s += rot;
+              } else {
+                if (b & 1) d1s += rot; else d0s += rot;
+              }
+            }
+            own[i] = u0s + u1s;
+            dnv[i] = d0s + d1s;
+          }
+        };
+        if (__all_sync(kFullMask, pvalid)) rows(std::false_type{});
+        else rows(std::true_type{});
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&y_empty);
+#pragma unroll 1
+        for (int ph = 0; ph < nph; ++ph) {
+          if (ph == myph) {
+#pragma unroll
+            for (int i = 0; i < AH; ++i)
+              if (a0 + i < a1) rowb[(a0 + i) * A.Wc] += own[i];
+            __syncwarp();
+            if (lane < P) {
+#pragma unroll
+              for (int i = 0; i < AH; ++i)
+                if (a0 + i < a1) rowb[(a0 + i) * A.Wc + 32] += dnv[i];
+            }
+          }
+          RT_WAIT(rc, 1, named_sync(2, 32 * kChColWarps));
+        }
+      }
+      // flush the band window: output rows u0-P .. u0+BR-1 (window row r = output row u0-P+r)
+      float* dst = A.part + ((static_cast<size_t>(kg) * A.N + it.n) * A.nbands + it.band) *
+                                static_cast<size_t>(A.BR + P) * A.W;
+      const int nrows = A.BR + P;
+      for (int e = et; e < nrows * A.W; e += 32 * kChColWarps) {
+        const int r = e / A.W, j = e - r * A.W;
+        dst[e] = win[r * A.Wc + j + P] * inv2;  // exact: power of two
+      }
+      named_sync(2, 32 * kChColWarps);
+      for (int e = et; e < A.WL; e += 32 * kChColWarps) win[e] = 0.f;
+      named_sync(2, 32 * kChColWarps);
+    }
+    if (warp == kChColBase && lane == 0) RT_DUMP(rc, A.dbg, 3);
   }
 
   tc_before();
@@ -394,53 +730,67 @@ code_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const ChArgs A) {
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
-typedef CUresult (*PFN_encodeTiled_ch)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-PFN_encodeTiled_ch encode_fn_ch() {
-  static PFN_encodeTiled_ch fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled_ch>(p);
+// r += sum_kg sum_{bands b covering row i} part[kg][n][b][i - b BR + P][j]  (fixed order)
+__global__ void code_a3_fixup_kernel(const float* __restrict__ part, int nkg, int N, int H, int W, int P, int BR,
+                                     int nbands, float* __restrict__ r) {
+  const size_t win = static_cast<size_t>(BR + P) * W;
+  const size_t kstride = static_cast<size_t>(N) * nbands * win;
+  const int64_t total = static_cast<int64_t>(N) * H * W;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = e / W;
+    const int j = static_cast<int>(e - row * W);
+    const int n = static_cast<int>(row / H), i = static_cast<int>(row - static_cast<int64_t>(n) * H);
+    const int b0 = i / BR;
+    int b1 = (i + P) / BR;
+    if (b1 > nbands - 1) b1 = nbands - 1;
+    float v = 0.f;
+    for (int kg = 0; kg < nkg; ++kg) {
+      const float* pk = part + kg * kstride + static_cast<size_t>(n) * nbands * win;
+      for (int b = b0; b <= b1; ++b) v += pk[b * win + static_cast<size_t>(i - b * BR + P) * W + j];
+    }
+    r[e] += v;
   }
-  return fn;
-}
-
-template <int S, int NC>
-cudaError_t run_code_h(const CUtensorMap& tm, const ChArgs& a, int grid, int smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(code_h_kernel<S, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kChSmemMax);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  code_h_kernel<S, NC><<<grid, kChThreads, smem, st>>>(tm, a);
-  return cudaGetLastError();
 }
 
 template <int S>
-cudaError_t run_code_h_nc(const CUtensorMap& tm, const ChArgs& a, int grid, int smem, cudaStream_t st) {
-  switch (a.Npad / 4) {
-    case 4: return run_code_h<S, 4>(tm, a, grid, smem, st);
-    case 8: return run_code_h<S, 8>(tm, a, grid, smem, st);
-    case 12: return run_code_h<S, 12>(tm, a, grid, smem, st);
-    case 16: return run_code_h<S, 16>(tm, a, grid, smem, st);
-    case 20: return run_code_h<S, 20>(tm, a, grid, smem, st);
-    case 24: return run_code_h<S, 24>(tm, a, grid, smem, st);
-    case 28: return run_code_h<S, 28>(tm, a, grid, smem, st);
-    default: return cudaErrorInvalidValue;
+cudaError_t run_code_h(const ChArgs& a, int grid, int smem, cudaStream_t st) {
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&code_h_kernel<S>), kChSmemMax);
+  if (e != cudaSuccess) return e;
+#ifdef CSC_ROLE_TIMING
+  static unsigned long long* dbg = nullptr;
+  static int calls = 0;
+  if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 32 * 1024);
+  cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 32 * 1024, st);
+  ChArgs b = a;
+  b.dbg = dbg;
+  code_h_kernel<S><<<grid, kChThreads, smem, st>>>(b);
+  if (++calls % 4 == 0) {
+    static unsigned long long h[32 * 1024];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, dbg, sizeof(unsigned long long) * 32 * grid, cudaMemcpyDeviceToHost);
+    double t[32] = {0};
+    for (int bk = 0; bk < grid; ++bk)
+      for (int i = 0; i < 32; ++i) t[i] += static_cast<double>(h[bk * 32 + i]) / grid;
+    fprintf(stderr,
+            "[code_h roles] mma: total %.0f w_accempty %.0f w_afull %.0f w_dzfull %.0f w_yempty %.0f | conv: total %.0f "
+            "w_stage %.0f w_aempty %.0f w_end %.0f | epi: total %.0f w_accfull %.0f w_cpasync %.0f | col: total %.0f "
+            "w_yfull %.0f w_phase %.0f\n",
+            t[7], t[0], t[1], t[2], t[3], t[15], t[8], t[9], t[10], t[23], t[16], t[17], t[31], t[24], t[25]);
   }
+#else
+  code_h_kernel<S><<<grid, kChThreads, smem, st>>>(a);
+#endif
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------- host side
 bool code_h_supported(const Geom& g) {
-  return g.N > 0 && (g.S == 3 || g.S == 5 || g.S == 7 || g.S == 9 || g.S == 11) && g.Wc >= 8 &&
-         (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 && encode_fn_ch() != nullptr;
+  // TMA views of z and of the selection words: rows of Hc*Wc elements must be 16-byte multiples
+  return g.N > 0 && (g.S == 3 || g.S == 5 || g.S == 7 || g.S == 9 || g.S == 11) &&
+         (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 && tmap_available();
 }
 
 CodeTcPlan code_h_plan(const Geom& g, int num_sms) {
@@ -448,64 +798,79 @@ CodeTcPlan code_h_plan(const Geom& g, int num_sms) {
   p.nkg = ceil_div(g.K, 112);
   p.KC = ceil_div(g.K, p.nkg);
   p.Npad = (p.KC + 15) / 16 * 16;
+  p.ngroups = p.Npad / 16;
+  p.wnc = 16;
+  p.wper = p.ngroups;
   p.b_bytes = 2 * p.Npad * 128;
   int pitch = g.Wc + g.P;
   while (pitch % 32 != 0) ++pitch;
   p.pitch = pitch;
   const int plane = g.Hc * g.Wc;
-  p.sw_words = static_cast<size_t>(4 * p.nkg) * plane;
+  p.sw_words = static_cast<size_t>(p.nkg) * p.ngroups * plane;
   const int G = num_sms / p.nkg > 0 ? num_sms / p.nkg : 1;
-  const int64_t total = static_cast<int64_t>(g.N > 0 ? g.N : 1) * plane;
-  int64_t L = total / (8 * static_cast<int64_t>(G));
-  L = (L + kChTile - 1) / kChTile * kChTile;
-  if (L < kChTile) L = kChTile;
-  if (L > 4096) L = 4096;
-  const int zbytes = 2 * kChEpiWarps * (p.Npad / 4) * 32 * 4;
-  const int smem_fixed = 1024 + 2 * p.b_bytes + zbytes;
-  auto rows_for = [&](int64_t len) { return static_cast<int>((len + g.Wc - 1) / g.Wc) + 1 + g.P; };
-  while (L > kChTile && smem_fixed + 2 * rows_for(L) * pitch * 4 > kChSmemMax) L -= kChTile;
-  p.L = static_cast<int>(L);
-  p.rs_rows = rows_for(L);
+  const int n = g.N > 0 ? g.N : 1;
+  const int smem_fixed = 1024 + 2 * p.b_bytes + kChEpiWarps * (kZBuf + kWBuf) * 4;
+  auto smem_for = [&](int br) {
+    const int rs = (br + g.P) * pitch;
+    const int wl = (br + g.P) * g.Wc + 192;
+    return smem_fixed + 2 * rs * 4 + wl * 4;
+  };
+  // band height: the fewest rounds of items over the G CTAs x rows per band (tail balance), largest on ties
+  int best = 0;
+  int64_t best_cost = 0;
+  for (int br = 1; br <= 32 && br <= g.Hc; ++br) {
+    if (smem_for(br) > kChSmemMax) break;
+    if ((br * g.Wc) % 4 != 0) continue;  // every band starts 16-B aligned (TMA box starts)
+    const int nb = ceil_div(g.Hc, br);
+    const int64_t rounds = ceil_div(n * nb, G);
+    const int64_t cost = rounds * (br + 1);  // +1: per-band staging / flush overhead in row units
+    if (best == 0 || cost <= best_cost) {
+      best = br;
+      best_cost = cost;
+    }
+  }
+  if (best == 0) {
+    p.ok = false;
+    return p;
+  }
+  p.BR = best;
+  p.nbands = ceil_div(g.Hc, p.BR);
+  p.rs_rows = p.BR + g.P;
   p.rs_floats = p.rs_rows * pitch;
-  p.nseg = ceil_div(plane, p.L);
-  p.nitems = g.N * p.nseg;
+  p.WL = (p.BR + g.P) * g.Wc + 192;
+  p.nitems = g.N * p.nbands;
   p.G = p.nitems < G ? (p.nitems > 0 ? p.nitems : 1) : G;
   p.grid = p.G * p.nkg;
-  p.smem = smem_fixed + 2 * p.rs_floats * 4;
+  p.smem = smem_for(p.BR);
+  p.a3_floats = static_cast<size_t>(p.nkg) * g.N * p.nbands * (p.BR + g.P) * g.W;
   p.ok = p.smem <= kChSmemMax;
   p.half = true;
   return p;
 }
 
-cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
-                          const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
-                          uint32_t* zmax, cudaStream_t st, bool plain, int tau_stride) {
-  static const float* cached_z = nullptr;
-  static Geom cached_g{};
-  static int cached_nc = 0;
-  static CUtensorMap tm;
-  const int NC = p.Npad / 4;
-  if (z != cached_z || std::memcmp(&cached_g, &g, sizeof(Geom)) != 0 || cached_nc != NC) {
-    PFN_encodeTiled_ch enc = encode_fn_ch();
-    if (!enc) return cudaErrorNotSupported;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Hc) * g.Wc, static_cast<cuuint64_t>(g.N) * g.K};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Hc) * g.Wc * 4};
-    const cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(NC)};
-    const cuuint32_t estr[2] = {1u, 1u};
-    CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, z, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return cudaErrorInvalidPitchValue;
-    cached_z = z;
-    cached_g = g;
-    cached_nc = NC;
-  }
+cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, TmapCache* tmc, const float* r, const float* d,
+                          float* z, const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
+                          uint32_t* zmax, cudaStream_t st, bool plain, int tau_stride, float* a3_part) {
   ChArgs a{};
+  if (!plain) {
+    const uint64_t plane = static_cast<uint64_t>(g.Hc) * g.Wc;
+    cudaError_t e = tmap_2d(tmc[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, z, plane, static_cast<uint64_t>(g.N) * g.K,
+                            plane * 4, 32, 16, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+    if (e != cudaSuccess) return e;
+    a.tm_z = tmc[0].map;
+    if (words != nullptr) {
+      e = tmap_2d(tmc[1], CU_TENSOR_MAP_DATA_TYPE_UINT32, words, plane, static_cast<uint64_t>(p.nkg) * p.ngroups,
+                  plane * 4, 32, 1, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+      if (e != cudaSuccess) return e;
+      a.tm_w = tmc[1].map;
+    }
+  }
   a.r = r; a.d = d; a.z = z; a.mask = words; a.tau = tau_dev; a.lam = lam; a.rmax = rmax; a.zmax = zmax;
+  a.part = plain ? nullptr : a3_part;
   a.N = g.N; a.K = g.K; a.S = g.S; a.H = g.H; a.W = g.W; a.Hc = g.Hc; a.Wc = g.Wc; a.P = g.P;
-  a.KC = p.KC; a.Npad = p.Npad; a.nkg = p.nkg; a.G = p.G;
-  a.L = p.L; a.nseg = p.nseg; a.nitems = p.nitems;
-  a.pitch = p.pitch; a.rs_rows = p.rs_rows; a.rs_floats = p.rs_floats; a.b_bytes = p.b_bytes;
+  a.KC = p.KC; a.Npad = p.Npad; a.nkg = p.nkg; a.G = p.G; a.ngroups = p.ngroups;
+  a.BR = p.BR; a.nbands = p.nbands; a.nitems = p.nitems; a.WL = p.WL;
+  a.pitch = p.pitch; a.rs_floats = p.rs_floats; a.b_bytes = p.b_bytes;
   a.plain = plain ? 1 : 0;
   a.tau_stride = tau_stride;
   if (plain) {
@@ -513,13 +878,19 @@ cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, co
     a.zmax = nullptr;
   }
   switch (g.S) {
-    case 3: return run_code_h_nc<3>(tm, a, p.grid, p.smem, st);
-    case 5: return run_code_h_nc<5>(tm, a, p.grid, p.smem, st);
-    case 7: return run_code_h_nc<7>(tm, a, p.grid, p.smem, st);
-    case 9: return run_code_h_nc<9>(tm, a, p.grid, p.smem, st);
-    case 11: return run_code_h_nc<11>(tm, a, p.grid, p.smem, st);
+    case 3: return run_code_h<3>(a, p.grid, p.smem, st);
+    case 5: return run_code_h<5>(a, p.grid, p.smem, st);
+    case 7: return run_code_h<7>(a, p.grid, p.smem, st);
+    case 9: return run_code_h<9>(a, p.grid, p.smem, st);
+    case 11: return run_code_h<11>(a, p.grid, p.smem, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_code_a3_fixup(const Geom& g, const CodeTcPlan& p, const float* part, float* r, cudaStream_t st) {
+  if (g.N == 0) return cudaSuccess;
+  code_a3_fixup_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, p.nkg, g.N, g.H, g.W, g.P, p.BR, p.nbands, r);
+  return cudaGetLastError();
 }
 
 }  // namespace csc

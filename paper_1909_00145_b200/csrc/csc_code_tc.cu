@@ -330,14 +330,14 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 __device__ __forceinline__ uint32_t word_of(const uint4& b, int i) {
   return i == 0 ? b.x : (i == 1 ? b.y : (i == 2 ? b.z : b.w));
 }
-__global__ void mask_selwords_kernel(int K, int KC, int NC, int nblk, int64_t plane, uint64_t seed, uint32_t iter,
-                                     uint64_t thr, int mode, uint32_t* __restrict__ sw) {
+__global__ void mask_selwords_kernel(int K, int KC, int NC, int nper, int nblk, int64_t plane, uint64_t seed,
+                                     uint32_t iter, uint64_t thr, int mode, uint32_t* __restrict__ sw) {
   const int64_t nq = (plane + 3) / 4;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= static_cast<int64_t>(nblk) * nq) return;
   const int blk = static_cast<int>(tid / nq);
   const int64_t p0 = (tid - static_cast<int64_t>(blk) * nq) * 4;
-  const int kg = blk >> 2, cb = blk & 3;
+  const int kg = blk / nper, cb = blk - kg * nper;
   const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
   uint32_t out[4] = {0u, 0u, 0u, 0u};
   for (int i = 0; i < NC; ++i) {
@@ -422,6 +422,8 @@ CodeTcPlan code_tc_plan(const Geom& g, int num_sms) {
   p.pitch = pitch;
   const int plane = g.Hc * g.Wc;
   p.sw_words = static_cast<size_t>(4 * p.nkg) * plane;
+  p.wnc = p.Npad / 4;
+  p.wper = 4;
   const int G = num_sms / p.nkg > 0 ? num_sms / p.nkg : 1;
   const int64_t total = static_cast<int64_t>(g.N > 0 ? g.N : 1) * plane;
   int64_t L = total / (8 * static_cast<int64_t>(G));
@@ -446,10 +448,10 @@ CodeTcPlan code_tc_plan(const Geom& g, int num_sms) {
 cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
                                  uint32_t* words, cudaStream_t st, int mode) {
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
-  const int nblk = 4 * p.nkg;
+  const int nblk = p.wper * p.nkg;
   const int64_t total = static_cast<int64_t>(nblk) * ((plane + 3) / 4);
-  mask_selwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g.K, p.KC, p.Npad / 4, nblk, plane,
-                                                                                 seed, iter, thr, mode, words);
+  mask_selwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g.K, p.KC, p.wnc, p.wper, nblk,
+                                                                                 plane, seed, iter, thr, mode, words);
   return cudaGetLastError();
 }
 

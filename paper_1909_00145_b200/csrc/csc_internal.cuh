@@ -2,9 +2,29 @@
 // and the sm_100a kernels (csc_kernels.cu).  Not part of the public ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace csc {
+
+// A 2D TMA tensor map cached with the pointer / shape it encodes.  Owned by a context (csc_ctx), so
+// contexts on different devices or threads never share one (include/csc.h: one context per
+// (rank, device, stream)).
+struct TmapCache {
+  const void* ptr = nullptr;
+  uint64_t key[4] = {0, 0, 0, 0};
+  bool valid = false;
+  alignas(64) CUtensorMap map;
+};
+// Encode (or reuse) a 2D tiled map: dims {d0 (contiguous), d1}, row stride stride1 bytes, box {b0, b1};
+// no interleave, zero fill out of bounds.  cudaErrorNotSupported when the driver entry point is absent,
+// cudaErrorInvalidValue when the shape / alignment is not encodable.
+cudaError_t tmap_2d(TmapCache& c, CUtensorMapDataType dt, const void* ptr, uint64_t d0, uint64_t d1, uint64_t stride1,
+                    uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw, CUtensorMapL2promotion promo);
+bool tmap_available();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (function, device): the attribute is a
+// per-device setting, so a process-wide flag would leave a second device unconfigured.
+cudaError_t set_smem_attr_once(const void* func, int bytes);
 
 struct Geom {
   int N, K, S, H, W, Hc, Wc, P;
@@ -154,23 +174,31 @@ cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, const float* z, co
 // ---- tensor-core (tcgen05, 3xTF32) dense-then-mask code step, csc_code_tc.cu
 struct CodeTcPlan {
   int KC, Npad, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, b_bytes;
-  size_t sw_words;  // selection-word mask size (4 * nkg * Hc * Wc words)
+  size_t sw_words;  // selection-word mask size (wper * nkg * Hc * Wc words)
+  int wnc, wper;    // selection words: wnc filters per word, wper word blocks per filter group
   int grid, smem;
   bool ok;
   bool half;        // true: the fp16-split kernel (csc_code_h.cu)
+  // csc_code_h.cu: items are bands of BR code rows; ngroups 16-filter groups per filter group;
+  // a3' band partials [nkg][N][nbands][BR+P][W] (a3_floats)
+  int ngroups, BR, nbands, WL;
+  size_t a3_floats;
 };
 bool code_tc_supported(const Geom& g);
 CodeTcPlan code_tc_plan(const Geom& g, int num_sms);
-// Mask as selection words sw[4*nkg][Hc*Wc]: bit i of sw[kg*4+cb][p] = mask(kg*KC + cb*(Npad/4) + i, p).
+// Mask as selection words sw[wper*nkg][Hc*Wc]: bit i of sw[kg*wper+cb][p] = mask(kg*KC + cb*wnc + i, p).
 cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
                                  uint32_t* words, cudaStream_t st, int mode = 0);
 // fp16-split variant (csc_code_h.cu): Hc*Wc % 4 == 0 (TMA view of z); rmax = max|r| (float bits).
 bool code_h_supported(const Geom& g);
 CodeTcPlan code_h_plan(const Geom& g, int num_sms);
-cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
-                          const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
+// a3_part != nullptr (and !plain): the incremental residual r' = r + D dz is written as band partials
+// [nkg][N][nbands][BR+P][W]; launch_code_a3_fixup then adds them to r (a3').
+cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, TmapCache* tmc, const float* r, const float* d,
+                          float* z, const uint32_t* words, const float* tau_dev, float lam, const uint32_t* rmax,
                           uint32_t* zmax, cudaStream_t st,
-                          bool plain = false, int tau_stride = 0);
+                          bool plain = false, int tau_stride = 0, float* a3_part = nullptr);
+cudaError_t launch_code_a3_fixup(const Geom& g, const CodeTcPlan& p, const float* part, float* r, cudaStream_t st);
 // words == nullptr: every code selected (p = 1).
 cudaError_t launch_code_tc(const Geom& g, const CodeTcPlan& p, const float* r, const float* d, float* z,
                            const uint32_t* words, const float* tau_dev, float lam, uint32_t* zmax, cudaStream_t st,

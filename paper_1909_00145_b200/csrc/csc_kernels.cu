@@ -13,6 +13,10 @@
 // Everything is FP32 state with FP64 cross-thread/cross-block sums in a fixed
 // order (deterministic run to run).  This file shares no code with oracle/.
 #include "csc_internal.cuh"
+#include <cstring>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -925,6 +929,68 @@ cudaError_t launch_resid_shift(const float* x, float* r, int64_t n, float sign, 
 cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st) {
   neg_copy_kernel<<<kFinalizeBlocks, 256, 0, st>>>(x, r, n);
   return cudaGetLastError();
+}
+
+}  // namespace csc
+
+// ---------------------------------------------------------------- TMA maps and launch attributes
+namespace csc {
+namespace {
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled_t encode_tiled() {
+  static std::once_flag once;
+  static PFN_encodeTiled_t fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  });
+  return fn;
+}
+std::mutex g_attr_mu;
+}  // namespace
+
+bool tmap_available() { return encode_tiled() != nullptr; }
+
+cudaError_t tmap_2d(TmapCache& c, CUtensorMapDataType dt, const void* ptr, uint64_t d0, uint64_t d1, uint64_t stride1,
+                    uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw, CUtensorMapL2promotion promo) {
+  const uint64_t key[4] = {d0, d1, stride1,
+                           (static_cast<uint64_t>(b0) << 32) | (static_cast<uint64_t>(b1) << 8) |
+                               (static_cast<uint64_t>(sw) << 4) | static_cast<uint64_t>(dt)};
+  if (c.valid && c.ptr == ptr && std::memcmp(c.key, key, sizeof(key)) == 0) return cudaSuccess;
+  PFN_encodeTiled_t enc = encode_tiled();
+  if (!enc) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {d0, d1};
+  const cuuint64_t strides[1] = {stride1};
+  const cuuint32_t box[2] = {b0, b1};
+  const cuuint32_t estr[2] = {1u, 1u};
+  CUresult cr = enc(&c.map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                    promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    c.valid = false;
+    return cudaErrorInvalidValue;
+  }
+  c.ptr = ptr;
+  std::memcpy(c.key, key, sizeof(key));
+  c.valid = true;
+  return cudaSuccess;
+}
+
+cudaError_t set_smem_attr_once(const void* func, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::vector<std::pair<const void*, int>> done;  // (function, device) pairs configured
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  for (const auto& d : done)
+    if (d.first == func && d.second == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(func, dev);
+  return e;
 }
 
 }  // namespace csc
