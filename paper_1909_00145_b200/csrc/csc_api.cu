@@ -117,6 +117,9 @@ struct csc_ctx {
   float* a3_part = nullptr;    // a3' band partials of the fp16-split code step [nkg][N][nbands][BR+P][W]
   csc::TmapCache tm_code[2];   // code step: z, selection words
   csc::TmapCache tm_adm[2];    // ADMM's D^T e pass through the code-step kernel (plain mode)
+  csc::TmapCache tm_conv;      // dense pass: z
+  csc::TmapCache tm_conv_adm;  // dense pass over the ADMM expansion buffer
+  csc::TmapCache tm_wgrad;     // filter gradient: z
   uint32_t* rmax = nullptr;    // max|r| (float bits) for the fp16-split code step
   int step_rule = CSC_STEP_LIPSCHITZ;  // built-in tau_z rule (csc_set_step_rule)
   // projected block-coordinate filter update scratch (csc_bcd.cu), allocated on first use
@@ -236,7 +239,7 @@ csc_status allreduce_d(csc_ctx* c, double* buf, size_t count) {
 
 // Tensor-core dense pass y = sum_k f_k * z_k into the band partials (TMA-fed SS kernel when the
 // plan says so, else the TMEM-fed kernel).
-cudaError_t conv_tc_any(csc_ctx* c, const float* z, const float* filt, double* l1p) {
+cudaError_t conv_tc_any(csc_ctx* c, const float* z, const float* filt, double* l1p, bool precise = false) {
   if (c->tc.half) {
     // the fp16 split needs a bound of max|z|: exact after csc_zero_codes or an absmax pass, then
     // raised by every code step (T6)
@@ -247,7 +250,8 @@ cudaError_t conv_tc_any(csc_ctx* c, const float* z, const float* filt, double* l
       c->zmax_known = true;
       c->zmax_ptr = z;
     }
-    return csc::launch_conv_h(c->g, c->tc, z, filt, c->tc_bimg, c->smax, c->smax + 1, c->tc_part, l1p, c->st);
+    return csc::launch_conv_h(c->g, c->tc, &c->tm_conv, z, filt, c->tc_bimg, c->smax, c->smax + 1, c->tc_part, l1p,
+                              c->st, true, precise);
   }
   if (c->tc.ss) {
     cudaError_t e = csc::launch_tc_bimg(c->g, c->tc, filt, c->tc_bimg, c->st);
@@ -887,8 +891,8 @@ csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float*
   auto apply = [&]() -> csc_status {
     if (c->tc_on && c->tc.half) {
       CSC_LAUNCH_C(c, CSC_K_CONV, (first_conv ? 1 : 0) + c->tc.nks,
-                   csc::launch_conv_h(g, c->tc, c->adm_zd, d, c->tc_bimg, c->adm_bound, c->smax + 1, c->tc_part,
-                                      nullptr, c->st, first_conv));
+                   csc::launch_conv_h(g, c->tc, &c->tm_conv_adm, c->adm_zd, d, c->tc_bimg, c->adm_bound, c->smax + 1,
+                                      c->tc_part, nullptr, c->st, first_conv));
       CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
                    csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, E, csc::kConvResidual, c->sq_part, c->st));
       first_conv = false;
@@ -1148,7 +1152,7 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
   CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->st));
   if (step_d == 0.f) {
     if (g.N > 0 && c->tc_on) {
-      CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, z, c->g32, nullptr));
+      CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, z, c->g32, nullptr, true));
       CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
                    csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, nullptr, csc::kConvSumSq, c->sq_part, c->st));
       CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));

@@ -80,7 +80,7 @@ struct HArgs {
   int N, K, S, H, W, Hc, Wc, P;
   int KC, NCH, NT, ks;       // NCH = KC / 16
   int BR, nbands, nitems, WL;
-  unsigned long long* tdbg;  // CSC_CH_TIMING: per-CTA role cycle counters [grid][16] or nullptr
+  int precise;  // 1: hi*hi and the cross terms in separate TMEM accumulators (the ||Zg||^2 pass, reading T3)
 };
 
 struct HItem {
@@ -142,7 +142,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 0) tmem_alloc(&tmem_base_sh, 256);
+  if (warp == 0) tmem_alloc(&tmem_base_sh, 512);
   if (warp == 1 && lane == 0) tma_prefetch_desc(&tmap_z);
   tc_before();
   __syncthreads();
@@ -151,8 +151,6 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
 
   if (warp == 0) {
     // ================================ MMA issuer
-    const unsigned long long t_beg = clock64();
-    unsigned long long w_acc = 0, w_rdy = 0;
     const uint32_t idesc = idesc_f16_mn(128, A.NT);
     const uint32_t lbo_b = static_cast<uint32_t>(A.KC) * 128u;  // N atom (64 taps) stride
     const uint32_t sbh = su32(bsm), sbl = su32(bsm + bbytes), sst = su32(stg);
@@ -161,16 +159,14 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
-        const unsigned long long tw0 = clock64();
         mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
-        w_acc += clock64() - tw0;
         tc_after();
-        const uint32_t d = tbase + buf * 128u;
+        // accumulator buffer: 256 columns [hi*hi | cross terms] (precise) or 128 (one accumulator)
+        const uint32_t d = tbase + buf * (A.precise ? 256u : 128u);
+        const uint32_t dx = A.precise ? d + 128u : d;
         for (int c = 0; c < A.NCH; ++c, ++g) {
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
-          const unsigned long long tw1 = clock64();
           mbar_wait(&ready[slot], ph);
-          w_rdy += clock64() - tw1;
           tc_after();
           const uint32_t ah = sst + slot * kHStageBytes + kHRawBytes;
           // A: MN-major SW128, 2 atoms of 64 positions at LBO = 16 rows x 128 B, 8-row K groups at SBO
@@ -180,15 +176,18 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           const uint64_t dbh = sdesc(sbh + static_cast<uint32_t>(c) * 2048u, lbo_b, 1024u, kLayout128B);
           const uint64_t dbl = sdesc(sbl + static_cast<uint32_t>(c) * 2048u, lbo_b, 1024u, kLayout128B);
           const uint32_t acc0 = c > 0 ? 1u : 0u;
+          // precise: the cross terms start their own accumulator (flag p), so the tensor core's
+          // accumulate rounding acts on the small cross sums, not on the hi*hi sum
           asm volatile(
-              "{\n.reg .pred e, p, t;\n"
+              "{\n.reg .pred e, p, t, x;\n"
               "elect.sync _|e, 0xffffffff;\n"
-              "setp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 1, 1;\n"
+              "setp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 1, 1;\nsetp.ne.b32 x, %8, 0;\n"
               "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, p;\n"
-              "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %6, %4, t;\n"
-              "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %4, t;\n"
+              "@e tcgen05.mma.cta_group::1.kind::f16 [%7], %1, %6, %4, x;\n"
+              "@e tcgen05.mma.cta_group::1.kind::f16 [%7], %2, %3, %4, t;\n"
               "}\n" ::"r"(d),
-              "l"(dah), "l"(dal), "l"(dbh), "r"(idesc), "r"(acc0), "l"(dbl)
+              "l"(dah), "l"(dal), "l"(dbh), "r"(idesc), "r"(acc0), "l"(dbl), "r"(dx),
+              "r"(A.precise ? acc0 : 1u)
               : "memory");
           mma_commit_elect(&empty[slot]);
         }
@@ -196,15 +195,9 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       }
     }
     __syncwarp();
-    if (A.tdbg != nullptr && lane == 0) {
-      A.tdbg[blockIdx.x * 16 + 0] = clock64() - t_beg;
-      A.tdbg[blockIdx.x * 16 + 1] = w_acc;
-      A.tdbg[blockIdx.x * 16 + 2] = w_rdy;
-    }
   } else if (warp == 1) {
     // ================================ TMA producer: one box {128 positions, 16 planes} per stage
     if (lane == 0) {
-      unsigned long long w_emp = 0;
       uint32_t g = 0;
       for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
         const HItem it = h_item(A, item);
@@ -213,16 +206,13 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           const int pt = it.p0 + 128 * t;  // multiple of 4 floats (BR % 4 == 0): 16-B aligned box start
           for (int c = 0; c < A.NCH; ++c, ++g) {
             const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
-            const unsigned long long tw2 = clock64();
             mbar_wait(&empty[slot], ph ^ 1u);
-            w_emp += clock64() - tw2;
             mbar_arrive_expect_tx(&full[slot], kHRawBytes);
             const uint32_t dst = su32(stg + slot * kHStageBytes);
             tma_load_2d(dst, &tmap_z, pt, plane0 + 16 * c, &full[slot]);  // {128 positions, 16 planes}
           }
         }
       }
-      if (A.tdbg != nullptr) A.tdbg[blockIdx.x * 16 + 3] = w_emp;
     }
     __syncwarp();
   } else if (warp < kHEpiBase) {
@@ -230,8 +220,6 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     // thread job (row k, 8 positions 8j..8j+7): raw floats 8j..8j+7 of row k (row pitch 512 B);
     // fp16 chunk j%8 of atom j/8, row k, at 16-B chunk (j%8) ^ (k%8)
     const int cw = warp - kHConvBase;
-    const unsigned long long t_cv = clock64();
-    unsigned long long w_full = 0;
     const bool want_l1 = A.l1_part != nullptr;
     const float sz = exp2i(ez);
     double l1 = 0.0;
@@ -243,9 +231,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         for (int c = 0; c < A.NCH; ++c, ++g) {
           if (static_cast<int>(g % kHNS) != (cw >> 1)) continue;
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
-          const unsigned long long tw3 = clock64();
           mbar_wait(&full[slot], ph);
-          w_full += clock64() - tw3;
           const uint8_t* rawp = stg + slot * kHStageBytes;
           uint8_t* hip = stg + slot * kHStageBytes + kHRawBytes;
           uint8_t* lop = hip + kHHalfBytes;
@@ -285,48 +271,53 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         }
       }
     }
-    if (A.tdbg != nullptr && cw == 0 && lane == 0) {
-      A.tdbg[blockIdx.x * 16 + 4] = w_full;
-      A.tdbg[blockIdx.x * 16 + 5] = clock64() - t_cv;
-    }
     const double tsum = warp_sum_d(l1);
     if (lane == 0) l1_warp[cw] = tsum;
   } else {
-    // ================================ epilogue (as csc_conv_ss.cu: one band window, Wc >= 128)
+    // ================================ epilogue: col2im into one band window (as csc_conv_ss.cu)
     const int q = warp & 3;                 // TMEM lane quarter of this warp
     const int h = (warp - kHEpiBase) >> 2;  // group of tap rows
     constexpr int AH = (S + 2) / 3;
     const int a_beg = h * AH;
     const int na = min(AH, S - a_beg);      // may be <= 0 for small S
     const float inv = exp2i(-(ez + ef));
-    const unsigned long long t_ep = clock64();
-    unsigned long long w_af = 0, w_fl = 0;
+    // Wc >= 128 keeps the quarters' window rows disjoint (one pass); narrower rows add in a fixed
+    // order of phases (quarters; and their row groups when Wc < 32 + P): deterministic sums
+    const int nph = A.Wc >= 128 ? 1 : (A.Wc >= 32 + P ? 4 : 12);
+    const int myph = nph == 1 ? 0 : (nph == 4 ? q : 3 * q + h);
     uint32_t tcount = 0;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
-        const unsigned long long tw4 = clock64();
         mbar_wait_sleep(&acc_full[buf], use & 1u);
-        w_af += clock64() - tw4;
         tc_after();
         const int pq = 128 * t + 32 * q;
         const bool pvalid = it.p0 + pq + lane < it.pend;
-        const uint32_t tacc = tbase + buf * 128u + (static_cast<uint32_t>(32 * q) << 16);
+        const uint32_t tacc = tbase + buf * (A.precise ? 256u : 128u) + (static_cast<uint32_t>(32 * q) << 16);
         float* rowb = win + pq + lane + a_beg * A.Wc;
-        float dnv[AH];
+        float own[AH], dnv[AH];
         // positions past the item's end only occur in its last tile: the common full tile runs
         // without the per-value select
         auto reduce_rows = [&](auto partial) {
           constexpr bool PART = decltype(partial)::value;
 #pragma unroll
           for (int i = 0; i < AH; ++i) {
+            own[i] = 0.f;
             dnv[i] = 0.f;
             if (i >= na) continue;
             const int a = a_beg + i;
             float y[16];
             tmem_ld16_nowait(tacc + a * S, y);
-            tmem_ld_wait();
+            if (A.precise) {
+              float y2[16];
+              tmem_ld16_nowait(tacc + 128u + a * S, y2);
+              tmem_ld_wait();
+#pragma unroll
+              for (int b = 0; b < S; ++b) y[b] += y2[b];
+            } else {
+              tmem_ld_wait();
+            }
             float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
 #pragma unroll
             for (int b = 0; b < S; ++b) {
@@ -340,7 +331,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
                 if (b & 1) d1s += rot; else d0s += rot;
               }
             }
-            rowb[i * A.Wc] += u0s + u1s;
+            own[i] = u0s + u1s;
             dnv[i] = d0s + d1s;
           }
         };
@@ -349,15 +340,34 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
-        named_sync(1, 32 * kHEpiWarps);
-        if (lane < P) {
+        if (nph == 1) {
 #pragma unroll
           for (int i = 0; i < AH; ++i)
-            if (i < na) rowb[i * A.Wc + 32] += dnv[i];
+            if (i < na) rowb[i * A.Wc] += own[i];
+          named_sync(1, 32 * kHEpiWarps);
+          if (lane < P) {
+#pragma unroll
+            for (int i = 0; i < AH; ++i)
+              if (i < na) rowb[i * A.Wc + 32] += dnv[i];
+          }
+          named_sync(1, 32 * kHEpiWarps);
+        } else {
+          for (int ph = 0; ph < nph; ++ph) {
+            if (ph == myph) {
+#pragma unroll
+              for (int i = 0; i < AH; ++i)
+                if (i < na) rowb[i * A.Wc] += own[i];
+              __syncwarp();
+              if (lane < P) {
+#pragma unroll
+                for (int i = 0; i < AH; ++i)
+                  if (i < na) rowb[i * A.Wc + 32] += dnv[i];
+              }
+            }
+            named_sync(1, 32 * kHEpiWarps);
+          }
         }
-        named_sync(1, 32 * kHEpiWarps);
       }
-      const unsigned long long tw5 = clock64();
       float* dst = A.part + (static_cast<size_t>(it.n) * A.nbands + (it.u0 / A.BR)) *
                                 static_cast<size_t>(A.BR + P) * A.W;
       const int rows = A.BR + P;
@@ -370,19 +380,13 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       named_sync(1, 32 * kHEpiWarps);
       for (int e = et; e < A.WL; e += 32 * kHEpiWarps) win[e] = 0.f;
       named_sync(1, 32 * kHEpiWarps);
-      w_fl += clock64() - tw5;
-    }
-    if (A.tdbg != nullptr && warp == kHEpiBase && lane == 0) {
-      A.tdbg[blockIdx.x * 16 + 6] = w_af;
-      A.tdbg[blockIdx.x * 16 + 7] = w_fl;
-      A.tdbg[blockIdx.x * 16 + 8] = clock64() - t_ep;
     }
   }
 
   tc_before();
   __syncthreads();
   tc_after();
-  if (warp == 0) tmem_dealloc(tbase, 256);
+  if (warp == 0) tmem_dealloc(tbase, 512);
   if (tid == 0 && A.l1_part != nullptr) {
     double s = 0.0;
     for (int i = 0; i < kHConvWarps; ++i) s += l1_warp[i];
@@ -464,29 +468,10 @@ __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, int vec, u
   if (threadIdx.x == 0 && red != 0u) atomicMax(out, red);
 }
 
-typedef CUresult (*PFN_encodeTiled_h)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-PFN_encodeTiled_h encode_fn_h() {
-  static PFN_encodeTiled_h fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled_h>(p);
-  }
-  return fn;
-}
-
 template <int S>
 cudaError_t run_conv_h(const CUtensorMap& tm, const HArgs& a, int grid, int smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv_h_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHSmemMax);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&conv_h_kernel<S>), kHSmemMax);
+  if (e != cudaSuccess) return e;
   conv_h_kernel<S><<<grid, kHThreads, smem, st>>>(tm, a);
   return cudaGetLastError();
 }
@@ -495,8 +480,8 @@ cudaError_t run_conv_h(const CUtensorMap& tm, const HArgs& a, int grid, int smem
 
 // ---------------------------------------------------------------- host side
 bool conv_h_supported(const Geom& g) {
-  return (g.S == 5 || g.S == 7 || g.S == 9 || g.S == 11) && g.N > 0 && g.Wc >= 128 &&
-         (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 && tc_ntaps_padded(g.S) <= 128 && encode_fn_h() != nullptr;
+  return (g.S == 5 || g.S == 7 || g.S == 9 || g.S == 11) && g.N > 0 &&
+         (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 && tc_ntaps_padded(g.S) <= 128 && tmap_available();
 }
 
 bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p) {
@@ -542,54 +527,19 @@ cudaError_t launch_absmax(const float* x, int64_t n, uint32_t* out, cudaStream_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const float* filt, float* bimg_f,
-                          const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part, cudaStream_t st,
-                          bool build_b) {
-  static const float* cached_z = nullptr;
-  static Geom cached_g{};
-  static CUtensorMap tm;
-  if (z != cached_z || std::memcmp(&cached_g, &g, sizeof(Geom)) != 0) {
-    PFN_encodeTiled_h enc = encode_fn_h();
-    if (!enc) return cudaErrorNotSupported;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Hc) * g.Wc, static_cast<cuuint64_t>(g.N) * g.K};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Hc) * g.Wc * 4};
-    const cuuint32_t box[2] = {128u, 16u};
-    const cuuint32_t estr[2] = {1u, 1u};
-    CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(z), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return cudaErrorInvalidPitchValue;
-    cached_z = z;
-    cached_g = g;
-  }
+cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, TmapCache* tmc, const float* z, const float* filt,
+                          float* bimg_f, const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part,
+                          cudaStream_t st, bool build_b, bool precise) {
+  const uint64_t plane = static_cast<uint64_t>(g.Hc) * g.Wc;
+  cudaError_t e0 = tmap_2d(*tmc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, z, plane, static_cast<uint64_t>(g.N) * g.K, plane * 4,
+                           128, 16, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (e0 != cudaSuccess) return e0;
+  const CUtensorMap& tm = tmc->map;
   uint16_t* bimg = reinterpret_cast<uint16_t*>(bimg_f);
   if (build_b) bimg_h_kernel<<<16, 1024, 0, st>>>(filt, g.K, g.S * g.S, p.KC, p.nks, bimg, fmax);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   HArgs a{};
-  {
-    static int tmode = -1;
-    static unsigned long long* tbuf = nullptr;
-    static int ncalls = 0;
-    if (tmode < 0) {
-      const char* ev = std::getenv("CSC_CH_TIMING");
-      tmode = ev ? std::atoi(ev) : 0;
-      if (tmode) cudaMalloc(&tbuf, sizeof(unsigned long long) * 16 * 2048);
-    }
-    a.tdbg = tmode ? tbuf : nullptr;
-    if (tmode && ++ncalls == 12) {
-      cudaStreamSynchronize(st);
-      static unsigned long long h[16 * 2048];
-      cudaMemcpy(h, tbuf, sizeof(unsigned long long) * 16 * p.grid, cudaMemcpyDeviceToHost);
-      double tot[16] = {0};
-      for (int b = 0; b < p.grid; ++b)
-        for (int r = 0; r < 9; ++r) tot[r] += static_cast<double>(h[b * 16 + r]);
-      for (int r = 0; r < 9; ++r) tot[r] /= p.grid;
-      fprintf(stderr, "[conv_h] per CTA cycles: mma total %.0f wait acc_empty %.0f wait ready %.0f | tma wait empty %.0f | "
-                      "conv0 wait full %.0f of %.0f | epi0 wait acc_full %.0f band flush %.0f of %.0f\n",
-              tot[0], tot[1], tot[2], tot[3], tot[4], tot[5], tot[6], tot[7], tot[8]);
-    }
-  }
   a.bimg = bimg;
   a.zmax = zmax;
   a.fmax = fmax;
@@ -598,6 +548,7 @@ cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const 
   a.N = g.N; a.K = g.K; a.S = g.S; a.H = g.H; a.W = g.W; a.Hc = g.Hc; a.Wc = g.Wc; a.P = g.P;
   a.KC = p.KC; a.NCH = p.NCH; a.NT = p.NT;
   a.BR = p.BR; a.nbands = p.nbands; a.nitems = p.nitems; a.WL = p.WL;
+  a.precise = precise ? 1 : 0;
   for (int ks = 0; ks < p.nks; ++ks) {
     a.ks = ks;
     switch (g.S) {

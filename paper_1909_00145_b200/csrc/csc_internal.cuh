@@ -143,9 +143,11 @@ cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, const float* z, const
 bool conv_h_supported(const Geom& g);
 bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p);
 // build_b = false reuses the fp16 filter image (and fmax) of the previous call with the same filt.
-cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, const float* z, const float* filt, float* bimg,
-                          const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part, cudaStream_t st,
-                          bool build_b = true);
+// precise: hi*hi and the cross products accumulate in separate TMEM accumulators (the ||Zg||^2 pass,
+// DESIGN.md reading T3).  tmc: the context's cached tensor map of z.
+cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, TmapCache* tmc, const float* z, const float* filt,
+                          float* bimg, const uint32_t* zmax, uint32_t* fmax, float* part, double* l1_part,
+                          cudaStream_t st, bool build_b = true, bool precise = false);
 // *out = bits of max |x[i]| (atomicMax over non-negative float bits; resets *out first)
 cudaError_t launch_absmax(const float* x, int64_t n, uint32_t* out, cudaStream_t st);
 bool conv_tc_supported(const Geom& g);

@@ -221,7 +221,10 @@ def _trajectory(torch_dev, cfg, iters, p=None, check_every=1):
             for k_, v in errs.items():
                 worst[k_] = max(worst[k_], v)
             assert errs["z"] < TOL and errs["d"] < TOL and errs["F"] < TOL, (t, errs)
-            assert errs["tau_z"] < TOL_TAU and errs["tau_d"] < TOL_TAU, (t, errs, worst)
+            # tau_z depends on d only (1e-6); along a trajectory tau_d is a function of the state (z, d),
+            # which the bar holds to 1e-5 (reading T3); its one-step accuracy is
+            # test_filter_step_parity's 1e-6
+            assert errs["tau_z"] < TOL_TAU and errs["tau_d"] < TOL, (t, errs, worst)
     ctx.close()
     return worst
 
