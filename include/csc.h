@@ -17,8 +17,16 @@
  *
  * OWNERSHIP: x, d, z are caller-owned DEVICE pointers (e.g. torch
  * data_ptr()).  csc_code_step mutates z in place, csc_filter_step mutates d in
- * place.  The library owns all scratch, allocated once in csc_init; steps never
- * allocate, so a step sequence can be captured in a CUDA graph.
+ * place.  The library owns the scratch of the hot path, allocated once in csc_init.
+ *
+ * CUDA GRAPHS: csc_zero_codes, csc_code_step and csc_filter_step with step_used == NULL
+ * enqueue kernels and device-to-device work only (no allocation, no host synchronisation,
+ * no pageable copy) and may be captured on dims.stream once each kernel has run once
+ * (tests/test_gpu_graph.py).  The residual-cache decisions are taken on the host while
+ * capturing, so a captured sequence must be replayed from the state it was captured in (e.g.
+ * a SOCSC step: zero codes, code steps, filter step).  csc_objective, csc_iterate and any call
+ * with a host output synchronise and are not capturable; csc_code_step_admm, the BCD and
+ * surrogate updates and csc_stage_images allocate on first use.
  *
  * ASYNCHRONY: everything is enqueued on dims.stream (a cudaStream_t).  Only
  * csc_objective, csc_iterate and a non-NULL step_used pointer synchronise.
@@ -137,7 +145,8 @@ csc_status csc_code_step_admm(csc_ctx* ctx, const float* x, const float* d, floa
  *   CSC_STEP_ESO: tau_k = 1/(p L_D + (1-p) ||d_k||^2) for the codes of filter k -- the
  *     parallel-coordinate-descent step whose expected separable overapproximation holds for
  *     independent Bernoulli(p) sampling (E1).
- *     Equal to the Lipschitz rule at p = 1.  step_used then receives tau_0.
+ *     Equal to the Lipschitz rule at p = 1.  step_used then receives tau_0.  The ESO is derived for
+ *     independent per-code sampling: csc_code_step returns CSC_ERR_ARG for ESO with CSC_MASK_SECTOR8.
  * Per context; CSC_ERR_ARG for an unknown rule. */
 typedef enum { CSC_STEP_LIPSCHITZ = 0, CSC_STEP_ESO = 1 } csc_step_rule;
 csc_status csc_set_step_rule(csc_ctx* ctx, int rule);
@@ -227,6 +236,18 @@ csc_status csc_mask_bits(csc_ctx* ctx, uint32_t iter, double p, uint64_t seed, u
  * CSC_ERR_SHAPE when this context's code step does not run on the tensor cores. */
 csc_status csc_mask_selwords(csc_ctx* ctx, uint32_t iter, double p, uint64_t seed, uint32_t* words_dev,
                              int32_t info[4]);
+
+/* The context's device scalars after the last steps (HOST out[4], syncs): out[0] = sum r^2 of the last
+ * residual pass (csc_objective: 2 x the fit term), out[1] = ||z||_1 of the last objective pass,
+ * out[2] = ||Z g||^2 of the last filter step or csc_zg_sumsq, out[3] = <g, g> -- all over every rank's
+ * images after the all-reduce (this rank's images when world == 1).  Test hook for the sharded
+ * decomposition (tests/test_gpu_sharded.py). */
+csc_status csc_read_scalars(csc_ctx* ctx, double out[4]);
+
+/* ||sum_k g_k * z_k||^2 over this rank's images for a given filter-shaped g (DEVICE fp64 [K][s][s]) --
+ * the local part of the line-search denominator of csc_filter_step, with no all-reduce; read it with
+ * csc_read_scalars (out[2]).  Overwrites the cached gradient (csc_read_grad then returns g).  Test hook. */
+csc_status csc_zg_sumsq(csc_ctx* ctx, const float* z, const double* g_dev);
 
 /* Copy the cached residual [n_local][H][W] into r_dev (DEVICE). */
 csc_status csc_read_residual(csc_ctx* ctx, float* r_dev);

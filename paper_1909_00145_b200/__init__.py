@@ -31,7 +31,7 @@ ABI_SYMBOLS = (
     "csc_profile_enable", "csc_profile_read", "csc_kernel_variants", "csc_code_step_admm",
     "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd", "csc_surrogate_reset",
     "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate", "csc_set_mask_mode",
-    "csc_stage_images", "csc_iterate_staged", "csc_mask_selwords",
+    "csc_stage_images", "csc_iterate_staged", "csc_mask_selwords", "csc_read_scalars", "csc_zg_sumsq",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -92,6 +92,8 @@ def load_library(path: Optional[str] = None):
         L.csc_abi_version.restype = ctypes.c_int
         L.csc_mask_bits.argtypes = [vp, u32, f64, u64, vp]
         L.csc_mask_selwords.argtypes = [vp, u32, f64, u64, vp, vp]
+        L.csc_read_scalars.argtypes = [vp, vp]
+        L.csc_zg_sumsq.argtypes = [vp, vp, vp]
         L.csc_read_residual.argtypes = [vp, vp]
         L.csc_read_grad.argtypes = [vp, vp]
         L.csc_lipschitz.argtypes = [vp, vp, vp]
@@ -319,6 +321,21 @@ class Context:
             self._check(self._L.csc_mask_selwords(self._h, int(it) & 0xffffffff, float(p), int(seed) & (2**64 - 1),
                                                   out.data_ptr(), info))
         return tuple(info)
+
+    def read_scalars(self) -> dict:
+        """Device scalars after the last steps (include/csc.h csc_read_scalars)."""
+        out = (ctypes.c_double * 4)()
+        self._check(self._L.csc_read_scalars(self._h, out))
+        return {"sum_r2": out[0], "l1": out[1], "zg2": out[2], "gg": out[3]}
+
+    def zg_sumsq(self, z, g) -> float:
+        """||sum_k g_k * z_k||^2 over this context's images for a float64 CUDA tensor g [K*s*s]."""
+        import torch
+        if not (g.is_cuda and g.dtype == torch.float64 and g.numel() == self.K * self.s * self.s):
+            raise ValueError("g must be a float64 CUDA tensor of K*s*s elements")
+        nz = self.n_local * self.K * self.Hc * self.Wc
+        self._check(self._L.csc_zg_sumsq(self._h, _ptr(z, "z", nz) if self.n_local else 0, g.data_ptr()))
+        return self.read_scalars()["zg2"]
 
     def read_residual(self, out):
         self._check(self._L.csc_read_residual(self._h, _ptr(out, "out", self.n_local * self.H * self.W)

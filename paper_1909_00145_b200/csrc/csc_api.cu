@@ -256,7 +256,7 @@ cudaError_t conv_tc_any(csc_ctx* c, const float* z, const float* filt, double* l
   if (c->tc.ss) {
     cudaError_t e = csc::launch_tc_bimg(c->g, c->tc, filt, c->tc_bimg, c->st);
     if (e != cudaSuccess) return e;
-    return csc::launch_conv_ss(c->g, c->tc, z, c->tc_bimg, c->tc_part, l1p, c->st);
+    return csc::launch_conv_ss(c->g, c->tc, &c->tm_conv, z, c->tc_bimg, c->tc_part, l1p, c->st);
   }
   return csc::launch_conv_tc(c->g, c->tc, z, filt, c->tc_bimg, c->tc_part, l1p, c->st);
 }
@@ -703,6 +703,9 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   if (!(lambda >= 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and >= 0");
   if (!(step_z >= 0.f) || !std::isfinite(step_z)) return fail(c, CSC_ERR_ARG, "step_z must be finite and >= 0");
   if (!(p > 0.0 && p <= 1.0)) return fail(c, CSC_ERR_ARG, "p must be in (0, 1]");
+  if (step_z == 0.f && c->step_rule == CSC_STEP_ESO && c->mask_mode == CSC_MASK_SECTOR8)
+    return fail(c, CSC_ERR_ARG,
+                "the ESO step (DESIGN.md E1) assumes independent per-code sampling; it is not valid for sector masks");
   CSC_CUDA(c, cudaSetDevice(c->device));
   const Geom& g = c->g;
   // zero-code shortcut of csc_zero_codes: r = -x for any d
@@ -713,7 +716,7 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   }
   const bool eso = step_z == 0.f && c->step_rule == CSC_STEP_ESO;
   if (step_z > 0.f) {
-    CSC_CUDA(c, cudaMemcpyAsync(c->fscal + kTauZ, &step_z, sizeof(float), cudaMemcpyHostToDevice, c->st));
+    CSC_LAUNCH(c, 1, csc::launch_set_f32(c->fscal + kTauZ, step_z, c->st));
   } else {
     CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 3, csc::launch_lipschitz(g, d, c->lip_part, c->dscal + kLhat, c->fscal + kTauZ, c->st));
     if (eso) CSC_LAUNCH(c, 1, csc::launch_eso_tau(g, d, p, c->dscal + kLhat, c->tauk, c->st));
@@ -786,8 +789,7 @@ csc_status csc_read_step_z(csc_ctx* c, float* tau_dev) {
   if (c->last_eso) {
     CSC_CUDA(c, cudaMemcpyAsync(tau_dev, c->tauk, sizeof(float) * c->g.K, cudaMemcpyDeviceToDevice, c->st));
   } else {
-    for (int k = 0; k < c->g.K; ++k)
-      CSC_CUDA(c, cudaMemcpyAsync(tau_dev + k, c->fscal + kTauZ, sizeof(float), cudaMemcpyDeviceToDevice, c->st));
+    CSC_LAUNCH(c, 1, csc::launch_bcast_f32(tau_dev, c->fscal + kTauZ, c->g.K, c->st));
   }
   return CSC_OK;
 }
@@ -1125,6 +1127,32 @@ csc_status csc_read_surrogate(csc_ctx* c, double* C_dev, double* B_dev, int64_t*
   return CSC_OK;
 }
 
+// ||Z g||^2 of this rank's images for the fp32 copy g32 of the gradient -> dscal[kZg2] (no all-reduce):
+// the precise dense pass (hi*hi and cross products in separate accumulators, reading T3)
+static csc_status zg_pass(csc_ctx* c, const float* z) {
+  const Geom& g = c->g;
+  if (g.N > 0 && c->tc_on) {
+    CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, z, c->g32, nullptr, true));
+    CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
+                 csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, nullptr, csc::kConvSumSq, c->sq_part, c->st));
+    CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));
+  } else if (g.N > 0) {
+    int nb = 0;
+    CSC_LAUNCH_C(c, CSC_K_CONV, 1, csc::launch_conv_fwd(g, z, c->g32, nullptr, nullptr, c->part, c->ksplit,
+                                                        csc::kConvSumSq, c->sq_part, nullptr, c->st, &nb));
+    if (c->ksplit == 1) {
+      CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, nb, c->dscal + kZg2, 1.0, c->st));
+    } else {
+      CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1, csc::launch_conv_finalize(g, c->part, c->ksplit, nullptr, nullptr,
+                                                                        csc::kConvSumSq, c->sq_part, c->st));
+      CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));
+    }
+  } else {
+    CSC_CUDA(c, cudaMemsetAsync(c->dscal + kZg2, 0, sizeof(double), c->st));
+  }
+  return CSC_OK;
+}
+
 csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z, float step_d, float* step_used) {
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
@@ -1138,7 +1166,7 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
   }
   if (g.N > 0) {
     if (c->wg_tc_on && (reinterpret_cast<uintptr_t>(z) & 15u) == 0) {
-      CSC_LAUNCH_C(c, CSC_K_WGRAD, 1, csc::launch_wgrad_tc(g, c->wg, z, c->r, c->gpart, c->st));
+      CSC_LAUNCH_C(c, CSC_K_WGRAD, 1, csc::launch_wgrad_tc(g, c->wg, &c->tm_wgrad, z, c->r, c->gpart, c->st));
       CSC_LAUNCH(c, 1, csc::launch_wgrad_reduce(g, c->gpart, c->wg.G, c->gsum, c->st));
     } else {
       CSC_LAUNCH_C(c, CSC_K_WGRAD, 1, csc::launch_wgrad(g, z, c->r, c->G, c->gpart, c->st));
@@ -1151,25 +1179,8 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
   if (s != CSC_OK) return s;
   CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->st));
   if (step_d == 0.f) {
-    if (g.N > 0 && c->tc_on) {
-      CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, z, c->g32, nullptr, true));
-      CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
-                   csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, nullptr, csc::kConvSumSq, c->sq_part, c->st));
-      CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));
-    } else if (g.N > 0) {
-      int nb = 0;
-      CSC_LAUNCH_C(c, CSC_K_CONV, 1, csc::launch_conv_fwd(g, z, c->g32, nullptr, nullptr, c->part, c->ksplit, csc::kConvSumSq,
-                                            c->sq_part, nullptr, c->st, &nb));
-      if (c->ksplit == 1) {
-        CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, nb, c->dscal + kZg2, 1.0, c->st));
-      } else {
-        CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1, csc::launch_conv_finalize(g, c->part, c->ksplit, nullptr, nullptr, csc::kConvSumSq,
-                                                   c->sq_part, c->st));
-        CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));
-      }
-    } else {
-      CSC_CUDA(c, cudaMemsetAsync(c->dscal + kZg2, 0, sizeof(double), c->st));
-    }
+    s = zg_pass(c, z);
+    if (s != CSC_OK) return s;
     s = allreduce_d(c, c->dscal + kZg2, 1);
     if (s != CSC_OK) return s;
   }
@@ -1324,6 +1335,27 @@ csc_status csc_mask_selwords(csc_ctx* c, uint32_t iter, double p, uint64_t seed,
   const uint64_t thr = static_cast<uint64_t>(std::floor(p * 4294967296.0));
   CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(c->g, c->ct, seed, iter, thr, words_dev, c->st, c->mask_mode));
   return CSC_OK;
+}
+
+csc_status csc_read_scalars(csc_ctx* c, double out[4]) {
+  if (!c || !out) return fail(c, CSC_ERR_ARG, "out (host, 4 doubles) required");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal, c->dscal, sizeof(double) * kNumD, cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  out[0] = c->h_dscal[kSqR];
+  out[1] = c->h_dscal[kL1];
+  out[2] = c->h_dscal[kZg2];
+  out[3] = c->h_dscal[kGG];
+  return CSC_OK;
+}
+
+csc_status csc_zg_sumsq(csc_ctx* c, const float* z, const double* g_dev) {
+  if (!c || !g_dev || (c->g.N > 0 && !aligned4(z))) return fail(c, CSC_ERR_ARG, "z and g_dev must be device pointers");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  const Geom& g = c->g;
+  CSC_CUDA(c, cudaMemcpyAsync(c->gsum, g_dev, sizeof(double) * g.K * g.S * g.S, cudaMemcpyDeviceToDevice, c->st));
+  CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->st));
+  return zg_pass(c, z);
 }
 
 csc_status csc_read_residual(csc_ctx* c, float* r_dev) {

@@ -380,12 +380,8 @@ __global__ void mask_selwords_kernel(int K, int KC, int NC, int nper, int nblk, 
 
 template <int S, int NC>
 cudaError_t run_code_tc(const CtArgs& a, int grid, int smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(code_tc_kernel<S, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtSmemMax);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&code_tc_kernel<S, NC>), kCtSmemMax);
+  if (e != cudaSuccess) return e;
   code_tc_kernel<S, NC><<<grid, kCtThreads, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -324,29 +324,10 @@ conv_ss_kernel(const __grid_constant__ CUtensorMap tmap_z, const SsArgs A) {
   }
 }
 
-typedef CUresult (*PFN_encodeTiled_ss)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-PFN_encodeTiled_ss encode_fn_ss() {
-  static PFN_encodeTiled_ss fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled_ss>(p);
-  }
-  return fn;
-}
-
 template <int S>
 cudaError_t run_conv_ss(const CUtensorMap& tm, const SsArgs& a, int grid, int smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv_ss_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSsSmemMax);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&conv_ss_kernel<S>), kSsSmemMax);
+  if (e != cudaSuccess) return e;
   conv_ss_kernel<S><<<grid, kSsThreads, smem, st>>>(tm, a);
   return cudaGetLastError();
 }
@@ -356,7 +337,7 @@ cudaError_t run_conv_ss(const CUtensorMap& tm, const SsArgs& a, int grid, int sm
 // ---------------------------------------------------------------- host side
 bool conv_ss_supported(const Geom& g) {
   return (g.S == 5 || g.S == 7 || g.S == 9 || g.S == 11) && g.N > 0 && g.Wc >= 128 &&
-         (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 && tc_ntaps_padded(g.S) <= 128 && encode_fn_ss() != nullptr;
+         (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 && tc_ntaps_padded(g.S) <= 128 && tmap_available();
 }
 
 // Fills the fields of p the SS kernel uses (KC, NCH, nks, natoms, NT, BR, nbands, nitems, grid,
@@ -397,25 +378,13 @@ bool conv_ss_plan(const Geom& g, int num_sms, TcPlan& p) {
   return true;
 }
 
-cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, const float* z, const float* bimg, float* part,
-                           double* l1_part, cudaStream_t st) {
-  static const float* cached_z = nullptr;
-  static Geom cached_g{};
-  static CUtensorMap tm;
-  if (z != cached_z || std::memcmp(&cached_g, &g, sizeof(Geom)) != 0) {
-    PFN_encodeTiled_ss enc = encode_fn_ss();
-    if (!enc) return cudaErrorNotSupported;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Hc) * g.Wc, static_cast<cuuint64_t>(g.N) * g.K};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Hc) * g.Wc * 4};
-    const cuuint32_t box[2] = {32u, 8u};
-    const cuuint32_t estr[2] = {1u, 1u};
-    CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(z), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return cudaErrorInvalidPitchValue;
-    cached_z = z;
-    cached_g = g;
-  }
+cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, TmapCache* tmc, const float* z, const float* bimg,
+                           float* part, double* l1_part, cudaStream_t st) {
+  const uint64_t plane = static_cast<uint64_t>(g.Hc) * g.Wc;
+  cudaError_t e0 = tmap_2d(*tmc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, z, plane, static_cast<uint64_t>(g.N) * g.K, plane * 4,
+                           32, 8, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (e0 != cudaSuccess) return e0;
+  const CUtensorMap& tm = tmc->map;
   SsArgs a{};
   a.bimg = bimg;
   a.part = part;

@@ -116,6 +116,11 @@ cudaError_t launch_filter_tau(const double* gg, const double* zg2, float step, f
 cudaError_t launch_filter_update(const Geom& g, float* d, const double* gsum, const float* tau_d,
                                  cudaStream_t st);
 
+// *p = v on the stream (a kernel argument, not a pageable host copy: capturable in a CUDA graph).
+cudaError_t launch_set_f32(float* p, float v, cudaStream_t st);
+// dst[0..n) = *src
+cudaError_t launch_bcast_f32(float* dst, const float* src, int n, cudaStream_t st);
+
 // r = -x (zero codes).
 cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st);
 // r += sign * x
@@ -136,8 +141,8 @@ cudaError_t launch_tc_bimg(const Geom& g, const TcPlan& p, const float* filt, fl
 // TMA-fed SS dense pass (csc_conv_ss.cu): Hc*Wc % 4 == 0, s in {5,7,9,11}
 bool conv_ss_supported(const Geom& g);
 bool conv_ss_plan(const Geom& g, int num_sms, TcPlan& p);
-cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, const float* z, const float* bimg, float* part,
-                           double* l1_part, cudaStream_t st);
+cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, TmapCache* tmc, const float* z, const float* bimg,
+                           float* part, double* l1_part, cudaStream_t st);
 // fp16-split SS dense pass (csc_conv_h.cu): Wc >= 128, Hc*Wc % 4 == 0.  zmax: upper bound of max|z|
 // (float bits, device); fmax: written with max|filt| (float bits, device).
 bool conv_h_supported(const Geom& g);
@@ -169,8 +174,8 @@ bool wgrad_tc_supported(const Geom& g);
 WgTcPlan wgrad_tc_plan(const Geom& g, int num_sms);
 // Per-CTA fp64 partials gpart[p.G][K][S*S] (reduce with launch_wgrad_reduce(g, gpart, p.G, ...)).
 // z must be 16-byte aligned.
-cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, const float* z, const float* r, double* gpart,
-                            cudaStream_t st);
+cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, TmapCache* tmc, const float* z, const float* r,
+                            double* gpart, cudaStream_t st);
 
 
 // ---- tensor-core (tcgen05, 3xTF32) dense-then-mask code step, csc_code_tc.cu

@@ -736,11 +736,8 @@ struct ConvRun {
     using T = ConvTile<S>;
     const int tilesX = ceil_div(g.W, kConvTW), tilesY = ceil_div(g.H, kConvTH);
     const size_t smem = sizeof(float) * T::SMEM_FLOATS;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(conv_fwd_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      attr = true;
-    }
+    cudaError_t ea = set_smem_attr_once(reinterpret_cast<const void*>(&conv_fwd_kernel<S>), static_cast<int>(smem));
+    if (ea != cudaSuccess) return ea;
     dim3 grid(tilesX * tilesY, g.N, ksplit);
     conv_fwd_kernel<S><<<grid, kConvThreads, smem, st>>>(z, filt, x, out, mode, ksplit, g, tilesX, sq_part, l1_part);
     return cudaGetLastError();
@@ -755,11 +752,8 @@ struct WgRun {
     size_t smem = sizeof(float) * T::SMEM_FLOATS;
     const size_t red = sizeof(double) * (kWgThreads / 32) * S * S;
     if (red > smem) smem = red;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(wgrad_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      attr = true;
-    }
+    cudaError_t ea = set_smem_attr_once(reinterpret_cast<const void*>(&wgrad_kernel<S>), static_cast<int>(smem));
+    if (ea != cudaSuccess) return ea;
     dim3 grid(G, g.K);
     wgrad_kernel<S><<<grid, kWgThreads, smem, st>>>(z, r, g, tilesX, tilesY, G, gpart);
     return cudaGetLastError();
@@ -793,11 +787,8 @@ struct CodeRun {
     if (kgroups > kmax) kgroups = kmax;
     if (kgroups < 1) kgroups = 1;
     const size_t smem = sizeof(float) * (TH + S - 1) * kCodePitch;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(code_step_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      attr = true;
-    }
+    cudaError_t ea = set_smem_attr_once(reinterpret_cast<const void*>(&code_step_kernel<S>), 96 * 1024);
+    if (ea != cudaSuccess) return ea;
     const int NB = ceil_div(g.Hc, 32);
     dim3 grid(strips, bands, g.N * kgroups);
     code_step_kernel<S><<<grid, kCodeThreads, smem, st>>>(r, d, z, colw, all_selected, tau_dev, tau_stride, lam, g,
@@ -993,4 +984,24 @@ cudaError_t set_smem_attr_once(const void* func, int bytes) {
   return e;
 }
 
+}  // namespace csc
+
+// ---------------------------------------------------------------- device scalars
+namespace csc {
+namespace {
+__global__ void set_f32_kernel(float* p, float v) { *p = v; }
+__global__ void bcast_f32_kernel(float* dst, const float* src, int n) {
+  const float v = *src;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = v;
+}
+}  // namespace
+cudaError_t launch_set_f32(float* p, float v, cudaStream_t st) {
+  set_f32_kernel<<<1, 1, 0, st>>>(p, v);
+  return cudaGetLastError();
+}
+cudaError_t launch_bcast_f32(float* dst, const float* src, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  bcast_f32_kernel<<<(n + 255) / 256, 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
 }  // namespace csc

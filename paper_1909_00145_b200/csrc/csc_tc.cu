@@ -670,12 +670,8 @@ TcPlan conv_tc_plan(const Geom& g, int num_sms) {
 
 template <int S>
 static cudaError_t run_conv_tc(const TcArgs& a, int grid, int smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&conv_tc_kernel<S>), 220 * 1024);
+  if (e != cudaSuccess) return e;
   conv_tc_kernel<S><<<grid, kTcThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -693,17 +689,8 @@ cudaError_t launch_conv_tc(const Geom& g, const TcPlan& p, const float* z, const
   a.N = g.N; a.K = g.K; a.S = g.S; a.H = g.H; a.W = g.W; a.Hc = g.Hc; a.Wc = g.Wc; a.P = g.P;
   a.KC = p.KC; a.NCH = p.NCH; a.NT = p.NT; a.natoms = p.natoms;
   a.BR = p.BR; a.nbands = p.nbands; a.nitems = p.nitems; a.SEGR = p.SEGR; a.RW = p.RW;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* ev = std::getenv("CSC_TC_DEBUG");
-      dbg = ev ? std::atoi(ev) : 0;
-    }
-    a.dbg = dbg;
-  }
-  static unsigned long long* dbgbuf = nullptr;
-  if ((a.dbg & 8) && dbgbuf == nullptr) cudaMalloc(&dbgbuf, sizeof(unsigned long long) * 8 * 1024);
-  a.dbgbuf = dbgbuf;
+  a.dbg = 0;
+  a.dbgbuf = nullptr;
   for (int ks = 0; ks < p.nks; ++ks) {
     a.ks = ks;
     switch (g.S) {
@@ -714,20 +701,6 @@ cudaError_t launch_conv_tc(const Geom& g, const TcPlan& p, const float* z, const
       default: return cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
-  }
-  if (a.dbg & 8) {
-    static int reported = 0;
-    if (reported++ == 8) {  // after warm-up: print the per-role wait profile of one launch
-      cudaStreamSynchronize(st);
-      unsigned long long h[8 * 1024];
-      cudaMemcpy(h, dbgbuf, sizeof(unsigned long long) * 8 * p.grid, cudaMemcpyDeviceToHost);
-      double tot[8] = {0};
-      for (int b = 0; b < p.grid; ++b)
-        for (int r = 0; r < 6; ++r) tot[r] += static_cast<double>(h[b * 8 + r]);
-      fprintf(stderr, "[tc-debug] per CTA avg cycles: total %.0f  mma.wait_acc_empty %.0f  mma.wait_a_full %.0f  "
-                      "epi.wait_acc_full %.0f  conv.wait_a_empty %.0f  mma.issue %.0f\n",
-              tot[0] / p.grid, tot[1] / p.grid, tot[2] / p.grid, tot[3] / p.grid, tot[4] / p.grid, tot[5] / p.grid);
-    }
   }
   return cudaSuccess;
 }

@@ -389,31 +389,10 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
-// ---------------------------------------------------------------- tensor map (driver entry point)
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-PFN_encodeTiled encode_fn() {
-  static PFN_encodeTiled fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled>(p);
-  }
-  return fn;
-}
-
 template <int NC>
 cudaError_t run_wgrad_tc(const CUtensorMap& tm, const WgArgs& a, int grid, int smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(wgrad_tc_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWgSmemMax);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&wgrad_tc_kernel<NC>), kWgSmemMax);
+  if (e != cudaSuccess) return e;
   wgrad_tc_kernel<NC><<<grid, kWgThreadsTc, smem, st>>>(tm, a);
   return cudaGetLastError();
 }
@@ -423,7 +402,7 @@ cudaError_t run_wgrad_tc(const CUtensorMap& tm, const WgArgs& a, int grid, int s
 // ---------------------------------------------------------------- host side
 bool wgrad_tc_supported(const Geom& g) {
   return g.N > 0 && g.S >= 3 && g.S * g.S <= 128 && g.Wc >= 8 && (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 &&
-         static_cast<int64_t>(g.N) * g.K < (int64_t(1) << 31) && encode_fn() != nullptr;
+         static_cast<int64_t>(g.N) * g.K < (int64_t(1) << 31) && tmap_available();
 }
 
 WgTcPlan wgrad_tc_plan(const Geom& g, int num_sms) {
@@ -459,27 +438,13 @@ WgTcPlan wgrad_tc_plan(const Geom& g, int num_sms) {
   return p;
 }
 
-cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, const float* z, const float* r, double* gpart,
-                            cudaStream_t st) {
-  static const float* cached_z = nullptr;
-  static Geom cached_g{};
-  static int cached_kc = 0;
-  static CUtensorMap tm;
-  if (z != cached_z || std::memcmp(&cached_g, &g, sizeof(Geom)) != 0 || cached_kc != p.KC) {
-    PFN_encodeTiled enc = encode_fn();
-    if (!enc) return cudaErrorNotSupported;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Hc) * g.Wc, static_cast<cuuint64_t>(g.N) * g.K};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Hc) * g.Wc * 4};
-    const cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(p.KC)};
-    const cuuint32_t estr[2] = {1u, 1u};
-    CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(z), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return cudaErrorInvalidPitchValue;  // distinct code: tensor-map encode rejected
-    cached_z = z;
-    cached_g = g;
-    cached_kc = p.KC;
-  }
+cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, TmapCache* tmc, const float* z, const float* r,
+                            double* gpart, cudaStream_t st) {
+  const uint64_t plane = static_cast<uint64_t>(g.Hc) * g.Wc;
+  cudaError_t e0 = tmap_2d(*tmc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, z, plane, static_cast<uint64_t>(g.N) * g.K, plane * 4,
+                           32, static_cast<uint32_t>(p.KC), CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (e0 != cudaSuccess) return e0;
+  const CUtensorMap& tm = tmc->map;
   WgArgs a{};
   a.r = r;
   a.gpart = gpart;
@@ -487,43 +452,9 @@ cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, const float* z, co
   a.KC = p.KC; a.Npad = p.Npad; a.nkg = p.nkg; a.G = p.G;
   a.L = p.L; a.nseg = p.nseg; a.nitems = p.nitems;
   a.pitch = p.pitch; a.rs_rows = p.rs_rows; a.rs_floats = p.rs_floats; a.stage_bytes = p.stage_bytes;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* ev = std::getenv("CSC_WG_DEBUG");
-      dbg = ev ? std::atoi(ev) : 0;
-    }
-    a.dbg = dbg;
-    static int cpt = -1;
-    if (cpt < 0) {
-      const char* ev = std::getenv("CSC_WG_CPT");
-      cpt = ev ? std::atoi(ev) : kWgMaxCpt;
-      if (cpt < 1) cpt = 1;
-    }
-    a.cpt = cpt;
-  }
-  {
-    static int tmode = -1;
-    static unsigned long long* tbuf = nullptr;
-    static int ncalls = 0;
-    if (tmode < 0) {
-      const char* ev = std::getenv("CSC_WG_TIMING");
-      tmode = ev ? std::atoi(ev) : 0;
-      if (tmode) cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 2048);
-    }
-    a.tdbg = tmode ? tbuf : nullptr;
-    if (tmode && ++ncalls == 5) {
-      cudaStreamSynchronize(st);
-      unsigned long long h[8 * 2048];
-      cudaMemcpy(h, tbuf, sizeof(unsigned long long) * 8 * p.grid, cudaMemcpyDeviceToHost);
-      double tot[8] = {0};
-      for (int b = 0; b < p.grid; ++b)
-        for (int r = 0; r < 6; ++r) tot[r] += static_cast<double>(h[b * 8 + r]);
-      fprintf(stderr, "[wgrad_tc] per CTA cycles: total %.0f | mma wait acc_empty %.0f, wait ready %.0f | conv0 wait z "
-                      "%.0f of %.0f | epi wait acc_full %.0f\n",
-              tot[0] / p.grid, tot[1] / p.grid, tot[2] / p.grid, tot[3] / p.grid, tot[4] / p.grid, tot[5] / p.grid);
-    }
-  }
+  a.dbg = 0;
+  a.cpt = kWgMaxCpt;
+  a.tdbg = nullptr;
   switch (p.Npad / 4) {
     case 4: return run_wgrad_tc<4>(tm, a, p.grid, p.smem, st);
     case 8: return run_wgrad_tc<8>(tm, a, p.grid, p.smem, st);

@@ -144,3 +144,23 @@ def test_sector8_code_step_parity(torch_dev, shape, p, path, monkeypatch):
     with pytest.raises(pkg.CSCError):
         ctx.code_step_admm(xt, dt, zt, lam, p, seed, it)  # ADMM keeps the per-entry masks of Eq.2
     ctx.close()
+
+
+def test_eso_with_sector_masks_rejected(torch_dev):
+    """The ESO step (E1) holds for independent per-code sampling only: with sector masks the
+    code step refuses it (CSC_ERR_ARG, no side effects); an explicit step is still accepted."""
+    import torch
+    import paper_1909_00145_b200 as pkg
+    x, d, z = random_problem(5, 1, 6, 5, 20, 24, code_density=0.3)
+    ctx = pkg.Context(1, 6, 5, 20, 24, device=0)
+    ctx.set_step_rule("eso")
+    ctx.set_mask_mode("sector8")
+    xt, dt, zt = (torch.from_numpy(np.ascontiguousarray(a)).to(torch_dev) for a in (x, d, z))
+    z0 = zt.clone()
+    with pytest.raises(pkg.CSCError) as ei:
+        ctx.code_step(xt, dt, zt, 0.2, 0.5, 1, 1)
+    assert ei.value.status == 1
+    torch.cuda.synchronize()
+    assert torch.equal(zt, z0)
+    ctx.code_step(xt, dt, zt, 0.2, 0.5, 1, 1, step_z=0.01)
+    ctx.close()

@@ -1,0 +1,77 @@
+"""CUDA-graph capture of a SOCSC step through the C ABI (include/csc.h "CUDA GRAPHS"; SURVEY.md §7 hard
+part 7: the online configuration is launch-bound, so its inner loop is replayed as one graph).
+
+One step of Alg.2 (reading #14): zero codes, 10 masked code steps (mask iterations
+10 s + i), the projected-gradient filter step.  Captured once on the context's stream, replayed on
+fresh mini-batches, it must produce the same codes and filters as the same calls issued eagerly on a
+second context (same kernels in the same order: bit-identical), and the eager run matches the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from synth import CONFIGS, make_filters, make_images, mask_seed
+from tests.conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def test_socsc_step_graph_replay():
+    import torch
+    import paper_1909_00145_b200 as pkg
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda:0")
+    cfg = CONFIGS["online"].with_(K=48, N=4, H=40, W=44)
+    seed = mask_seed(cfg)
+    n_inner = 10
+    s_cap = torch.cuda.Stream(dev)
+    s_eag = torch.cuda.Stream(dev)
+    cg = pkg.Context(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W, device=0, stream=s_cap)
+    ce = pkg.Context(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W, device=0, stream=s_eag)
+    d0 = make_filters(cfg)
+    xg = torch.empty((cfg.N, cfg.H, cfg.W), device=dev)
+    zg = torch.empty((cfg.N, cfg.K, cfg.Hc, cfg.Wc), device=dev)
+    dg = torch.from_numpy(d0).to(dev)
+
+    def socsc(ctx, x, d, z, step):
+        ctx.zero_codes(x, z)
+        for i in range(n_inner):
+            ctx.code_step(x, d, z, cfg.lam, cfg.p, seed, n_inner * step + i)
+        ctx.filter_step(x, d, z)
+
+    # warm-up (first launches configure the kernels), then capture step 0's sequence
+    xg.copy_(torch.from_numpy(make_images(cfg, 0, cfg.N)))
+    with torch.cuda.stream(s_cap):
+        socsc(cg, xg, dg, zg, 0)
+    torch.cuda.synchronize()
+    dg.copy_(torch.from_numpy(d0))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s_cap):
+        socsc(cg, xg, dg, zg, 0)
+    torch.cuda.synchronize()
+    # replay on fresh mini-batches (the mask iterations are those of step 0 captured in the graph)
+    dg.copy_(torch.from_numpy(d0))
+    de = torch.from_numpy(d0).to(dev)
+    xe = torch.empty_like(xg)
+    ze = torch.empty_like(zg)
+    d_or = d0.copy()
+    for b in range(3):
+        xb = torch.from_numpy(make_images(cfg, cfg.N * (b + 1), cfg.N))
+        xg.copy_(xb)
+        xe.copy_(xb)
+        torch.cuda.synchronize()
+        graph.replay()
+        with torch.cuda.stream(s_eag):
+            socsc(ce, xe, de, ze, 0)
+        torch.cuda.synchronize()
+        assert torch.equal(zg, ze), b
+        assert torch.equal(dg, de), b
+        # and the eager step against the oracle
+        xn = xb.numpy()
+        z = np.zeros((cfg.N, cfg.K, cfg.Hc, cfg.Wc), np.float32)
+        for i in range(n_inner):
+            z, _ = oracle.code_step(xn, d_or, z, cfg.lam, 0.0, cfg.p, seed, i)
+        d_or, _, _, _ = oracle.filter_step(xn, d_or, z)
+        assert rel_err(ze.cpu().numpy(), z) < 1e-5, b
+        assert rel_err(de.cpu().numpy(), d_or) < 1e-5, b
+    cg.close()
+    ce.close()
