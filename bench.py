@@ -238,41 +238,73 @@ def _dist():
     return ws, rank, local
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_step(cfg, x, d, z, t, oracle):
+    """One step of the workload on the oracle: an SBCSC iteration (Alg.1), or for the online
+    configuration an SOCSC step (Alg.2, reading #14: z = 0, 10 code steps, filter step, objective)."""
+    if cfg.online:
+        import numpy as np
+        z = np.zeros_like(z)
+        for i in range(cfg.n_inner):
+            z, _ = oracle.code_step(x, d, z, cfg.lam, 0.0, cfg.p, _seed(cfg), cfg.n_inner * t + i)
+        d, _, _, _ = oracle.filter_step(x, d, z)
+        oracle.objective(x, d, z, cfg.lam)
+        return d, z
+    it = oracle.iteration(x, d, z, cfg.lam, cfg.p, _seed(cfg), t)
+    return it["d"], it["z"]
+
+
+def _seed(cfg):
+    from synth import mask_seed
+    return mask_seed(cfg)
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only)."""
-    import numpy as np
+    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only; the other ranks
+    exit without work).  Each step is a bounded sample of the workload: the same iteration on
+    --ref-images of the N images with every host thread busy (the oracle's passes are parallel over
+    image rows, the code step over (image, filter)), its time scaled by N / sample to the full
+    workload (the work is linear in the number of images)."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
     import oracle
-    from synth import config_by_name, make_codes, make_filters, make_images, mask_seed
+    from synth import config_by_name, make_codes, make_filters, make_images
     cfg = config_by_name(args.config, args.p)
     n_img = max(1, min(cfg.N, args.ref_images))
     sub = cfg.with_(N=n_img)
     x, d, z = make_images(sub), make_filters(sub), make_codes(sub)
-    seed = mask_seed(cfg)
     for t in range(1, args.warmup + 1):
-        it = oracle.iteration(x, d, z, cfg.lam, cfg.p, seed, t)
-        z, d = it["z"], it["d"]
+        d, z = _oracle_step(cfg, x, d, z, t, oracle)
     times = []
     for t in range(args.warmup + 1, args.warmup + 1 + args.steps):
         t0 = time.perf_counter()
-        it = oracle.iteration(x, d, z, cfg.lam, cfg.p, seed, t)
+        d, z = _oracle_step(cfg, x, d, z, t, oracle)
         times.append(time.perf_counter() - t0)
-        z, d = it["z"], it["d"]
     per_sample = sum(times) / len(times)
-    per_full = per_sample * cfg.N / n_img  # the per-image passes dominate; scaled to the full workload
+    per_full = per_sample * cfg.N / n_img
     value = 1.0 / per_full
     cores = oracle.num_threads()
     line = {
         "impl": "reference", "metric": "csc_iterations_per_s", "value": value, "unit": "it/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_full * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64-accum/f32-state",
-        "data": "synthetic", "config": _config_dict(cfg, ws),
-        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{args.steps} oracle iterations on {n_img} of {cfg.N} images "
-                                   f"(scaled x{cfg.N / n_img:g}); {per_sample:.2f} s per sampled iteration"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 state, f64 sums (CPU oracle)", "data": "synthetic", "config": _config_dict(cfg, ws),
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "cpu_model": _cpu_model(), "kind": "oracle",
+                         "sample": f"{args.steps} steps, each the full step on {n_img} of {cfg.N} images with "
+                                   f"{cores} threads ({per_sample:.2f} s), scaled x{cfg.N / n_img:g}"},
         "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "fits_in_driver_run": True,
     }
     print(json.dumps(line), flush=True)
 
@@ -286,19 +318,18 @@ def _config_dict(cfg, ws):
             else "L2 flushed between steps"}
 
 
-def _cpu_baseline(cfg, n_img=2):
-    """Oracle on a bounded sample (rank 0, N=1 only): one iteration on n_img images, scaled."""
+def _cpu_baseline(cfg):
+    """The oracle on the host cores (rank 0, N = 1 only): ONE full step of the benched workload (all N
+    images; M = 1, no extrapolation), every host thread."""
     import oracle
-    from synth import make_codes, make_filters, make_images, mask_seed
-    sub = cfg.with_(N=n_img)
-    x, d, z = make_images(sub), make_filters(sub), make_codes(sub)
+    from synth import make_codes, make_filters, make_images
+    x, d, z = make_images(cfg), make_filters(cfg), make_codes(cfg)
     t0 = time.perf_counter()
-    oracle.iteration(x, d, z, cfg.lam, cfg.p, mask_seed(cfg), 1)
+    _oracle_step(cfg, x, d, z, 1, oracle)
     dt = time.perf_counter() - t0
-    per_full = dt * cfg.N / n_img
-    return {"value": 1.0 / per_full, "unit": "it/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"1 oracle iteration (iteration 1) on {n_img} of {cfg.N} images, {dt:.2f} s, "
-                      f"scaled x{cfg.N / n_img:g} to the full workload"}
+    return {"value": 1.0 / dt, "unit": "it/s", "cores": oracle.num_threads(), "cpu_model": _cpu_model(),
+            "kind": "oracle",
+            "sample": f"M = 1 full step (step 1) on all {cfg.N} images, {dt:.1f} s, {oracle.num_threads()} threads"}
 
 
 def run_ours(args):
@@ -307,6 +338,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1909_00145_b200 as pkg
+    from paper_1909_00145_b200 import dist as cdist
     from synth import config_by_name, make_codes, make_filters, make_images, mask_seed
 
     ws, rank, local = _dist()
@@ -315,8 +347,7 @@ def run_ours(args):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = config_by_name(args.config, args.p)
-    n0 = (rank * cfg.N) // ws
-    n1 = ((rank + 1) * cfg.N) // ws
+    n0, n1 = cdist.shard(cfg.N, ws, rank)
     nl = n1 - n0
     x_np = make_images(cfg, n0, nl)
     d_np = make_filters(cfg)
@@ -324,13 +355,7 @@ def run_ours(args):
     x = torch.from_numpy(x_np).to(dev)
     d = torch.from_numpy(d_np).to(dev)
     z = torch.zeros((nl, cfg.K, cfg.Hc, cfg.Wc), dtype=torch.float32, device=dev)
-    nccl_id = None
-    if ws > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(pkg.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    nccl_id = cdist.broadcast_nccl_id(device=dev) if ws > 1 else None
     stream = torch.cuda.current_stream(dev)
     ctx = pkg.Context(nl, cfg.K, cfg.s, cfg.H, cfg.W, world=ws, rank=rank, device=local, stream=stream,
                       nccl_id=nccl_id)
@@ -420,6 +445,12 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     staged = not (admm or bcd or sur)
+    if staged:  # one untimed staged iteration (the first call allocates the staging buffers and copy stream)
+        it += 1
+        ctx.stage_images(x_host, 0)
+        ctx.iterate_staged(x, d, z, cfg.lam, cfg.p, seed, it, 0)
+        torch.cuda.synchronize()
+    barrier()
     t0 = time.perf_counter()
     if staged:
         ctx.stage_images(x_host, 0)
@@ -449,7 +480,9 @@ def run_ours(args):
         line = {
             "metric": "csc_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 state; fp16 3-term split products on the tensor cores, fp32 accumulate, fp64 reductions",
+            "data": "synthetic",
             "config": dict(_config_dict(cfg, ws), code_solver=args.code_solver, filter_solver=args.filter_solver,
                            step_rule=args.step_rule, mask=args.mask),
             "roofline": dict(rl[dom], dominant_class=dom),
@@ -462,7 +495,165 @@ def run_ours(args):
             "clocks": clk,
         }
         if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = _cpu_baseline(cfg, args.cpu_images)
+            line["cpu_baseline"] = _cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def run_online(args):
+    """Config 4 (BASELINE.json configs[3]) as the paper's SOCSC step (Alg.2; reading #14): a
+    fresh mini-batch of 8 images per step (images 8 s .. 8 s + 7 of the seeded stream, sharded over the
+    ranks), codes reset to zero, 10 masked code steps with mask iterations 10 s + i, the projected-gradient
+    filter step and the objective over the batch.  The zero / code / filter sequence is captured once as a
+    CUDA graph on the library's stream and replayed every step (the mask iterations come from a
+    device-side offset, csc_set_iter_offset); the objective (a host read) follows each replay."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1909_00145_b200 as pkg
+    from paper_1909_00145_b200 import dist as cdist
+    from synth import config_by_name, make_filters, make_images, mask_seed
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = config_by_name(args.config, args.p)
+    nb, n_inner = cfg.N, cfg.n_inner
+    n0, n1 = cdist.shard(nb, ws, rank)
+    nl = n1 - n0
+    n_steps = args.warmup + 2 + 2 * args.steps
+    pool = np.stack([make_images(cfg, nb * st + n0, nl) for st in range(n_steps)])
+    pool_dev = torch.from_numpy(pool).to(dev)
+    pool_pin = torch.from_numpy(pool).pin_memory()
+    d = torch.from_numpy(make_filters(cfg)).to(dev)
+    x = torch.empty((nl, cfg.H, cfg.W), dtype=torch.float32, device=dev)
+    z = torch.empty((nl, cfg.K, cfg.Hc, cfg.Wc), dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)
+    nid = cdist.broadcast_nccl_id(device=dev) if ws > 1 else None
+    ctx = pkg.Context(nl, cfg.K, cfg.s, cfg.H, cfg.W, world=ws, rank=rank, device=local, stream=stream, nccl_id=nid)
+    off = torch.zeros(1, dtype=torch.int32, device=dev)
+    ctx.set_iter_offset(off)
+    seed = mask_seed(cfg)
+
+    def calls():
+        ctx.zero_codes(x, z)
+        for i in range(n_inner):
+            ctx.code_step(x, d, z, cfg.lam, cfg.p, seed, i)
+        ctx.filter_step(x, d, z)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier(device_ids=[local])
+
+    with torch.cuda.stream(stream):
+        x.copy_(pool_dev[0])
+        calls()
+        ctx.objective(x, d, z, cfg.lam)
+        torch.cuda.synchronize()
+        l0 = ctx.launch_count
+        ctx.objective(x, d, z, cfg.lam)
+        obj_launches = ctx.launch_count - l0
+        # eager steps with per-launch event timing: the kernel-class breakdown (graphs are not profiled)
+        ctx.profile_enable(True)
+        n_prof = 3
+        for st in range(1, 1 + n_prof):
+            x.copy_(pool_dev[st])
+            off.fill_(n_inner * st)
+            calls()
+            ctx.objective(x, d, z, cfg.lam)
+        prof = ctx.profile_read()
+        ctx.profile_enable(False)
+        torch.cuda.synchronize()
+        l0 = ctx.launch_count
+        graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        calls()
+    graph_launches = ctx.launch_count - l0
+    torch.cuda.synchronize()
+
+    def step(st, src):
+        x.copy_(src[st], non_blocking=True)
+        off.fill_(n_inner * st)
+        graph.replay()
+        return ctx.objective(x, d, z, cfg.lam)
+
+    with torch.cuda.stream(stream):
+        st = 0
+        for _ in range(args.warmup):
+            step(st, pool_dev)
+            st += 1
+        clocks = ClockSampler(local)
+        clocks.start()
+        barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        t_total = 0.0
+        objs = []
+        for _ in range(args.steps):
+            ev0.record(stream)
+            F = step(st, pool_dev)
+            ev1.record(stream)
+            ev1.synchronize()
+            t_total += ev0.elapsed_time(ev1)
+            objs.append(F[0])
+            st += 1
+        torch.cuda.synchronize()
+        barrier()
+        clk = clocks.stop()
+        tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        value = args.steps / (t_ms / 1e3)
+        # e2e: each step's mini-batch uploaded from pinned host memory, the objective read back
+        step(st, pool_pin)
+        st += 1
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step(st, pool_pin)
+            st += 1
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = args.steps / (float(te.item()) / 1e3)
+    if rank == 0:
+        rl = kernel_rooflines(prof, cfg, nl, n_prof, ctx.variants)
+        dom = max(rl, key=lambda k: rl[k]["ms_per_step"])
+        eager_ms = sum(v[0] for v in prof.values()) / n_prof
+        kernels = {k: {"ms_per_step": v[0] / n_prof, "launches_per_step": v[1] / n_prof} for k, v in prof.items()}
+        line = {
+            "metric": "csc_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32 state; fp16 3-term split products on the tensor cores, fp32 accumulate, fp64 reductions",
+            "data": "synthetic",
+            "config": dict(_config_dict(cfg, ws), step="SOCSC (Alg.2): z = 0, 10 masked code steps (mask t = 10 s + i), "
+                                                       "projected-gradient filter step, objective over the batch",
+                           n_inner=n_inner, mini_batch=nb, cuda_graph=True,
+                           l2="codes 155 MB per mini-batch (partly L2-resident); a fresh batch every step"),
+            "roofline": dict(rl[dom], dominant_class=dom, note="kernel times from 3 eager profiled steps"),
+            "kernel_rooflines": rl,
+            "kernels": kernels,
+            "eager_ms_per_step_kernels": eager_ms,
+            "objective_last": objs[-1] if objs else None,
+            "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": 4 * nl * cfg.H * cfg.W,
+                    "d2h_bytes_per_step": 80},
+            "gpu_launches": (graph_launches + obj_launches) * args.steps,
+            "launches_per_step": graph_launches + obj_launches,
+            "clocks": clk,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = _cpu_baseline(cfg)
         print(json.dumps(line), flush=True)
     ctx.close()
     if ws > 1:
@@ -477,8 +668,7 @@ def main():
     ap.add_argument("--config", default="sweep")
     ap.add_argument("--p", type=float, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-images", type=int, default=1)
-    ap.add_argument("--cpu-images", type=int, default=2)
+    ap.add_argument("--ref-images", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--filter-solver", default="pg", choices=["pg", "bcd", "surrogate"],
                     help="pg: the north_star projected-gradient filter step (default); bcd: the paper's "
@@ -495,6 +685,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "online":
+        run_online(args)
     else:
         run_ours(args)
 

@@ -160,6 +160,13 @@ csc_status csc_set_step_rule(csc_ctx* ctx, int rule);
 typedef enum { CSC_MASK_ENTRY = 0, CSC_MASK_SECTOR8 = 1 } csc_mask_mode;
 csc_status csc_set_mask_mode(csc_ctx* ctx, int mode);
 
+/* Device-side mask-iteration offset for CUDA-graph replays of a stream of steps: with offset_dev set
+ * (DEVICE uint32, NULL to clear), the code step's mask uses iteration iter + *offset_dev, read on the
+ * device when the mask kernel runs (a graph captured once is replayed with a new offset written into
+ * offset_dev between replays; SOCSC mask iterations 10 s + i, reading #14).  The test hooks
+ * (csc_mask_bits, csc_mask_selwords) and the ADMM solver ignore it.  CSC_ERR_ARG for a misaligned pointer. */
+csc_status csc_set_iter_offset(csc_ctx* ctx, const uint32_t* offset_dev);
+
 /* Test hook: the K step sizes tau_z of the last code step (DEVICE fp32 [K]; the same value K
  * times unless that step used the ESO rule). */
 csc_status csc_read_step_z(csc_ctx* ctx, float* tau_dev);

@@ -32,6 +32,7 @@ ABI_SYMBOLS = (
     "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd", "csc_surrogate_reset",
     "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate", "csc_set_mask_mode",
     "csc_stage_images", "csc_iterate_staged", "csc_mask_selwords", "csc_read_scalars", "csc_zg_sumsq",
+    "csc_set_iter_offset",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -93,6 +94,7 @@ def load_library(path: Optional[str] = None):
         L.csc_mask_bits.argtypes = [vp, u32, f64, u64, vp]
         L.csc_mask_selwords.argtypes = [vp, u32, f64, u64, vp, vp]
         L.csc_read_scalars.argtypes = [vp, vp]
+        L.csc_set_iter_offset.argtypes = [vp, vp]
         L.csc_zg_sumsq.argtypes = [vp, vp, vp]
         L.csc_read_residual.argtypes = [vp, vp]
         L.csc_read_grad.argtypes = [vp, vp]
@@ -321,6 +323,18 @@ class Context:
             self._check(self._L.csc_mask_selwords(self._h, int(it) & 0xffffffff, float(p), int(seed) & (2**64 - 1),
                                                   out.data_ptr(), info))
         return tuple(info)
+
+    def set_iter_offset(self, offset) -> None:
+        """Mask iteration = iter + offset[0] read on the device (include/csc.h csc_set_iter_offset);
+        offset: int32 CUDA tensor of 1 element kept alive by the caller, or None to clear."""
+        import torch
+        if offset is None:
+            self._check(self._L.csc_set_iter_offset(self._h, None))
+            return
+        if not (offset.is_cuda and offset.dtype == torch.int32 and offset.numel() >= 1):
+            raise ValueError("offset must be an int32 CUDA tensor")
+        self._iter_off = offset
+        self._check(self._L.csc_set_iter_offset(self._h, offset.data_ptr()))
 
     def read_scalars(self) -> dict:
         """Device scalars after the last steps (include/csc.h csc_read_scalars)."""

@@ -138,6 +138,7 @@ struct csc_ctx {
   int64_t sur_t = 0;
   bool last_eso = false;       // the last code step used per-filter taus
   int mask_mode = CSC_MASK_ENTRY;  // csc_set_mask_mode
+  const uint32_t* iter_off = nullptr;  // csc_set_iter_offset: device-side mask-iteration offset
   // double-buffered image staging (csc_stage_images / csc_iterate_staged)
   cudaStream_t cp_st = nullptr;
   float* stage[2] = {nullptr, nullptr};
@@ -731,7 +732,8 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   if (g.N > 0) {
     if (c->ct_on) {
       if (!all_selected)
-        CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(g, c->ct, seed, iter, thr, c->mwords, c->st, c->mask_mode));
+        CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_selwords(g, c->ct, seed, iter, thr, c->mwords, c->st, c->mask_mode,
+                                                                 c->iter_off));
       if (c->ct.half) {
         // masked step fused with the incremental residual r' = r + D dz (a3'): the cache then holds
         // D z_new - x for (x, d, z) and the filter step needs no dense residual pass
@@ -747,7 +749,9 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
                                          lambda, zbound(c, z), c->st, tau_stride));
       }
     } else {
-      if (!all_selected) CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st, c->mask_mode));
+      if (!all_selected)
+        CSC_LAUNCH_C(c, CSC_K_MASK, 1, csc::launch_mask_colwords(g, seed, iter, thr, c->colw, c->st, c->mask_mode,
+                                                                 c->iter_off));
       CSC_LAUNCH_C(c, CSC_K_CODE_STEP, 1, csc::launch_code_step(g, c->r, d, z, c->colw, all_selected, tau_dev, lambda,
                                                                 zbound(c, z), c->st, tau_stride));
     }
@@ -780,6 +784,13 @@ csc_status csc_set_mask_mode(csc_ctx* c, int mode) {
   if (!c) return CSC_ERR_ARG;
   if (mode != CSC_MASK_ENTRY && mode != CSC_MASK_SECTOR8) return fail(c, CSC_ERR_ARG, "unknown mask mode");
   c->mask_mode = mode;
+  return CSC_OK;
+}
+
+csc_status csc_set_iter_offset(csc_ctx* c, const uint32_t* offset_dev) {
+  if (!c) return CSC_ERR_ARG;
+  if (offset_dev != nullptr && !aligned4(offset_dev)) return fail(c, CSC_ERR_ARG, "offset_dev must be a device pointer");
+  c->iter_off = offset_dev;
   return CSC_OK;
 }
 

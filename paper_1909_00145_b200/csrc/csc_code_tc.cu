@@ -331,7 +331,9 @@ __device__ __forceinline__ uint32_t word_of(const uint4& b, int i) {
   return i == 0 ? b.x : (i == 1 ? b.y : (i == 2 ? b.z : b.w));
 }
 __global__ void mask_selwords_kernel(int K, int KC, int NC, int nper, int nblk, int64_t plane, uint64_t seed,
-                                     uint32_t iter, uint64_t thr, int mode, uint32_t* __restrict__ sw) {
+                                     uint32_t iter, const uint32_t* __restrict__ iter_off, uint64_t thr, int mode,
+                                     uint32_t* __restrict__ sw) {
+  if (iter_off != nullptr) iter += *iter_off;  // device-side step counter (CUDA-graph replays)
   const int64_t nq = (plane + 3) / 4;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= static_cast<int64_t>(nblk) * nq) return;
@@ -442,12 +444,13 @@ CodeTcPlan code_tc_plan(const Geom& g, int num_sms) {
 }
 
 cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
-                                 uint32_t* words, cudaStream_t st, int mode) {
+                                 uint32_t* words, cudaStream_t st, int mode, const uint32_t* iter_off) {
   const int64_t plane = static_cast<int64_t>(g.Hc) * g.Wc;
   const int nblk = p.wper * p.nkg;
   const int64_t total = static_cast<int64_t>(nblk) * ((plane + 3) / 4);
   mask_selwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g.K, p.KC, p.wnc, p.wper, nblk,
-                                                                                 plane, seed, iter, thr, mode, words);
+                                                                                 plane, seed, iter, iter_off, thr, mode,
+                                                                                 words);
   return cudaGetLastError();
 }
 

@@ -89,8 +89,9 @@ cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, do
 // Mask (Philox4x32-10) -- internal column-word layout for the code step:
 //   colw[(k*NB + ub)*Wc + v] bit r = mask(k, 32*ub + r, v), NB = ceil(Hc/32).
 // mode 0: per-entry Bernoulli (Eq.2); mode 1: one draw per aligned 8-coordinate block (E5)
+// iter_off (device, nullable): the mask iteration is iter + *iter_off, read at launch (graph replays)
 cudaError_t launch_mask_colwords(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr,
-                                 uint32_t* colw, cudaStream_t st, int mode = 0);
+                                 uint32_t* colw, cudaStream_t st, int mode = 0, const uint32_t* iter_off = nullptr);
 // Canonical layout for the test hook.
 cudaError_t launch_mask_bits(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr,
                              uint32_t* bits, cudaStream_t st, int mode = 0);
@@ -195,7 +196,7 @@ bool code_tc_supported(const Geom& g);
 CodeTcPlan code_tc_plan(const Geom& g, int num_sms);
 // Mask as selection words sw[wper*nkg][Hc*Wc]: bit i of sw[kg*wper+cb][p] = mask(kg*KC + cb*wnc + i, p).
 cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t seed, uint32_t iter, uint64_t thr,
-                                 uint32_t* words, cudaStream_t st, int mode = 0);
+                                 uint32_t* words, cudaStream_t st, int mode = 0, const uint32_t* iter_off = nullptr);
 // fp16-split variant (csc_code_h.cu): Hc*Wc % 4 == 0 (TMA view of z); rmax = max|r| (float bits).
 bool code_h_supported(const Geom& g);
 CodeTcPlan code_h_plan(const Geom& g, int num_sms);

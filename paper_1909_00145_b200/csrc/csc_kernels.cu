@@ -153,8 +153,9 @@ __global__ void mask_bits_kernel(uint64_t total, uint64_t seed, uint32_t iter, u
 
 // Column-word layout for the code step: thread per (k, ub, quad of 4 columns);
 // colw[(k*NB+ub)*Wc+v] bit r = mask(k, 32*ub+r, v).  Rows >= Hc are 0.
-__global__ void mask_colwords_kernel(Geom g, int NB, uint64_t seed, uint32_t iter, uint64_t thr, int mode,
-                                     uint32_t* __restrict__ colw) {
+__global__ void mask_colwords_kernel(Geom g, int NB, uint64_t seed, uint32_t iter, const uint32_t* iter_off,
+                                     uint64_t thr, int mode, uint32_t* __restrict__ colw) {
+  if (iter_off != nullptr) iter += *iter_off;  // device-side step counter (CUDA-graph replays)
   const int nq = (g.Wc + 3) / 4;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t total = static_cast<int64_t>(g.K) * NB * nq;
@@ -841,11 +842,11 @@ cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, do
 }
 
 cudaError_t launch_mask_colwords(const Geom& g, uint64_t seed, uint32_t iter, uint64_t thr, uint32_t* colw,
-                                 cudaStream_t st, int mode) {
+                                 cudaStream_t st, int mode, const uint32_t* iter_off) {
   const int NB = ceil_div(g.Hc, 32);
   const int64_t total = static_cast<int64_t>(g.K) * NB * ceil_div(g.Wc, 4);
-  mask_colwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g, NB, seed, iter, thr, mode,
-                                                                                    colw);
+  mask_colwords_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(g, NB, seed, iter, iter_off, thr,
+                                                                                    mode, colw);
   return cudaGetLastError();
 }
 

@@ -3,7 +3,8 @@ part 7: the online configuration is launch-bound, so its inner loop is replayed 
 
 One step of Alg.2 (reading #14): zero codes, 10 masked code steps (mask iterations
 10 s + i), the projected-gradient filter step.  Captured once on the context's stream, replayed on
-fresh mini-batches, it must produce the same codes and filters as the same calls issued eagerly on a
+fresh mini-batches with the step's mask iterations supplied through the device-side offset
+(csc_set_iter_offset), it must produce the same codes and filters as the same calls issued eagerly on a
 second context (same kernels in the same order: bit-identical), and the eager run matches the oracle."""
 import numpy as np
 import pytest
@@ -38,6 +39,9 @@ def test_socsc_step_graph_replay():
             ctx.code_step(x, d, z, cfg.lam, cfg.p, seed, n_inner * step + i)
         ctx.filter_step(x, d, z)
 
+    off = torch.zeros(1, dtype=torch.int32, device=dev)
+    cg.set_iter_offset(off)
+
     # warm-up (first launches configure the kernels), then capture step 0's sequence
     xg.copy_(torch.from_numpy(make_images(cfg, 0, cfg.N)))
     with torch.cuda.stream(s_cap):
@@ -48,7 +52,7 @@ def test_socsc_step_graph_replay():
     with torch.cuda.graph(graph, stream=s_cap):
         socsc(cg, xg, dg, zg, 0)
     torch.cuda.synchronize()
-    # replay on fresh mini-batches (the mask iterations are those of step 0 captured in the graph)
+    # replay on fresh mini-batches: step s uses mask iterations 10 s + i through the device offset
     dg.copy_(torch.from_numpy(d0))
     de = torch.from_numpy(d0).to(dev)
     xe = torch.empty_like(xg)
@@ -56,12 +60,14 @@ def test_socsc_step_graph_replay():
     d_or = d0.copy()
     for b in range(3):
         xb = torch.from_numpy(make_images(cfg, cfg.N * (b + 1), cfg.N))
+        step = b + 1
         xg.copy_(xb)
         xe.copy_(xb)
+        off.fill_(n_inner * step)
         torch.cuda.synchronize()
         graph.replay()
         with torch.cuda.stream(s_eag):
-            socsc(ce, xe, de, ze, 0)
+            socsc(ce, xe, de, ze, step)
         torch.cuda.synchronize()
         assert torch.equal(zg, ze), b
         assert torch.equal(dg, de), b
@@ -69,7 +75,7 @@ def test_socsc_step_graph_replay():
         xn = xb.numpy()
         z = np.zeros((cfg.N, cfg.K, cfg.Hc, cfg.Wc), np.float32)
         for i in range(n_inner):
-            z, _ = oracle.code_step(xn, d_or, z, cfg.lam, 0.0, cfg.p, seed, i)
+            z, _ = oracle.code_step(xn, d_or, z, cfg.lam, 0.0, cfg.p, seed, n_inner * step + i)
         d_or, _, _, _ = oracle.filter_step(xn, d_or, z)
         assert rel_err(ze.cpu().numpy(), z) < 1e-5, b
         assert rel_err(de.cpu().numpy(), d_or) < 1e-5, b
