@@ -905,7 +905,7 @@ csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float*
     if (c->tc_on && c->tc.half) {
       CSC_LAUNCH_C(c, CSC_K_CONV, (first_conv ? 1 : 0) + c->tc.nks,
                    csc::launch_conv_h(g, c->tc, &c->tm_conv_adm, c->adm_zd, d, c->tc_bimg, c->adm_bound, c->smax + 1,
-                                      c->tc_part, nullptr, c->st, first_conv));
+                                      c->tc_part, nullptr, c->st, first_conv, /*precise=*/true));
       CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
                    csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, E, csc::kConvResidual, c->sq_part, c->st));
       first_conv = false;

@@ -193,6 +193,7 @@ struct ChArgs {
   int b_bytes;           // one of hi / lo: 2 K-atoms x Npad rows x 128 B
   int plain;             // 1: z <- c at every position (no z read, no step / shrinkage / mask / a3')
   int tau_stride;        // 0: tau[0] for every filter; 1: tau[k] per filter (ESO rule)
+  int precise;           // plain mode: hi*hi and the cross terms in separate accumulators
   unsigned long long* dbg;  // CSC_ROLE_TIMING: [grid][4 roles][8] cycle counters
 };
 
@@ -226,6 +227,8 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
   const int gi = blockIdx.x % A.G, kg = blockIdx.x / A.G;
   const bool plain = A.plain != 0;
   const bool a3p = !plain && A.part != nullptr;
+  // plain mode (ADMM's D^T e) with separate hi*hi / cross accumulators, single-buffered (T3)
+  const bool prec = plain && A.precise != 0;
   const uint32_t raw = su32(smraw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* sm = smraw + (base - raw);
@@ -353,10 +356,11 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     for (int item = gi; item < A.nitems; item += A.G) {
       const ChItem it = ch_item(A, item);
       for (int tl = 0; tl < it.ntiles; ++tl, ++tcount) {
-        const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        const uint32_t buf = prec ? 0u : (tcount & 1u), use = prec ? tcount : (tcount >> 1);
         RT_WAIT(rc, 0, mbar_wait_backoff(&acc_empty[buf], (use & 1u) ^ 1u, 32));
         tc_after();
         const uint32_t dcol = t_acc + buf * static_cast<uint32_t>(A.Npad);
+        const uint32_t dxc = prec ? dcol + static_cast<uint32_t>(A.Npad) : dcol;  // cross-term accumulator
         for (int j = 0; j < 2; ++j, ++g) {  // 2 slots of 4 K16-steps (64 taps)
           const uint32_t slot = g % kChNS, ph = (g / kChNS) & 1u;
           RT_WAIT(rc, 1, mbar_wait_backoff(&a_full[slot], ph, 32));
@@ -369,14 +373,15 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
             const uint64_t dbl = sdesc(sbl + j * katom + 32u * e, 16u, 1024u, kLayout128B);
             const uint32_t acc0 = (j > 0 || e > 0) ? 1u : 0u;
             asm volatile(
-                "{\n.reg .pred e, p, t;\n"
+                "{\n.reg .pred e, p, t, x;\n"
                 "elect.sync _|e, 0xffffffff;\n"
-                "setp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 1, 1;\n"
+                "setp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 1, 1;\nsetp.ne.b32 x, %8, 0;\n"
                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %4, p;\n"
-                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %6, %4, t;\n"
-                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %4, t;\n"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%7], [%1], %6, %4, x;\n"
+                "@e tcgen05.mma.cta_group::1.kind::f16 [%7], [%2], %3, %4, t;\n"
                 "}\n" ::"r"(dcol),
-                "r"(ah + 8u * e), "r"(ah + 32u + 8u * e), "l"(dbh), "r"(idesc), "r"(acc0), "l"(dbl)
+                "r"(ah + 8u * e), "r"(ah + 32u + 8u * e), "l"(dbh), "r"(idesc), "r"(acc0), "l"(dbl), "r"(dxc),
+                "r"(prec ? acc0 : 1u)
                 : "memory");
           }
           mma_commit_elect(&a_empty[slot]);
@@ -533,7 +538,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     for (int s0 = 0; s0 < kChChunks; ++s0) issue(item, tl, it, 0u, s0);
     if (ni < A.nitems) step(ni, ntl, nit);
     while (item < A.nitems) {
-      const uint32_t buf = tcount & 1u, use = tcount >> 1;
+      const uint32_t buf = prec ? 0u : (tcount & 1u), use = prec ? tcount : (tcount >> 1);
       const int p = it.p0 + tl * kChTile + 32 * q + lane;
       const bool pok = p < it.p1;
       const int ga = static_cast<int>((jq + tcount) % kChEpiPerQ);
@@ -564,6 +569,16 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 8; ++i) c[8 + i] = c8[i];
+          if (prec) {  // + the cross-term accumulator (fp32 add, round to nearest)
+            const uint32_t cx = colb + static_cast<uint32_t>(A.Npad) + 16u * gg;
+            tmem_ld8_nowait(tq + cx, c8);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) c[i] += c8[i];
+            tmem_ld8_nowait(tq + cx + 8u, c8);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) c[8 + i] += c8[i];
+          }
         }
         float* zb = zrow + static_cast<size_t>(16 * gg) * plane;
         if (plain) {
@@ -872,6 +887,7 @@ cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, TmapCache* tmc, co
   a.BR = p.BR; a.nbands = p.nbands; a.nitems = p.nitems; a.WL = p.WL;
   a.pitch = p.pitch; a.rs_floats = p.rs_floats; a.b_bytes = p.b_bytes;
   a.plain = plain ? 1 : 0;
+  a.precise = plain ? 1 : 0;  // the plain correlation (ADMM) always takes the precise accumulation
   a.tau_stride = tau_stride;
   if (plain) {
     a.mask = nullptr;

@@ -1,12 +1,12 @@
 """GPU parity of the ADMM masked-LASSO code solver (
 include/csc.h csc_code_step_admm) against oracle.admm_code_step (pinned in tests/test_oracle_admm.py).
 
-Bar: codes within TOL_ADMM relative (norm-wise, reading R9) of the fp64 oracle after one step of
-10 ADMM x 5 CG iterations; codes off the mask bit-identical (R2).  TOL_ADMM = 2e-5 is derived in
-DESIGN.md reading A7: one step applies the operator 50 times, and the output's relative error is
-~7-10x the per-application relative error (measured by perturbing an fp64 dense-matrix run,
-tests/test_admm_tolerance.py); the dense passes carry ~1e-6 per application after cancellation
-(fp16 / tf32 3-term splits, fp32 accumulation), so ~1e-5 is expected and 2e-5 is the bar.
+Bar: codes within TOL_ADMM = 1e-5 relative (norm-wise, reading R9) of the fp64 oracle after one step
+of 10 ADMM x 5 CG iterations (the north_star bar); codes off the mask bit-identical (R2).  One step
+applies the operator 50 times and amplifies a per-application relative error ~7-10x
+(tests/test_admm_tolerance.py, reading A7); the operator's tensor-core passes therefore
+accumulate the hi*hi products and the cross products of the fp16 split in separate TMEM
+accumulators (reading T3), which keeps the per-application error near 1e-7.
 """
 import numpy as np
 import pytest
@@ -17,7 +17,7 @@ from tests.conftest import rel_err
 
 pytestmark = pytest.mark.gpu
 
-TOL_ADMM = 2e-5
+TOL_ADMM = 1e-5
 
 
 @pytest.fixture(scope="module")
