@@ -217,13 +217,15 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     __syncwarp();
   } else if (warp < kHEpiBase) {
     // ================================ converters: a pair of warps per stage slot (g mod kHNS = cw / 2)
-    // thread job (row k, 8 positions 8j..8j+7): raw floats 8j..8j+7 of row k (row pitch 512 B);
-    // fp16 chunk j%8 of atom j/8, row k, at 16-B chunk (j%8) ^ (k%8)
+    // a warp converts whole rows: lane i takes raw floats 4i..4i+3 of row k (one conflict-free 512-B
+    // row per warp instruction) and writes their fp16 hi / lo as the 8-B half (i & 1) of the 16-B chunk
+    // (i/2) & 7 of atom i/16, swizzled to chunk ((i/2) & 7) ^ (k & 7) (SWIZZLE_128B, MN-major)
     const int cw = warp - kHConvBase;
     const bool want_l1 = A.l1_part != nullptr;
     const float sz = exp2i(ez);
     double l1 = 0.0;
     uint32_t g = 0;
+    const int atom = lane >> 4, cidx = (lane >> 1) & 7, half8 = (lane & 1) * 8;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t) {
@@ -237,30 +239,20 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           uint8_t* lop = hip + kHHalfBytes;
           float s1 = 0.f;
 #pragma unroll 4
-          for (int rep = 0; rep < 4; ++rep) {
-            const int job = lane + 32 * (2 * rep + (cw & 1));   // 0..255, the pair splits the stage
-            const int k = job >> 4, j = job & 15;
-            const float4* src = reinterpret_cast<const float4*>(rawp + k * 512 + j * 32);
-            const float4 x0 = src[0], x1 = src[1];
-            float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-            uint32_t hv[4], lv[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float a = v[2 * i] * sz, b = v[2 * i + 1] * sz;
-              const float ha = rn11(a), hb = rn11(b);
-              hv[i] = pack_h2(ha, hb);
-              lv[i] = pack_h2(a - ha, b - hb);
-            }
-            const int off = (j >> 3) * 2048 + k * 128 + (((j & 7) ^ (k & 7)) << 4);
-            *reinterpret_cast<uint4*>(hip + off) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-            *reinterpret_cast<uint4*>(lop + off) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+          for (int rr = 0; rr < 8; ++rr) {
+            const int k = 2 * rr + (cw & 1);  // the pair splits the stage's 16 rows
+            const float4 x0 = reinterpret_cast<const float4*>(rawp + k * 512)[lane];
+            const float a0 = x0.x * sz, a1 = x0.y * sz, a2 = x0.z * sz, a3 = x0.w * sz;
+            const float h0 = rn11(a0), h1 = rn11(a1), h2 = rn11(a2), h3 = rn11(a3);
+            const int off = atom * 2048 + k * 128 + ((cidx ^ (k & 7)) << 4) + half8;
+            *reinterpret_cast<uint2*>(hip + off) = make_uint2(pack_h2(h0, h1), pack_h2(h2, h3));
+            *reinterpret_cast<uint2*>(lop + off) = make_uint2(pack_h2(a0 - h0, a1 - h1), pack_h2(a2 - h2, a3 - h3));
             if (want_l1) {
               const int kk = A.ks * A.KC + 16 * c + k;
-              const int p = pt + 8 * j;
+              const int p = pt + 4 * lane;
               if (kk < A.K) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  if (p + i < it.pend) s1 += fabsf(v[i]);
+                s1 += (p < it.pend ? fabsf(x0.x) : 0.f) + (p + 1 < it.pend ? fabsf(x0.y) : 0.f) +
+                      (p + 2 < it.pend ? fabsf(x0.z) : 0.f) + (p + 3 < it.pend ? fabsf(x0.w) : 0.f);
               }
             }
           }
@@ -307,11 +299,11 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
             dnv[i] = 0.f;
             if (i >= na) continue;
             const int a = a_beg + i;
-            float y[16];
-            tmem_ld16_nowait(tacc + a * S, y);
+            float y[S];
+            tmem_ld_row<S>(tacc + a * S, y);
             if (A.precise) {
-              float y2[16];
-              tmem_ld16_nowait(tacc + 128u + a * S, y2);
+              float y2[S];
+              tmem_ld_row<S>(tacc + 128u + a * S, y2);
               tmem_ld_wait();
 #pragma unroll
               for (int b = 0; b < S; ++b) y[b] += y2[b];

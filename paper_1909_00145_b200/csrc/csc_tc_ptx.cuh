@@ -123,6 +123,50 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float (&f)[16])
 #pragma unroll
   for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
 }
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, float (&f)[8]) {
+  uint32_t v[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[i]);
+}
+// the S accumulator columns of one tap row (exact widths: no TMEM read bandwidth spent on padding)
+__device__ __forceinline__ void tmem_ld_x1(uint32_t taddr, float& f) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(v) : "r"(taddr) : "memory");
+  f = __uint_as_float(v);
+}
+__device__ __forceinline__ void tmem_ld_x2(uint32_t taddr, float& f0, float& f1) {
+  uint32_t v0, v1;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(v0), "=r"(v1) : "r"(taddr) : "memory");
+  f0 = __uint_as_float(v0);
+  f1 = __uint_as_float(v1);
+}
+template <int S>
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&y)[S]) {
+  int c = 0;
+  if constexpr (S >= 8) {
+    float t[8];
+    tmem_ld8_nowait(taddr, t);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) y[i] = t[i];
+    c = 8;
+  }
+  if constexpr ((S & 4) != 0) {
+    float t[4];
+    tmem_ld4_nowait(taddr + c, t);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) y[(S >= 8 ? 8 : 0) + i] = t[i];
+  }
+  constexpr int c2 = (S >= 8 ? 8 : 0) + ((S & 4) != 0 ? 4 : 0);
+  if constexpr ((S & 2) != 0) tmem_ld_x2(taddr + c2, y[c2], y[c2 + 1]);
+  constexpr int c1 = c2 + ((S & 2) != 0 ? 2 : 0);
+  if constexpr ((S & 1) != 0) tmem_ld_x1(taddr + c1, y[c1]);
+  (void)c;
+}
+
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
