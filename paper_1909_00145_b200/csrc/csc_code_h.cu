@@ -50,13 +50,12 @@ namespace {
 using namespace tcx;
 
 constexpr int kChNS = 2;          // im2col slots (4 K16-steps = 64 taps each) in TMEM
-constexpr int kChConvWarps = 4;
 constexpr int kChEpiWarps = 12;  // 3 per TMEM lane quarter
-constexpr int kChColWarps = 8;   // 2 per TMEM lane quarter (tap rows split)
+constexpr int kChHelpWarps = 8;  // 2 per TMEM lane quarter: the im2col of the next tile and the col2im of the last
 constexpr int kChEpiPerQ = kChEpiWarps / 4;
 constexpr int kChChunks = (8 + kChEpiPerQ - 1) / kChEpiPerQ;  // 16-filter groups per warp per tile (Npad <= 128)
-constexpr int kChConvBase = 1, kChEpiBase = kChConvBase + kChConvWarps, kChColBase = kChEpiBase + kChEpiWarps;
-constexpr int kChWarps = kChColBase + kChColWarps;
+constexpr int kChEpiBase = 1, kChHelpBase = kChEpiBase + kChEpiWarps;
+constexpr int kChWarps = kChHelpBase + kChHelpWarps;
 constexpr int kChThreads = 32 * kChWarps;
 constexpr int kChTile = 128;
 constexpr int kChSmemMax = 226 * 1024;
@@ -151,6 +150,7 @@ struct ChArgs {
   int tau_stride;        // 0: tau[0] for every filter; 1: tau[k] per filter (ESO rule)
   int precise;           // plain mode: hi*hi and the cross terms in separate accumulators
   unsigned long long* dbg;  // CSC_ROLE_TIMING: [grid][4 roles][8] cycle counters
+  int dbgflags;             // CSC_ROLE_TIMING builds: CSC_CH_DBG experiment switches
 };
 
 struct ChItem {
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
   fence_async_shared();
   if (tid == 0) {
     for (int i = 0; i < kChNS; ++i) {
-      mbar_init(&a_full[i], kChConvWarps);
+      mbar_init(&a_full[i], kChHelpWarps);
       mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       mbar_init(&dz_full[i], kChEpiWarps);
     }
     mbar_init(&y_full, 1);
-    mbar_init(&y_empty, kChColWarps);
+    mbar_init(&y_empty, kChHelpWarps);
     for (int w = 0; w < kChEpiWarps; ++w)
       for (int c = 0; c < kChChunks; ++c) mbar_init(&zfull[w][c], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -349,96 +349,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     if (a3p && tcount > 0) gemm2(tcount - 1);
     __syncwarp();
     if (lane == 0) RT_DUMP(rc, A.dbg, 0);
-  } else if (warp < kChEpiBase) {
-    // ================================ converters: im2col(r) -> TMEM, two fp16 taps per column
-    const int cw = warp - kChConvBase;  // 0..7
-    const int q = warp & 3;
-    const uint32_t tq = (static_cast<uint32_t>(32 * q) << 16);
-    const int ct = tid - 32 * kChConvBase;
-    const float sr = exp2i_h(er);
-    RoleClock rc;
-    // The band's residual rows u0-P .. u1-1 (columns -P .. Wc-1, zero outside the image), scaled by
-    // 2^er and split once per band into fp16 hi / lo PAIRS: hp[row][c] = (hi(r[row][c-P]), hi(r[row][c-P+1])),
-    // lp likewise.  A TMEM column of the im2col holds two consecutive taps (a, b), (a, b+1) of one
-    // position, which is then a single 32-bit shared load of each array (no per-tap arithmetic).
-    uint32_t* hp = reinterpret_cast<uint32_t*>(rs);
-    uint32_t* lp = hp + A.rs_floats;
-    auto fill = [&](int item) {
-      const ChItem it = ch_item(A, item);
-      const float* rn = A.r + static_cast<size_t>(it.n) * A.H * A.W;
-      for (int e = ct; e < A.rs_floats; e += 32 * kChConvWarps) {
-        const int rho = e / A.pitch, c = e - rho * A.pitch;
-        const int i = it.u0 - P + rho, jj = c - P;
-        const bool iok = i >= 0 && i < A.H;
-        const float* rr = rn + static_cast<size_t>(iok ? i : 0) * A.W;
-        const float x0 = (iok && jj >= 0 && jj < A.W) ? __ldg(rr + jj) * sr : 0.f;
-        const float x1 = (iok && jj + 1 >= 0 && jj + 1 < A.W) ? __ldg(rr + jj + 1) * sr : 0.f;
-        const float h0 = rn11_h(x0), h1 = rn11_h(x1);
-        hp[e] = pack_h2_h(h0, h1);
-        lp[e] = pack_h2_h(x0 - h0, x1 - h1);
-      }
-    };
-    {
-      uint32_t g = 0;
-      for (int item = gi; item < A.nitems; item += A.G) {
-        const ChItem it = ch_item(A, item);
-        RT_WAIT(rc, 2, named_sync(1, 32 * kChConvWarps));  // every converter is done with the last band
-        fill(item);
-        RT_WAIT(rc, 0, named_sync(1, 32 * kChConvWarps));
-        for (int tl = 0; tl < it.ntiles; ++tl) {
-          const int p = it.p0 + tl * kChTile + 32 * q + lane;
-          const bool pok = p < it.p1;
-          const int u = p / A.Wc, v = p - u * A.Wc;
-          const int o = pok ? (u - it.u0) * A.pitch + v : 0;
-          const uint32_t* sh = hp + o;
-          const uint32_t* sl = lp + o;
-#pragma unroll
-          for (int j = 0; j < 2; ++j, ++g) {  // slot j: taps 64 j .. 64 j + 63
-            const uint32_t slot = g % kChNS, ph = (g / kChNS) & 1u;
-            RT_WAIT(rc, 1, mbar_wait_backoff(&a_empty[slot], ph ^ 1u, 512));
-            tc_after();
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {  // K16-step within the slot
-              uint32_t hv[8], lv[8];
-#pragma unroll
-              for (int jj = 0; jj < 8; ++jj) {
-                const int t0 = 64 * j + 16 * e + 2 * jj, t1 = t0 + 1;
-                const int a0 = t0 / S, b0 = t0 % S, a1 = t1 / S, b1 = t1 % S;
-                uint32_t xh = 0u, xl = 0u;
-                if (t0 < S2) {
-                  const int o0 = a0 * A.pitch + b0;
-                  if (t1 < S2 && a1 == a0) {  // both taps in one row: the stored pair
-                    xh = sh[o0];
-                    xl = sl[o0];
-                  } else {                     // the pair straddles two tap rows (or ends the taps)
-                    const uint32_t h0 = sh[o0], l0 = sl[o0];
-                    if (t1 < S2) {
-                      const int o1 = a1 * A.pitch + b1;
-                      xh = __byte_perm(h0, sh[o1], 0x5410);
-                      xl = __byte_perm(l0, sl[o1], 0x5410);
-                    } else {
-                      xh = h0 & 0xFFFFu;
-                      xl = l0 & 0xFFFFu;
-                    }
-                  }
-                }
-                hv[jj] = pok ? xh : 0u;
-                lv[jj] = pok ? xl : 0u;
-              }
-              const uint32_t col = t_a + slot * 64u + 8u * e;
-              tmem_st8(tq + col, hv);
-              tmem_st8(tq + col + 32u, lv);
-            }
-            tmem_st_wait();
-            tc_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&a_full[slot]);
-          }
-        }
-      }
-    }
-    if (cw == 0 && lane == 0) RT_DUMP(rc, A.dbg, 1);
-  } else if (warp < kChColBase) {
+  } else if (warp < kChHelpBase) {
     // ================================ epilogue: z <- S(z - tau c) on masked codes, dz -> TMEM
     const int ew = warp - kChEpiBase;  // 0..15
     const int q = warp & 3;
@@ -516,6 +427,12 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
         const int k0 = kbase + 16 * gg;
         const uint32_t kv = kvalid(k0);
         float c[16];
+#ifdef CSC_ROLE_TIMING
+        if (A.dbgflags & 2) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) c[i] = 0.f;
+        } else
+#endif
         {
           float c8[8];
           tmem_ld8_nowait(tq + colb + 16u * gg, c8);
@@ -553,33 +470,57 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
         __syncwarp();
         issue(ni, ntl, nit, tcount + 1, s);  // refill the chunk with the next tile's slice
         uint32_t hv[8], lv[8];
+        // filters past the group's end are padding (K = 100: 4 of the last group's 16 are real)
+        const int npair = kv == 0xFFFFu ? 8 : (32 - __clz(kv) + 1) >> 1;
         auto body = [&](auto per_k) {
           constexpr bool PK = decltype(per_k)::value;
           float* zp = zb;
 #pragma unroll
           for (int i2 = 0; i2 < 8; ++i2) {
-            float dzp[2];
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              const int i = 2 * i2 + h2;
-              const float tk = PK ? __ldg(A.tau + min(k0 + i, A.K - 1)) : tau;
-              const float kk = PK ? tk * A.lam : kappa;
-              // -tau * (c * 2^-(er+ed)) with one multiply: scaling by a power of two is exact
-              const float w = fmaf(PK ? -tk * inv : ntinv, c[i], zc[i]);
-              const float nz = w - fminf(fmaxf(w, -kk), kk);  // S_kk(w): w -/+ kk outside [-kk, kk], +0 inside
-              const bool ch = (wb & (1u << i)) != 0u && nz != zc[i];
-              if (ch) *zp = nz;
-              zp += plane;
-              // max |z| bound: every code of the slice was loaded, so |S(z - tau c)| over all of them bounds
-              // the changed codes and the unchanged ones keep the previous bound
-              wmax = fmaxf(wmax, fabsf(nz));
-              dzp[h2] = ch ? (nz - zc[i]) * sdz : 0.f;
+            if (i2 >= npair) {  // warp-uniform
+              hv[i2] = 0u;
+              lv[i2] = 0u;
+              continue;
             }
-            const float h0 = rn11_h(dzp[0]), h1 = rn11_h(dzp[1]);
+            const int i = 2 * i2;
+            // -tau * (c * 2^-(er+ed)) with one multiply: scaling by a power of two is exact; the pair of
+            // codes goes through the packed fp32 pipe (FFMA2 / FADD2 / FMUL2, each lane exact fp32)
+            float tk0 = tau, tk1 = tau, kk0 = kappa, kk1 = kappa;
+            if (PK) {
+              tk0 = __ldg(A.tau + min(k0 + i, A.K - 1));
+              tk1 = __ldg(A.tau + min(k0 + i + 1, A.K - 1));
+              kk0 = tk0 * A.lam;
+              kk1 = tk1 * A.lam;
+            }
+            const float2 zc2 = make_float2(zc[i], zc[i + 1]);
+            const float2 w = __ffma2_rn(PK ? make_float2(-tk0 * inv, -tk1 * inv) : make_float2(ntinv, ntinv),
+                                        make_float2(c[i], c[i + 1]), zc2);
+            const float2 cl = make_float2(fminf(fmaxf(w.x, -kk0), kk0), fminf(fmaxf(w.y, -kk1), kk1));
+            const float2 nz = __fadd2_rn(w, make_float2(-cl.x, -cl.y));  // S_kk(w): w -/+ kk outside, +0 inside
+            const bool ch0 = (wb & (1u << i)) != 0u && nz.x != zc2.x;
+            const bool ch1 = (wb & (2u << i)) != 0u && nz.y != zc2.y;
+            if (ch0) *zp = nz.x;
+            zp += plane;
+            if (ch1) *zp = nz.y;
+            zp += plane;
+            // max |z| bound: every code of the slice was loaded, so |S(z - tau c)| over all of them bounds
+            // the changed codes and the unchanged ones keep the previous bound
+            wmax = fmaxf(wmax, fmaxf(fabsf(nz.x), fabsf(nz.y)));
+            const float2 dz = __fmul2_rn(__fadd2_rn(make_float2(ch0 ? nz.x : zc2.x, ch1 ? nz.y : zc2.y),
+                                                    make_float2(-zc2.x, -zc2.y)),
+                                         make_float2(sdz, sdz));
+            const float h0 = rn11_h(dz.x), h1 = rn11_h(dz.y);
+            const float2 lo = __fadd2_rn(dz, make_float2(-h0, -h1));
             hv[i2] = pack_h2_h(h0, h1);
-            lv[i2] = pack_h2_h(dzp[0] - h0, dzp[1] - h1);
+            lv[i2] = pack_h2_h(lo.x, lo.y);
           }
         };
+#ifdef CSC_ROLE_TIMING
+        if (A.dbgflags & 1) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) hv[i] = lv[i] = __float_as_uint(c[i] * zc[i]);
+        } else
+#endif
         if (A.tau_stride) body(std::true_type{});
         else body(std::false_type{});
         if (a3p) {
@@ -606,93 +547,219 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wbm = max(wbm, __shfl_xor_sync(kFullMask, wbm, o));
     if (lane == 0 && A.zmax != nullptr && wbm != 0u) atomicMax(A.zmax, wbm);
-  } else if (a3p) {
-    // ================================ col2im of Y = D dz into the band window (a3')
+  } else {
+    // ================================ helpers (8 = 4 TMEM lane quarters x 2): per tile t, the im2col of
+    // tile t (their half of each slot's K16-steps), then the col2im of tile t-1 (their half of the tap rows)
     const int q = warp & 3;
-    const int half = (warp - kChColBase) >> 2;  // tap rows [a0, a1) of this warp
+    const int hh = (warp - kChHelpBase) >> 2;  // 0, 1
+    const uint32_t tq = (static_cast<uint32_t>(32 * q) << 16);
+    const int ht = tid - 32 * kChHelpBase;     // 0..255
+    const float sr = exp2i_h(er);
+    RoleClock rc;
+    // The band's residual rows u0-P .. u1-1 (columns -P .. Wc-1, zero outside the image), scaled by
+    // 2^er and split once per band into fp16 hi / lo PAIRS: hp[row][c] = (hi(r[row][c-P]), hi(r[row][c-P+1])),
+    // lp likewise.  A TMEM column of the im2col holds two consecutive taps (a, b), (a, b+1) of one
+    // position, which is then a single 32-bit shared load of each array (no per-tap arithmetic).
+    uint32_t* hp = reinterpret_cast<uint32_t*>(rs);
+    uint32_t* lp = hp + A.rs_floats;
+    auto fill = [&](const ChItem& it) {
+      const float* rn = A.r + static_cast<size_t>(it.n) * A.H * A.W;
+      for (int e = ht; e < A.rs_floats; e += 32 * kChHelpWarps) {
+        const int rho = e / A.pitch, c = e - rho * A.pitch;
+        const int i = it.u0 - P + rho, jj = c - P;
+        const bool iok = i >= 0 && i < A.H;
+        const float* rr = rn + static_cast<size_t>(iok ? i : 0) * A.W;
+        const float x0 = (iok && jj >= 0 && jj < A.W) ? __ldg(rr + jj) * sr : 0.f;
+        const float x1 = (iok && jj + 1 >= 0 && jj + 1 < A.W) ? __ldg(rr + jj + 1) * sr : 0.f;
+        const float h0 = rn11_h(x0), h1 = rn11_h(x1);
+        hp[e] = pack_h2_h(h0, h1);
+        lp[e] = pack_h2_h(x0 - h0, x1 - h1);
+      }
+    };
+    // im2col of tile (it, tl), count tc: for each slot j, this warp's K16-steps 2 hh, 2 hh + 1
+    auto convert = [&](const ChItem& it, int tl, uint32_t tc) {
+      const int p = it.p0 + tl * kChTile + 32 * q + lane;
+      const bool pok = p < it.p1;
+      const int u = p / A.Wc, v = p - u * A.Wc;
+      const int o = pok ? (u - it.u0) * A.pitch + v : 0;
+      const uint32_t* sh = hp + o;
+      const uint32_t* sl = lp + o;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {  // slot j: taps 64 j .. 64 j + 63
+        RT_WAIT(rc, 1, mbar_wait_backoff(&a_empty[j], (tc & 1u) ^ 1u, 128));
+        tc_after();
+        auto cols = [&](auto ec) {
+          constexpr int E0 = decltype(ec)::value;
+#pragma unroll
+          for (int ee = 0; ee < 2; ++ee) {
+            const int e = E0 + ee;  // K16-step within the slot
+            uint32_t hv[8], lv[8];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int t0 = 64 * j + 16 * e + 2 * jj, t1 = t0 + 1;
+              const int a0 = t0 / S, b0 = t0 % S, a1 = t1 / S, b1 = t1 % S;
+              uint32_t xh = 0u, xl = 0u;
+              if (t0 < S2) {
+                const int o0 = a0 * A.pitch + b0;
+                if (t1 < S2 && a1 == a0) {  // both taps in one row: the stored pair
+                  xh = sh[o0];
+                  xl = sl[o0];
+                } else {                     // the pair straddles two tap rows (or ends the taps)
+                  const uint32_t h0 = sh[o0], l0 = sl[o0];
+                  if (t1 < S2) {
+                    const int o1 = a1 * A.pitch + b1;
+                    xh = __byte_perm(h0, sh[o1], 0x5410);
+                    xl = __byte_perm(l0, sl[o1], 0x5410);
+                  } else {
+                    xh = h0 & 0xFFFFu;
+                    xl = l0 & 0xFFFFu;
+                  }
+                }
+              }
+              hv[jj] = pok ? xh : 0u;
+              lv[jj] = pok ? xl : 0u;
+            }
+            const uint32_t col = t_a + j * 64u + 8u * e;
+            tmem_st8(tq + col, hv);
+            tmem_st8(tq + col + 32u, lv);
+          }
+        };
+        if (hh == 0) cols(std::integral_constant<int, 0>{});
+        else cols(std::integral_constant<int, 2>{});
+        tmem_st_wait();
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[j]);
+      }
+    };
+    // col2im of Y of tile (it, t), count tc, into the band window
     constexpr int AH = (S + 1) / 2;
-    const int a0 = half * AH, a1 = half ? S : AH;
+    const int a0 = hh * AH, a1 = hh ? S : AH;
     const float inv2 = exp2i_h(-(edz + ed));
     // add phases: the quarters in order (and the two row halves of a quarter in order when their windows
     // can overlap, Wc < 32 + P): deterministic fp32 sums
     const bool split = A.Wc < 32 + P;
     const int nph = split ? 8 : 4;
-    const int myph = split ? 2 * q + half : q;
-    uint32_t tcount = 0;
-    const int et = tid - 32 * kChColBase;
-    RoleClock rc;
-    for (int item = gi; item < A.nitems; item += A.G) {
-      const ChItem it = ch_item(A, item);
-      for (int t = 0; t < it.ntiles; ++t, ++tcount) {
-        RT_WAIT(rc, 0, mbar_wait_backoff(&y_full, tcount & 1u, 256));
-        tc_after();
-        const int pq = 128 * t + 32 * q;
-        const bool pvalid = it.p0 + pq + lane < it.p1;
-        const uint32_t tacc = t_y + (static_cast<uint32_t>(32 * q) << 16);
-        float* rowb = win + pq + lane;
-        float own[AH], dnv[AH];
-        auto rows = [&](auto partial) {
-          constexpr bool PART = decltype(partial)::value;
+    const int myph = split ? 2 * q + hh : q;
+    auto col2im = [&](const ChItem& it, int t, uint32_t tc) {
+      RT_WAIT(rc, 0, mbar_wait_backoff(&y_full, tc & 1u, 256));
+      tc_after();
+      const int pq = 128 * t + 32 * q;
+      const bool pvalid = it.p0 + pq + lane < it.p1;
+      const uint32_t tacc = t_y + (static_cast<uint32_t>(32 * q) << 16);
+      float* rowb = win + pq + lane;
+      float own[AH], dnv[AH];
+      auto rows = [&](auto partial) {
+        constexpr bool PART = decltype(partial)::value;
 #pragma unroll
-          for (int i = 0; i < AH; ++i) {
-            own[i] = 0.f;
-            dnv[i] = 0.f;
-            const int a = a0 + i;
-            if (a >= a1) continue;
-            float y[S];
-            tmem_ld_row<S>(tacc + a * S, y);
-            tmem_ld_wait();
-            float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
+        for (int i = 0; i < AH; ++i) {
+          own[i] = 0.f;
+          dnv[i] = 0.f;
+          const int a = a0 + i;
+          if (a >= a1) continue;
+          float y[S];
+          tmem_ld_row<S>(tacc + a * S, y);
+          tmem_ld_wait();
+          float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
 #pragma unroll
-            for (int b = 0; b < S; ++b) {
-              // one rotation serves both parts: lanes >= b get position lane-b of this quarter, lanes < b
-              // get position lane-b+32, the halo that belongs to the next quarter's first lanes
-              const float yv = PART ? (pvalid ? y[b] : 0.f) : y[b];
-              const float rot = b == 0 ? yv : __shfl_sync(kFullMask, yv, (lane - b) & 31);
-              if (lane >= b) {
-                if (b & 1) u1s += rot; else u0s += rot;
-              } else {
-                if (b & 1) d1s += rot; else d0s += rot;
-              }
+          for (int b = 0; b < S; ++b) {
+            // one rotation serves both parts: lanes >= b get position lane-b of this quarter, lanes < b
+            // get position lane-b+32, the halo that belongs to the next quarter's first lanes
+            const float yv = PART ? (pvalid ? y[b] : 0.f) : y[b];
+            const float rot = b == 0 ? yv : __shfl_sync(kFullMask, yv, (lane - b) & 31);
+            if (lane >= b) {
+              if (b & 1) u1s += rot; else u0s += rot;
+            } else {
+              if (b & 1) d1s += rot; else d0s += rot;
             }
-            own[i] = u0s + u1s;
-            dnv[i] = d0s + d1s;
           }
-        };
-        if (__all_sync(kFullMask, pvalid)) rows(std::false_type{});
-        else rows(std::true_type{});
-        tc_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&y_empty);
+          own[i] = u0s + u1s;
+          dnv[i] = d0s + d1s;
+        }
+      };
+      if (__all_sync(kFullMask, pvalid)) rows(std::false_type{});
+      else rows(std::true_type{});
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&y_empty);
 #pragma unroll 1
-        for (int ph = 0; ph < nph; ++ph) {
-          if (ph == myph) {
+      for (int ph = 0; ph < nph; ++ph) {
+        if (ph == myph) {
+#pragma unroll
+          for (int i = 0; i < AH; ++i)
+            if (a0 + i < a1) rowb[(a0 + i) * A.Wc] += own[i];
+          __syncwarp();
+          if (lane < P) {
 #pragma unroll
             for (int i = 0; i < AH; ++i)
-              if (a0 + i < a1) rowb[(a0 + i) * A.Wc] += own[i];
-            __syncwarp();
-            if (lane < P) {
-#pragma unroll
-              for (int i = 0; i < AH; ++i)
-                if (a0 + i < a1) rowb[(a0 + i) * A.Wc + 32] += dnv[i];
-            }
+              if (a0 + i < a1) rowb[(a0 + i) * A.Wc + 32] += dnv[i];
           }
-          RT_WAIT(rc, 1, named_sync(2, 32 * kChColWarps));
         }
+        RT_WAIT(rc, 2, named_sync(2, 32 * kChHelpWarps));
       }
-      // flush the band window: output rows u0-P .. u0+BR-1 (window row r = output row u0-P+r)
+    };
+    // flush the band window: output rows u0-P .. u0+BR-1 (window row r = output row u0-P+r)
+    auto flush = [&](const ChItem& it) {
       float* dst = A.part + ((static_cast<size_t>(kg) * A.N + it.n) * A.nbands + it.band) *
                                 static_cast<size_t>(A.BR + P) * A.W;
       const int nrows = A.BR + P;
-      for (int e = et; e < nrows * A.W; e += 32 * kChColWarps) {
-        const int r = e / A.W, j = e - r * A.W;
-        dst[e] = win[r * A.Wc + j + P] * inv2;  // exact: power of two
+      for (int e = ht; e < nrows * A.W; e += 32 * kChHelpWarps) {
+        const int r = e / A.W, jc = e - r * A.W;
+        dst[e] = win[r * A.Wc + jc + P] * inv2;  // exact: power of two
       }
-      named_sync(2, 32 * kChColWarps);
-      for (int e = et; e < A.WL; e += 32 * kChColWarps) win[e] = 0.f;
-      named_sync(2, 32 * kChColWarps);
+      named_sync(2, 32 * kChHelpWarps);
+      for (int e = ht; e < A.WL; e += 32 * kChHelpWarps) win[e] = 0.f;
+      named_sync(2, 32 * kChHelpWarps);
+    };
+    // per tile t: the im2col of tile t+1 (the tensor pipe needs it right after C(t)), then the col2im of
+    // tile t-1 (its Y is ready once GEMM 2 of t-1, issued after C(t), completes)
+    int item = gi;
+    if (item < A.nitems) {
+      ChItem it = ch_item(A, item);
+      int tl = 0;
+      ChItem pit = it;
+      int ptl = 0;
+      int nitem = item, ntl = 0;
+      ChItem nit = it;
+      auto step = [&](int& itm, int& t, ChItem& c) {
+        if (++t >= c.ntiles) {
+          t = 0;
+          itm += A.G;
+          if (itm < A.nitems) c = ch_item(A, itm);
+        }
+      };
+      fill(it);
+      RT_WAIT(rc, 3, named_sync(1, 32 * kChHelpWarps));
+      convert(it, 0, 0u);
+      step(nitem, ntl, nit);
+      uint32_t tcount = 0;
+      while (item < A.nitems) {
+        if (nitem < A.nitems) {
+          if (nitem != item) {  // a new band: every helper is past its last use of the residual pairs
+            RT_WAIT(rc, 3, named_sync(1, 32 * kChHelpWarps));
+            fill(nit);
+            RT_WAIT(rc, 3, named_sync(1, 32 * kChHelpWarps));
+          }
+          convert(nit, ntl, tcount + 1);
+        }
+        if (a3p && tcount > 0) {
+          col2im(pit, ptl, tcount - 1);
+          if (ptl == pit.ntiles - 1) flush(pit);
+        }
+        pit = it;
+        ptl = tl;
+        item = nitem;
+        tl = ntl;
+        it = nit;
+        if (nitem < A.nitems) step(nitem, ntl, nit);
+        ++tcount;
+      }
+      if (a3p && tcount > 0) {
+        col2im(pit, ptl, tcount - 1);
+        flush(pit);
+      }
     }
-    if (warp == kChColBase && lane == 0) RT_DUMP(rc, A.dbg, 3);
+    if (warp == kChHelpBase && lane == 0) RT_DUMP(rc, A.dbg, 1);
   }
 
   tc_before();
@@ -735,6 +802,7 @@ cudaError_t run_code_h(const ChArgs& a, int grid, int smem, cudaStream_t st) {
   cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 32 * 1024, st);
   ChArgs b = a;
   b.dbg = dbg;
+  b.dbgflags = std::getenv("CSC_CH_DBG") ? std::atoi(std::getenv("CSC_CH_DBG")) : 0;
   code_h_kernel<S><<<grid, kChThreads, smem, st>>>(b);
   if (++calls % 4 == 0) {
     static unsigned long long h[32 * 1024];
@@ -744,10 +812,9 @@ cudaError_t run_code_h(const ChArgs& a, int grid, int smem, cudaStream_t st) {
     for (int bk = 0; bk < grid; ++bk)
       for (int i = 0; i < 32; ++i) t[i] += static_cast<double>(h[bk * 32 + i]) / grid;
     fprintf(stderr,
-            "[code_h roles] mma: total %.0f w_accempty %.0f w_afull %.0f w_dzfull %.0f w_yempty %.0f | conv: total %.0f "
-            "w_stage %.0f w_aempty %.0f w_end %.0f | epi: total %.0f w_accfull %.0f w_cpasync %.0f | col: total %.0f "
-            "w_yfull %.0f w_phase %.0f\n",
-            t[7], t[0], t[1], t[2], t[3], t[15], t[8], t[9], t[10], t[23], t[16], t[17], t[31], t[24], t[25]);
+            "[code_h roles] mma: total %.0f w_accempty %.0f w_afull %.0f w_dzfull %.0f w_yempty %.0f | helper: total "
+            "%.0f w_yfull %.0f w_aempty %.0f w_phase %.0f w_fill %.0f | epi: total %.0f w_accfull %.0f w_zfull %.0f\n",
+            t[7], t[0], t[1], t[2], t[3], t[15], t[8], t[9], t[10], t[11], t[23], t[16], t[17]);
   }
 #else
   code_h_kernel<S><<<grid, kChThreads, smem, st>>>(a);
