@@ -95,6 +95,11 @@ struct csc_ctx {
   float* h_fscal = nullptr;
   // residual cache
   bool cache_valid = false;
+  // L_D(d) and tau_z = 1/L_D of the filters last used (d changes only through the filter steps, which
+  // clear it, or outside the API, which requires csc_invalidate): one bound per filter update, not per
+  // code step (config 4 runs 10 code steps per filter step)
+  bool lip_valid = false;
+  const float* lip_d = nullptr;
   const float* cx = nullptr;
   const float* cd = nullptr;
   const float* cz = nullptr;
@@ -673,6 +678,7 @@ csc_status csc_invalidate(csc_ctx* c) {
   if (!c) return CSC_ERR_ARG;
   c->cache_valid = false;
   c->zmax_known = false;
+  c->lip_valid = false;
   return CSC_OK;
 }
 
@@ -718,8 +724,14 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
   const bool eso = step_z == 0.f && c->step_rule == CSC_STEP_ESO;
   if (step_z > 0.f) {
     CSC_LAUNCH(c, 1, csc::launch_set_f32(c->fscal + kTauZ, step_z, c->st));
+    c->lip_valid = false;  // the tau_z slot now holds the explicit step
   } else {
-    CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 3, csc::launch_lipschitz(g, d, c->lip_part, c->dscal + kLhat, c->fscal + kTauZ, c->st));
+    if (!(c->lip_valid && c->lip_d == d)) {
+      CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 3,
+                   csc::launch_lipschitz(g, d, c->lip_part, c->dscal + kLhat, c->fscal + kTauZ, c->st));
+      c->lip_valid = true;
+      c->lip_d = d;
+    }
     if (eso) CSC_LAUNCH(c, 1, csc::launch_eso_tau(g, d, p, c->dscal + kLhat, c->tauk, c->st));
   }
   c->last_eso = eso;
@@ -1118,6 +1130,7 @@ csc_status csc_filter_step_surrogate(csc_ctx* c, float* d, int sweeps, uint8_t* 
       CSC_LAUNCH_C(c, CSC_K_BCD, 2, csc::launch_sur_filter(g, k, c->sur_C, c->sur_B, c->bcd_ainv, c->bcd_flags, d,
                                                            c->bcd_vec, c->bcd_vec + M, c->st));
   c->cache_valid = false;  // d changed
+  c->lip_valid = false;
   if (flags_out) {
     CSC_CUDA(c, cudaMemcpyAsync(flags_out, c->bcd_flags, static_cast<size_t>(g.K), cudaMemcpyDeviceToHost, c->st));
     CSC_CUDA(c, cudaStreamSynchronize(c->st));
@@ -1198,6 +1211,7 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
   CSC_LAUNCH(c, 1, csc::launch_filter_tau(c->dscal + kGG, c->dscal + kZg2, step_d, c->fscal + kTauD, c->st));
   CSC_LAUNCH(c, 1, csc::launch_filter_update(g, d, c->gsum, c->fscal + kTauD, c->st));
   c->cache_valid = false;  // d changed
+  c->lip_valid = false;
   if (step_used) {
     CSC_CUDA(c, cudaMemcpyAsync(c->h_fscal + kTauD, c->fscal + kTauD, sizeof(float), cudaMemcpyDeviceToHost, c->st));
     CSC_CUDA(c, cudaStreamSynchronize(c->st));
@@ -1389,6 +1403,7 @@ csc_status csc_lipschitz(csc_ctx* c, const float* d, double* out) {
   if (!c || !aligned4(d) || !out) return fail(c, CSC_ERR_ARG, "d (device) and out (host) required");
   CSC_CUDA(c, cudaSetDevice(c->device));
   CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 3, csc::launch_lipschitz(c->g, d, c->lip_part, c->dscal + kLhat, nullptr, c->st));
+  c->lip_valid = false;  // kLhat now describes this d
   CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal + kLhat, c->dscal + kLhat, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CSC_CUDA(c, cudaStreamSynchronize(c->st));
   *out = c->h_dscal[kLhat];

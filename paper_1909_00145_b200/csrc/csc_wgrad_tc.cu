@@ -338,38 +338,51 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
     const int ew = warp - kWgEpiBase;  // 0..15
     const int q = warp & 3;
     const int cb = ew >> 2;            // column block (NC columns)
-    double acc[NC];
+    // the tile sums (fp32 from TMEM) accumulate in compensated (Kahan) fp32 pairs: fp64-grade sums over a
+    // CTA's tiles at fp32 pipe cost (packed FADD2), instead of an F2F.F64 + DADD per element and tile
+    float2 sum[NC / 2], cmp[NC / 2];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NC / 2; ++i) {
+      sum[i] = make_float2(0.f, 0.f);
+      cmp[i] = make_float2(0.f, 0.f);
+    }
     const uint32_t tq = (static_cast<uint32_t>(32 * q) << 16);
-    unsigned long long w_af = 0;
     uint32_t tcount = 0;
     for (int item = gi; item < A.nitems; item += A.G) {
       const WgItem it = wg_item(A, item);
       const int ntl = wg_ntiles(it.nch, A.cpt);
       for (int tl = 0; tl < ntl; ++tl, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
-        const unsigned long long tw3 = clock64();
         mbar_wait_sleep(&acc_full[buf], use & 1u);
-        w_af += clock64() - tw3;
         tc_after();
         const uint32_t col = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
+        float f[NC];
 #pragma unroll
         for (int j = 0; j < NC / 4; ++j) {
-          float f[4] = {0.f, 0.f, 0.f, 0.f};
-          if (!(A.dbg & 8)) {
-            tmem_ld4_nowait(tq + col + 4u * j, f);
-            tmem_ld_wait();
-          }
+          float f4[4];
+          tmem_ld4_nowait(tq + col + 4u * j, f4);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[4 * j + i] += static_cast<double>(f[i]);
+          for (int i = 0; i < 4; ++i) f[4 * j + i] = f4[i];
         }
+        tmem_ld_wait();
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
+#pragma unroll
+        for (int i = 0; i < NC / 2; ++i) {
+          const float2 y = __fadd2_rn(make_float2(f[2 * i], f[2 * i + 1]), make_float2(-cmp[i].x, -cmp[i].y));
+          const float2 t = __fadd2_rn(sum[i], y);
+          cmp[i] = __fadd2_rn(__fadd2_rn(t, make_float2(-sum[i].x, -sum[i].y)), make_float2(-y.x, -y.y));
+          sum[i] = t;
+        }
       }
     }
-    if (A.tdbg != nullptr && warp == kWgEpiBase && lane == 0) A.tdbg[blockIdx.x * 8 + 5] = w_af;
+    double acc[NC];
+#pragma unroll
+    for (int i = 0; i < NC / 2; ++i) {
+      acc[2 * i] = static_cast<double>(sum[i].x) - static_cast<double>(cmp[i].x);
+      acc[2 * i + 1] = static_cast<double>(sum[i].y) - static_cast<double>(cmp[i].y);
+    }
     // per-CTA partial: gpart[gi][k][t]
     const int t = 32 * q + lane;
     const int S2 = A.S * A.S;
