@@ -1049,6 +1049,7 @@ csc_status csc_filter_step_bcd(csc_ctx* c, const float* x, float* d, const float
     }
   }
   // the residual cache now belongs to the updated filters
+  c->lip_valid = false;  // d changed
   c->cache_valid = true;
   c->cx = x;
   c->cd = d;
