@@ -62,7 +62,8 @@ def load_library(path: Optional[str] = None):
     with _lib_lock:
         if _lib is not None:
             return _lib
-        p = path or LIB_PATH
+        # CSC_LIB_PATH: load another build of the same library (side-by-side A/B timing of two builds)
+        p = path or os.environ.get("CSC_LIB_PATH") or LIB_PATH
         if not os.path.exists(p):
             raise ImportError(f"{p} not found: the CUDA extension is not built "
                               "(run `python -c 'import __graft_entry__ as g; g.build()'`)")

@@ -285,8 +285,8 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     // GEMM 2 of tile u: Y = dz(u) x B (B read MN-major: taps contiguous, filters = K rows)
     auto gemm2 = [&](uint32_t u) {
       const uint32_t bu = u & 1u;
-      RT_WAIT(rc, 2, mbar_wait_backoff(&dz_full[bu], (u >> 1) & 1u, 32));
-      RT_WAIT(rc, 3, mbar_wait_backoff(&y_empty, (u & 1u) ^ 1u, 32));
+      RT_WAIT(rc, 2, mbar_wait_sleep(&dz_full[bu], (u >> 1) & 1u));
+      RT_WAIT(rc, 3, mbar_wait_sleep(&y_empty, (u & 1u) ^ 1u));
       tc_after();
       const uint32_t acol = t_acc + bu * static_cast<uint32_t>(A.Npad);
       for (int c = 0; c < A.ngroups; ++c) {
@@ -313,13 +313,13 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       const ChItem it = ch_item(A, item);
       for (int tl = 0; tl < it.ntiles; ++tl, ++tcount) {
         const uint32_t buf = prec ? 0u : (tcount & 1u), use = prec ? tcount : (tcount >> 1);
-        RT_WAIT(rc, 0, mbar_wait_backoff(&acc_empty[buf], (use & 1u) ^ 1u, 32));
+        RT_WAIT(rc, 0, mbar_wait_sleep(&acc_empty[buf], (use & 1u) ^ 1u));
         tc_after();
         const uint32_t dcol = t_acc + buf * static_cast<uint32_t>(A.Npad);
         const uint32_t dxc = prec ? dcol + static_cast<uint32_t>(A.Npad) : dcol;  // cross-term accumulator
         for (int j = 0; j < 2; ++j, ++g) {  // 2 slots of 4 K16-steps (64 taps)
           const uint32_t slot = g % kChNS, ph = (g / kChNS) & 1u;
-          RT_WAIT(rc, 1, mbar_wait_backoff(&a_full[slot], ph, 32));
+          RT_WAIT(rc, 1, mbar_wait_sleep(&a_full[slot], ph));
           tc_after();
           const uint32_t ah = t_a + slot * 64u;
 #pragma unroll
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       const int p = it.p0 + tl * kChTile + 32 * q + lane;
       const bool pok = p < it.p1;
       const int ga = static_cast<int>((jq + tcount) % kChEpiPerQ);
-      RT_WAIT(rc, 0, mbar_wait_backoff(&acc_full[buf], use & 1u, 64));
+      RT_WAIT(rc, 0, mbar_wait_sleep(&acc_full[buf], use & 1u));
       tc_after();
       const uint32_t colb = t_acc + buf * static_cast<uint32_t>(A.Npad);
       float* zrow = A.z + (static_cast<size_t>(it.n) * A.K + kbase) * plane + p;
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
         const int gg = ga + kChEpiPerQ * s;
         if (gg >= A.ngroups) {
           if (!plain) {
-            RT_WAIT(rc, 1, mbar_wait_backoff(&zfull[ew][s], tcount & 1u, 32));
+            RT_WAIT(rc, 1, mbar_wait_sleep(&zfull[ew][s], tcount & 1u));
             __syncwarp();
             issue(ni, ntl, nit, tcount + 1, s);
           }
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
           for (int i = 0; i < 16; ++i) st_global_if(zb + static_cast<size_t>(i) * plane, c[i] * inv, (pv >> i) & 1u);
           continue;
         }
-        RT_WAIT(rc, 1, mbar_wait_backoff(&zfull[ew][s], tcount & 1u, 32));
+        RT_WAIT(rc, 1, mbar_wait_sleep(&zfull[ew][s], tcount & 1u));
         const uint32_t wb = (masked ? ws0[s * 32 + lane] : 0xFFFFu) & (pok ? kv : 0u);
         float zc[16];
         const float* zr = zs0 + s * 512 + lane;
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       const uint32_t* sl = lp + o;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {  // slot j: taps 64 j .. 64 j + 63
-        RT_WAIT(rc, 1, mbar_wait_backoff(&a_empty[j], (tc & 1u) ^ 1u, 128));
+        RT_WAIT(rc, 1, mbar_wait_sleep(&a_empty[j], (tc & 1u) ^ 1u));
         tc_after();
         auto cols = [&](auto ec) {
           constexpr int E0 = decltype(ec)::value;
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     const int nph = split ? 8 : 4;
     const int myph = split ? 2 * q + hh : q;
     auto col2im = [&](const ChItem& it, int t, uint32_t tc) {
-      RT_WAIT(rc, 0, mbar_wait_backoff(&y_full, tc & 1u, 256));
+      RT_WAIT(rc, 0, mbar_wait_sleep(&y_full, tc & 1u));
       tc_after();
       const int pq = 128 * t + 32 * q;
       const bool pvalid = it.p0 + pq + lane < it.p1;
@@ -791,6 +791,30 @@ __global__ void code_a3_fixup_kernel(const float* __restrict__ part, int nkg, in
   }
 }
 
+// the same with 4 columns per thread (W % 4 == 0, 16-B aligned buffers): one float4 per band partial
+__global__ void code_a3_fixup4_kernel(const float4* __restrict__ part, int nkg, int N, int H, int W4, int P, int BR,
+                                      int nbands, float4* __restrict__ r) {
+  const size_t win4 = static_cast<size_t>(BR + P) * W4;
+  const size_t kstride4 = static_cast<size_t>(N) * nbands * win4;
+  const int total = N * H * W4;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int row = e / W4, j4 = e - row * W4;
+    const int n = row / H, i = row - n * H;
+    const int b0 = i / BR;
+    int b1 = (i + P) / BR;
+    if (b1 > nbands - 1) b1 = nbands - 1;
+    float4 v = r[e];
+    for (int kg = 0; kg < nkg; ++kg) {
+      const float4* pk = part + kg * kstride4 + static_cast<size_t>(n) * nbands * win4;
+      for (int b = b0; b <= b1; ++b) {
+        const float4 t = __ldg(pk + b * win4 + static_cast<size_t>(i - b * BR + P) * W4 + j4);
+        v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
+      }
+    }
+    r[e] = v;
+  }
+}
+
 template <int S>
 cudaError_t run_code_h(const ChArgs& a, int grid, int smem, cudaStream_t st) {
   cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&code_h_kernel<S>), kChSmemMax);
@@ -928,7 +952,15 @@ cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, TmapCache* tmc, co
 
 cudaError_t launch_code_a3_fixup(const Geom& g, const CodeTcPlan& p, const float* part, float* r, cudaStream_t st) {
   if (g.N == 0) return cudaSuccess;
-  code_a3_fixup_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, p.nkg, g.N, g.H, g.W, g.P, p.BR, p.nbands, r);
+  if (g.W % 4 == 0 && (reinterpret_cast<uintptr_t>(part) & 15u) == 0 && (reinterpret_cast<uintptr_t>(r) & 15u) == 0 &&
+      static_cast<int64_t>(g.N) * g.H * (g.W / 4) < (int64_t(1) << 31)) {
+    const int total = g.N * g.H * (g.W / 4);
+    const int blocks = total / 256 + 1 < kFinalizeBlocks * 2 ? total / 256 + 1 : kFinalizeBlocks * 2;
+    code_a3_fixup4_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(part), p.nkg, g.N, g.H, g.W / 4,
+                                                   g.P, p.BR, p.nbands, reinterpret_cast<float4*>(r));
+  } else {
+    code_a3_fixup_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, p.nkg, g.N, g.H, g.W, g.P, p.BR, p.nbands, r);
+  }
   return cudaGetLastError();
 }
 

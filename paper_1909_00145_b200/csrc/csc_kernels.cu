@@ -478,12 +478,32 @@ wgrad_kernel(const float* __restrict__ z, const float* __restrict__ r, Geom g, i
   }
 }
 
-__global__ void wgrad_reduce_kernel(const double* __restrict__ gpart, int G, int nel, double* __restrict__ gsum) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= nel) return;
-  double s = 0.0;
-  for (int gi = 0; gi < G; ++gi) s += gpart[static_cast<int64_t>(gi) * nel + e];
-  gsum[e] = s;
+// 32 elements x 8 partial slices per 256-thread block: slice y sums partials y, y+8, ... (4 loads in
+// flight), then the 8 slice sums are added in slice order -- a fixed order, so the result is deterministic
+__global__ void __launch_bounds__(256) wgrad_reduce_kernel(const double* __restrict__ gpart, int G, int nel,
+                                                           double* __restrict__ gsum) {
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + tx;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (e < nel) {
+    int gi = ty;
+    for (; gi + 24 < G; gi += 32) {
+      s0 += __ldg(gpart + static_cast<int64_t>(gi) * nel + e);
+      s1 += __ldg(gpart + static_cast<int64_t>(gi + 8) * nel + e);
+      s2 += __ldg(gpart + static_cast<int64_t>(gi + 16) * nel + e);
+      s3 += __ldg(gpart + static_cast<int64_t>(gi + 24) * nel + e);
+    }
+    for (; gi < G; gi += 8) s0 += __ldg(gpart + static_cast<int64_t>(gi) * nel + e);
+  }
+  red[ty][tx] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (ty == 0 && e < nel) {
+    double s = red[0][tx];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) s += red[y][tx];
+    gsum[e] = s;
+  }
 }
 
 __global__ void grad_finish_kernel(const double* __restrict__ gsum, int nel, float* __restrict__ g32,
@@ -831,7 +851,7 @@ cudaError_t launch_wgrad(const Geom& g, const float* z, const float* r, int G, d
 
 cudaError_t launch_wgrad_reduce(const Geom& g, const double* gpart, int G, double* gsum, cudaStream_t st) {
   const int nel = g.K * g.S * g.S;
-  wgrad_reduce_kernel<<<ceil_div(nel, 256), 256, 0, st>>>(gpart, G, nel, gsum);
+  wgrad_reduce_kernel<<<ceil_div(nel, 32), 256, 0, st>>>(gpart, G, nel, gsum);
   return cudaGetLastError();
 }
 
