@@ -265,6 +265,24 @@ csc_status csc_read_grad(csc_ctx* ctx, double* g_dev);
 /* L_D(d) (reading R8) computed on the device; result to *out (HOST, syncs). */
 csc_status csc_lipschitz(csc_ctx* ctx, const float* d, double* out);
 
+/* ---- observability (per-iteration trace; the Fig.1 caption's time per iteration and
+ * objective) ---- */
+
+/* Number of nonzero entries of v (DEVICE fp32, n entries) -> *count (HOST, syncs).  One counting kernel
+ * on the context stream (the codes' nnz column of the per-iteration trace); not on the iteration path. */
+csc_status csc_count_nonzero(csc_ctx* ctx, const float* v, int64_t n, uint64_t* count);
+
+/* NVTX ranges ("csc_code_step", "csc_filter_step", "csc_objective", "csc_iterate", ...) around every
+ * entry point of this context when enable != 0 (header-only NVTX v3: no cost without an attached tool).
+ * Also switched on at csc_init by the environment variable CSC_NVTX=1. */
+csc_status csc_set_nvtx(csc_ctx* ctx, int enable);
+
+/* Poll the NCCL communicator for an asynchronous error (ncclCommGetAsyncError): CSC_OK when none (or
+ * world == 1), CSC_ERR_NCCL with the NCCL error string in csc_last_error otherwise.  A rank whose peer
+ * died sees the failure here instead of hanging in the next all-reduce's synchronisation; call it
+ * between iterations (it does not synchronise the stream). */
+csc_status csc_comm_check(csc_ctx* ctx);
+
 /* Number of kernel launches this context has enqueued (for bench accounting). */
 uint64_t csc_launch_count(const csc_ctx* ctx);
 

@@ -32,7 +32,7 @@ ABI_SYMBOLS = (
     "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd", "csc_surrogate_reset",
     "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate", "csc_set_mask_mode",
     "csc_stage_images", "csc_iterate_staged", "csc_mask_selwords", "csc_read_scalars", "csc_zg_sumsq",
-    "csc_set_iter_offset",
+    "csc_set_iter_offset", "csc_count_nonzero", "csc_set_nvtx", "csc_comm_check",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -100,6 +100,9 @@ def load_library(path: Optional[str] = None):
         L.csc_read_residual.argtypes = [vp, vp]
         L.csc_read_grad.argtypes = [vp, vp]
         L.csc_lipschitz.argtypes = [vp, vp, vp]
+        L.csc_count_nonzero.argtypes = [vp, vp, ctypes.c_int64, ctypes.POINTER(u64)]
+        L.csc_set_nvtx.argtypes = [vp, ctypes.c_int]
+        L.csc_comm_check.argtypes = [vp]
         L.csc_launch_count.argtypes = [vp]
         L.csc_launch_count.restype = u64
         L.csc_profile_enable.argtypes = [vp, ctypes.c_int]
@@ -366,6 +369,21 @@ class Context:
         out = ctypes.c_double(0.0)
         self._check(self._L.csc_lipschitz(self._h, _ptr(d, "d"), ctypes.byref(out)))
         return float(out.value)
+
+    def count_nonzero(self, v) -> int:
+        """Number of nonzero entries of a float32 CUDA tensor (include/csc.h csc_count_nonzero; syncs)."""
+        n = ctypes.c_uint64(0)
+        numel = int(v.numel())
+        self._check(self._L.csc_count_nonzero(self._h, _ptr(v, "v") if numel else None, numel, ctypes.byref(n)))
+        return int(n.value)
+
+    def set_nvtx(self, on: bool = True):
+        """NVTX ranges around every entry point of this context (csc_set_nvtx)."""
+        self._check(self._L.csc_set_nvtx(self._h, 1 if on else 0))
+
+    def comm_check(self):
+        """Raise CSCError if the NCCL communicator reports an asynchronous error (csc_comm_check)."""
+        self._check(self._L.csc_comm_check(self._h))
 
     def profile_enable(self, on: bool = True):
         self._check(self._L.csc_profile_enable(self._h, 1 if on else 0))

@@ -12,6 +12,7 @@
 
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -38,6 +39,7 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   bool load(std::string* err) {
     if (h) return true;
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
@@ -54,6 +56,7 @@ struct NcclApi {
     CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(h, "ncclAllReduce"));
     GetErrorString = reinterpret_cast<decltype(GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    CommGetAsyncError = reinterpret_cast<decltype(CommGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
     if (!GetUniqueId || !CommInitRank || !CommDestroy || !AllReduce || !GetErrorString) {
       *err = "libnccl.so.2 lacks required symbols";
       return false;
@@ -67,7 +70,7 @@ std::mutex g_nccl_mu;
 constexpr double kBcdRidge = 1e-10;  // DESIGN.md reading B2
 
 // device scalar slots
-enum DSlot { kSqR = 0, kL1 = 1, kZg2 = 2, kGG = 3, kLhat = 4, kNumD = 8 };
+enum DSlot { kSqR = 0, kL1 = 1, kZg2 = 2, kGG = 3, kLhat = 4, kCnt = 7, kNumD = 8 };  // kCnt: csc_count_nonzero (host mirror only)
 enum FSlot { kTauZ = 0, kTauD = 1, kNumF = 4 };
 
 }  // namespace
@@ -170,6 +173,8 @@ struct csc_ctx {
   float* adm_vec = nullptr;     // 7 compact vectors W Y U R PV Q ATB [N][cap]
   int64_t adm_cap = 0;
   ncclComm_t comm = nullptr;
+  bool nvtx = false;  // csc_set_nvtx / CSC_NVTX=1
+  uint64_t* cnt_dev = nullptr;  // csc_count_nonzero
   uint64_t launches = 0;
   std::string err;
   // profiling
@@ -182,6 +187,17 @@ struct csc_ctx {
 };
 
 namespace {
+
+// NVTX range around one entry point (csc_set_nvtx); header-only NVTX v3, inert without a tool
+struct NvtxScope {
+  bool on;
+  NvtxScope(const csc_ctx* c, const char* name) : on(c != nullptr && c->nvtx) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxScope() {
+    if (on) nvtxRangePop();
+  }
+};
 
 csc_status fail(csc_ctx* c, csc_status s, const std::string& msg) {
   if (c) c->err = msg;
@@ -477,6 +493,10 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   ok = ok && alloc(reinterpret_cast<void**>(&c->l1_part), sizeof(double) * cap);
   // tensor-core filter gradient unless CSC_WGRAD_PATH=simt (needs Hc*Wc % 4 == 0 for the TMA view of z)
   {
+    const char* nv = std::getenv("CSC_NVTX");
+    c->nvtx = nv != nullptr && std::atoi(nv) != 0;
+  }
+  {
     const char* ev = std::getenv("CSC_WGRAD_PATH");
     const bool force_simt = ev != nullptr && std::string(ev) == "simt";
     if (!force_simt && csc::wgrad_tc_supported(g)) {
@@ -624,6 +644,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->l1_part);
   cudaFree(c->gpart);
   cudaFree(c->gsum);
+  cudaFree(c->cnt_dev);
   cudaFree(c->g32);
   cudaFree(c->colw);
   cudaFree(c->mwords);
@@ -683,6 +704,7 @@ csc_status csc_invalidate(csc_ctx* c) {
 }
 
 csc_status csc_zero_codes(csc_ctx* c, const float* x, float* z) {
+  NvtxScope nvtx_scope(c, "csc_zero_codes");
   if (!c) return CSC_ERR_ARG;
   if (c->g.N > 0 && (!aligned4(x) || !aligned4(z))) return fail(c, CSC_ERR_ARG, "x, z must be device pointers");
   CSC_CUDA(c, cudaSetDevice(c->device));
@@ -705,6 +727,7 @@ csc_status csc_zero_codes(csc_ctx* c, const float* x, float* z) {
 
 csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, float lambda, float step_z,
                          double p, uint64_t seed, uint32_t iter, float* step_used) {
+  NvtxScope nvtx_scope(c, "csc_code_step");
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
   if (!(lambda >= 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and >= 0");
@@ -819,6 +842,7 @@ csc_status csc_read_step_z(csc_ctx* c, float* tau_dev) {
 
 csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float* z, float lambda, float rho,
                               float alpha, int n_admm, int n_cg, double p, uint64_t seed, uint32_t iter) {
+  NvtxScope nvtx_scope(c, "csc_code_step_admm");
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
   if (!(lambda > 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and > 0");
@@ -993,6 +1017,7 @@ csc_status csc_code_step_admm(csc_ctx* c, const float* x, const float* d, float*
 
 csc_status csc_filter_step_bcd(csc_ctx* c, const float* x, float* d, const float* z, int sweeps,
                                uint8_t* flags_out) {
+  NvtxScope nvtx_scope(c, "csc_filter_step_bcd");
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
   if (sweeps < 1) return fail(c, CSC_ERR_ARG, "sweeps must be >= 1");
@@ -1089,6 +1114,7 @@ csc_status csc_surrogate_reset(csc_ctx* c) {
 }
 
 csc_status csc_surrogate_update(csc_ctx* c, const float* x, const float* z) {
+  NvtxScope nvtx_scope(c, "csc_surrogate_update");
   if (!c) return CSC_ERR_ARG;
   if (c->g.N > 0 && (!aligned4(x) || !aligned4(z))) return fail(c, CSC_ERR_ARG, "x, z must be device pointers");
   if (c->sur_C == nullptr) {
@@ -1118,6 +1144,7 @@ csc_status csc_surrogate_update(csc_ctx* c, const float* x, const float* z) {
 }
 
 csc_status csc_filter_step_surrogate(csc_ctx* c, float* d, int sweeps, uint8_t* flags_out) {
+  NvtxScope nvtx_scope(c, "csc_filter_step_surrogate");
   if (!c || !aligned4(d)) return fail(c, CSC_ERR_ARG, "d must be a device pointer");
   if (sweeps < 1) return fail(c, CSC_ERR_ARG, "sweeps must be >= 1");
   if (c->sur_C == nullptr || c->sur_t < 1) return fail(c, CSC_ERR_ARG, "no surrogate: call csc_surrogate_update first");
@@ -1179,6 +1206,7 @@ static csc_status zg_pass(csc_ctx* c, const float* z) {
 }
 
 csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z, float step_d, float* step_used) {
+  NvtxScope nvtx_scope(c, "csc_filter_step");
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
   if (!(step_d >= 0.f) || !std::isfinite(step_d)) return fail(c, CSC_ERR_ARG, "step_d must be finite and >= 0");
@@ -1244,6 +1272,7 @@ static csc_status objective_finish(csc_ctx* c, float lambda, double out[3]) {
 }
 
 csc_status csc_objective(csc_ctx* c, const float* x, const float* d, const float* z, float lambda, double out[3]) {
+  NvtxScope nvtx_scope(c, "csc_objective");
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
   if (!out) return fail(c, CSC_ERR_ARG, "out must be a host pointer to 3 doubles");
@@ -1292,6 +1321,7 @@ csc_status csc_iterate(csc_ctx* c, const float* x_host, float* x, float* d, floa
 static csc_status iterate_impl(csc_ctx* c, const float* x_host, int slot, float* x, float* d, float* z, float lambda,
                                float step_z, float step_d, double p, uint64_t seed, uint32_t iter, double obj_out[3],
                                float taus_out[2]) {
+  NvtxScope nvtx_scope(c, slot >= 0 ? "csc_iterate_staged" : "csc_iterate");
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
   if (!obj_out) return fail(c, CSC_ERR_ARG, "obj_out must be a host pointer to 3 doubles");
@@ -1397,6 +1427,36 @@ csc_status csc_read_grad(csc_ctx* c, double* g_dev) {
   CSC_CUDA(c, cudaSetDevice(c->device));
   CSC_CUDA(c, cudaMemcpyAsync(g_dev, c->gsum, sizeof(double) * c->g.K * c->g.S * c->g.S, cudaMemcpyDeviceToDevice,
                               c->st));
+  return CSC_OK;
+}
+
+csc_status csc_count_nonzero(csc_ctx* c, const float* v, int64_t n, uint64_t* count) {
+  if (!c || !count || n < 0 || (n > 0 && !aligned4(v))) return fail(c, CSC_ERR_ARG, "v (device), n >= 0, count (host)");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  if (!c->cnt_dev) CSC_CUDA(c, cudaMalloc(&c->cnt_dev, sizeof(uint64_t)));
+  CSC_CUDA(c, cudaMemsetAsync(c->cnt_dev, 0, sizeof(uint64_t), c->st));
+  if (n > 0) CSC_LAUNCH(c, 1, csc::launch_count_nonzero(v, n, c->cnt_dev, c->st));
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal + kCnt, c->cnt_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  std::memcpy(count, c->h_dscal + kCnt, sizeof(uint64_t));
+  return CSC_OK;
+}
+
+csc_status csc_set_nvtx(csc_ctx* c, int enable) {
+  if (!c) return CSC_ERR_ARG;
+  c->nvtx = enable != 0;
+  return CSC_OK;
+}
+
+csc_status csc_comm_check(csc_ctx* c) {
+  if (!c) return CSC_ERR_ARG;
+  if (c->world <= 1 || c->comm == nullptr) return CSC_OK;
+  if (!g_nccl.CommGetAsyncError) return fail(c, CSC_ERR_NCCL, "libnccl.so.2 lacks ncclCommGetAsyncError");
+  ncclResult_t ar = ncclSuccess;
+  const ncclResult_t r = g_nccl.CommGetAsyncError(c->comm, &ar);
+  if (r != ncclSuccess) return fail(c, CSC_ERR_NCCL, std::string("ncclCommGetAsyncError: ") + g_nccl.GetErrorString(r));
+  if (ar != ncclSuccess && ar != ncclInProgress)
+    return fail(c, CSC_ERR_NCCL, std::string("NCCL asynchronous error: ") + g_nccl.GetErrorString(ar));
   return CSC_OK;
 }
 

@@ -125,6 +125,7 @@ cudaError_t launch_bcast_f32(float* dst, const float* src, int n, cudaStream_t s
 // r = -x (zero codes).
 cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st);
 // r += sign * x
+cudaError_t launch_count_nonzero(const float* v, int64_t n, uint64_t* out, cudaStream_t st);
 cudaError_t launch_resid_shift(const float* x, float* r, int64_t n, float sign, cudaStream_t st);
 
 // ---- tensor-core (tcgen05, 3xTF32) dense pass, csc_tc.cu

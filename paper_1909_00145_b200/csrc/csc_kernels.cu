@@ -933,6 +933,31 @@ __global__ void axpy_sign_kernel(const float* __restrict__ x, float* __restrict_
     r[i] = fmaf(sign, x[i], r[i]);
 }
 
+// number of nonzero entries (csc_count_nonzero; the trace's nnz column): per-warp ballot counts, one
+// 64-bit atomic per block
+__global__ void __launch_bounds__(256) count_nonzero_kernel(const float* __restrict__ v, int64_t n,
+                                                            unsigned long long* __restrict__ out) {
+  __shared__ unsigned int wsum[8];
+  unsigned int c = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    c += v[i] != 0.f ? 1u : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < 8; ++w) t += wsum[w];
+    atomicAdd(out, t);
+  }
+}
+
+cudaError_t launch_count_nonzero(const float* v, int64_t n, uint64_t* out, cudaStream_t st) {
+  count_nonzero_kernel<<<kFinalizeBlocks * 4, 256, 0, st>>>(v, n, reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_resid_shift(const float* x, float* r, int64_t n, float sign, cudaStream_t st) {
   axpy_sign_kernel<<<kFinalizeBlocks, 256, 0, st>>>(x, r, n, sign);
   return cudaGetLastError();
