@@ -472,12 +472,14 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
         uint32_t hv[8], lv[8];
         // filters past the group's end are padding (K = 100: 4 of the last group's 16 are real)
         const int npair = kv == 0xFFFFu ? 8 : (32 - __clz(kv) + 1) >> 1;
-        auto body = [&](auto per_k) {
+        auto body = [&](auto per_k, auto full) {
           constexpr bool PK = decltype(per_k)::value;
-          float* zp = zb;
+          constexpr bool FULL = decltype(full)::value;
+          float* zp = zb;          // even filter rows of the slice
+          float* zq = zb + plane;  // odd rows
 #pragma unroll
           for (int i2 = 0; i2 < 8; ++i2) {
-            if (i2 >= npair) {  // warp-uniform
+            if (!FULL && i2 >= npair) {  // warp-uniform
               hv[i2] = 0u;
               lv[i2] = 0u;
               continue;
@@ -497,18 +499,18 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
                                         make_float2(c[i], c[i + 1]), zc2);
             const float2 cl = make_float2(fminf(fmaxf(w.x, -kk0), kk0), fminf(fmaxf(w.y, -kk1), kk1));
             const float2 nz = __fadd2_rn(w, make_float2(-cl.x, -cl.y));  // S_kk(w): w -/+ kk outside, +0 inside
-            const bool ch0 = (wb & (1u << i)) != 0u && nz.x != zc2.x;
-            const bool ch1 = (wb & (2u << i)) != 0u && nz.y != zc2.y;
-            if (ch0) *zp = nz.x;
-            zp += plane;
-            if (ch1) *zp = nz.y;
-            zp += plane;
+            // z_new - z_old on the selected codes, 0 elsewhere; a code changes iff its difference is
+            // nonzero (x - y == 0 iff x == y in IEEE arithmetic with gradual underflow)
+            const float2 dd = __fadd2_rn(nz, make_float2(-zc2.x, -zc2.y));
+            const float2 dsel = make_float2((wb & (1u << i)) != 0u ? dd.x : 0.f, (wb & (2u << i)) != 0u ? dd.y : 0.f);
+            if (dsel.x != 0.f) *zp = nz.x;
+            if (dsel.y != 0.f) *zq = nz.y;
+            zp += 2 * plane;
+            zq += 2 * plane;
             // max |z| bound: every code of the slice was loaded, so |S(z - tau c)| over all of them bounds
             // the changed codes and the unchanged ones keep the previous bound
             wmax = fmaxf(wmax, fmaxf(fabsf(nz.x), fabsf(nz.y)));
-            const float2 dz = __fmul2_rn(__fadd2_rn(make_float2(ch0 ? nz.x : zc2.x, ch1 ? nz.y : zc2.y),
-                                                    make_float2(-zc2.x, -zc2.y)),
-                                         make_float2(sdz, sdz));
+            const float2 dz = __fmul2_rn(dsel, make_float2(sdz, sdz));
             const float h0 = rn11_h(dz.x), h1 = rn11_h(dz.y);
             const float2 lo = __fadd2_rn(dz, make_float2(-h0, -h1));
             hv[i2] = pack_h2_h(h0, h1);
@@ -521,8 +523,9 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
           for (int i = 0; i < 8; ++i) hv[i] = lv[i] = __float_as_uint(c[i] * zc[i]);
         } else
 #endif
-        if (A.tau_stride) body(std::true_type{});
-        else body(std::false_type{});
+        if (A.tau_stride) body(std::true_type{}, std::false_type{});
+        else if (kv == 0xFFFFu) body(std::false_type{}, std::true_type{});
+        else body(std::false_type{}, std::false_type{});
         if (a3p) {
           tmem_st8(tq + colb + 16u * gg, hv);
           tmem_st8(tq + colb + 16u * gg + 8u, lv);
@@ -638,6 +641,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     const float inv2 = exp2i_h(-(edz + ed));
     // add phases: the quarters in order (and the two row halves of a quarter in order when their windows
     // can overlap, Wc < 32 + P): deterministic fp32 sums
+    const bool wide = A.Wc >= kChTile;
     const bool split = A.Wc < 32 + P;
     const int nph = split ? 8 : 4;
     const int myph = split ? 2 * q + hh : q;
@@ -682,6 +686,21 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&y_empty);
+      if (wide) {
+        // Wc >= 128: the own values of all quarters and tap-row halves hit distinct window cells, and so do
+        // the halo values; two phases (own, then halo) keep every cell's sum in a fixed order
+#pragma unroll
+        for (int i = 0; i < AH; ++i)
+          if (a0 + i < a1) rowb[(a0 + i) * A.Wc] += own[i];
+        RT_WAIT(rc, 2, named_sync(2, 32 * kChHelpWarps));
+        if (lane < P) {
+#pragma unroll
+          for (int i = 0; i < AH; ++i)
+            if (a0 + i < a1) rowb[(a0 + i) * A.Wc + 32] += dnv[i];
+        }
+        RT_WAIT(rc, 2, named_sync(2, 32 * kChHelpWarps));
+        return;
+      }
 #pragma unroll 1
       for (int ph = 0; ph < nph; ++ph) {
         if (ph == myph) {
