@@ -472,14 +472,13 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
         uint32_t hv[8], lv[8];
         // filters past the group's end are padding (K = 100: 4 of the last group's 16 are real)
         const int npair = kv == 0xFFFFu ? 8 : (32 - __clz(kv) + 1) >> 1;
-        auto body = [&](auto per_k, auto full) {
+        auto body = [&](auto per_k) {
           constexpr bool PK = decltype(per_k)::value;
-          constexpr bool FULL = decltype(full)::value;
           float* zp = zb;          // even filter rows of the slice
           float* zq = zb + plane;  // odd rows
 #pragma unroll
           for (int i2 = 0; i2 < 8; ++i2) {
-            if (!FULL && i2 >= npair) {  // warp-uniform
+            if (i2 >= npair) {  // warp-uniform
               hv[i2] = 0u;
               lv[i2] = 0u;
               continue;
@@ -523,9 +522,8 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
           for (int i = 0; i < 8; ++i) hv[i] = lv[i] = __float_as_uint(c[i] * zc[i]);
         } else
 #endif
-        if (A.tau_stride) body(std::true_type{}, std::false_type{});
-        else if (kv == 0xFFFFu) body(std::false_type{}, std::true_type{});
-        else body(std::false_type{}, std::false_type{});
+        if (A.tau_stride) body(std::true_type{});
+        else body(std::false_type{});
         if (a3p) {
           tmem_st8(tq + colb + 16u * gg, hv);
           tmem_st8(tq + colb + 16u * gg + 8u, lv);
