@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
 conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
   constexpr int P = S - 1;
   extern __shared__ uint8_t smraw[];
-  __shared__ __align__(8) uint64_t full[kHNS], ready[kHNS], empty[kHNS], acc_full[2], acc_empty[2];
+  // per stage slot: full (TMA -> converters), rempty (converters done reading the raw tile -> TMA),
+  // ready (hi / lo written -> MMA), empty (MMA done reading hi / lo -> converters)
+  __shared__ __align__(8) uint64_t full[kHNS], rempty[kHNS], ready[kHNS], empty[kHNS], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ double l1_warp[kHConvWarps];
 
@@ -135,6 +137,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       mbar_init(&full[i], 1);
       mbar_init(&ready[i], 2);
       mbar_init(&empty[i], 1);
+      mbar_init(&rempty[i], 2);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -206,7 +209,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           const int pt = it.p0 + 128 * t;  // multiple of 4 floats (BR % 4 == 0): 16-B aligned box start
           for (int c = 0; c < A.NCH; ++c, ++g) {
             const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
-            mbar_wait(&empty[slot], ph ^ 1u);
+            mbar_wait(&rempty[slot], ph ^ 1u);  // the raw tile is free once converted (not once multiplied)
             mbar_arrive_expect_tx(&full[slot], kHRawBytes);
             const uint32_t dst = su32(stg + slot * kHStageBytes);
             tma_load_2d(dst, &tmap_z, pt, plane0 + 16 * c, &full[slot]);  // {128 positions, 16 planes}
@@ -234,6 +237,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           if (static_cast<int>(g % kHNS) != (cw >> 1)) continue;
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
           mbar_wait(&full[slot], ph);
+          mbar_wait(&empty[slot], ph ^ 1u);  // the MMA has finished with this slot's previous hi / lo
           const uint8_t* rawp = stg + slot * kHStageBytes;
           uint8_t* hip = stg + slot * kHStageBytes + kHRawBytes;
           uint8_t* lop = hip + kHHalfBytes;
@@ -257,9 +261,12 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
             }
           }
           if (want_l1) l1 += static_cast<double>(s1);
-          fence_async_shared();
+          fence_async_shared();  // hi / lo writes before the MMA's reads; raw reads before the TMA refill
           __syncwarp();
-          if (lane == 0) mbar_arrive(&ready[slot]);
+          if (lane == 0) {
+            mbar_arrive(&ready[slot]);
+            mbar_arrive(&rempty[slot]);
+          }
         }
       }
     }
