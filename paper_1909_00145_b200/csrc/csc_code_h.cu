@@ -50,7 +50,7 @@ namespace {
 using namespace tcx;
 
 constexpr int kChNS = 2;          // im2col slots (4 K16-steps = 64 taps each) in TMEM
-constexpr int kChEpiWarps = 12;  // 3 per TMEM lane quarter
+constexpr int kChEpiWarps = 16;  // 4 per TMEM lane quarter
 constexpr int kChHelpWarps = 8;  // 2 per TMEM lane quarter: the im2col of the next tile and the col2im of the last
 constexpr int kChEpiPerQ = kChEpiWarps / 4;
 constexpr int kChChunks = (8 + kChEpiPerQ - 1) / kChEpiPerQ;  // 16-filter groups per warp per tile (Npad <= 128)
