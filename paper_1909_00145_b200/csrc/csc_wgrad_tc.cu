@@ -46,6 +46,7 @@ constexpr int kWgEpiWarps = 16;   // epilogue warps (4 per lane quarter)
 constexpr int kWgConvBase = 2, kWgEpiBase = kWgConvBase + kWgConvWarps;
 constexpr int kWgWarps = kWgEpiBase + kWgEpiWarps;
 constexpr int kWgThreadsTc = 32 * kWgWarps;
+constexpr int kWgFlush = 32;     // accumulator tiles summed in fp32 before each fp64 flush (epilogue)
 constexpr int kWgMaxCpt = 2;      // chunks (32 positions) per accumulator tile (default; CSC_WG_CPT overrides)
 constexpr int kWgSmemMax = 220 * 1024;
 
@@ -227,7 +228,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
       cp_async_commit();
     };
     uint32_t g = 0;
-    unsigned long long w_zf = 0;
+    unsigned long long w_zf = 0, w_lo = 0, w_im = 0, w_st = 0;
     const unsigned long long t_cv = clock64();
     int ibuf = 0;
     if (gi < A.nitems) stage_r(gi, 0);
@@ -262,6 +263,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
         const unsigned long long tw2 = clock64();
         mbar_wait_sleep(&z_full[slot], ph);
         w_zf += clock64() - tw2;
+        const unsigned long long tl0 = clock64();
         // (1) lo copy of the z stage (elementwise, the swizzle is irrelevant)
         if (!(A.dbg & 16)) {
           float4* hi4 = reinterpret_cast<float4*>(stages + slot * 2 * A.stage_bytes);
@@ -279,6 +281,8 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
             lo4[e] = l;
           }
         }
+        const unsigned long long tl1 = clock64();
+        w_lo += tl1 - tl0;
         // (2) im2col of r into the A slot: the 4 K-steps of this chunk for this lane quarter.
         // R[(u,v)][(a,b)] = r[u-P+a][v-P+b] = rs[u - u_first + a][v + b]
 #pragma unroll
@@ -290,10 +294,12 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
               const int o = (u - it.u_first) * A.pitch + v;
               const float* srch = rtile + o;
               const float* srcl = rtilel + o;
+              // lanes of taps t >= s^2 load the tile at tap offset 0: their accumulator rows are never
+              // read (the epilogue stores t < s^2 only), and D row t depends on A row t alone
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                hv[j] = tap_ok ? __float_as_uint(srch[j]) : 0u;
-                lv[j] = tap_ok ? __float_as_uint(srcl[j]) : 0u;
+                hv[j] = __float_as_uint(srch[j]);
+                lv[j] = __float_as_uint(srcl[j]);
               }
             } else {
               // row wrap (Wc >= 8: at most one) or end of the item
@@ -302,7 +308,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
                 const int vj = v + j;
                 const bool wrap = vj >= A.Wc;
                 const int uu = wrap ? u + 1 : u, vv = wrap ? vj - A.Wc : vj;
-                const bool ok = tap_ok && p + j < it.p1;
+                const bool ok = p + j < it.p1;
                 const int o = (uu - it.u_first) * A.pitch + vv;
                 hv[j] = ok ? __float_as_uint(rtile[o]) : 0u;
                 lv[j] = ok ? __float_as_uint(rtilel[o]) : 0u;
@@ -320,10 +326,13 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
             ++u;
           }
         }
+        const unsigned long long tl2 = clock64();
+        w_im += tl2 - tl1;
         fence_async_shared();
         tmem_st_wait();
         tc_before();
         __syncwarp();
+        w_st += clock64() - tl2;
         if (lane == 0) mbar_arrive(&ready[slot]);
       }
       named_sync(1, 32 * kWgConvWarps);  // everyone is done reading rs[ibuf] before it is restaged
@@ -332,20 +341,46 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
     if (A.tdbg != nullptr && warp == kWgConvBase && lane == 0) {
       A.tdbg[blockIdx.x * 8 + 3] = w_zf;
       A.tdbg[blockIdx.x * 8 + 4] = clock64() - t_cv;
+      A.tdbg[blockIdx.x * 8 + 5] = w_lo;
+      A.tdbg[blockIdx.x * 8 + 6] = w_im;
+      A.tdbg[blockIdx.x * 8 + 7] = w_st;
     }
   } else {
     // ================================ epilogue
     const int ew = warp - kWgEpiBase;  // 0..15
     const int q = warp & 3;
     const int cb = ew >> 2;            // column block (NC columns)
-    // the tile sums (fp32 from TMEM) accumulate in compensated (Kahan) fp32 pairs: fp64-grade sums over a
-    // CTA's tiles at fp32 pipe cost (packed FADD2), instead of an F2F.F64 + DADD per element and tile
-    float2 sum[NC / 2], cmp[NC / 2];
+    // the tile sums (fp32 from TMEM) accumulate in plain fp32 registers over kWgFlush tiles (round to
+    // nearest: an unbiased error of ~sqrt(kWgFlush) 2^-24 of the block sum), and each block sum is added
+    // into the CTA's fp64 partial gpart[gi] in global memory (L2-resident, this CTA's own rows): NC live
+    // accumulators instead of a 2 NC-register compensated state (which spilled at 72 registers)
+    const int t = 32 * q + lane;
+    const int S2 = A.S * A.S;
+    float acc[NC];
 #pragma unroll
-    for (int i = 0; i < NC / 2; ++i) {
-      sum[i] = make_float2(0.f, 0.f);
-      cmp[i] = make_float2(0.f, 0.f);
-    }
+    for (int i = 0; i < NC; ++i) acc[i] = 0.f;
+    int nacc = 0;
+    bool first = true;
+    double* const gp0 = A.gpart + (static_cast<size_t>(gi) * A.K + kg * A.KC + cb * NC) * S2 + t;
+    const int nvalid = min(NC, min(A.KC - cb * NC, A.K - kg * A.KC - cb * NC));  // real filters of the block
+    auto flush = [&]() {
+      if (t < S2) {
+        // the first block is stored, later ones are added with fire-and-forget fp64 reductions; one thread
+        // owns each element, and same-address operations of a thread keep program order: deterministic
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          if (i < nvalid) {
+            double* gp = gp0 + static_cast<size_t>(i) * S2;
+            if (first) *gp = static_cast<double>(acc[i]);
+            else atomicAdd(gp, static_cast<double>(acc[i]));
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NC; ++i) acc[i] = 0.f;
+      first = false;
+      nacc = 0;
+    };
     const uint32_t tq = (static_cast<uint32_t>(32 * q) << 16);
     uint32_t tcount = 0;
     for (int item = gi; item < A.nitems; item += A.G) {
@@ -358,41 +393,23 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const WgArgs A) {
         const uint32_t col = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
         float f[NC];
 #pragma unroll
-        for (int j = 0; j < NC / 4; ++j) {
-          float f4[4];
-          tmem_ld4_nowait(tq + col + 4u * j, f4);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) f[4 * j + i] = f4[i];
-        }
+        for (int j = 0; j < NC / 4; ++j) tmem_ld4_nowait(tq + col + 4u * j, *reinterpret_cast<float(*)[4]>(f + 4 * j));
         tmem_ld_wait();
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
 #pragma unroll
         for (int i = 0; i < NC / 2; ++i) {
-          const float2 y = __fadd2_rn(make_float2(f[2 * i], f[2 * i + 1]), make_float2(-cmp[i].x, -cmp[i].y));
-          const float2 t = __fadd2_rn(sum[i], y);
-          cmp[i] = __fadd2_rn(__fadd2_rn(t, make_float2(-sum[i].x, -sum[i].y)), make_float2(-y.x, -y.y));
-          sum[i] = t;
+          const float2 a2 = __fadd2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), make_float2(f[2 * i], f[2 * i + 1]));
+          acc[2 * i] = a2.x;
+          acc[2 * i + 1] = a2.y;
         }
+        const bool last = tl + 1 == ntl && item + A.G >= A.nitems;
+        if (++nacc == kWgFlush || last) flush();
       }
     }
-    double acc[NC];
-#pragma unroll
-    for (int i = 0; i < NC / 2; ++i) {
-      acc[2 * i] = static_cast<double>(sum[i].x) - static_cast<double>(cmp[i].x);
-      acc[2 * i + 1] = static_cast<double>(sum[i].y) - static_cast<double>(cmp[i].y);
-    }
-    // per-CTA partial: gpart[gi][k][t]
-    const int t = 32 * q + lane;
-    const int S2 = A.S * A.S;
-    if (t < S2) {
-#pragma unroll
-      for (int i = 0; i < NC; ++i) {
-        const int k = kg * A.KC + cb * NC + i;
-        if (cb * NC + i < A.KC && k < A.K)
-          A.gpart[(static_cast<size_t>(gi) * A.K + k) * S2 + t] = acc[i];
-      }
+    if (first && t < S2) {  // no tiles: a zero partial
+      for (int i = 0; i < nvalid; ++i) gp0[static_cast<size_t>(i) * S2] = 0.0;
     }
   }
 
@@ -406,7 +423,29 @@ template <int NC>
 cudaError_t run_wgrad_tc(const CUtensorMap& tm, const WgArgs& a, int grid, int smem, cudaStream_t st) {
   cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&wgrad_tc_kernel<NC>), kWgSmemMax);
   if (e != cudaSuccess) return e;
+#ifdef CSC_ROLE_TIMING
+  static unsigned long long* dbg = nullptr;
+  static int calls = 0;
+  if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 8 * 1024);
+  cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 8 * 1024, st);
+  WgArgs b = a;
+  b.tdbg = dbg;
+  wgrad_tc_kernel<NC><<<grid, kWgThreadsTc, smem, st>>>(tm, b);
+  if (++calls % 4 == 0) {
+    static unsigned long long h[8 * 1024];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, dbg, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost);
+    double t[8] = {0};
+    for (int bk = 0; bk < grid; ++bk)
+      for (int i = 0; i < 8; ++i) t[i] += static_cast<double>(h[bk * 8 + i]) / grid;
+    fprintf(stderr,
+            "[wgrad roles] mma: total %.0f w_accempty %.0f w_ready %.0f | conv0: w_z %.0f total %.0f lo %.0f im2col %.0f "
+            "stwait %.0f\n",
+            t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+  }
+#else
   wgrad_tc_kernel<NC><<<grid, kWgThreadsTc, smem, st>>>(tm, a);
+#endif
   return cudaGetLastError();
 }
 
