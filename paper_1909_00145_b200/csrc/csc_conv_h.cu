@@ -71,6 +71,12 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+#ifdef CSC_ROLE_TIMING
+#define HT_NOW() clock64()
+#else
+#define HT_NOW() 0ull
+#endif
+
 struct HArgs {
   const uint16_t* bimg;      // [nks][2][2 atoms][KC][64] fp16, SW128
   const uint32_t* zmax;      // bound on max |z| (float bits)
@@ -81,6 +87,7 @@ struct HArgs {
   int KC, NCH, NT, ks;       // NCH = KC / 16
   int BR, nbands, nitems, WL;
   int precise;  // 1: hi*hi and the cross terms in separate TMEM accumulators (the ||Zg||^2 pass, reading T3)
+  unsigned long long* dbg;  // CSC_ROLE_TIMING builds: per-CTA role cycle counters [grid][16]
 };
 
 struct HItem {
@@ -158,18 +165,23 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     const uint32_t lbo_b = static_cast<uint32_t>(A.KC) * 128u;  // N atom (64 taps) stride
     const uint32_t sbh = su32(bsm), sbl = su32(bsm + bbytes), sst = su32(stg);
     uint32_t g = 0, tcount = 0;
+    unsigned long long t0 = HT_NOW(), w_ae = 0, w_rd = 0;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        unsigned long long ta = HT_NOW();
         mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
+        w_ae += HT_NOW() - ta;
         tc_after();
         // accumulator buffer: 256 columns [hi*hi | cross terms] (precise) or 128 (one accumulator)
         const uint32_t d = tbase + buf * (A.precise ? 256u : 128u);
         const uint32_t dx = A.precise ? d + 128u : d;
         for (int c = 0; c < A.NCH; ++c, ++g) {
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+          unsigned long long tb = HT_NOW();
           mbar_wait(&ready[slot], ph);
+          w_rd += HT_NOW() - tb;
           tc_after();
           const uint32_t ah = sst + slot * kHStageBytes + kHRawBytes;
           // A: MN-major SW128, 2 atoms of 64 positions at LBO = 16 rows x 128 B, 8-row K groups at SBO
@@ -196,6 +208,11 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         }
         mma_commit_elect(&acc_full[buf]);
       }
+    }
+    if (A.dbg && lane == 0) {
+      A.dbg[blockIdx.x * 16 + 0] = HT_NOW() - t0;
+      A.dbg[blockIdx.x * 16 + 1] = w_ae;
+      A.dbg[blockIdx.x * 16 + 2] = w_rd;
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -225,6 +242,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     // (i/2) & 7 of atom i/16, swizzled to chunk ((i/2) & 7) ^ (k & 7) (SWIZZLE_128B, MN-major)
     const int cw = warp - kHConvBase;
     const bool want_l1 = A.l1_part != nullptr;
+    unsigned long long c_t0 = HT_NOW(), c_wf = 0, c_we = 0;
     const float sz = exp2i(ez);
     double l1 = 0.0;
     uint32_t g = 0;
@@ -236,8 +254,12 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         for (int c = 0; c < A.NCH; ++c, ++g) {
           if (static_cast<int>(g % kHNS) != (cw >> 1)) continue;
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+          unsigned long long tw = HT_NOW();
           mbar_wait(&full[slot], ph);
+          unsigned long long tw2 = HT_NOW();
           mbar_wait(&empty[slot], ph ^ 1u);  // the MMA has finished with this slot's previous hi / lo
+          c_wf += tw2 - tw;
+          c_we += HT_NOW() - tw2;
           const uint8_t* rawp = stg + slot * kHStageBytes;
           uint8_t* hip = stg + slot * kHStageBytes + kHRawBytes;
           uint8_t* lop = hip + kHHalfBytes;
@@ -272,6 +294,11 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     }
     const double tsum = warp_sum_d(l1);
     if (lane == 0) l1_warp[cw] = tsum;
+    if (A.dbg && cw == 0 && lane == 0) {
+      A.dbg[blockIdx.x * 16 + 3] = HT_NOW() - c_t0;
+      A.dbg[blockIdx.x * 16 + 4] = c_wf;
+      A.dbg[blockIdx.x * 16 + 5] = c_we;
+    }
   } else {
     // ================================ epilogue: col2im into one band window (as csc_conv_ss.cu)
     const int q = warp & 3;                 // TMEM lane quarter of this warp
@@ -285,11 +312,14 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     const int nph = A.Wc >= 128 ? 1 : (A.Wc >= 32 + P ? 4 : 12);
     const int myph = nph == 1 ? 0 : (nph == 4 ? q : 3 * q + h);
     uint32_t tcount = 0;
+    unsigned long long e_t0 = HT_NOW(), e_wa = 0;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
+        unsigned long long te = HT_NOW();
         mbar_wait_sleep(&acc_full[buf], use & 1u);
+        e_wa += HT_NOW() - te;
         tc_after();
         const int pq = 128 * t + 32 * q;
         const bool pvalid = it.p0 + pq + lane < it.pend;
@@ -379,6 +409,10 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       named_sync(1, 32 * kHEpiWarps);
       for (int e = et; e < A.WL; e += 32 * kHEpiWarps) win[e] = 0.f;
       named_sync(1, 32 * kHEpiWarps);
+    }
+    if (A.dbg && warp == kHEpiBase && lane == 0) {
+      A.dbg[blockIdx.x * 16 + 6] = HT_NOW() - e_t0;
+      A.dbg[blockIdx.x * 16 + 7] = e_wa;
     }
   }
 
@@ -471,7 +505,29 @@ template <int S>
 cudaError_t run_conv_h(const CUtensorMap& tm, const HArgs& a, int grid, int smem, cudaStream_t st) {
   cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&conv_h_kernel<S>), kHSmemMax);
   if (e != cudaSuccess) return e;
+#ifdef CSC_ROLE_TIMING
+  static unsigned long long* dbg = nullptr;
+  static int calls = 0;
+  if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 16 * 1024);
+  cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 1024, st);
+  HArgs b = a;
+  b.dbg = dbg;
+  conv_h_kernel<S><<<grid, kHThreads, smem, st>>>(tm, b);
+  if (++calls % 4 == 0) {
+    static unsigned long long h[16 * 1024];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, dbg, sizeof(unsigned long long) * 16 * grid, cudaMemcpyDeviceToHost);
+    double t[16] = {0};
+    for (int bk = 0; bk < grid; ++bk)
+      for (int i = 0; i < 16; ++i) t[i] += static_cast<double>(h[bk * 16 + i]) / grid;
+    fprintf(stderr,
+            "[conv_h roles p%d] mma: total %.0f w_accempty %.0f w_ready %.0f | conv0: total %.0f w_full %.0f w_empty %.0f | "
+            "epi0: total %.0f w_accfull %.0f\n",
+            a.precise, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+  }
+#else
   conv_h_kernel<S><<<grid, kHThreads, smem, st>>>(tm, a);
+#endif
   return cudaGetLastError();
 }
 
