@@ -70,7 +70,9 @@ std::mutex g_nccl_mu;
 constexpr double kBcdRidge = 1e-10;  // DESIGN.md reading B2
 
 // device scalar slots
-enum DSlot { kSqR = 0, kL1 = 1, kZg2 = 2, kGG = 3, kLhat = 4, kCnt = 7, kNumD = 8 };  // kCnt: csc_count_nonzero (host mirror only)
+// kCounter: a block counter of the fused fixup reductions (zero, cleared by each launch); kCnt:
+// csc_count_nonzero (host mirror only)
+enum DSlot { kSqR = 0, kL1 = 1, kZg2 = 2, kGG = 3, kLhat = 4, kCounter = 6, kCnt = 7, kNumD = 8 };
 enum FSlot { kTauZ = 0, kTauD = 1, kNumF = 4 };
 
 }  // namespace
@@ -174,6 +176,7 @@ struct csc_ctx {
   int64_t adm_cap = 0;
   ncclComm_t comm = nullptr;
   bool nvtx = false;  // csc_set_nvtx / CSC_NVTX=1
+  double* gf_scratch = nullptr;  // grad_finish block sums + counter
   uint64_t* cnt_dev = nullptr;  // csc_count_nonzero
   uint64_t launches = 0;
   std::string err;
@@ -295,11 +298,16 @@ csc_status dense_residual(csc_ctx* c, const float* x, const float* d, const floa
   }
   if (c->tc_on) {
     CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, z, d, l1p));
+    csc::FixupSums fs;
+    fs.out_sq = c->dscal + kSqR;
+    if (want_l1) {
+      fs.l1_part = c->l1_part;
+      fs.nl1 = c->tc.nks * c->tc.grid;
+      fs.out_l1 = c->dscal + kL1;
+    }
+    fs.counter = reinterpret_cast<unsigned long long*>(c->dscal + kCounter);
     CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
-                 csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, x, c->r, csc::kConvResidual, c->sq_part, c->st));
-    CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kSqR, 1.0, c->st));
-    if (want_l1)
-      CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->l1_part, c->tc.nks * c->tc.grid, c->dscal + kL1, 1.0, c->st));
+                 csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, x, c->r, csc::kConvResidual, c->sq_part, c->st, &fs));
     c->cache_valid = true;
     c->cx = x;
     c->cd = d;
@@ -532,6 +540,7 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   ok = ok && alloc(reinterpret_cast<void**>(&c->colw), sizeof(uint32_t) * static_cast<size_t>(g.K) * NB * g.Wc);
   ok = ok && alloc(reinterpret_cast<void**>(&c->lip_part), sizeof(double) * (64 * 64 * csc::ceil_div(g.K, 2) + 64));
   ok = ok && alloc(reinterpret_cast<void**>(&c->dscal), sizeof(double) * kNumD);
+  ok = ok && alloc(reinterpret_cast<void**>(&c->gf_scratch), sizeof(double) * (csc::ceil_div(g.K * g.S * g.S, 256) + 1));
   ok = ok && alloc(reinterpret_cast<void**>(&c->fscal), sizeof(float) * kNumF);
   ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_dscal), sizeof(double) * kNumD) == cudaSuccess;
   ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_fscal), sizeof(float) * kNumF) == cudaSuccess;
@@ -564,6 +573,9 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
     return init_fail(CSC_ERR_OOM, "device allocation failed in csc_init");
   }
   cudaMemsetAsync(c->dscal, 0, sizeof(double) * kNumD, c->st);
+  cudaMemsetAsync(c->gf_scratch, 0, sizeof(double) * (csc::ceil_div(g.K * g.S * g.S, 256) + 1), c->st);
+  // the Lipschitz kernel's max / counter state past the partials starts at zero (launch_lipschitz)
+  cudaMemsetAsync(c->lip_part, 0, sizeof(double) * (64 * 64 * csc::ceil_div(g.K, 2) + 64), c->st);
   cudaMemsetAsync(c->fscal, 0, sizeof(float) * kNumF, c->st);
   cudaMemsetAsync(c->gsum, 0, sizeof(double) * g.K * M, c->st);
 
@@ -645,6 +657,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->gpart);
   cudaFree(c->gsum);
   cudaFree(c->cnt_dev);
+  cudaFree(c->gf_scratch);
   cudaFree(c->g32);
   cudaFree(c->colw);
   cudaFree(c->mwords);
@@ -750,7 +763,7 @@ csc_status csc_code_step(csc_ctx* c, const float* x, const float* d, float* z, f
     c->lip_valid = false;  // the tau_z slot now holds the explicit step
   } else {
     if (!(c->lip_valid && c->lip_d == d)) {
-      CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 3,
+      CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 2,
                    csc::launch_lipschitz(g, d, c->lip_part, c->dscal + kLhat, c->fscal + kTauZ, c->st));
       c->lip_valid = true;
       c->lip_d = d;
@@ -1185,9 +1198,12 @@ static csc_status zg_pass(csc_ctx* c, const float* z) {
   const Geom& g = c->g;
   if (g.N > 0 && c->tc_on) {
     CSC_LAUNCH_C(c, CSC_K_CONV, 1 + c->tc.nks, conv_tc_any(c, z, c->g32, nullptr, true));
+    csc::FixupSums fs;
+    fs.out_sq = c->dscal + kZg2;
+    fs.counter = reinterpret_cast<unsigned long long*>(c->dscal + kCounter);
     CSC_LAUNCH_C(c, CSC_K_CONV_FINALIZE, 1,
-                 csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, nullptr, csc::kConvSumSq, c->sq_part, c->st));
-    CSC_LAUNCH(c, 1, csc::launch_reduce_sum(c->sq_part, csc::kFinalizeBlocks, c->dscal + kZg2, 1.0, c->st));
+                 csc::launch_conv_tc_fixup(g, c->tc, c->tc_part, nullptr, nullptr, csc::kConvSumSq, c->sq_part, c->st,
+                                           &fs));
   } else if (g.N > 0) {
     int nb = 0;
     CSC_LAUNCH_C(c, CSC_K_CONV, 1, csc::launch_conv_fwd(g, z, c->g32, nullptr, nullptr, c->part, c->ksplit,
@@ -1230,7 +1246,7 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
   }
   s = allreduce_d(c, c->gsum, static_cast<size_t>(g.K) * M);
   if (s != CSC_OK) return s;
-  CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->st));
+  CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->gf_scratch, c->st));
   if (step_d == 0.f) {
     s = zg_pass(c, z);
     if (s != CSC_OK) return s;
@@ -1410,7 +1426,7 @@ csc_status csc_zg_sumsq(csc_ctx* c, const float* z, const double* g_dev) {
   CSC_CUDA(c, cudaSetDevice(c->device));
   const Geom& g = c->g;
   CSC_CUDA(c, cudaMemcpyAsync(c->gsum, g_dev, sizeof(double) * g.K * g.S * g.S, cudaMemcpyDeviceToDevice, c->st));
-  CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->st));
+  CSC_LAUNCH(c, 1, csc::launch_grad_finish(g, c->gsum, c->g32, c->dscal + kGG, c->gf_scratch, c->st));
   return zg_pass(c, z);
 }
 
@@ -1463,7 +1479,7 @@ csc_status csc_comm_check(csc_ctx* c) {
 csc_status csc_lipschitz(csc_ctx* c, const float* d, double* out) {
   if (!c || !aligned4(d) || !out) return fail(c, CSC_ERR_ARG, "d (device) and out (host) required");
   CSC_CUDA(c, cudaSetDevice(c->device));
-  CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 3, csc::launch_lipschitz(c->g, d, c->lip_part, c->dscal + kLhat, nullptr, c->st));
+  CSC_LAUNCH_C(c, CSC_K_LIPSCHITZ, 2, csc::launch_lipschitz(c->g, d, c->lip_part, c->dscal + kLhat, nullptr, c->st));
   c->lip_valid = false;  // kLhat now describes this d
   CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal + kLhat, c->dscal + kLhat, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CSC_CUDA(c, cudaStreamSynchronize(c->st));

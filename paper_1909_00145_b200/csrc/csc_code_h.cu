@@ -972,7 +972,7 @@ cudaError_t launch_code_a3_fixup(const Geom& g, const CodeTcPlan& p, const float
   if (g.W % 4 == 0 && (reinterpret_cast<uintptr_t>(part) & 15u) == 0 && (reinterpret_cast<uintptr_t>(r) & 15u) == 0 &&
       static_cast<int64_t>(g.N) * g.H * (g.W / 4) < (int64_t(1) << 31)) {
     const int total = g.N * g.H * (g.W / 4);
-    const int blocks = total / 256 + 1 < kFinalizeBlocks * 2 ? total / 256 + 1 : kFinalizeBlocks * 2;
+    const int blocks = total / 256 + 1;  // one float4 per thread: every load in flight at once
     code_a3_fixup4_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(part), p.nkg, g.N, g.H, g.W / 4,
                                                    g.P, p.BR, p.nbands, reinterpret_cast<float4*>(r));
   } else {

@@ -83,7 +83,8 @@ cudaError_t launch_wgrad(const Geom& g, const float* z, const float* r, int G, d
 cudaError_t launch_wgrad_reduce(const Geom& g, const double* gpart, int G, double* gsum,
                                 cudaStream_t st);
 // g32 = (float)gsum, gg_out = sum gsum^2 (fp64) -- after the cross-rank all-reduce.
-cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, double* gg_out,
+// scratch: ceil(K s^2 / 256) + 1 doubles, the last one zero (a block counter the kernel clears)
+cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, double* gg_out, double* scratch,
                                cudaStream_t st);
 
 // Mask (Philox4x32-10) -- internal column-word layout for the code step:
@@ -163,8 +164,17 @@ TcPlan conv_tc_plan(const Geom& g, int num_sms);
 cudaError_t launch_conv_tc(const Geom& g, const TcPlan& p, const float* z, const float* filt, float* bimg,
                            float* part, double* l1_part, cudaStream_t st);
 // part -> r = y - x (residual mode) or sum y^2 (sum-of-squares mode); per-block partials -> sq_part[kFinalizeBlocks].
+// the fixup's own reductions (fsum != nullptr): sum r^2 -> out_sq and sum of the nl1 partials l1_part
+// -> out_l1 (optional), in fixed orders; counter: one zero-initialised 64-bit word the launch clears
+struct FixupSums {
+  double* out_sq = nullptr;
+  const double* l1_part = nullptr;
+  int nl1 = 0;
+  double* out_l1 = nullptr;
+  unsigned long long* counter = nullptr;
+};
 cudaError_t launch_conv_tc_fixup(const Geom& g, const TcPlan& p, const float* part, const float* x, float* r,
-                                 int mode, double* sq_part, cudaStream_t st);
+                                 int mode, double* sq_part, cudaStream_t st, const FixupSums* fsum = nullptr);
 
 
 // ---- tensor-core (tcgen05, 3xTF32) filter gradient, csc_wgrad_tc.cu

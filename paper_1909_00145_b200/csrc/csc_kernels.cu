@@ -506,16 +506,35 @@ __global__ void __launch_bounds__(256) wgrad_reduce_kernel(const double* __restr
   }
 }
 
-__global__ void grad_finish_kernel(const double* __restrict__ gsum, int nel, float* __restrict__ g32,
-                                   double* __restrict__ gg_out) {
+// g32 = fp32(g) and <g, g>: one element per thread, block sums into scratch[blockIdx.x], and the last
+// block adds the block sums in block order (deterministic) into *gg_out and clears the block counter
+// (scratch[gridDim.x], zero at allocation)
+__global__ void __launch_bounds__(256) grad_finish_kernel(const double* __restrict__ gsum, int nel,
+                                                         float* __restrict__ g32, double* __restrict__ gg_out,
+                                                         double* __restrict__ scratch) {
+  __shared__ bool last;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
-  for (int i = threadIdx.x; i < nel; i += blockDim.x) {
+  if (i < nel) {
     const double v = gsum[i];
     g32[i] = static_cast<float>(v);
-    s += v * v;
+    s = v * v;
   }
   const double t = block_sum_d(s);
-  if (threadIdx.x == 0) *gg_out = t;
+  if (threadIdx.x == 0) {
+    scratch[blockIdx.x] = t;
+    __threadfence();
+    auto* cnt = reinterpret_cast<unsigned long long*>(scratch + gridDim.x);
+    last = atomicAdd(cnt, 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double tot = 0.0;
+    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) tot += __ldcg(scratch + b);
+    *gg_out = tot;
+    *reinterpret_cast<unsigned long long*>(scratch + gridDim.x) = 0ull;
+  }
 }
 
 // ------------------------------------------------------------------ code step
@@ -674,30 +693,50 @@ __global__ void __launch_bounds__(kLipThreads) lipschitz_partial_kernel(const fl
   }
 }
 
-// Per grid point: sum of the filter-chunk partials (fixed order); per block: the max over its
-// points -> bmax[blockIdx.x].  Then lipschitz_max_kernel takes the max over the blocks.
-constexpr int kLipFinalBlocks = 16;
-__global__ void __launch_bounds__(256) lipschitz_final_kernel(const double* __restrict__ part, int nkc,
-                                                             double* __restrict__ bmax) {
-  double best = 0.0;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kLipG * kLipG; e += gridDim.x * blockDim.x) {
-    double s = 0.0;
-#pragma unroll 10
-    for (int kc = 0; kc < nkc; ++kc) s += part[static_cast<int64_t>(kc) * kLipG * kLipG + e];
-    best = fmax(best, s);
+// One kernel for the sum over filter chunks and the max: block = 64 grid points x 4 chunk ranges of the
+// filter-chunk partials (each summed in order, then the 4 in order: a fixed order), the block max into
+// a 64-bit atomic max (non-negative doubles order as their bits), the last block writes L and 1/L and
+// clears the max and the block counter for the next launch (state[0] = max bits, state[1] = count).
+__global__ void __launch_bounds__(256) lipschitz_final2_kernel(const double* __restrict__ part, int nkc,
+                                                              unsigned long long* __restrict__ state,
+                                                              double* __restrict__ lhat, float* __restrict__ tau_out) {
+  __shared__ double ps[4][64];
+  __shared__ bool last;
+  const int pl = threadIdx.x & 63, ch = threadIdx.x >> 6;
+  const int pt = blockIdx.x * 64 + pl;
+  const int per = (nkc + 3) / 4;
+  const int c0 = ch * per, c1 = min(nkc, c0 + per);
+  double s = 0.0;
+#pragma unroll 8
+  for (int kc = c0; kc < c1; ++kc) s += __ldg(part + static_cast<int64_t>(kc) * kLipG * kLipG + pt);
+  ps[ch][pl] = s;
+  __syncthreads();
+  double m = 0.0;
+  if (threadIdx.x < 64) {
+    m = ((ps[0][pl] + ps[1][pl]) + ps[2][pl]) + ps[3][pl];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   }
-  const double m = block_max_d(best);
-  if (threadIdx.x == 0) bmax[blockIdx.x] = m;
+  if (threadIdx.x == 0) ps[0][0] = m;
+  __syncthreads();
+  if (threadIdx.x == 32) ps[0][0] = fmax(ps[0][0], m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(state, static_cast<unsigned long long>(__double_as_longlong(ps[0][0])));
+    __threadfence();
+    last = atomicAdd(state + 1, 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const double L = __longlong_as_double(static_cast<long long>(atomicAdd(state, 0ull)));
+    *lhat = L;
+    if (tau_out != nullptr) *tau_out = L > 0.0 ? static_cast<float>(1.0 / L) : 0.f;
+    state[0] = 0ull;
+    state[1] = 0ull;
+  }
 }
 
-__global__ void lipschitz_max_kernel(const double* __restrict__ bmax, double* __restrict__ lhat,
-                                     float* __restrict__ tau_out) {
-  if (threadIdx.x != 0) return;
-  double m = 0.0;
-  for (int b = 0; b < kLipFinalBlocks; ++b) m = fmax(m, bmax[b]);
-  *lhat = m;
-  if (tau_out != nullptr) *tau_out = m > 0.0 ? static_cast<float>(1.0 / m) : 0.f;
-}
 
 // ------------------------------------------------------------------ filter update
 __global__ void filter_tau_kernel(const double* __restrict__ gg, const double* __restrict__ zg2, float step,
@@ -855,9 +894,10 @@ cudaError_t launch_wgrad_reduce(const Geom& g, const double* gpart, int G, doubl
   return cudaGetLastError();
 }
 
-cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, double* gg_out, cudaStream_t st) {
+cudaError_t launch_grad_finish(const Geom& g, const double* gsum, float* g32, double* gg_out, double* scratch,
+                               cudaStream_t st) {
   const int nel = g.K * g.S * g.S;
-  grad_finish_kernel<<<1, 1024, 0, st>>>(gsum, nel, g32, gg_out);
+  grad_finish_kernel<<<ceil_div(nel, 256), 256, 0, st>>>(gsum, nel, g32, gg_out, scratch);
   return cudaGetLastError();
 }
 
@@ -909,9 +949,10 @@ cudaError_t launch_lipschitz(const Geom& g, const float* d, double* part, double
   lipschitz_partial_kernel<<<dim3(nkc, 4), kLipThreads, 0, st>>>(d, g, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  double* bmax = part + static_cast<int64_t>(nkc) * kLipG * kLipG;  // lip_part has room (see csc_init)
-  lipschitz_final_kernel<<<kLipFinalBlocks, 256, 0, st>>>(part, nkc, bmax);
-  lipschitz_max_kernel<<<1, 32, 0, st>>>(bmax, lhat, tau_out);
+  // lip_part has 64 doubles of room past the partials (see csc_init): the final kernel's max / counter
+  // state, zero at allocation and cleared by each launch's last block
+  auto* state = reinterpret_cast<unsigned long long*>(part + static_cast<int64_t>(nkc) * kLipG * kLipG);
+  lipschitz_final2_kernel<<<kLipG * kLipG / 64, 256, 0, st>>>(part, nkc, state, lhat, tau_out);
   return cudaGetLastError();
 }
 

@@ -570,39 +570,78 @@ __global__ void tc_fixup_kernel(const float* __restrict__ part, int N, int H, in
   }
 }
 
+// The fixup's reductions in its last block (one launch less per dense pass): the block sums of r^2 in
+// block order -> *out_sq, and the ||z||_1 partials of the dense pass (if any) in order -> *out_l1; the
+// block counter (zero at allocation) is cleared for the next launch.
+__device__ void fixup_finish(const double* sq_part, const FixupSums& fs) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(fs.counter, 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double t = 0.0;
+  for (int b = 0; b < static_cast<int>(gridDim.x); ++b) t += __ldcg(sq_part + b);
+  *fs.out_sq = t;
+  if (fs.l1_part != nullptr) {
+    double u = 0.0;
+    for (int b = 0; b < fs.nl1; ++b) u += __ldcg(fs.l1_part + b);
+    *fs.out_l1 = u;
+  }
+  *fs.counter = 0ull;
+}
+
 // Same as tc_fixup_kernel for W % 4 == 0 with 16-B aligned buffers: a thread takes 4 consecutive
 // columns (float4) and the block covers 256 / (W/4) rows at once, so each thread has its loads of
 // several rows in flight instead of one dependent chain per element.
 __global__ void tc_fixup4_kernel(const float* __restrict__ part, int N, int H, int W, int P, int BR, int nbands,
                                  const float4* __restrict__ x, float4* __restrict__ r, int mode,
-                                 double* __restrict__ sq_part) {
+                                 double* __restrict__ sq_part, FixupSums fs) {
   const size_t win = static_cast<size_t>(BR + P) * W;
   const int W4 = W / 4;
   const int rpb = blockDim.x / W4 > 0 ? blockDim.x / W4 : 1;  // rows per block step
   const int rr = threadIdx.x / W4, j4 = threadIdx.x - rr * W4;
   double sq = 0.0;
   if (rr < rpb && j4 < W4) {
-    for (int row = blockIdx.x * rpb + rr; row < N * H; row += gridDim.x * rpb) {
-      const int n = row / H, i = row - n * H;
-      const int b0 = i / BR;
-      int b1 = (i + P) / BR;
-      if (b1 > nbands - 1) b1 = nbands - 1;
-      const float* pk = part + static_cast<size_t>(n) * nbands * win;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int b = b0; b <= b1; ++b) {
-        const float4 t = reinterpret_cast<const float4*>(pk + b * win + static_cast<size_t>(i - b * BR + P) * W)[j4];
-        v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
-      }
-      const size_t o4 = static_cast<size_t>(row) * W4 + j4;
-      if (mode == kConvResidual) {
-        if (x != nullptr) {
-          const float4 xv = x[o4];
-          v.x -= xv.x; v.y -= xv.y; v.z -= xv.z; v.w -= xv.w;
+    // two rows per thread per step with all their loads issued first (a row spans at most two bands
+    // when P < BR; a third band, if any, is added after)
+    const int stride = gridDim.x * rpb;
+    for (int row0 = blockIdx.x * rpb + rr; row0 < N * H; row0 += 2 * stride) {
+      float4 v[2], xv[2];
+      int rows[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = row0 + h * stride;
+        rows[h] = row;
+        v[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+        xv[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < N * H) {
+          const int n = row / H, i = row - n * H;
+          const int b0 = i / BR;
+          int b1 = (i + P) / BR;
+          if (b1 > nbands - 1) b1 = nbands - 1;
+          const float* pk = part + static_cast<size_t>(n) * nbands * win;
+          for (int b = b0; b <= b1; ++b) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(pk + b * win + static_cast<size_t>(i - b * BR + P) * W) + j4);
+            v[h].x += t.x; v[h].y += t.y; v[h].z += t.z; v[h].w += t.w;
+          }
+          if (mode == kConvResidual && x != nullptr) xv[h] = __ldg(x + static_cast<size_t>(row) * W4 + j4);
         }
-        r[o4] = v;
       }
-      sq += static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y + static_cast<double>(v.z) * v.z +
-            static_cast<double>(v.w) * v.w;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (rows[h] >= N * H) continue;
+        float4 w = v[h];
+        if (mode == kConvResidual) {
+          w.x -= xv[h].x; w.y -= xv[h].y; w.z -= xv[h].z; w.w -= xv[h].w;
+          r[static_cast<size_t>(rows[h]) * W4 + j4] = w;
+        }
+        sq += static_cast<double>(w.x) * w.x + static_cast<double>(w.y) * w.y + static_cast<double>(w.z) * w.z +
+              static_cast<double>(w.w) * w.w;
+      }
     }
   }
   __shared__ double red[32];
@@ -616,6 +655,7 @@ __global__ void tc_fixup4_kernel(const float* __restrict__ part, int N, int H, i
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
     sq_part[blockIdx.x] = s;
   }
+  if (fs.out_sq != nullptr) fixup_finish(sq_part, fs);
 }
 
 }  // namespace
@@ -711,16 +751,21 @@ cudaError_t launch_tc_bimg(const Geom& g, const TcPlan& p, const float* filt, fl
 }
 
 cudaError_t launch_conv_tc_fixup(const Geom& g, const TcPlan& p, const float* part, const float* x, float* r,
-                                 int mode, double* sq_part, cudaStream_t st) {
+                                 int mode, double* sq_part, cudaStream_t st, const FixupSums* fsum) {
   if (g.W % 4 == 0 && g.W <= 1024 && (reinterpret_cast<uintptr_t>(part) & 15u) == 0 &&
       (x == nullptr || (reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
       (r == nullptr || (reinterpret_cast<uintptr_t>(r) & 15u) == 0)) {
     tc_fixup4_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, g.N, g.H, g.W, g.P, p.BR, p.nbands,
                                                        reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(r),
-                                                       mode, sq_part);
+                                                       mode, sq_part, fsum ? *fsum : FixupSums{});
   } else {
     tc_fixup_kernel<<<kFinalizeBlocks, 256, 0, st>>>(part, g.N, g.H, g.W, g.P, p.BR, p.nbands, p.nks, x, r, mode,
                                                       sq_part);
+    if (fsum != nullptr) {
+      cudaError_t e = launch_reduce_sum(sq_part, kFinalizeBlocks, fsum->out_sq, 1.0, st);
+      if (e != cudaSuccess) return e;
+      if (fsum->l1_part != nullptr) return launch_reduce_sum(fsum->l1_part, fsum->nl1, fsum->out_l1, 1.0, st);
+    }
   }
   return cudaGetLastError();
 }
