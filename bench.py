@@ -67,6 +67,10 @@ def _traffic():
         return {}
 
 
+# kernel classes timed with CUDA events inside the timed region (kernel_rooflines reads these)
+ROOFLINE_CLASSES = ("conv", "wgrad", "code_step", "admm", "bcd")
+
+
 def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox", filter_solver="pg"):
     """Per kernel class: algorithmic work per launch / measured average launch time vs its roofs.
     Algorithmic units: dense pass / filter gradient 2*N*K*s^2*H*W FLOP and a read of
@@ -356,7 +360,11 @@ def run_ours(args):
     d = torch.from_numpy(d_np).to(dev)
     z = torch.zeros((nl, cfg.K, cfg.Hc, cfg.Wc), dtype=torch.float32, device=dev)
     nccl_id = cdist.broadcast_nccl_id(device=dev) if ws > 1 else None
-    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    # the library's stream: a dedicated stream (a CUDA graph cannot be captured on the legacy default
+    # stream); torch's work of the timed loop (L2 flush, events) goes to the same stream
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx = pkg.Context(nl, cfg.K, cfg.s, cfg.H, cfg.W, world=ws, rank=rank, device=local, stream=stream,
                       nccl_id=nccl_id)
     if args.step_rule != "lipschitz":
@@ -399,14 +407,51 @@ def run_ours(args):
             ctx.filter_step(x, d, z)
         return ctx.objective(x, d, z, cfg.lam), None
 
+    # mask iterations: iter + *off (csc_set_iter_offset); 0 for the eager calls, the step's iteration for
+    # the graph replays
+    off = torch.zeros(1, dtype=torch.int32, device=dev)
+    ctx.set_iter_offset(off)
     it = 0
     for _ in range(args.warmup):
         it += 1
         step(it)
     torch.cuda.synchronize()
 
-    # ---- timed region: device-resident inputs
-    ctx.profile_enable(True)
+    # ---- timed region: device-resident inputs.  The prox / projected-gradient iteration (code step,
+    # filter step, objective pass) is captured once as a CUDA graph and replayed every step, the step's
+    # mask iteration written to the device offset first; each step then reads F (csc_objective_read,
+    # host sync) as csc_iterate does.  The kernel durations of the roofline come from a second capture of
+    # the same iteration with CUDA events around the long kernels (external event-record nodes), replayed
+    # as many times right after the timed region: the event nodes cost ~4% of a step, so they are kept
+    # out of the timed graph.  The other solvers (--code-solver admm, --filter-solver bcd|surrogate)
+    # allocate on first use and run eagerly, with events on the long kernels inside the timed loop.
+    use_graph = not (admm or bcd or sur) and not args.no_graph
+    graph = graph_ev = None
+    graph_launches = 0
+    if use_graph:
+        def body():
+            ctx.code_step(x, d, z, cfg.lam, cfg.p, seed, 0)
+            ctx.filter_step(x, d, z)
+            ctx.objective_enqueue(x, d, z)
+        it += 1
+        off.fill_(it)
+        ctx.profile_enable(True, classes=ROOFLINE_CLASSES)  # one eager profiled run fills the event pool
+        body()
+        ctx.objective_read(cfg.lam)
+        ctx.profile_read()
+        ctx.profile_enable(False)
+        graph = torch.cuda.CUDAGraph()
+        lc0 = ctx.launch_count
+        with torch.cuda.graph(graph, stream=stream):
+            body()
+        graph_launches = ctx.launch_count - lc0
+        ctx.profile_enable(True, classes=ROOFLINE_CLASSES)
+        graph_ev = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_ev, stream=stream):
+            body()
+        torch.cuda.synchronize()
+    else:
+        ctx.profile_enable(True, classes=ROOFLINE_CLASSES)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -420,23 +465,59 @@ def run_ours(args):
         it += 1
         if l2_flush is not None:
             l2_flush.fill_(float(it))
-        ev0.record(stream)
-        obj, taus = step(it)
-        ev1.record(stream)
+        if graph is not None:
+            off.fill_(it)
+            ev0.record(stream)
+            graph.replay()
+            ev1.record(stream)
+            obj = ctx.objective_read(cfg.lam)
+        else:
+            ev0.record(stream)
+            obj, taus = step(it)
+            ev1.record(stream)
         ev1.synchronize()
         t_total += ev0.elapsed_time(ev1)
         objs.append(obj[0])
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    launches = ctx.launch_count - l0
+    launches = (graph_launches * args.steps) if graph is not None else ctx.launch_count - l0
+    if graph_ev is not None:
+        # the kernel-timing replays: the same iteration with event nodes around the long kernels
+        for _ in range(args.steps):
+            it += 1
+            if l2_flush is not None:
+                l2_flush.fill_(float(it))
+            off.fill_(it)
+            graph_ev.replay()
+            ctx.objective_read(cfg.lam)
+            ctx.profile_sample()
     prof = ctx.profile_read()
     ctx.profile_enable(False)
+    off.fill_(0)
     tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_ms = float(tt.item())
     value = args.steps / (t_ms / 1e3)
+    if rank == 0:
+        print(f"[bench] timed region: {value:.2f} it/s, {t_ms / args.steps:.4f} ms/step", file=sys.stderr, flush=True)
+
+    # ---- the per-class breakdown of every kernel class (untimed: events on every launch)
+    ctx.profile_enable(True)
+    tb0 = torch.cuda.Event(enable_timing=True)
+    tb1 = torch.cuda.Event(enable_timing=True)
+    tb0.record(stream)
+    for _ in range(args.steps):
+        it += 1
+        if l2_flush is not None:
+            l2_flush.fill_(float(it))
+        step(it)
+    tb1.record(stream)
+    tb1.synchronize()
+    prof_all = ctx.profile_read()
+    t_prof = tb0.elapsed_time(tb1)
+    ctx.profile_enable(False)
 
     # ---- e2e: same iteration through the C ABI with the step's images uploaded from pinned host memory.
     # Hot path: double-buffered -- step i+1's images are staged (async H2D on the library's copy stream)
@@ -476,7 +557,7 @@ def run_ours(args):
         rl = kernel_rooflines(prof, cfg, nl, args.steps, ctx.variants, args.code_solver, args.filter_solver)
         dom = max(rl, key=lambda k: rl[k]["ms_per_step"])
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
-                       "share": v[0] / max(t_total, 1e-9)} for k, v in prof.items()}
+                       "share": v[0] / max(t_prof, 1e-9)} for k, v in prof_all.items()}
         line = {
             "metric": "csc_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
@@ -484,10 +565,12 @@ def run_ours(args):
             "dtype": "f32 state; fp16 3-term split products on the tensor cores, fp32 accumulate, fp64 reductions",
             "data": "synthetic",
             "config": dict(_config_dict(cfg, ws), code_solver=args.code_solver, filter_solver=args.filter_solver,
-                           step_rule=args.step_rule, mask=args.mask),
+                           step_rule=args.step_rule, mask=args.mask, cuda_graph=graph is not None),
             "roofline": dict(rl[dom], dominant_class=dom),
             "kernel_rooflines": rl,
             "kernels": kernels,
+            "kernels_note": "every class, from a second profiled pass of the same number of steps (events on every "
+                            "launch); the timed region times only the roofline classes " + "/".join(ROOFLINE_CLASSES),
             "objective_last": objs[-1] if objs else None,
             "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": 4 * nl * cfg.H * cfg.W,
                     "d2h_bytes_per_step": 80},
@@ -670,6 +753,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-images", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager csc_iterate calls instead of graph replays")
     ap.add_argument("--filter-solver", default="pg", choices=["pg", "bcd", "surrogate"],
                     help="pg: the north_star projected-gradient filter step (default); bcd: the paper's "
                          "projected block-coordinate update, one warm-started sweep (SURVEY.md §8f NEXT-3); "

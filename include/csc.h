@@ -24,8 +24,9 @@
  * no pageable copy) and may be captured on dims.stream once each kernel has run once
  * (tests/test_gpu_graph.py).  The residual-cache decisions are taken on the host while
  * capturing, so a captured sequence must be replayed from the state it was captured in (e.g.
- * a SOCSC step: zero codes, code steps, filter step).  csc_objective, csc_iterate and any call
- * with a host output synchronise and are not capturable; csc_code_step_admm, the BCD and
+ * a SOCSC step: zero codes, code steps, filter step; or a whole iteration with
+ * csc_objective_enqueue).  csc_objective, csc_iterate and any call with a host output synchronise
+ * and are not capturable; csc_code_step_admm, the BCD and
  * surrogate updates and csc_stage_images allocate on first use.
  *
  * ASYNCHRONY: everything is enqueued on dims.stream (a cudaStream_t).  Only
@@ -112,6 +113,15 @@ csc_status csc_filter_step(csc_ctx* ctx, const float* x, float* d, const float* 
  * residual cache.  Collective; synchronises the stream. */
 csc_status csc_objective(csc_ctx* ctx, const float* x, const float* d, const float* z,
                          float lambda, double out[3]);
+
+/* csc_objective in two halves.  csc_objective_enqueue enqueues the objective pass (the dense residual
+ * pass, which refreshes the residual cache, its reductions and, world > 1, their all-reduce) and a copy
+ * of the resulting device scalars into the context's pinned host mirror, without synchronising: it may
+ * be captured in a CUDA graph together with csc_code_step / csc_filter_step (one whole iteration, the
+ * mask iteration supplied through csc_set_iter_offset).  csc_objective_read synchronises the stream and
+ * returns out[3] as csc_objective for the last enqueued pass.  Collective (enqueue). */
+csc_status csc_objective_enqueue(csc_ctx* ctx, const float* x, const float* d, const float* z);
+csc_status csc_objective_read(csc_ctx* ctx, float lambda, double out[3]);
 
 /* One SBCSC outer iteration (Alg.1): [x_host -> x upload] ->
  * csc_code_step(iter) -> csc_filter_step -> csc_objective.  When the residual cache
@@ -302,6 +312,16 @@ typedef enum {
 
 /* Enable (1) / disable (0) per-launch event timing; enabling resets the totals. */
 csc_status csc_profile_enable(csc_ctx* ctx, int enable);
+
+/* Add the elapsed times of the event pairs recorded so far to the per-class totals and keep the pairs
+ * (syncs the stream).  For CUDA graphs captured while profiling was enabled: every replay re-records the
+ * captured events, so calling this after each replay accumulates each replay's kernel times. */
+csc_status csc_profile_sample(csc_ctx* ctx);
+
+/* Which kernel classes are timed while profiling is enabled: bit c = csc_kernel_class c (default: all).
+ * Each timed launch records two CUDA events on the context stream; timing only the long kernels keeps
+ * that host-side cost out of a timed loop (launches of untimed classes still count). */
+csc_status csc_profile_set_classes(csc_ctx* ctx, uint32_t class_mask);
 
 /* Synchronises the stream, then returns the accumulated device time (ms) and the
  * number of launches of kernel class cls since csc_profile_enable(ctx, 1). */

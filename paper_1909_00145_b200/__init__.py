@@ -32,7 +32,8 @@ ABI_SYMBOLS = (
     "csc_set_step_rule", "csc_read_step_z", "csc_filter_step_bcd", "csc_surrogate_reset",
     "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate", "csc_set_mask_mode",
     "csc_stage_images", "csc_iterate_staged", "csc_mask_selwords", "csc_read_scalars", "csc_zg_sumsq",
-    "csc_set_iter_offset", "csc_count_nonzero", "csc_set_nvtx", "csc_comm_check",
+    "csc_set_iter_offset", "csc_count_nonzero", "csc_set_nvtx", "csc_comm_check", "csc_profile_set_classes",
+    "csc_objective_enqueue", "csc_objective_read", "csc_profile_sample",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -106,6 +107,10 @@ def load_library(path: Optional[str] = None):
         L.csc_launch_count.argtypes = [vp]
         L.csc_launch_count.restype = u64
         L.csc_profile_enable.argtypes = [vp, ctypes.c_int]
+        L.csc_profile_set_classes.argtypes = [vp, u32]
+        L.csc_profile_sample.argtypes = [vp]
+        L.csc_objective_enqueue.argtypes = [vp, vp, vp, vp]
+        L.csc_objective_read.argtypes = [vp, f32, vp]
         L.csc_profile_read.argtypes = [vp, ctypes.c_int, ctypes.POINTER(f64), ctypes.POINTER(u64)]
         L.csc_kernel_variants.argtypes = [vp]
         L.csc_kernel_variants.restype = u32
@@ -260,6 +265,17 @@ class Context:
         self._check(self._L.csc_objective(self._h, px, pd, pz, float(lam), out))
         return float(out[0]), float(out[1]), float(out[2])
 
+    def objective_enqueue(self, x, d, z) -> None:
+        """The objective pass without synchronising (csc_objective_enqueue; capturable in a CUDA graph)."""
+        px, pd, pz = self._xdz(x, d, z)
+        self._check(self._L.csc_objective_enqueue(self._h, px, pd, pz))
+
+    def objective_read(self, lam: float) -> Tuple[float, float, float]:
+        """(F, fit, l1) of the last enqueued objective pass (csc_objective_read; syncs)."""
+        out = (ctypes.c_double * 3)()
+        self._check(self._L.csc_objective_read(self._h, float(lam), out))
+        return float(out[0]), float(out[1]), float(out[2])
+
     def iterate(self, x, d, z, lam: float, p: float, seed: int, it: int, *, x_host=None,
                 step_z: float = 0.0, step_d: float = 0.0):
         """One SBCSC iteration (code step, filter step, objective).  x_host: optional pinned CPU
@@ -385,8 +401,16 @@ class Context:
         """Raise CSCError if the NCCL communicator reports an asynchronous error (csc_comm_check)."""
         self._check(self._L.csc_comm_check(self._h))
 
-    def profile_enable(self, on: bool = True):
+    def profile_enable(self, on: bool = True, classes=None):
+        """Per-launch event timing on (resets the totals); classes: names from KERNEL_CLASSES to time
+        (None: all) -- csc_profile_set_classes."""
+        mask = 0xFFFFFFFF if classes is None else sum(1 << KERNEL_CLASSES.index(c) for c in classes)
+        self._check(self._L.csc_profile_set_classes(self._h, mask))
         self._check(self._L.csc_profile_enable(self._h, 1 if on else 0))
+
+    def profile_sample(self) -> None:
+        """Accumulate the recorded event pairs and keep them (csc_profile_sample: after graph replays)."""
+        self._check(self._L.csc_profile_sample(self._h))
 
     def profile_read(self) -> dict:
         """{class: (total_ms, launches)} accumulated since profile_enable(True) (syncs)."""

@@ -183,8 +183,11 @@ struct csc_ctx {
   // profiling
   struct Rec { cudaEvent_t a, b; int cls; };
   bool prof_on = false;
+  uint32_t prof_mask = 0xFFFFFFFFu;  // kernel classes timed while prof_on (csc_profile_set_classes)
+  bool sampled = false;              // csc_profile_sample accumulated the pending pairs (keep them)
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
+  std::vector<cudaEvent_t> retired;  // events of sampled (graph-captured) pairs, destroyed with the context
   double prof_ms[CSC_K_NCLASS] = {0};
   uint64_t prof_n[CSC_K_NCLASS] = {0};
 };
@@ -225,20 +228,30 @@ cudaEvent_t prof_event(csc_ctx* c) {
   return e;
 }
 
+// A profiling event on the context stream; under stream capture it becomes an external event-record node
+// of the graph (re-recorded by every replay, csc_profile_sample)
+void prof_record(csc_ctx* c, cudaEvent_t e) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, c->st, cudaEventRecordExternal);
+  else cudaEventRecord(e, c->st);
+}
+
 // Launch `call` (nk kernels of class cls); with profiling on, bracket it with events.
 #define CSC_LAUNCH_C(ctx, cls, nk, call)                                                         \
   do {                                                                                           \
     cudaEvent_t _ea = nullptr, _eb = nullptr;                                                    \
-    if ((ctx)->prof_on) {                                                                        \
+    const bool _pr = (ctx)->prof_on && (((ctx)->prof_mask >> (cls)) & 1u);                       \
+    if (_pr) {                                                                                   \
       _ea = prof_event(ctx);                                                                     \
       _eb = prof_event(ctx);                                                                     \
-      cudaEventRecord(_ea, (ctx)->st);                                                           \
+      prof_record(ctx, _ea);                                                                     \
     }                                                                                            \
     cudaError_t _e = (call);                                                                     \
     if (_e != cudaSuccess)                                                                       \
       return fail((ctx), CSC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));      \
-    if ((ctx)->prof_on) {                                                                        \
-      cudaEventRecord(_eb, (ctx)->st);                                                           \
+    if (_pr) {                                                                                   \
+      prof_record(ctx, _eb);                                                                     \
       (ctx)->pending.push_back({_ea, _eb, (cls)});                                               \
     }                                                                                            \
     (ctx)->launches += (nk);                                                                     \
@@ -612,10 +625,13 @@ csc_status csc_profile_enable(csc_ctx* c, int enable) {
   CSC_CUDA(c, cudaSetDevice(c->device));
   CSC_CUDA(c, cudaStreamSynchronize(c->st));
   for (auto& r : c->pending) {
-    c->pool.push_back(r.a);
-    c->pool.push_back(r.b);
+    // sampled pairs may still be recorded by a captured graph: retire them instead of reusing them
+    auto& dst = c->sampled ? c->retired : c->pool;
+    dst.push_back(r.a);
+    dst.push_back(r.b);
   }
   c->pending.clear();
+  c->sampled = false;
   for (int i = 0; i < CSC_K_NCLASS; ++i) {
     c->prof_ms[i] = 0.0;
     c->prof_n[i] = 0;
@@ -624,8 +640,8 @@ csc_status csc_profile_enable(csc_ctx* c, int enable) {
   return CSC_OK;
 }
 
-csc_status csc_profile_read(csc_ctx* c, int cls, double* total_ms, uint64_t* launches) {
-  if (!c || cls < 0 || cls >= CSC_K_NCLASS) return fail(c, CSC_ERR_ARG, "bad kernel class");
+csc_status csc_profile_sample(csc_ctx* c) {
+  if (!c) return CSC_ERR_ARG;
   CSC_CUDA(c, cudaSetDevice(c->device));
   CSC_CUDA(c, cudaStreamSynchronize(c->st));
   for (auto& r : c->pending) {
@@ -633,10 +649,32 @@ csc_status csc_profile_read(csc_ctx* c, int cls, double* total_ms, uint64_t* lau
     CSC_CUDA(c, cudaEventElapsedTime(&ms, r.a, r.b));
     c->prof_ms[r.cls] += ms;
     c->prof_n[r.cls] += 1;
-    c->pool.push_back(r.a);
-    c->pool.push_back(r.b);
   }
-  c->pending.clear();
+  c->sampled = true;  // the pairs stay (a graph replays them); csc_profile_read then only reports
+  return CSC_OK;
+}
+
+csc_status csc_profile_set_classes(csc_ctx* c, uint32_t class_mask) {
+  if (!c) return CSC_ERR_ARG;
+  c->prof_mask = class_mask;
+  return CSC_OK;
+}
+
+csc_status csc_profile_read(csc_ctx* c, int cls, double* total_ms, uint64_t* launches) {
+  if (!c || cls < 0 || cls >= CSC_K_NCLASS) return fail(c, CSC_ERR_ARG, "bad kernel class");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  CSC_CUDA(c, cudaStreamSynchronize(c->st));
+  if (!c->sampled) {  // (csc_profile_sample already added the pairs it keeps)
+    for (auto& r : c->pending) {
+      float ms = 0.f;
+      CSC_CUDA(c, cudaEventElapsedTime(&ms, r.a, r.b));
+      c->prof_ms[r.cls] += ms;
+      c->prof_n[r.cls] += 1;
+      c->pool.push_back(r.a);
+      c->pool.push_back(r.b);
+    }
+    c->pending.clear();
+  }
   if (total_ms) *total_ms = c->prof_ms[cls];
   if (launches) *launches = c->prof_n[cls];
   return CSC_OK;
@@ -649,6 +687,7 @@ csc_status csc_destroy(csc_ctx* c) {
     cudaEventDestroy(r.b);
   }
   for (auto e : c->pool) cudaEventDestroy(e);
+  for (auto e : c->retired) cudaEventDestroy(e);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   cudaFree(c->r);
   cudaFree(c->part);
@@ -1296,6 +1335,21 @@ csc_status csc_objective(csc_ctx* c, const float* x, const float* d, const float
   CSC_CUDA(c, cudaSetDevice(c->device));
   s = objective_enqueue(c, x, d, z);
   if (s != CSC_OK) return s;
+  return objective_finish(c, lambda, out);
+}
+
+csc_status csc_objective_enqueue(csc_ctx* c, const float* x, const float* d, const float* z) {
+  NvtxScope nvtx_scope(c, "csc_objective_enqueue");
+  csc_status s = check_ptrs(c, x, d, z);
+  if (s != CSC_OK) return s;
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  return objective_enqueue(c, x, d, z);
+}
+
+csc_status csc_objective_read(csc_ctx* c, float lambda, double out[3]) {
+  if (!c || !out) return fail(c, CSC_ERR_ARG, "out must be a host pointer to 3 doubles");
+  if (!(lambda >= 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and >= 0");
+  CSC_CUDA(c, cudaSetDevice(c->device));
   return objective_finish(c, lambda, out);
 }
 

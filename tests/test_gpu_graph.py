@@ -81,3 +81,63 @@ def test_socsc_step_graph_replay():
         assert rel_err(de.cpu().numpy(), d_or) < 1e-5, b
     cg.close()
     ce.close()
+
+
+def test_iteration_graph_replay_matches_iterate():
+    """A whole SBCSC iteration (Alg.1: csc_code_step, csc_filter_step, csc_objective_enqueue) captured once
+    and replayed with the mask iteration in the device offset gives the same codes, filters and objective
+    as csc_iterate called eagerly on a second context (bench.py's timed loop)."""
+    import torch
+    import paper_1909_00145_b200 as pkg
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda:0")
+    cfg = CONFIGS["batch"].with_(K=40, N=3, H=44, W=40, p=0.2)
+    seed = mask_seed(cfg)
+    x = torch.from_numpy(make_images(cfg)).to(dev)
+    d0 = make_filters(cfg)
+    s_g, s_e = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    cg = pkg.Context(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W, device=0, stream=s_g)
+    ce = pkg.Context(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W, device=0, stream=s_e)
+    dg, de = torch.from_numpy(d0).to(dev), torch.from_numpy(d0).to(dev)
+    zg = torch.zeros((cfg.N, cfg.K, cfg.Hc, cfg.Wc), device=dev)
+    ze = torch.zeros_like(zg)
+    off = torch.zeros(1, dtype=torch.int32, device=dev)
+    cg.set_iter_offset(off)
+    torch.cuda.synchronize()
+    # two eager iterations on both contexts (the steady state the graph is captured in)
+    for it in (1, 2):
+        Fg = cg.iterate(x, dg, zg, cfg.lam, cfg.p, seed, it)[0]
+        Fe = ce.iterate(x, de, ze, cfg.lam, cfg.p, seed, it)[0]
+        assert Fg == Fe
+    torch.cuda.synchronize()
+
+    def body():
+        cg.code_step(x, dg, zg, cfg.lam, cfg.p, seed, 0)
+        cg.filter_step(x, dg, zg)
+        cg.objective_enqueue(x, dg, zg)
+
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s_g):
+        # warm the capture path once eagerly at iteration 3
+        off.fill_(3)
+        body()
+        Fg3 = cg.objective_read(cfg.lam)
+    Fe3 = ce.iterate(x, de, ze, cfg.lam, cfg.p, seed, 3)[0]
+    assert Fg3 == Fe3
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph, stream=s_g):
+        body()
+    for it in (4, 5, 6):
+        with torch.cuda.stream(s_g):
+            off.fill_(it)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s_g):  # replay on the context's stream (objective_read syncs that stream)
+            graph.replay()
+        Fg = cg.objective_read(cfg.lam)
+        Fe = ce.iterate(x, de, ze, cfg.lam, cfg.p, seed, it)[0]
+        torch.cuda.synchronize()
+        assert Fg == Fe, it
+        assert torch.equal(zg, ze), it
+        assert torch.equal(dg, de), it
+    cg.close()
+    ce.close()
