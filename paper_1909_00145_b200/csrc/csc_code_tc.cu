@@ -342,10 +342,11 @@ __global__ void mask_selwords_kernel(int K, int KC, int NC, int nper, int nblk, 
   const int kg = blk / nper, cb = blk - kg * nper;
   const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
   uint32_t out[4] = {0u, 0u, 0u, 0u};
-  for (int i = 0; i < NC; ++i) {
-    const int kl = cb * NC + i;
-    const int k = kg * KC + kl;
-    if (kl >= KC || k >= K) break;
+  const int nvalid = min(NC, min(KC - cb * NC, K - kg * KC - cb * NC));  // filters of this word
+  // the filters' Philox draws are independent: unrolled, several 10-round chains are in flight at once
+#pragma unroll 4
+  for (int i = 0; i < nvalid; ++i) {
+    const int k = kg * KC + cb * NC + i;
     const uint64_t l0 = static_cast<uint64_t>(k) * plane + p0;
     if (mode == 1) {
       // block-structured masks (E5): one draw per aligned 8-coordinate block b = l >> 3
