@@ -769,8 +769,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    elif args.config == "online":
-        run_online(args)
+    elif args.config == "online" and args.code_solver == "prox" and args.filter_solver == "pg":
+        run_online(args)  # the SOCSC step; the NEXT-row solvers run the iteration of run_ours on config 4
     else:
         run_ours(args)
 
