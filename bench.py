@@ -114,6 +114,9 @@ def kernel_rooflines(prof, cfg, nl, steps, variants, solver="prox", filter_solve
                 out[name] = {"kernel": "conv_fwd_kernel (SIMT FP32)", "bound": "alu",
                              "achieved": dense_flops / (avg / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
                              "peak_note": f"148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz:.0f} MHz (derived)"}
+        elif name == "wgrad" and variants & 64:
+            out[name] = two_roofs("wgrad_h_kernel (tcgen05 kind::f16 3-term split, TMA z + TMEM im2col(r))", avg,
+                                  bf16_tflops / 3.0, f"{kind} bf16/fp16 {bf16_tflops:.0f} TF/s / 3 products")
         elif name == "wgrad" and variants & 2:
             out[name] = two_roofs("wgrad_tc_kernel (tcgen05 3xTF32, TMA z + TMEM im2col(r))", avg, tf32_peak / 3.0,
                                   f"{kind} bf16 {bf16_tflops:.0f} TF/s x {TF32_PER_BF16:.3f} (tf32/bf16 nominal) / 3")

@@ -334,8 +334,9 @@ csc_status csc_profile_read(csc_ctx* ctx, int cls, double* total_ms, uint64_t* l
  *   bit 3  the dense passes use the TMA-fed shared-memory-operand kernel (csc_conv_ss.cu)
  *   bit 4  the dense passes use the fp16-split TMA-fed kernel (csc_conv_h.cu, T6)
  *   bit 5  the code step uses the fp16-split kernel with TMA-fed code tiles (csc_code_h.cu)
+ *   bit 6  the filter gradient uses the fp16-split kernel at the fp16 rate (csc_wgrad_h.cu)
  * The choice is fixed at csc_init from the shape (and CSC_DENSE_PATH / CSC_WGRAD_PATH /
- * CSC_CODE_PATH = simt). */
+ * CSC_CODE_PATH = simt; CSC_WGRAD_PATH = tf32 selects the 3xTF32 filter gradient). */
 uint32_t csc_kernel_variants(const csc_ctx* ctx);
 
 #ifdef __cplusplus

@@ -120,6 +120,10 @@ struct csc_ctx {
   // tensor-core filter gradient (csc_wgrad_tc.cu)
   bool wg_tc_on = false;
   csc::WgTcPlan wg{};
+  // fp16-rate filter gradient (csc_wgrad_h.cu): needs the max|z| bound of the fp16 dense path
+  bool wh_on = false;
+  csc::WhPlan wh{};
+  uint32_t* wmax = nullptr;    // max|r'| (float bits) for the fp16-split filter gradient
   // tensor-core dense-then-mask code step (csc_code_tc.cu)
   bool ct_on = false;
   csc::CodeTcPlan ct{};
@@ -277,17 +281,23 @@ csc_status allreduce_d(csc_ctx* c, double* buf, size_t count) {
 
 // Tensor-core dense pass y = sum_k f_k * z_k into the band partials (TMA-fed SS kernel when the
 // plan says so, else the TMEM-fed kernel).
+// The fp16 split needs a bound of max|z|: exact after csc_zero_codes or an absmax pass, then raised by
+// every code step (T6).
+cudaError_t ensure_zmax(csc_ctx* c, const float* z) {
+  if (!c->zmax_known || c->zmax_ptr != z) {
+    cudaError_t e = csc::launch_absmax(z, static_cast<int64_t>(c->g.N) * c->g.K * c->g.Hc * c->g.Wc, c->smax, c->st);
+    if (e != cudaSuccess) return e;
+    c->launches += 1;
+    c->zmax_known = true;
+    c->zmax_ptr = z;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t conv_tc_any(csc_ctx* c, const float* z, const float* filt, double* l1p, bool precise = false) {
   if (c->tc.half) {
-    // the fp16 split needs a bound of max|z|: exact after csc_zero_codes or an absmax pass, then
-    // raised by every code step (T6)
-    if (!c->zmax_known || c->zmax_ptr != z) {
-      cudaError_t e = csc::launch_absmax(z, static_cast<int64_t>(c->g.N) * c->g.K * c->g.Hc * c->g.Wc, c->smax, c->st);
-      if (e != cudaSuccess) return e;
-      c->launches += 1;
-      c->zmax_known = true;
-      c->zmax_ptr = z;
-    }
+    cudaError_t ez = ensure_zmax(c, z);
+    if (ez != cudaSuccess) return ez;
     return csc::launch_conv_h(c->g, c->tc, &c->tm_conv, z, filt, c->tc_bimg, c->smax, c->smax + 1, c->tc_part, l1p,
                               c->st, true, precise);
   }
@@ -420,7 +430,7 @@ uint32_t csc_kernel_variants(const csc_ctx* ctx) {
   if (!ctx) return 0;
   return (ctx->tc_on ? 1u : 0u) | (ctx->wg_tc_on ? 2u : 0u) | (ctx->ct_on ? 4u : 0u) |
          (ctx->tc_on && ctx->tc.ss ? 8u : 0u) | (ctx->tc_on && ctx->tc.half ? 16u : 0u) |
-         (ctx->ct_on && ctx->ct.half ? 32u : 0u);
+         (ctx->ct_on && ctx->ct.half ? 32u : 0u) | (ctx->wh_on && ctx->tc_on && ctx->tc.half ? 64u : 0u);
 }
 
 csc_status csc_nccl_unique_id(uint8_t out[128]) {
@@ -520,9 +530,15 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   {
     const char* ev = std::getenv("CSC_WGRAD_PATH");
     const bool force_simt = ev != nullptr && std::string(ev) == "simt";
+    const bool force_tf32 = ev != nullptr && std::string(ev) == "tf32";
     if (!force_simt && csc::wgrad_tc_supported(g)) {
       c->wg = csc::wgrad_tc_plan(g, prop.multiProcessorCount);
       c->wg_tc_on = true;
+    }
+    if (!force_simt && !force_tf32 && csc::wgrad_h_supported(g)) {
+      c->wh = csc::wgrad_h_plan(g, prop.multiProcessorCount);
+      c->wh_on = c->wh.ok;
+      if (c->wh_on) ok = ok && alloc(reinterpret_cast<void**>(&c->wmax), sizeof(uint32_t) * 2);
     }
   }
   // tensor-core code step unless CSC_CODE_PATH=simt
@@ -545,7 +561,8 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
       }
     }
   }
-  const int gpart_groups = c->wg_tc_on && c->wg.G > G ? c->wg.G : G;
+  int gpart_groups = c->wg_tc_on && c->wg.G > G ? c->wg.G : G;
+  if (c->wh_on && c->wh.G > gpart_groups) gpart_groups = c->wh.G;
   ok = ok && alloc(reinterpret_cast<void**>(&c->gpart), sizeof(double) * static_cast<size_t>(gpart_groups) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->gsum), sizeof(double) * g.K * M);
   ok = ok && alloc(reinterpret_cast<void**>(&c->g32), sizeof(float) * g.K * M);
@@ -702,6 +719,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->mwords);
   cudaFree(c->a3_part);
   cudaFree(c->rmax);
+  cudaFree(c->wmax);
   cudaFree(c->tauk);
   cudaFree(c->bcd_gpart);
   cudaFree(c->bcd_ainv);
@@ -1273,7 +1291,14 @@ csc_status csc_filter_step(csc_ctx* c, const float* x, float* d, const float* z,
     if (s != CSC_OK) return s;
   }
   if (g.N > 0) {
-    if (c->wg_tc_on && (reinterpret_cast<uintptr_t>(z) & 15u) == 0) {
+    if (c->wh_on && c->tc_on && c->tc.half && (reinterpret_cast<uintptr_t>(z) & 15u) == 0) {
+      // fp16-rate split: the bound of max|z| (as the dense pass) and max|r'|
+      CSC_CUDA(c, ensure_zmax(c, z));
+      CSC_LAUNCH(c, 1, csc::launch_absmax(c->r, n_pix(g), c->wmax, c->st));
+      CSC_LAUNCH_C(c, CSC_K_WGRAD, 1,
+                   csc::launch_wgrad_h(g, c->wh, &c->tm_wgrad, z, c->r, c->smax, c->wmax, c->gpart, c->st));
+      CSC_LAUNCH(c, 1, csc::launch_wgrad_reduce(g, c->gpart, c->wh.G, c->gsum, c->st));
+    } else if (c->wg_tc_on && (reinterpret_cast<uintptr_t>(z) & 15u) == 0) {
       CSC_LAUNCH_C(c, CSC_K_WGRAD, 1, csc::launch_wgrad_tc(g, c->wg, &c->tm_wgrad, z, c->r, c->gpart, c->st));
       CSC_LAUNCH(c, 1, csc::launch_wgrad_reduce(g, c->gpart, c->wg.G, c->gsum, c->st));
     } else {

@@ -190,6 +190,18 @@ cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, TmapCache* tmc, co
                             double* gpart, cudaStream_t st);
 
 
+// ---- tensor-core filter gradient at the fp16 rate (kind::f16, 3-term split), csc_wgrad_h.cu
+struct WhPlan {
+  int KC, Npad, NCH, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, NB, cpt;
+  int grid, smem;
+  bool ok;
+};
+bool wgrad_h_supported(const Geom& g);
+WhPlan wgrad_h_plan(const Geom& g, int num_sms);
+// Per-CTA fp64 partials gpart[p.G][K][S*S] as launch_wgrad_tc; zmax bounds max|z|, rmax = max|r| (float bits).
+cudaError_t launch_wgrad_h(const Geom& g, const WhPlan& p, TmapCache* tmc, const float* z, const float* r,
+                           const uint32_t* zmax, const uint32_t* rmax, double* gpart, cudaStream_t st);
+
 // ---- tensor-core (tcgen05, 3xTF32) dense-then-mask code step, csc_code_tc.cu
 struct CodeTcPlan {
   int KC, Npad, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, b_bytes;

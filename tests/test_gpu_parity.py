@@ -175,11 +175,12 @@ def test_code_step_parity(torch_dev, shape, p, path, monkeypatch):
     ctx.close()
 
 
-@pytest.mark.parametrize("wg", ["tc", "simt"])
+@pytest.mark.parametrize("wg", ["h", "tf32", "simt"])
 @pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (1, 3, 3, 9, 9), (2, 130, 5, 36, 40),
                                    (1, 8, 7, 26, 22), (2, 40, 11, 256, 56), (5, 24, 9, 48, 63), (1, 100, 11, 12, 300)])
 def test_filter_step_parity(torch_dev, shape, wg, monkeypatch):
-    """Filter gradient g = Z^T r (tcgen05 3xTF32 kernel, or SIMT), exact line search, projection.
+    """Filter gradient g = Z^T r (tcgen05 kind::f16 3-term split kernel "h", the 3xTF32 kernel, or SIMT),
+    exact line search, projection.
     Shapes cover several k-groups (K=130), one partial chunk per row (Wc < 32), many bands,
     rows of 9-10 chunks, and Hc*Wc % 4 != 0 (TMA view impossible: SIMT path either way)."""
     import torch
@@ -188,6 +189,9 @@ def test_filter_step_parity(torch_dev, shape, wg, monkeypatch):
     x, d, z = random_problem(300 + K, N, K, s, H, W, code_density=0.3)
     ctx = _ctx(N, K, s, H, W)
     xt, dt, zt = _t(x, torch_dev), _t(d, torch_dev), _t(z, torch_dev)
+    Hc, Wc = H + s - 1, W + s - 1
+    if wg == "h" and ctx.variants & 16 and (Hc * Wc) % 4 == 0:
+        assert ctx.variants & 64  # the fp16-rate kernel is the one under test
     tau = ctx.filter_step(xt, dt, zt, want_step=True)
     g = torch.zeros(K * s * s, dtype=torch.float64, device=torch_dev)
     ctx.read_grad(g)
