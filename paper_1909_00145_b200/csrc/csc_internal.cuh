@@ -192,7 +192,7 @@ cudaError_t launch_wgrad_tc(const Geom& g, const WgTcPlan& p, TmapCache* tmc, co
 
 // ---- tensor-core filter gradient at the fp16 rate (kind::f16, 3-term split), csc_wgrad_h.cu
 struct WhPlan {
-  int KC, Npad, NCH, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, NB, cpt;
+  int KC, Npad, NCH, nkg, G, L, nseg, nitems, pitch, rs_rows, rs_floats, NB, NR, cpt;
   int grid, smem;
   bool ok;
 };

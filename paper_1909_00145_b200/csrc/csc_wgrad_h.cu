@@ -6,23 +6,25 @@
 // (r' = 0 outside the H x W image).  As a GEMM per CTA:  D[t][k] += sum_pos A[t][pos] B[k][pos],
 //   M = 128 taps (s^2 <= 121 used), N = Npad filters of one k-group, K = code positions, 16 per MMA.
 // Both operands are split after exact power-of-two scalings (reading T6, as csc_conv_h.cu):
-//   x_s = x 2^e,  hi = rn11(x_s) (an exact fp16),  lo = fp16_rn(x_s - hi),
+//   x_s = x 2^e,  hi = fp16_rn(x_s) (z) or rn11(x_s) (r'),  lo = fp16_rn(x_s - hi)  (x_s - hi is exact in fp32),
 //   D += A_hi B_hi + A_hi B_lo + A_lo B_hi   (2^-22 per product, like 3xTF32, at twice its rate).
 // e_z from the running bound of max|z| (the code step raises it), e_r from max|r'|.
 // Operands:
-//   B = z: TMA boxes {64 positions, 16 planes} (fp32, 4 KB) into a ring of raw slots; converter warps
-//       write the scaled fp16 hi / lo rows of one 64-position chunk in the canonical K-major SWIZZLE_128B
-//       layout (row = filter, 128 B = 64 positions, 16-B chunks XOR row) and release the raw slot at once.
+//   B = z: one TMA box {64 positions, KC planes} (fp32) per chunk into a ring of raw slots (one request per
+//       chunk: the producer's issue rate stays off the critical path); the converter warps write the scaled
+//       fp16 hi / lo rows in the canonical K-major SWIZZLE_128B layout (row = filter, 128 B = 64 positions,
+//       16-B chunks XOR row) and release the raw slot at once.
 //   A = im2col of r' in TMEM (lane = tap, one 32-bit column = two consecutive positions): the item's
-//       residual rows are staged by cp.async, scaled and split once into fp16 PAIRS hp[row][c] =
+//       residual rows are staged by cp.async and split into fp16 PAIRS (double-buffered, one item ahead, by the
+//       otherwise idle epilogue warps) hp[row][c] =
 //       (hi(r[c]), hi(r[c+1])), so a column is one shared load per lane (pitch = s mod 32: the 32 taps of
 //       a lane quarter hit 32 banks).
 // The accumulator restarts every tile (cpt chunks); the epilogue adds it into fp32 block sums that are
-// flushed into the CTA's fp64 partials every kWhFlush tiles, and wgrad_reduce_kernel sums the per-CTA
+// flushed into the CTA's fp64 partials every 2048 positions, and wgrad_reduce_kernel sums the per-CTA
 // partials in a fixed order (deterministic), exactly as csc_wgrad_tc.cu.
 //
-// CTA (persistent, 28 warps): warp 0 MMA, warp 1 TMA, warps 2..7 z converters (box g -> warp g mod 6),
-// warps 8..11 im2col (one per TMEM lane quarter), warps 12..27 epilogue (4 per lane quarter).
+// CTA (persistent, 32 warps): warp 0 MMA, warp 1 TMA, warps 2..7 z converters (all of them on every chunk),
+// warps 8..15 im2col (two groups of 4 lane quarters, alternate chunks), warps 16..31 epilogue (4 per quarter).
 #include "csc_internal.cuh"
 #include "csc_tc_ptx.cuh"
 
@@ -39,17 +41,16 @@ namespace {
 
 using namespace tcx;
 
-constexpr int kWhNR = 12;        // raw TMA slots (4 KB each)
+constexpr int kWhNRMax = 8;      // raw TMA slots (one {64 positions, KC planes} box = one chunk each)
 constexpr int kWhNA = 4;         // TMEM A slots (64 columns each: 4 K16-steps x (8 hi + 8 lo))
 constexpr int kWhZWarps = 6;
-constexpr int kWhIWarps = 4;
+constexpr int kWhIWarps = 8;     // two groups of 4 lane quarters, alternate chunks
 constexpr int kWhEpiWarps = 16;
 constexpr int kWhZBase = 2, kWhIBase = kWhZBase + kWhZWarps, kWhEpiBase = kWhIBase + kWhIWarps;
 constexpr int kWhWarps = kWhEpiBase + kWhEpiWarps;
 constexpr int kWhThreads = 32 * kWhWarps;
-constexpr int kWhRawBytes = 4096;  // {64 positions, 16 planes} fp32
 constexpr int kWhChunk = 64;       // positions per chunk (one SW128 atom of fp16 along K)
-constexpr int kWhFlush = 32;       // tiles summed in fp32 before each fp64 flush
+constexpr int kWhFlushPos = 2048;  // positions summed in fp32 (tensor core + epilogue) before each fp64 flush
 constexpr int kWhSmemMax = 226 * 1024;
 constexpr uint32_t kWhColA = 256;
 
@@ -72,6 +73,19 @@ __device__ __forceinline__ uint32_t pack_h2_w(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+#ifdef CSC_ROLE_TIMING
+#define WT_NOW() clock64()
+#define WT_ACC(var, stmt)                       \
+  do {                                          \
+    const unsigned long long _t = clock64();    \
+    stmt;                                       \
+    var += clock64() - _t;                      \
+  } while (0)
+#else
+#define WT_NOW() 0ull
+#define WT_ACC(var, stmt) stmt
+#endif
+
 struct WhArgs {
   const float* r;        // [N][H][W]
   const uint32_t* zmax;  // bound on max|z| (float bits)
@@ -81,7 +95,19 @@ struct WhArgs {
   int KC, Npad, NCH, nkg, G;
   int L, nseg, nitems;
   int pitch, rs_rows, rs_floats;
-  int NB, cpt;
+  int NB, NR, cpt;
+  unsigned long long* dbg;  // CSC_ROLE_TIMING builds: per-CTA role cycle counters [grid][16]
+};
+
+// position in a ring of n slots: slot index and the parity of the pass over the ring (no runtime modulo)
+struct Ring {
+  uint32_t slot = 0, ph = 0;
+  __device__ __forceinline__ void next(uint32_t n) {
+    if (++slot == n) {
+      slot = 0;
+      ph ^= 1u;
+    }
+  }
 };
 
 struct WhItem {
@@ -103,8 +129,9 @@ template <int NC>
 __global__ void __launch_bounds__(kWhThreads, 1)
 wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
   extern __shared__ uint8_t smraw[];
-  __shared__ __align__(8) uint64_t raw_full[kWhNR], raw_empty[kWhNR];
+  __shared__ __align__(8) uint64_t raw_full[kWhNRMax], raw_empty[kWhNRMax];
   __shared__ __align__(8) uint64_t b_ready[8], b_empty[8], a_ready[kWhNA], a_empty[kWhNA], acc_full[2], acc_empty[2];
+  __shared__ __align__(8) uint64_t pair_full[2], pair_empty[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, warp = __shfl_sync(kFullMask, tid >> 5, 0), lane = tid & 31;
@@ -114,28 +141,34 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
   uint8_t* sm = smraw + (base - raw);
   const int bbytes = A.Npad * 128;                       // one of hi / lo of a chunk
   uint8_t* bst = sm;                                     // [NB][hi | lo]
-  uint8_t* rawst = bst + 2 * A.NB * bbytes;              // [NR][16][64] fp32
-  float* rstage = reinterpret_cast<float*>(rawst + kWhNR * kWhRawBytes);  // [rs_rows][pitch] raw r'
-  uint32_t* hp = reinterpret_cast<uint32_t*>(rstage + A.rs_floats);       // hi pairs
-  uint32_t* lp = hp + A.rs_floats;                                        // lo pairs
+  const int rawbytes = A.KC * kWhChunk * 4;             // one TMA box {64 positions, KC planes} fp32
+  uint8_t* rawst = bst + 2 * A.NB * bbytes;              // [NR][KC][64] fp32
+  // residual pairs, double-buffered per item: [2][hi | lo][rs_rows][pitch]; rstage = raw rows of the next item
+  uint32_t* pairs = reinterpret_cast<uint32_t*>(rawst + A.NR * rawbytes);
+  float* rstage = reinterpret_cast<float*>(pairs + 4 * A.rs_floats);
   const int ez = scale_exp_w(*A.zmax), er = scale_exp_w(*A.rmax);
 
+  // B rows KC .. Npad-1 (padding filters) stay zero: the converters write rows < KC only
+  for (int e = tid; e < 2 * A.NB * bbytes / 16; e += kWhThreads) reinterpret_cast<int4*>(bst)[e] = make_int4(0, 0, 0, 0);
+  fence_async_shared();
   if (tid == 0) {
-    for (int i = 0; i < kWhNR; ++i) {
+    for (int i = 0; i < A.NR; ++i) {
       mbar_init(&raw_full[i], 1);
-      mbar_init(&raw_empty[i], 1);
+      mbar_init(&raw_empty[i], kWhZWarps);
     }
     for (int i = 0; i < A.NB; ++i) {
-      mbar_init(&b_ready[i], A.NCH);
+      mbar_init(&b_ready[i], kWhZWarps);
       mbar_init(&b_empty[i], 1);
     }
     for (int i = 0; i < kWhNA; ++i) {
-      mbar_init(&a_ready[i], kWhIWarps);
+      mbar_init(&a_ready[i], 4);
       mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], kWhEpiWarps);
+      mbar_init(&pair_full[i], kWhEpiWarps);
+      mbar_init(&pair_empty[i], kWhIWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -151,20 +184,22 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
   if (warp == 0) {
     // ================================ MMA issuer
     const uint32_t idesc = idesc_f16_kk_w(128, A.Npad);
-    uint32_t cc = 0, tcount = 0;
+    uint32_t tcount = 0;
+    Ring rb, ra;
+    unsigned long long t0 = WT_NOW(), w_acc = 0, w_b = 0, w_a = 0;
     for (int item = gi; item < A.nitems; item += A.G) {
       const WhItem it = wh_item(A, item);
       const int ntl = (it.nch + A.cpt - 1) / A.cpt;
       for (int tl = 0; tl < ntl; ++tl, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
-        mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
+        WT_ACC(w_acc, mbar_wait_sleep(&acc_empty[buf], (use & 1u) ^ 1u));
         tc_after();
         const uint32_t d = t_acc + buf * static_cast<uint32_t>(A.Npad);
         const int c0 = tl * A.cpt, c1 = min(c0 + A.cpt, it.nch);
-        for (int c = c0; c < c1; ++c, ++cc) {
-          const uint32_t bs = cc % A.NB, as = cc % kWhNA;
-          mbar_wait(&b_ready[bs], (cc / A.NB) & 1u);
-          mbar_wait(&a_ready[as], (cc / kWhNA) & 1u);
+        for (int c = c0; c < c1; ++c, rb.next(A.NB), ra.next(kWhNA)) {
+          const uint32_t bs = rb.slot, as = ra.slot;
+          WT_ACC(w_b, mbar_wait_sleep(&b_ready[bs], rb.ph));
+          WT_ACC(w_a, mbar_wait_sleep(&a_ready[as], ra.ph));
           tc_after();
           const int nks = min(4, (it.p1 - it.p0 - kWhChunk * c + 15) >> 4);
           const uint32_t sh = su32(bst + bs * 2 * bbytes), sl = sh + bbytes;
@@ -193,61 +228,76 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
         mma_commit_elect(&acc_full[buf]);
       }
     }
+    if (A.dbg && lane == 0) {
+      unsigned long long* o = A.dbg + blockIdx.x * 16;
+      o[0] = WT_NOW() - t0; o[1] = w_acc; o[2] = w_b; o[3] = w_a;
+    }
     __syncwarp();
   } else if (warp == 1) {
-    // ================================ TMA producer: NCH boxes {64 positions, 16 planes} per chunk
+    // ================================ TMA producer: one box {64 positions, KC planes} per chunk
     if (lane == 0) {
-      uint32_t g = 0;
+      Ring rr;
       const int plane0 = kg * A.KC;
+      unsigned long long t0 = WT_NOW(), w_e = 0;
       for (int item = gi; item < A.nitems; item += A.G) {
         const WhItem it = wh_item(A, item);
-        for (int c = 0; c < it.nch; ++c) {
-          for (int j = 0; j < A.NCH; ++j, ++g) {
-            const uint32_t slot = g % kWhNR, ph = (g / kWhNR) & 1u;
-            mbar_wait(&raw_empty[slot], ph ^ 1u);
-            mbar_arrive_expect_tx(&raw_full[slot], kWhRawBytes);
-            // the inner coordinate p0 + 64 c is a multiple of 4 floats: a 16-B aligned box start; rows past
-            // the group (or past the last plane: zero fill) meet D columns the epilogue never reads
-            tma_load_2d(su32(rawst + slot * kWhRawBytes), &tmap_z, it.p0 + kWhChunk * c, it.n * A.K + plane0 + 16 * j,
-                        &raw_full[slot]);
-          }
+        for (int c = 0; c < it.nch; ++c, rr.next(A.NR)) {
+          const uint32_t slot = rr.slot;
+          WT_ACC(w_e, mbar_wait_sleep(&raw_empty[slot], rr.ph ^ 1u));
+          mbar_arrive_expect_tx(&raw_full[slot], static_cast<uint32_t>(rawbytes));
+          // the inner coordinate p0 + 64 c is a multiple of 4 floats: a 16-B aligned box start (positions
+          // past the plane end are zero-filled; those past the item meet zero im2col columns)
+          tma_load_2d(su32(rawst + slot * rawbytes), &tmap_z, it.p0 + kWhChunk * c, it.n * A.K + plane0,
+                      &raw_full[slot]);
         }
+      }
+      if (A.dbg) {
+        unsigned long long* o = A.dbg + blockIdx.x * 16;
+        o[4] = WT_NOW() - t0; o[5] = w_e;
       }
     }
     __syncwarp();
   } else if (warp < kWhIBase) {
-    // ================================ z converters: box g (chunk g / NCH, rows 16 (g % NCH) ..) -> warp g % 6
-    // lane i, step s: row k = 2 s + i / 16 of the box, positions 4 (i % 16) .. +3 (one float4, a 512-B
-    // warp read per step), written as the 8-B half (i & 1) of the 16-B chunk (i % 16) / 2 of row 16 j + k,
-    // swizzled to chunk ((i % 16) / 2) ^ (row & 7)
+    // ================================ z converters: every warp converts row pairs w, w + 6, ... of every chunk.
+    // lane i, row pair rp: row k = 2 rp + i / 16, positions 4 (i % 16) .. +3 (one float4: a 512-B warp read),
+    // written as the 8-B half (i & 1) of the 16-B chunk (i % 16) / 2 of row k, swizzled to ((i % 16) / 2) ^ (k & 7)
     const int zw = warp - kWhZBase;
     const float sz = exp2i_w(ez);
+    const float2 sz2 = make_float2(sz, sz), mone2 = make_float2(-1.f, -1.f);
     const int cidx = (lane & 15) >> 1, half8 = (lane & 1) * 8;
-    uint32_t g = 0;
+    const int npairs = (A.KC + 1) >> 1;
+    Ring rr, rb;
+    unsigned long long t0 = WT_NOW(), w_f = 0, w_be = 0;
+    // hi = fp16_rn(x_s) (exact in fp16), lo = fp16_rn(x_s - hi) (x_s - hi exact in fp32): packed pair math
+    auto split2 = [&](float x0, float x1, uint32_t& hv, uint32_t& lv) {
+      const float2 a = __fmul2_rn(make_float2(x0, x1), sz2);
+      const __half2 h = __float22half2_rn(a);
+      const float2 l = __ffma2_rn(__half22float2(h), mone2, a);
+      const __half2 lh = __float22half2_rn(l);
+      hv = *reinterpret_cast<const uint32_t*>(&h);
+      lv = *reinterpret_cast<const uint32_t*>(&lh);
+    };
     for (int item = gi; item < A.nitems; item += A.G) {
       const WhItem it = wh_item(A, item);
-      const uint32_t ng = static_cast<uint32_t>(it.nch * A.NCH);
-      for (uint32_t b = 0; b < ng; ++b, ++g) {
-        if (static_cast<int>(g % kWhZWarps) != zw) continue;
-        const uint32_t slot = g % kWhNR, ph = (g / kWhNR) & 1u;
-        const uint32_t cc = g / A.NCH;  // CTA-wide chunk counter (every item has whole chunks of NCH boxes)
-        const int j = static_cast<int>(g % A.NCH);
-        const uint32_t bs = cc % A.NB;
-        mbar_wait(&raw_full[slot], ph);
-        mbar_wait(&b_empty[bs], ((cc / A.NB) & 1u) ^ 1u);  // the MMA is done with the stage's previous chunk
-        const uint8_t* rp = rawst + slot * kWhRawBytes;
-        uint8_t* hip = bst + bs * 2 * bbytes;
+      for (int c = 0; c < it.nch; ++c, rr.next(A.NR), rb.next(A.NB)) {
+        const uint32_t slot = rr.slot, bs = rb.slot;
+        WT_ACC(w_f, mbar_wait_sleep(&raw_full[slot], rr.ph));
+        WT_ACC(w_be, mbar_wait_sleep(&b_empty[bs], rb.ph ^ 1u));  // the MMA is done with the stage's previous chunk
+        const uint8_t* rp = rawst + slot * rawbytes + (lane & 15) * 16;
+        uint8_t* hip = bst + bs * 2 * bbytes + half8;
         uint8_t* lop = hip + bbytes;
-#pragma unroll 4
-        for (int s = 0; s < 8; ++s) {
-          const int k = 2 * s + (lane >> 4);
-          const float4 x = reinterpret_cast<const float4*>(rp + k * 256)[lane & 15];
-          const float a0 = x.x * sz, a1 = x.y * sz, a2 = x.z * sz, a3 = x.w * sz;
-          const float h0 = rn11_w(a0), h1 = rn11_w(a1), h2 = rn11_w(a2), h3 = rn11_w(a3);
-          const int row = 16 * j + k;
-          const int off = row * 128 + ((cidx ^ (row & 7)) << 4) + half8;
-          *reinterpret_cast<uint2*>(hip + off) = make_uint2(pack_h2_w(h0, h1), pack_h2_w(h2, h3));
-          *reinterpret_cast<uint2*>(lop + off) = make_uint2(pack_h2_w(a0 - h0, a1 - h1), pack_h2_w(a2 - h2, a3 - h3));
+#pragma unroll 3
+        for (int pr = zw; pr < npairs; pr += kWhZWarps) {
+          const int k = 2 * pr + (lane >> 4);
+          if (k < A.KC) {
+            const float4 x = *reinterpret_cast<const float4*>(rp + k * 256);
+            uint2 hv, lv;
+            split2(x.x, x.y, hv.x, lv.x);
+            split2(x.z, x.w, hv.y, lv.y);
+            const int off = k * 128 + ((cidx ^ (k & 7)) << 4);
+            *reinterpret_cast<uint2*>(hip + off) = hv;
+            *reinterpret_cast<uint2*>(lop + off) = lv;
+          }
         }
         fence_async_shared();  // generic writes before the MMA's async-proxy reads; raw reads before the refill
         __syncwarp();
@@ -257,48 +307,35 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
         }
       }
     }
+    if (A.dbg && zw == 0 && lane == 0) {
+      unsigned long long* o = A.dbg + blockIdx.x * 16;
+      o[6] = WT_NOW() - t0; o[7] = w_f; o[8] = w_be;
+    }
   } else if (warp < kWhEpiBase) {
-    // ================================ im2col: lane = tap t = 32 q + lane, two positions per TMEM column
-    const int q = warp - kWhIBase;
-    const int it_tid = tid - 32 * kWhIBase;  // 0..127
+    // ================================ im2col: lane = tap t = 32 q + lane, two positions per TMEM column;
+    // group grp of 4 warps takes the chunks of its parity (two chunks in flight)
+    const int iw = warp - kWhIBase;
+    const int q = iw & 3, grp = iw >> 2;
+    const int it_tid = tid - 32 * kWhIBase;  // 0..255
     const int t = 32 * q + lane;
     const int S2 = A.S * A.S;
     const int ta = t < S2 ? t / A.S : 0, tb = t < S2 ? t - ta * A.S : 0;
     const int toff = ta * A.pitch + tb;  // taps past s^2 read offset 0 (finite; their D rows are never read)
     const uint32_t tq = static_cast<uint32_t>(32 * q) << 16;
-    const float sr = exp2i_w(er);
-    // rstage[rho][c] = r'[n, u_first - P + rho, c - P] (0 outside the image)
-    auto stage = [&](int item) {
+    uint32_t cc = 0, ii = 0;
+    unsigned long long t0 = WT_NOW(), w_ae = 0, w_fill = 0;
+    for (int item = gi; item < A.nitems; item += A.G, ++ii) {
       const WhItem it = wh_item(A, item);
-      const float* rn = A.r + static_cast<size_t>(it.n) * A.H * A.W;
-      for (int e = it_tid; e < A.rs_floats; e += 32 * kWhIWarps) {
-        const int rho = e / A.pitch, c = e - rho * A.pitch;
-        const int i = it.u_first - A.P + rho, jc = c - A.P;
-        const bool ok = i >= 0 && i < A.H && jc >= 0 && jc < A.W;
-        cp_async4(su32(rstage + e), ok ? rn + static_cast<size_t>(i) * A.W + jc : rn, ok);
-      }
-      cp_async_commit();
-    };
-    uint32_t cc = 0;
-    if (gi < A.nitems) stage(gi);
-    for (int item = gi; item < A.nitems; item += A.G) {
-      const WhItem it = wh_item(A, item);
-      cp_async_wait<0>();
-      named_sync(1, 32 * kWhIWarps);  // the staged rows are complete; every warp is done with the old pairs
-      for (int e = it_tid; e < A.rs_floats; e += 32 * kWhIWarps) {
-        const float x0 = rstage[e] * sr;
-        const float x1 = (e + 1 < A.rs_floats ? rstage[e + 1] : 0.f) * sr;
-        const float h0 = rn11_w(x0), h1 = rn11_w(x1);
-        hp[e] = pack_h2_w(h0, h1);
-        lp[e] = pack_h2_w(x0 - h0, x1 - h1);
-      }
-      named_sync(1, 32 * kWhIWarps);  // pairs complete; the raw stage is free
-      if (item + A.G < A.nitems) stage(item + A.G);
+      const uint32_t pb = ii & 1u;
+      WT_ACC(w_fill, mbar_wait_sleep(&pair_full[pb], (ii >> 1) & 1u));  // the epilogue warps built this item's pairs
+      const uint32_t* hp = pairs + pb * 2 * A.rs_floats;
+      const uint32_t* lp = hp + A.rs_floats;
       const uint32_t* sh = hp + toff;
       const uint32_t* sl = lp + toff;
       for (int c = 0; c < it.nch; ++c, ++cc) {
+        if (static_cast<int>(cc & 1u) != grp) continue;
         const uint32_t as = cc % kWhNA;
-        mbar_wait_sleep(&a_empty[as], ((cc / kWhNA) & 1u) ^ 1u);
+        WT_ACC(w_ae, mbar_wait_sleep(&a_empty[as], ((cc / kWhNA) & 1u) ^ 1u));
         tc_after();
         const int pk = it.p0 + kWhChunk * c;
         int u = pk / A.Wc;
@@ -314,6 +351,24 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
             for (int jj = 0; jj < 8; ++jj) {
               hv[jj] = sh[o + 16 * e + 2 * jj];
               lv[jj] = sl[o + 16 * e + 2 * jj];
+            }
+            tmem_st8(tq + col0 + 8u * e, hv);
+            tmem_st8(tq + col0 + 32u + 8u * e, lv);
+          }
+        } else if ((A.Wc & 1) == 0 && A.Wc >= kWhChunk && pk + kWhChunk <= it.p1) {
+          // the chunk wraps into the next code row (once: Wc >= 64); Wc even: positions start even, so no pair
+          // straddles two rows
+          const int o0 = (u - it.u_first) * A.pitch;
+          const int o1 = o0 + A.pitch - A.Wc;  // offset of position v' >= Wc (row u + 1, column v' - Wc)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t hv[8], lv[8];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int vv = v + 16 * e + 2 * jj;
+              const int o = (vv < A.Wc ? o0 : o1) + vv;
+              hv[jj] = sh[o];
+              lv[jj] = sl[o];
             }
             tmem_st8(tq + col0 + 8u * e, hv);
             tmem_st8(tq + col0 + 32u + 8u * e, lv);
@@ -360,8 +415,13 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_ready[as]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pair_empty[pb]);  // done reading this item's pairs
     }
-    cp_async_wait<0>();
+    if (A.dbg && iw == 0 && lane == 0) {
+      unsigned long long* o = A.dbg + blockIdx.x * 16;
+      o[9] = WT_NOW() - t0; o[10] = w_ae; o[11] = w_fill;
+    }
   } else {
     // ================================ epilogue: D[t][k] (fp32, per tile) -> fp32 block sums -> fp64 partials
     const int ew = warp - kWhEpiBase;  // 0..15
@@ -397,34 +457,98 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
       nacc = 0;
     };
     const uint32_t tq = static_cast<uint32_t>(32 * q) << 16;
+    const int flush_tiles = max(1, kWhFlushPos / (kWhChunk * A.cpt));
+    // The epilogue warps (idle most of the time) also build the im2col's residual pairs, one item ahead:
+    // rstage[rho][c] = r'[n, u_first - P + rho, c - P] (0 outside the image) by cp.async one fill ahead, then
+    // scaled and split into hp[rho][c] = (hi(t[c]), hi(t[c+1])), lp likewise, in pair buffer (item & 1)
+    const int et = tid - 32 * kWhEpiBase;  // 0..511
+    const float sr = exp2i_w(er);
+    auto stage = [&](int item) {
+      const WhItem it = wh_item(A, item);
+      const float* rn = A.r + static_cast<size_t>(it.n) * A.H * A.W;
+      const int st_dc = (32 * kWhEpiWarps) % A.pitch, st_dr = (32 * kWhEpiWarps) / A.pitch;
+      const uint32_t st_dst0 = su32(rstage);
+      int c = et % A.pitch, rho = et / A.pitch;  // this thread's first element (row, column)
+      for (int e = et; e < A.rs_floats; e += 32 * kWhEpiWarps) {
+        const int i = it.u_first - A.P + rho, jc = c - A.P;
+        const bool ok = i >= 0 && i < A.H && jc >= 0 && jc < A.W;
+        cp_async4(st_dst0 + 4u * static_cast<uint32_t>(e), ok ? rn + static_cast<size_t>(i) * A.W + jc : rn, ok);
+        c += st_dc;
+        rho += st_dr;
+        if (c >= A.pitch) {
+          c -= A.pitch;
+          ++rho;
+        }
+      }
+      cp_async_commit();
+    };
+    // pairs of the ii-th item of this CTA (its rows are staged); then stage the rows of the next one
+    auto fill = [&](uint32_t ii, int item) {
+      const uint32_t pb = ii & 1u;
+      mbar_wait_sleep(&pair_empty[pb], ((ii >> 1) & 1u) ^ 1u);  // the im2col is done with item ii - 2
+      cp_async_wait<0>();
+      named_sync(2, 32 * kWhEpiWarps);
+      uint32_t* hp = pairs + pb * 2 * A.rs_floats;
+      uint32_t* lp = hp + A.rs_floats;
+      for (int e = et; e < A.rs_floats; e += 32 * kWhEpiWarps) {
+        const float x0 = rstage[e] * sr;
+        const float x1 = (e + 1 < A.rs_floats ? rstage[e + 1] : 0.f) * sr;
+        const float h0 = rn11_w(x0), h1 = rn11_w(x1);
+        hp[e] = pack_h2_w(h0, h1);
+        lp[e] = pack_h2_w(x0 - h0, x1 - h1);
+      }
+      named_sync(2, 32 * kWhEpiWarps);  // every epilogue thread is done reading rstage
+      if (item + A.G < A.nitems) stage(item + A.G);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pair_full[pb]);
+    };
+    if (gi < A.nitems) {
+      stage(gi);
+      fill(0u, gi);
+    }
+    uint32_t ii = 0;
+    constexpr int NB4 = 2;  // x4 loads per batch (the 64-register cap at 1024 threads)
     uint32_t tcount = 0;
-    for (int item = gi; item < A.nitems; item += A.G) {
+    unsigned long long t0 = WT_NOW(), w_af = 0;
+    for (int item = gi; item < A.nitems; item += A.G, ++ii) {
       const WhItem it = wh_item(A, item);
       const int ntl = (it.nch + A.cpt - 1) / A.cpt;
       for (int tl = 0; tl < ntl; ++tl, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
-        mbar_wait_sleep(&acc_full[buf], use & 1u);
+        WT_ACC(w_af, mbar_wait_sleep(&acc_full[buf], use & 1u));
         tc_after();
         const uint32_t col = t_acc + buf * static_cast<uint32_t>(A.Npad) + static_cast<uint32_t>(cb * NC);
+        // batches of loads in flight (the register cap does not hold all NC values at once)
 #pragma unroll
-        for (int j = 0; j < NC / 4; ++j) {
-          float f[4];
-          tmem_ld4_nowait(tq + col + 4u * j, f);
+        for (int j0 = 0; j0 < NC / 4; j0 += NB4) {
+          float f[4 * NB4];
+#pragma unroll
+          for (int j = 0; j < NB4; ++j)
+            if (j0 + j < NC / 4) tmem_ld4_nowait(tq + col + 4u * (j0 + j), *reinterpret_cast<float(*)[4]>(f + 4 * j));
           tmem_ld_wait();
-          acc[4 * j] += f[0];
-          acc[4 * j + 1] += f[1];
-          acc[4 * j + 2] += f[2];
-          acc[4 * j + 3] += f[3];
+#pragma unroll
+          for (int j = 0; j < NB4; ++j)
+            if (j0 + j < NC / 4) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[4 * (j0 + j) + i] += f[4 * j + i];
+            }
         }
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
         const bool last = tl + 1 == ntl && item + A.G >= A.nitems;
-        if (++nacc == kWhFlush || last) flush();
+        if (++nacc == flush_tiles || last) flush();
+        // after the first tile of item ii the im2col is past item ii - 1: build the pairs of item ii + 1
+        if (tl == 0 && item + A.G < A.nitems) fill(ii + 1, item + A.G);
       }
     }
     if (first && t < S2) {  // no tiles: a zero partial
       for (int i = 0; i < nvalid; ++i) gp0[static_cast<size_t>(i) * S2] = 0.0;
+    }
+    cp_async_wait<0>();
+    if (A.dbg && ew == 0 && lane == 0) {
+      unsigned long long* o = A.dbg + blockIdx.x * 16;
+      o[12] = WT_NOW() - t0; o[13] = w_af;
     }
   }
 
@@ -438,7 +562,30 @@ template <int NC>
 cudaError_t run_wgrad_h(const CUtensorMap& tm, const WhArgs& a, int grid, int smem, cudaStream_t st) {
   cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(&wgrad_h_kernel<NC>), kWhSmemMax);
   if (e != cudaSuccess) return e;
+#ifdef CSC_ROLE_TIMING
+  static unsigned long long* dbg = nullptr;
+  static int calls = 0;
+  if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 16 * 1024);
+  cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 1024, st);
+  WhArgs b = a;
+  b.dbg = dbg;
+  wgrad_h_kernel<NC><<<grid, kWhThreads, smem, st>>>(tm, b);
+  if (++calls % 4 == 0) {
+    static unsigned long long h[16 * 1024];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, dbg, sizeof(unsigned long long) * 16 * grid, cudaMemcpyDeviceToHost);
+    double t[16] = {0};
+    for (int bk = 0; bk < grid; ++bk)
+      for (int i = 0; i < 16; ++i) t[i] += static_cast<double>(h[bk * 16 + i]) / grid;
+    fprintf(stderr,
+            "[wgrad_h roles] mma: total %.0f w_accempty %.0f w_bready %.0f w_aready %.0f | tma: total %.0f w_rawempty %.0f | "
+            "zconv0: total %.0f w_rawfull %.0f w_bempty %.0f | im2col0: total %.0f w_aempty %.0f fill %.0f | epi0: total %.0f "
+            "w_accfull %.0f\n",
+            t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11], t[12], t[13]);
+  }
+#else
   wgrad_h_kernel<NC><<<grid, kWhThreads, smem, st>>>(tm, a);
+#endif
   return cudaGetLastError();
 }
 
@@ -472,13 +619,17 @@ WhPlan wgrad_h_plan(const Geom& g, int num_sms) {
   L = (L + 63) / 64 * 64;
   if (L < 256) L = 256;
   if (L > 4096) L = 4096;
-  auto smem_for = [&](int nb, int64_t len) {
-    return 1024 + 2 * nb * bbytes + kWhNR * kWhRawBytes + 3 * rows_for(len) * pitch * 4;
+  const int rawbytes = p.KC * 64 * 4;
+  auto smem_for = [&](int nb, int nr, int64_t len) {
+    return 1024 + 2 * nb * bbytes + nr * rawbytes + 5 * rows_for(len) * pitch * 4;
   };
-  int nb = 4;
-  while (nb > 2 && smem_for(nb, L) > kWhSmemMax) --nb;
-  while (L > 64 && smem_for(nb, L) > kWhSmemMax) L -= 64;
+  // raw slots first (bytes in flight), then B stages; shorter items when nothing else fits
+  int nb = 2, nr = 3;
+  while (nr < 4 && smem_for(nb, nr + 1, L) <= kWhSmemMax) ++nr;
+  while (nb < 4 && smem_for(nb + 1, nr, L) <= kWhSmemMax) ++nb;
+  while (L > 64 && smem_for(nb, nr, L) > kWhSmemMax) L -= 64;
   p.NB = nb;
+  p.NR = nr;
   p.L = static_cast<int>(L);
   p.rs_rows = rows_for(L);
   p.rs_floats = p.rs_rows * pitch;
@@ -486,13 +637,13 @@ WhPlan wgrad_h_plan(const Geom& g, int num_sms) {
   p.nitems = g.N * p.nseg;
   p.G = p.nitems < G ? (p.nitems > 0 ? p.nitems : 1) : G;
   p.grid = p.G * p.nkg;
-  p.smem = smem_for(nb, L);
-  p.cpt = 1;
+  p.smem = smem_for(nb, nr, L);
+  p.cpt = 2;  // 128 positions per accumulator tile (longer tensor-core accumulations lose accuracy: measured)
   {
     const char* ev = std::getenv("CSC_WH_CPT");
     if (ev != nullptr && std::atoi(ev) >= 1 && std::atoi(ev) <= 4) p.cpt = std::atoi(ev);
   }
-  p.ok = p.smem <= kWhSmemMax && p.NB >= 2;
+  p.ok = p.smem <= kWhSmemMax && p.NB >= 2 && p.NR >= 2 && p.KC <= 256;
   return p;
 }
 
@@ -500,7 +651,8 @@ cudaError_t launch_wgrad_h(const Geom& g, const WhPlan& p, TmapCache* tmc, const
                            const uint32_t* zmax, const uint32_t* rmax, double* gpart, cudaStream_t st) {
   const uint64_t plane = static_cast<uint64_t>(g.Hc) * g.Wc;
   cudaError_t e0 = tmap_2d(*tmc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, z, plane, static_cast<uint64_t>(g.N) * g.K, plane * 4,
-                           kWhChunk, 16, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+                           kWhChunk, static_cast<uint32_t>(p.KC), CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   if (e0 != cudaSuccess) return e0;
   const CUtensorMap& tm = tmc->map;
   WhArgs a{};
@@ -512,7 +664,7 @@ cudaError_t launch_wgrad_h(const Geom& g, const WhPlan& p, TmapCache* tmc, const
   a.KC = p.KC; a.Npad = p.Npad; a.NCH = p.NCH; a.nkg = p.nkg; a.G = p.G;
   a.L = p.L; a.nseg = p.nseg; a.nitems = p.nitems;
   a.pitch = p.pitch; a.rs_rows = p.rs_rows; a.rs_floats = p.rs_floats;
-  a.NB = p.NB; a.cpt = p.cpt;
+  a.NB = p.NB; a.NR = p.NR; a.cpt = p.cpt;
   switch (p.Npad / 4) {
     case 4: return run_wgrad_h<4>(tm, a, p.grid, p.smem, st);
     case 8: return run_wgrad_h<8>(tm, a, p.grid, p.smem, st);
