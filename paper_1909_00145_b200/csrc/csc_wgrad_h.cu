@@ -43,8 +43,9 @@ using namespace tcx;
 
 constexpr int kWhNRMax = 8;      // raw TMA slots (one {64 positions, KC planes} box = one chunk each)
 constexpr int kWhNA = 4;         // TMEM A slots (64 columns each: 4 K16-steps x (8 hi + 8 lo))
-constexpr int kWhZWarps = 6;
-constexpr int kWhIWarps = 8;     // two groups of 4 lane quarters, alternate chunks
+constexpr int kWhZWarps = 10;
+constexpr int kWhIGroups = 1;    // groups of 4 lane-quarter warps; group g takes the chunks c with c % groups == g
+constexpr int kWhIWarps = 4 * kWhIGroups;
 constexpr int kWhEpiWarps = 16;
 constexpr int kWhZBase = 2, kWhIBase = kWhZBase + kWhZWarps, kWhEpiBase = kWhIBase + kWhIWarps;
 constexpr int kWhWarps = kWhEpiBase + kWhEpiWarps;
@@ -333,7 +334,7 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
       const uint32_t* sh = hp + toff;
       const uint32_t* sl = lp + toff;
       for (int c = 0; c < it.nch; ++c, ++cc) {
-        if (static_cast<int>(cc & 1u) != grp) continue;
+        if (kWhIGroups > 1 && static_cast<int>(cc % kWhIGroups) != grp) continue;
         const uint32_t as = cc % kWhNA;
         WT_ACC(w_ae, mbar_wait_sleep(&a_empty[as], ((cc / kWhNA) & 1u) ^ 1u));
         tc_after();
