@@ -19,7 +19,8 @@
 // of converter warps into fp16 hi/lo tiles in the canonical MN-major SWIZZLE_128B layout (2 atoms
 // of 64 positions x 16 rows of 128 B, 16-B chunks XOR row).
 // CTA (persistent, 30 warps, <= 64 registers): warp 0 MMA, warp 1 TMA, warps 2..17 converters (a pair
-// per stage slot), warps 18..29 epilogue (4 TMEM lane quarters x 3 groups of tap rows).
+// per stage slot), warps 18..29 epilogue (4 TMEM lane quarters x 3 groups of tap rows); CSC_CH_NS /
+// CSC_CH_EPI_GROUPS change the split in tuning builds (fewer stages measured slower: 7 / 4 -> 0.391 ms).
 #include "csc_internal.cuh"
 #include "csc_tc_ptx.cuh"
 
@@ -37,9 +38,16 @@ namespace {
 
 using namespace tcx;
 
-constexpr int kHNS = 9;             // stages (16 filters of one tile each)
-constexpr int kHConvWarps = 18;  // 2 per stage slot (kHNS slots): a slot is always converted by the same pair
-constexpr int kHEpiWarps = 12;   // 4 lane quarters x 3 groups of tap rows
+#ifndef CSC_CH_NS
+#define CSC_CH_NS 9
+#endif
+#ifndef CSC_CH_EPI_GROUPS
+#define CSC_CH_EPI_GROUPS 3
+#endif
+constexpr int kHNS = CSC_CH_NS;     // stages (16 filters of one tile each)
+constexpr int kHConvWarps = 2 * kHNS;  // 2 per stage slot (kHNS slots): a slot is always converted by the same pair
+constexpr int kHEpiGroups = CSC_CH_EPI_GROUPS;  // groups of tap rows
+constexpr int kHEpiWarps = 4 * kHEpiGroups;     // 4 lane quarters x kHEpiGroups groups of tap rows
 constexpr int kHConvBase = 2, kHEpiBase = kHConvBase + kHConvWarps;
 constexpr int kHWarps = kHEpiBase + kHEpiWarps;
 constexpr int kHThreads = 32 * kHWarps;
@@ -303,14 +311,14 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     // ================================ epilogue: col2im into one band window (as csc_conv_ss.cu)
     const int q = warp & 3;                 // TMEM lane quarter of this warp
     const int h = (warp - kHEpiBase) >> 2;  // group of tap rows
-    constexpr int AH = (S + 2) / 3;
+    constexpr int AH = (S + kHEpiGroups - 1) / kHEpiGroups;
     const int a_beg = h * AH;
     const int na = min(AH, S - a_beg);      // may be <= 0 for small S
     const float inv = exp2i(-(ez + ef));
     // Wc >= 128 keeps the quarters' window rows disjoint (one pass); narrower rows add in a fixed
     // order of phases (quarters; and their row groups when Wc < 32 + P): deterministic sums
-    const int nph = A.Wc >= 128 ? 1 : (A.Wc >= 32 + P ? 4 : 12);
-    const int myph = nph == 1 ? 0 : (nph == 4 ? q : 3 * q + h);
+    const int nph = A.Wc >= 128 ? 1 : (A.Wc >= 32 + P ? 4 : 4 * kHEpiGroups);
+    const int myph = nph == 1 ? 0 : (nph == 4 ? q : kHEpiGroups * q + h);
     uint32_t tcount = 0;
     unsigned long long e_t0 = HT_NOW(), e_wa = 0;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
