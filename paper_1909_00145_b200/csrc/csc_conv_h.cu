@@ -15,12 +15,15 @@
 // survives the fp32 sum.
 //
 // Stage = 16 filter planes of one tile: one TMA box {128 positions, 16 planes} (fp32, no swizzle,
-// 8 KB: one request per stage keeps the TMA issue rate off the critical path), converted by a pair
-// of converter warps into fp16 hi/lo tiles in the canonical MN-major SWIZZLE_128B layout (2 atoms
-// of 64 positions x 16 rows of 128 B, 16-B chunks XOR row).
+// 8 KB: one request per stage keeps the TMA issue rate off the critical path) into a ring of 10 raw
+// slots, converted by a pair of converter warps into fp16 hi/lo tiles (a ring of 8 slots) in the
+// canonical MN-major SWIZZLE_128B layout (2 atoms of 64 positions x 16 rows of 128 B, 16-B chunks XOR
+// row); the raw slot is released once converted, the hi/lo slot once multiplied.
 // CTA (persistent, 30 warps, <= 64 registers): warp 0 MMA, warp 1 TMA, warps 2..17 converters (a pair
-// per stage slot), warps 18..29 epilogue (4 TMEM lane quarters x 3 groups of tap rows); CSC_CH_NS /
-// CSC_CH_EPI_GROUPS change the split in tuning builds (fewer stages measured slower: 7 / 4 -> 0.391 ms).
+// per hi/lo slot), warps 18..29 epilogue (4 TMEM lane quarters x 3 groups of tap rows).  CSC_CH_NS /
+// CSC_CH_NR / CSC_CH_EPI_GROUPS / CSC_CH_SPLIT_CVT change the split in tuning builds (A/B at config 3:
+// 9 coupled slots 0.338 ms, + cvt-based split 0.330, 8 hi/lo + 10 raw slots 0.326; 7 coupled slots with
+// 4 epilogue groups 0.391; the raw ring depth alone moves it by < 2%).
 #include "csc_internal.cuh"
 #include "csc_tc_ptx.cuh"
 
@@ -39,13 +42,20 @@ namespace {
 using namespace tcx;
 
 #ifndef CSC_CH_NS
-#define CSC_CH_NS 9
+#define CSC_CH_NS 8
+#endif
+#ifndef CSC_CH_NR
+#define CSC_CH_NR 10
+#endif
+#ifndef CSC_CH_SPLIT_CVT
+#define CSC_CH_SPLIT_CVT 1
 #endif
 #ifndef CSC_CH_EPI_GROUPS
 #define CSC_CH_EPI_GROUPS 3
 #endif
-constexpr int kHNS = CSC_CH_NS;     // stages (16 filters of one tile each)
-constexpr int kHConvWarps = 2 * kHNS;  // 2 per stage slot (kHNS slots): a slot is always converted by the same pair
+constexpr int kHNS = CSC_CH_NS;     // hi / lo slots (16 filters of one tile each)
+constexpr int kHNR = CSC_CH_NR;     // raw fp32 slots (TMA boxes in flight); >= kHNS
+constexpr int kHConvWarps = 2 * kHNS;  // 2 per hi / lo slot (kHNS slots): a slot is always converted by the same pair
 constexpr int kHEpiGroups = CSC_CH_EPI_GROUPS;  // groups of tap rows
 constexpr int kHEpiWarps = 4 * kHEpiGroups;     // 4 lane quarters x kHEpiGroups groups of tap rows
 constexpr int kHConvBase = 2, kHEpiBase = kHConvBase + kHConvWarps;
@@ -53,7 +63,7 @@ constexpr int kHWarps = kHEpiBase + kHEpiWarps;
 constexpr int kHThreads = 32 * kHWarps;
 constexpr int kHRawBytes = 8192;    // one TMA box: 16 planes x 128 positions (fp32, rows of 512 B)
 constexpr int kHHalfBytes = 4096;   // 2 atoms x 16 rows x 128 B (fp16), one of hi / lo
-constexpr int kHStageBytes = kHRawBytes + 2 * kHHalfBytes;
+constexpr int kHRingBytes = kHNR * kHRawBytes + kHNS * 2 * kHHalfBytes;
 constexpr int kHSmemMax = 226 * 1024;  // + the static smem stays under the 227 KB opt-in limit
 
 // instruction descriptor kind::f16: fp32 accumulate, fp16 A/B, both MN-major
@@ -126,7 +136,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
   extern __shared__ uint8_t smraw[];
   // per stage slot: full (TMA -> converters), rempty (converters done reading the raw tile -> TMA),
   // ready (hi / lo written -> MMA), empty (MMA done reading hi / lo -> converters)
-  __shared__ __align__(8) uint64_t full[kHNS], rempty[kHNS], ready[kHNS], empty[kHNS], acc_full[2], acc_empty[2];
+  __shared__ __align__(8) uint64_t full[kHNR], rempty[kHNR], ready[kHNS], empty[kHNS], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ double l1_warp[kHConvWarps];
 
@@ -137,7 +147,9 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
   const int bbytes = 2 * A.KC * 128;                   // one of hi / lo: 2 atoms x KC rows x 128 B
   uint8_t* bsm = sm;                                   // [hi | lo]
   uint8_t* stg = sm + 2 * bbytes;                      // [NS][raw 8 KB | hi 4 KB | lo 4 KB]
-  float* win = reinterpret_cast<float*>(stg + kHNS * kHStageBytes);  // [WL]
+  // stg = [kHNR raw slots of 8 KB][kHNS hi / lo slots of 8 KB]
+  uint8_t* hls = stg + kHNR * kHRawBytes;
+  float* win = reinterpret_cast<float*>(stg + kHRingBytes);  // [WL]
   const int ez = scale_exp(*A.zmax), ef = scale_exp(*A.fmax);
 
   {
@@ -148,11 +160,13 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
   }
   fence_async_shared();
   if (tid == 0) {
-    for (int i = 0; i < kHNS; ++i) {
+    for (int i = 0; i < kHNR; ++i) {
       mbar_init(&full[i], 1);
+      mbar_init(&rempty[i], 2);
+    }
+    for (int i = 0; i < kHNS; ++i) {
       mbar_init(&ready[i], 2);
       mbar_init(&empty[i], 1);
-      mbar_init(&rempty[i], 2);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -171,7 +185,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     // ================================ MMA issuer
     const uint32_t idesc = idesc_f16_mn(128, A.NT);
     const uint32_t lbo_b = static_cast<uint32_t>(A.KC) * 128u;  // N atom (64 taps) stride
-    const uint32_t sbh = su32(bsm), sbl = su32(bsm + bbytes), sst = su32(stg);
+    const uint32_t sbh = su32(bsm), sbl = su32(bsm + bbytes), sst = su32(hls);
     uint32_t g = 0, tcount = 0;
     unsigned long long t0 = HT_NOW(), w_ae = 0, w_rd = 0;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
@@ -191,7 +205,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           mbar_wait(&ready[slot], ph);
           w_rd += HT_NOW() - tb;
           tc_after();
-          const uint32_t ah = sst + slot * kHStageBytes + kHRawBytes;
+          const uint32_t ah = sst + slot * (2 * kHHalfBytes);
           // A: MN-major SW128, 2 atoms of 64 positions at LBO = 16 rows x 128 B, 8-row K groups at SBO
           const uint64_t dah = sdesc(ah, 2048u, 1024u, kLayout128B);
           const uint64_t dal = sdesc(ah + kHHalfBytes, 2048u, 1024u, kLayout128B);
@@ -233,10 +247,10 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
         for (int t = 0; t < it.ntiles; ++t) {
           const int pt = it.p0 + 128 * t;  // multiple of 4 floats (BR % 4 == 0): 16-B aligned box start
           for (int c = 0; c < A.NCH; ++c, ++g) {
-            const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+            const uint32_t slot = g % kHNR, ph = (g / kHNR) & 1u;
             mbar_wait(&rempty[slot], ph ^ 1u);  // the raw tile is free once converted (not once multiplied)
             mbar_arrive_expect_tx(&full[slot], kHRawBytes);
-            const uint32_t dst = su32(stg + slot * kHStageBytes);
+            const uint32_t dst = su32(stg + slot * kHRawBytes);
             tma_load_2d(dst, &tmap_z, pt, plane0 + 16 * c, &full[slot]);  // {128 positions, 16 planes}
           }
         }
@@ -255,32 +269,52 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     double l1 = 0.0;
     uint32_t g = 0;
     const int atom = lane >> 4, cidx = (lane >> 1) & 7, half8 = (lane & 1) * 8;
+    // hi = fp16_rn(x_s) (exact in fp16), lo = fp16_rn(x_s - hi) (x_s - hi exact in fp32): packed pair math
+    const float2 sz2 = make_float2(sz, sz), mone2 = make_float2(-1.f, -1.f);
+    auto split2 = [&](float x0, float x1, uint32_t& hv, uint32_t& lv) {
+      const float2 a = __fmul2_rn(make_float2(x0, x1), sz2);
+      const __half2 h = __float22half2_rn(a);
+      const float2 l = __ffma2_rn(__half22float2(h), mone2, a);
+      const __half2 lh = __float22half2_rn(l);
+      hv = *reinterpret_cast<const uint32_t*>(&h);
+      lv = *reinterpret_cast<const uint32_t*>(&lh);
+    };
+    (void)split2;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t) {
         const int pt = it.p0 + 128 * t;
         for (int c = 0; c < A.NCH; ++c, ++g) {
           if (static_cast<int>(g % kHNS) != (cw >> 1)) continue;
-          const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;
+          const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;      // hi / lo slot
+          const uint32_t rslot = g % kHNR, rph = (g / kHNR) & 1u;  // raw slot
           unsigned long long tw = HT_NOW();
-          mbar_wait(&full[slot], ph);
+          mbar_wait(&full[rslot], rph);
           unsigned long long tw2 = HT_NOW();
           mbar_wait(&empty[slot], ph ^ 1u);  // the MMA has finished with this slot's previous hi / lo
           c_wf += tw2 - tw;
           c_we += HT_NOW() - tw2;
-          const uint8_t* rawp = stg + slot * kHStageBytes;
-          uint8_t* hip = stg + slot * kHStageBytes + kHRawBytes;
+          const uint8_t* rawp = stg + rslot * kHRawBytes;
+          uint8_t* hip = hls + slot * (2 * kHHalfBytes);
           uint8_t* lop = hip + kHHalfBytes;
           float s1 = 0.f;
 #pragma unroll 4
           for (int rr = 0; rr < 8; ++rr) {
             const int k = 2 * rr + (cw & 1);  // the pair splits the stage's 16 rows
             const float4 x0 = reinterpret_cast<const float4*>(rawp + k * 512)[lane];
+            const int off = atom * 2048 + k * 128 + ((cidx ^ (k & 7)) << 4) + half8;
+#if CSC_CH_SPLIT_CVT
+            uint2 hv, lv;
+            split2(x0.x, x0.y, hv.x, lv.x);
+            split2(x0.z, x0.w, hv.y, lv.y);
+            *reinterpret_cast<uint2*>(hip + off) = hv;
+            *reinterpret_cast<uint2*>(lop + off) = lv;
+#else
             const float a0 = x0.x * sz, a1 = x0.y * sz, a2 = x0.z * sz, a3 = x0.w * sz;
             const float h0 = rn11(a0), h1 = rn11(a1), h2 = rn11(a2), h3 = rn11(a3);
-            const int off = atom * 2048 + k * 128 + ((cidx ^ (k & 7)) << 4) + half8;
             *reinterpret_cast<uint2*>(hip + off) = make_uint2(pack_h2(h0, h1), pack_h2(h2, h3));
             *reinterpret_cast<uint2*>(lop + off) = make_uint2(pack_h2(a0 - h0, a1 - h1), pack_h2(a2 - h2, a3 - h3));
+#endif
             if (want_l1) {
               const int kk = A.ks * A.KC + 16 * c + k;
               const int p = pt + 4 * lane;
@@ -295,7 +329,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
           __syncwarp();
           if (lane == 0) {
             mbar_arrive(&ready[slot]);
-            mbar_arrive(&rempty[slot]);
+            mbar_arrive(&rempty[rslot]);
           }
         }
       }
@@ -551,7 +585,7 @@ bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p) {
   p = TcPlan{};
   p.NT = 128;  // taps padded to 2 atoms of 64
   p.natoms = 2;
-  const int stages = kHNS * kHStageBytes;
+  const int stages = kHRingBytes;
   const int n = g.N > 0 ? g.N : 1;
   int BR = (g.Hc * n) / (6 * num_sms);
   BR = (BR / 4) * 4;
