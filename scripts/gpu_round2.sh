@@ -24,7 +24,7 @@ timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -s
 # one full iteration's launches (the iteration boundary: the Lipschitz kernels open each code step)
 python scripts/launch_summary.py $O/launches.csv > $O/launches.txt 2>&1
 python scripts/trace_run.py --config sweep --iters 100 --out $O/trace_sweep.csv > $O/trace.log 2>&1
-bash scripts/ncu_one.sh $TAG code_h conv_h wgrad_tc
+bash scripts/ncu_one.sh $TAG code_h conv_h wgrad_h
 # the NEXT rows, each on the configuration DESIGN.md §9-§12 quotes
 $B --config batch --code-solver admm --steps 5 --warmup 2 --no-cpu-baseline > $O/bench_admm_batch.log 2>&1
 $B --config sweep --code-solver admm --steps 3 --warmup 1 --no-cpu-baseline > $O/bench_admm_sweep.log 2>&1
