@@ -15,15 +15,14 @@
 // survives the fp32 sum.
 //
 // Stage = 16 filter planes of one tile: one TMA box {128 positions, 16 planes} (fp32, no swizzle,
-// 8 KB: one request per stage keeps the TMA issue rate off the critical path) into a ring of 10 raw
-// slots, converted by a pair of converter warps into fp16 hi/lo tiles (a ring of 8 slots) in the
-// canonical MN-major SWIZZLE_128B layout (2 atoms of 64 positions x 16 rows of 128 B, 16-B chunks XOR
-// row); the raw slot is released once converted, the hi/lo slot once multiplied.
-// CTA (persistent, 30 warps, <= 64 registers): warp 0 MMA, warp 1 TMA, warps 2..17 converters (a pair
-// per hi/lo slot), warps 18..29 epilogue (4 TMEM lane quarters x 3 groups of tap rows).  CSC_CH_NS /
-// CSC_CH_NR / CSC_CH_EPI_GROUPS / CSC_CH_SPLIT_CVT change the split in tuning builds (A/B at config 3:
-// 9 coupled slots 0.338 ms, + cvt-based split 0.330, 8 hi/lo + 10 raw slots 0.326; 7 coupled slots with
-// 4 epilogue groups 0.391; the raw ring depth alone moves it by < 2%).
+// 8 KB: one request per stage keeps the TMA issue rate off the critical path) into a raw slot, converted
+// by a pair of converter warps into fp16 hi/lo tiles in the canonical MN-major SWIZZLE_128B layout (2 atoms
+// of 64 positions x 16 rows of 128 B, 16-B chunks XOR row); the raw slot is released once converted, the
+// hi/lo slot once multiplied.
+// CTA (persistent, 32 warps, <= 64 registers): warp 0 MMA, warp 1 TMA, warps 2..19 converters (a pair
+// per slot), warps 20..31 epilogue (4 TMEM lane quarters x 3 groups of tap rows).  CSC_CH_NS / CSC_CH_NR /
+// CSC_CH_EPI_GROUPS / CSC_CH_SPLIT_CVT change the split in tuning builds (A/B at config 3: 9 slots with the
+// rn11 split 0.338 ms, with the cvt-based split 0.330; 7 slots and 4 epilogue groups 0.391; 5 / 5 0.457).
 #include "csc_internal.cuh"
 #include "csc_tc_ptx.cuh"
 
@@ -42,10 +41,10 @@ namespace {
 using namespace tcx;
 
 #ifndef CSC_CH_NS
-#define CSC_CH_NS 8
+#define CSC_CH_NS 9
 #endif
 #ifndef CSC_CH_NR
-#define CSC_CH_NR 10
+#define CSC_CH_NR CSC_CH_NS
 #endif
 #ifndef CSC_CH_SPLIT_CVT
 #define CSC_CH_SPLIT_CVT 1
@@ -55,6 +54,9 @@ using namespace tcx;
 #endif
 constexpr int kHNS = CSC_CH_NS;     // hi / lo slots (16 filters of one tile each)
 constexpr int kHNR = CSC_CH_NR;     // raw fp32 slots (TMA boxes in flight); >= kHNS
+// a raw slot's stages (g = r mod kHNR) must all go to one converter pair (g mod kHNS): a pair waits its
+// slots' phases in order, so no waiter ever runs a full phase ahead of the barrier (parity aliasing)
+static_assert(kHNR % kHNS == 0, "raw ring depth must be a multiple of the hi / lo ring depth");
 constexpr int kHConvWarps = 2 * kHNS;  // 2 per hi / lo slot (kHNS slots): a slot is always converted by the same pair
 constexpr int kHEpiGroups = CSC_CH_EPI_GROUPS;  // groups of tap rows
 constexpr int kHEpiWarps = 4 * kHEpiGroups;     // 4 lane quarters x kHEpiGroups groups of tap rows
