@@ -90,6 +90,14 @@ __device__ __forceinline__ void cp_async4_if(uint32_t smem_dst, const float* src
                "l"(src), "r"(p ? 1 : 0)
                : "memory");
 }
+// store v at base + off_bytes when sel != 0: one IMAD.WIDE for the address, the predicate from sel itself
+__device__ __forceinline__ void st_off_if_nz(float* base, uint32_t off_bytes, float v, float sel) {
+  asm volatile(
+      "{\n.reg .pred q;\n.reg .u64 a;\nsetp.ne.f32 q, %3, 0f00000000;\nmad.wide.u32 a, %1, 1, %0;\n@q st.global.f32 [a], %2;\n}\n" ::"l"(
+          base),
+      "r"(off_bytes), "f"(v), "f"(sel)
+      : "memory");
+}
 __device__ __forceinline__ void st_global_if(float* ptr, float v, bool p) {
   asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.f32 [%0], %1;\n}\n" ::"l"(ptr), "f"(v),
                "r"(p ? 1 : 0)
@@ -361,6 +369,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     const float ntinv = -tau * inv;
     const float sdz = exp2i_h(edz);
     const size_t plane = static_cast<size_t>(A.Hc) * A.Wc;
+    const uint32_t planeB = static_cast<uint32_t>(plane * 4);  // < 2^28 for every supported shape: 16 planeB < 2^32
     const int kbase = kg * A.KC;
     const int kend = min(kbase + A.KC, A.K);
     const bool masked = A.mask != nullptr;
@@ -474,8 +483,6 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
         const int npair = kv == 0xFFFFu ? 8 : (32 - __clz(kv) + 1) >> 1;
         auto body = [&](auto per_k) {
           constexpr bool PK = decltype(per_k)::value;
-          float* zp = zb;          // even filter rows of the slice
-          float* zq = zb + plane;  // odd rows
 #pragma unroll
           for (int i2 = 0; i2 < 8; ++i2) {
             if (i2 >= npair) {  // warp-uniform
@@ -502,18 +509,19 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
             // nonzero (x - y == 0 iff x == y in IEEE arithmetic with gradual underflow)
             const float2 dd = __fadd2_rn(nz, make_float2(-zc2.x, -zc2.y));
             const float2 dsel = make_float2((wb & (1u << i)) != 0u ? dd.x : 0.f, (wb & (2u << i)) != 0u ? dd.y : 0.f);
-            if (dsel.x != 0.f) *zp = nz.x;
-            if (dsel.y != 0.f) *zq = nz.y;
-            zp += 2 * plane;
-            zq += 2 * plane;
+            // filter rows i, i + 1 of the slice: uniform byte offsets i * plane * 4 (< 2^32) from the slice base
+            st_off_if_nz(zb, static_cast<uint32_t>(i) * planeB, nz.x, dsel.x);
+            st_off_if_nz(zb, static_cast<uint32_t>(i + 1) * planeB, nz.y, dsel.y);
             // max |z| bound: every code of the slice was loaded, so |S(z - tau c)| over all of them bounds
             // the changed codes and the unchanged ones keep the previous bound
             wmax = fmaxf(wmax, fmaxf(fabsf(nz.x), fabsf(nz.y)));
+            // dz split: hi = fp16_rn(dz_s), lo = fp16_rn(dz_s - hi) (dz_s - hi exact in fp32; T6)
             const float2 dz = __fmul2_rn(dsel, make_float2(sdz, sdz));
-            const float h0 = rn11_h(dz.x), h1 = rn11_h(dz.y);
-            const float2 lo = __fadd2_rn(dz, make_float2(-h0, -h1));
-            hv[i2] = pack_h2_h(h0, h1);
-            lv[i2] = pack_h2_h(lo.x, lo.y);
+            const __half2 h2 = __float22half2_rn(dz);
+            const float2 lo = __ffma2_rn(__half22float2(h2), make_float2(-1.f, -1.f), dz);
+            const __half2 l2 = __float22half2_rn(lo);
+            hv[i2] = *reinterpret_cast<const uint32_t*>(&h2);
+            lv[i2] = *reinterpret_cast<const uint32_t*>(&l2);
           }
         };
 #ifdef CSC_ROLE_TIMING
