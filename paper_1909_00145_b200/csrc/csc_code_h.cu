@@ -644,6 +644,9 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     // col2im of Y of tile (it, t), count tc, into the band window
     constexpr int AH = (S + 1) / 2;
     const int a0 = hh * AH, a1 = hh ? S : AH;
+    float hm[S];  // [lane < b]: the rotations of tap b that belong to the next quarter (col2im halo)
+#pragma unroll
+    for (int b = 0; b < S; ++b) hm[b] = lane < b ? 1.f : 0.f;
     const float inv2 = exp2i_h(-(edz + ed));
     // add phases: the quarters in order (and the two row halves of a quarter in order when their windows
     // can overlap, Wc < 32 + P): deterministic fp32 sums
@@ -659,32 +662,39 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       const uint32_t tacc = t_y + (static_cast<uint32_t>(32 * q) << 16);
       float* rowb = win + pq + lane;
       float own[AH], dnv[AH];
+      // two tap rows at a time through the packed fp32 pipe: one rotation per tap serves both parts (lanes
+      // >= b get position lane-b of this quarter, lanes < b position lane-b+32, the halo of the next quarter's
+      // first lanes); tot sums every rotation, hal the halo ones (x hm[b] = [lane < b], exact), own = tot - hal
       auto rows = [&](auto partial) {
         constexpr bool PART = decltype(partial)::value;
 #pragma unroll
-        for (int i = 0; i < AH; ++i) {
-          own[i] = 0.f;
-          dnv[i] = 0.f;
+        for (int i = 0; i < AH; i += 2) {
+          own[i] = dnv[i] = 0.f;
+          if (i + 1 < AH) own[i + 1] = dnv[i + 1] = 0.f;
           const int a = a0 + i;
           if (a >= a1) continue;
-          float y[S];
-          tmem_ld_row<S>(tacc + a * S, y);
+          const bool two = i + 1 < AH && a + 1 < a1;  // warp-uniform
+          float y0[S], y1[S];
+          tmem_ld_row<S>(tacc + a * S, y0);
+          if (two) tmem_ld_row<S>(tacc + (a + 1) * S, y1);
           tmem_ld_wait();
-          float u0s = 0.f, u1s = 0.f, d0s = 0.f, d1s = 0.f;
+          float2 tot = make_float2(0.f, 0.f), hal = make_float2(0.f, 0.f);
 #pragma unroll
           for (int b = 0; b < S; ++b) {
-            // one rotation serves both parts: lanes >= b get position lane-b of this quarter, lanes < b
-            // get position lane-b+32, the halo that belongs to the next quarter's first lanes
-            const float yv = PART ? (pvalid ? y[b] : 0.f) : y[b];
-            const float rot = b == 0 ? yv : __shfl_sync(kFullMask, yv, (lane - b) & 31);
-            if (lane >= b) {
-              if (b & 1) u1s += rot; else u0s += rot;
-            } else {
-              if (b & 1) d1s += rot; else d0s += rot;
-            }
+            const float v0 = PART ? (pvalid ? y0[b] : 0.f) : y0[b];
+            const float v1 = two ? (PART ? (pvalid ? y1[b] : 0.f) : y1[b]) : 0.f;
+            const float2 rot = b == 0 ? make_float2(v0, v1)
+                                      : make_float2(__shfl_sync(kFullMask, v0, (lane - b) & 31),
+                                                    __shfl_sync(kFullMask, v1, (lane - b) & 31));
+            tot = __fadd2_rn(tot, rot);
+            if (b > 0) hal = __ffma2_rn(rot, make_float2(hm[b], hm[b]), hal);
           }
-          own[i] = u0s + u1s;
-          dnv[i] = d0s + d1s;
+          own[i] = tot.x - hal.x;
+          dnv[i] = hal.x;
+          if (i + 1 < AH) {
+            own[i + 1] = tot.y - hal.y;
+            dnv[i + 1] = hal.y;
+          }
         }
       };
       if (__all_sync(kFullMask, pvalid)) rows(std::false_type{});
