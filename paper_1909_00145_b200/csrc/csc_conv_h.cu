@@ -356,7 +356,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     const int nph = A.Wc >= 128 ? 1 : (A.Wc >= 32 + P ? 4 : 4 * kHEpiGroups);
     const int myph = nph == 1 ? 0 : (nph == 4 ? q : kHEpiGroups * q + h);
     uint32_t tcount = 0;
-    unsigned long long e_t0 = HT_NOW(), e_wa = 0;
+    unsigned long long e_t0 = HT_NOW(), e_wa = 0, e_red = 0, e_win = 0, e_fl = 0;
     for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
@@ -408,11 +408,14 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
             dnv[i] = d0s + d1s;
           }
         };
+        const unsigned long long tr0 = HT_NOW();
         if (__all_sync(kFullMask, pvalid)) reduce_rows(std::false_type{});
         else reduce_rows(std::true_type{});
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        const unsigned long long tr1 = HT_NOW();
+        e_red += tr1 - tr0;
         if (nph == 1) {
 #pragma unroll
           for (int i = 0; i < AH; ++i)
@@ -440,7 +443,9 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
             named_sync(1, 32 * kHEpiWarps);
           }
         }
+        e_win += HT_NOW() - tr1;
       }
+      const unsigned long long tf0 = HT_NOW();
       float* dst = A.part + (static_cast<size_t>(it.n) * A.nbands + (it.u0 / A.BR)) *
                                 static_cast<size_t>(A.BR + P) * A.W;
       const int rows = A.BR + P;
@@ -453,10 +458,14 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       named_sync(1, 32 * kHEpiWarps);
       for (int e = et; e < A.WL; e += 32 * kHEpiWarps) win[e] = 0.f;
       named_sync(1, 32 * kHEpiWarps);
+      e_fl += HT_NOW() - tf0;
     }
     if (A.dbg && warp == kHEpiBase && lane == 0) {
       A.dbg[blockIdx.x * 16 + 6] = HT_NOW() - e_t0;
       A.dbg[blockIdx.x * 16 + 7] = e_wa;
+      A.dbg[blockIdx.x * 16 + 8] = e_red;
+      A.dbg[blockIdx.x * 16 + 9] = e_win;
+      A.dbg[blockIdx.x * 16 + 10] = e_fl;
     }
   }
 
@@ -566,8 +575,8 @@ cudaError_t run_conv_h(const CUtensorMap& tm, const HArgs& a, int grid, int smem
       for (int i = 0; i < 16; ++i) t[i] += static_cast<double>(h[bk * 16 + i]) / grid;
     fprintf(stderr,
             "[conv_h roles p%d] mma: total %.0f w_accempty %.0f w_ready %.0f | conv0: total %.0f w_full %.0f w_empty %.0f | "
-            "epi0: total %.0f w_accfull %.0f\n",
-            a.precise, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+            "epi0: total %.0f w_accfull %.0f reduce %.0f window %.0f flush %.0f\n",
+            a.precise, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[8], t[9], t[10]);
   }
 #else
   conv_h_kernel<S><<<grid, kHThreads, smem, st>>>(tm, a);
