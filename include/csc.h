@@ -222,6 +222,18 @@ csc_status csc_iterate_staged(csc_ctx* ctx, int slot, float* x, float* d, float*
                               float step_z, float step_d, double p, uint64_t seed, uint32_t iter,
                               double obj_out[3], float taus_out[2]);
 
+/* Pipelined csc_iterate_staged for streaming use: enqueues the iteration on the staged slot and returns
+ * at once with, in obj_prev / taus_prev (host), the objective {F, 1/2||r||^2, lambda||z||_1} and step sizes
+ * {tau_z, tau_d} of the PREVIOUS call, waiting only for that one (*have_prev = 1; 0 on the first call
+ * after csc_iterate_drain or csc_init).  The device therefore always has the next iteration queued while
+ * the host reads a result.  csc_iterate_drain waits for the last enqueued iteration and returns its
+ * values (*have = 0 when none is pending).  Same arithmetic and kernels as csc_iterate_staged; results
+ * are identical.  Allocates two pinned result slots on first use.  obj_prev / taus_prev may be NULL. */
+csc_status csc_iterate_staged_async(csc_ctx* ctx, int slot, float* x, float* d, float* z, float lambda,
+                                    float step_z, float step_d, double p, uint64_t seed, uint32_t iter,
+                                    double obj_prev[3], float taus_prev[2], int* have_prev);
+csc_status csc_iterate_drain(csc_ctx* ctx, double obj[3], float taus[2], int* have);
+
 /* Forget the residual cache (caller changed x, d or z outside the API). */
 csc_status csc_invalidate(csc_ctx* ctx);
 

@@ -33,7 +33,8 @@ ABI_SYMBOLS = (
     "csc_surrogate_update", "csc_filter_step_surrogate", "csc_read_surrogate", "csc_set_mask_mode",
     "csc_stage_images", "csc_iterate_staged", "csc_mask_selwords", "csc_read_scalars", "csc_zg_sumsq",
     "csc_set_iter_offset", "csc_count_nonzero", "csc_set_nvtx", "csc_comm_check", "csc_profile_set_classes",
-    "csc_objective_enqueue", "csc_objective_read", "csc_profile_sample",
+    "csc_objective_enqueue", "csc_objective_read", "csc_profile_sample", "csc_iterate_staged_async",
+    "csc_iterate_drain",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -77,6 +78,8 @@ def load_library(path: Optional[str] = None):
         L.csc_set_mask_mode.argtypes = [vp, ctypes.c_int]
         L.csc_stage_images.argtypes = [vp, vp, ctypes.c_int]
         L.csc_iterate_staged.argtypes = [vp, ctypes.c_int, vp, vp, vp, f32, f32, f32, f64, u64, u32, vp, vp]
+        L.csc_iterate_staged_async.argtypes = [vp, ctypes.c_int, vp, vp, vp, f32, f32, f32, f64, u64, u32, vp, vp, vp]
+        L.csc_iterate_drain.argtypes = [vp, vp, vp, vp]
         L.csc_filter_step_bcd.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
         L.csc_surrogate_reset.argtypes = [vp]
         L.csc_surrogate_update.argtypes = [vp, vp, vp]
@@ -312,6 +315,31 @@ class Context:
         self._check(self._L.csc_iterate_staged(self._h, int(slot), px, pd, pz, float(lam), float(step_z),
                                                float(step_d), float(p), int(seed) & (2**64 - 1),
                                                int(it) & 0xffffffff, obj, taus))
+        return (float(obj[0]), float(obj[1]), float(obj[2])), (float(taus[0]), float(taus[1]))
+
+    def iterate_staged_async(self, x, d, z, lam: float, p: float, seed: int, it: int, slot: int, *,
+                             step_z: float = 0.0, step_d: float = 0.0):
+        """Pipelined csc_iterate_staged (include/csc.h csc_iterate_staged_async): enqueues this iteration
+        and returns the previous call's ((F, 1/2||r||^2, lambda||z||_1), (tau_z, tau_d)), or None."""
+        px, pd, pz = self._xdz(x, d, z)
+        obj = (ctypes.c_double * 3)()
+        taus = (ctypes.c_float * 2)()
+        have = ctypes.c_int(0)
+        self._check(self._L.csc_iterate_staged_async(self._h, int(slot), px, pd, pz, float(lam), float(step_z),
+                                                     float(step_d), float(p), int(seed) & (2**64 - 1),
+                                                     int(it) & 0xffffffff, obj, taus, ctypes.byref(have)))
+        if not have.value:
+            return None
+        return (float(obj[0]), float(obj[1]), float(obj[2])), (float(taus[0]), float(taus[1]))
+
+    def iterate_drain(self):
+        """The results of the last csc_iterate_staged_async call (include/csc.h csc_iterate_drain), or None."""
+        obj = (ctypes.c_double * 3)()
+        taus = (ctypes.c_float * 2)()
+        have = ctypes.c_int(0)
+        self._check(self._L.csc_iterate_drain(self._h, obj, taus, ctypes.byref(have)))
+        if not have.value:
+            return None
         return (float(obj[0]), float(obj[1]), float(obj[2])), (float(taus[0]), float(taus[1]))
 
     def invalidate(self):

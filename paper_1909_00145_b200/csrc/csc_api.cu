@@ -98,6 +98,13 @@ struct csc_ctx {
   float* fscal = nullptr;
   double* h_dscal = nullptr;   // pinned host mirrors
   float* h_fscal = nullptr;
+  // pipelined iterations (csc_iterate_staged_async): a ring of 2 pinned result slots and their events
+  double* h_res_d[2] = {nullptr, nullptr};
+  float* h_res_f[2] = {nullptr, nullptr};
+  cudaEvent_t res_ev[2] = {nullptr, nullptr};
+  float res_lam[2] = {0.f, 0.f};
+  int res_pending = -1;  // slot of the enqueued iteration whose results were not returned yet
+  int res_next = 0;
   // residual cache
   bool cache_valid = false;
   // L_D(d) and tau_z = 1/L_D of the filters last used (d changes only through the filter steps, which
@@ -761,6 +768,11 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->fscal);
   cudaFreeHost(c->h_dscal);
   cudaFreeHost(c->h_fscal);
+  for (int i = 0; i < 2; ++i) {
+    cudaFreeHost(c->h_res_d[i]);
+    cudaFreeHost(c->h_res_f[i]);
+    if (c->res_ev[i]) cudaEventDestroy(c->res_ev[i]);
+  }
   delete c;
   return CSC_OK;
 }
@@ -1419,7 +1431,7 @@ static csc_status iterate_impl(csc_ctx* c, const float* x_host, int slot, float*
   NvtxScope nvtx_scope(c, slot >= 0 ? "csc_iterate_staged" : "csc_iterate");
   csc_status s = check_ptrs(c, x, d, z);
   if (s != CSC_OK) return s;
-  if (!obj_out) return fail(c, CSC_ERR_ARG, "obj_out must be a host pointer to 3 doubles");
+  if (!obj_out && slot < 0) return fail(c, CSC_ERR_ARG, "obj_out must be a host pointer to 3 doubles");
   if (!(lambda >= 0.f) || !std::isfinite(lambda)) return fail(c, CSC_ERR_ARG, "lambda must be finite and >= 0");
   if (!(step_z >= 0.f) || !std::isfinite(step_z) || !(step_d >= 0.f) || !std::isfinite(step_d))
     return fail(c, CSC_ERR_ARG, "steps must be finite and >= 0");
@@ -1430,28 +1442,30 @@ static csc_status iterate_impl(csc_ctx* c, const float* x_host, int slot, float*
     // previous iteration's objective pass, or z = 0 -- move it to the new images without a dense
     // pass: r <- (r + x_old) - x_new (a3', linearity)
     const bool shift = c->cache_valid && c->cx == x && c->cz == z && (c->cd == d || c->cd == nullptr);
-    if (shift) CSC_LAUNCH(c, 1, csc::launch_resid_shift(x, c->r, n_pix(c->g), 1.f, c->st));
     if (slot >= 0) {
       // staged images (csc_stage_images): the H2D copy ran on the copy stream, overlapped with the
-      // previous iteration; wait for it and copy device to device
+      // previous iteration; wait for it, then one pass moves the residual and copies the images in
       CSC_CUDA(c, cudaStreamWaitEvent(c->st, c->st_ready[slot], 0));
-      CSC_CUDA(c, cudaMemcpyAsync(x, c->stage[slot], sizeof(float) * n_pix(c->g), cudaMemcpyDeviceToDevice, c->st));
+      CSC_LAUNCH(c, 1, csc::launch_stage_swap(c->stage[slot], x, c->r, n_pix(c->g), shift, c->st));
       CSC_CUDA(c, cudaEventRecord(c->st_free[slot], c->st));
       c->st_used[slot] = true;
       c->staged[slot] = false;
     } else {
+      if (shift) CSC_LAUNCH(c, 1, csc::launch_resid_shift(x, c->r, n_pix(c->g), 1.f, c->st));
       CSC_CUDA(c, cudaMemcpyAsync(x, x_host, sizeof(float) * n_pix(c->g), cudaMemcpyHostToDevice, c->st));
+      if (shift) CSC_LAUNCH(c, 1, csc::launch_resid_shift(x, c->r, n_pix(c->g), -1.f, c->st));
     }
-    if (shift) {
-      CSC_LAUNCH(c, 1, csc::launch_resid_shift(x, c->r, n_pix(c->g), -1.f, c->st));
-    } else {
-      c->cache_valid = false;
-    }
+    if (!shift) c->cache_valid = false;
   }
   s = csc_code_step(c, x, d, z, lambda, step_z, p, seed, iter, nullptr);
   if (s != CSC_OK) return s;
   s = csc_filter_step(c, x, d, z, step_d, nullptr);
   if (s != CSC_OK) return s;
+  if (!obj_out) {  // pipelined call (csc_iterate_staged_async): the objective pass only, no host read
+    s = dense_residual(c, x, d, z, true);
+    if (s != CSC_OK) return s;
+    return allreduce_d(c, c->dscal + kSqR, 2);
+  }
   s = objective_enqueue(c, x, d, z);
   if (s != CSC_OK) return s;
   s = objective_finish(c, lambda, obj_out);
@@ -1460,6 +1474,71 @@ static csc_status iterate_impl(csc_ctx* c, const float* x_host, int slot, float*
     taus_out[1] = c->h_fscal[kTauD];
   }
   return s;
+}
+
+// results of the pipelined slot k (its event has completed)
+static csc_status res_read(csc_ctx* c, int k, double obj[3], float taus[2]) {
+  CSC_CUDA(c, cudaEventSynchronize(c->res_ev[k]));
+  const double half = 0.5 * c->h_res_d[k][kSqR];
+  const double l1 = static_cast<double>(c->res_lam[k]) * c->h_res_d[k][kL1];
+  if (obj) {
+    obj[0] = half + l1;
+    obj[1] = half;
+    obj[2] = l1;
+  }
+  if (taus) {
+    taus[0] = c->h_res_f[k][kTauZ];
+    taus[1] = c->h_res_f[k][kTauD];
+  }
+  if (!std::isfinite(half + l1)) return fail(c, CSC_ERR_NONFINITE, "objective is not finite");
+  return CSC_OK;
+}
+
+csc_status csc_iterate_staged_async(csc_ctx* c, int slot, float* x, float* d, float* z, float lambda, float step_z,
+                                    float step_d, double p, uint64_t seed, uint32_t iter, double obj_prev[3],
+                                    float taus_prev[2], int* have_prev) {
+  if (!c || slot < 0 || slot > 1 || !c->staged[slot]) return fail(c, CSC_ERR_ARG, "slot not staged");
+  if (!have_prev) return fail(c, CSC_ERR_ARG, "have_prev must be a host pointer");
+  *have_prev = 0;
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  if (c->h_res_d[0] == nullptr) {
+    for (int i = 0; i < 2; ++i) {
+      CSC_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_res_d[i]), sizeof(double) * kNumD));
+      CSC_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_res_f[i]), sizeof(float) * kNumF));
+      CSC_CUDA(c, cudaEventCreateWithFlags(&c->res_ev[i], cudaEventDisableTiming));
+    }
+  }
+  const int k = c->res_next;
+  if (c->res_pending == k) return fail(c, CSC_ERR_ARG, "internal: result slot still pending");
+  double dummy[3];
+  (void)dummy;
+  csc_status s = iterate_impl(c, nullptr, slot, x, d, z, lambda, step_z, step_d, p, seed, iter, nullptr, nullptr);
+  if (s != CSC_OK) return s;
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_res_d[k], c->dscal, sizeof(double) * kNumD, cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_res_f[k], c->fscal, sizeof(float) * kNumF, cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaEventRecord(c->res_ev[k], c->st));
+  c->res_lam[k] = lambda;
+  const int prev = c->res_pending;
+  c->res_pending = k;
+  c->res_next = k ^ 1;
+  if (prev >= 0) {
+    s = res_read(c, prev, obj_prev, taus_prev);
+    if (s != CSC_OK) return s;
+    *have_prev = 1;
+  }
+  return CSC_OK;
+}
+
+csc_status csc_iterate_drain(csc_ctx* c, double obj[3], float taus[2], int* have) {
+  if (!c || !have) return fail(c, CSC_ERR_ARG, "have must be a host pointer");
+  *have = 0;
+  if (c->res_pending < 0) return CSC_OK;
+  const int k = c->res_pending;
+  c->res_pending = -1;
+  csc_status s = res_read(c, k, obj, taus);
+  if (s != CSC_OK) return s;
+  *have = 1;
+  return CSC_OK;
 }
 
 csc_status csc_mask_bits(csc_ctx* c, uint32_t iter, double p, uint64_t seed, uint32_t* bits_dev) {

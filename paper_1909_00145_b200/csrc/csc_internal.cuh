@@ -128,6 +128,8 @@ cudaError_t launch_neg_copy(const float* x, float* r, int64_t n, cudaStream_t st
 // r += sign * x
 cudaError_t launch_count_nonzero(const float* v, int64_t n, uint64_t* out, cudaStream_t st);
 cudaError_t launch_resid_shift(const float* x, float* r, int64_t n, float sign, cudaStream_t st);
+// x <- xn and, when shift, r <- (r + x_old) - xn in one pass (csc_iterate_staged)
+cudaError_t launch_stage_swap(const float* xn, float* x, float* r, int64_t n, bool shift, cudaStream_t st);
 
 // ---- tensor-core (tcgen05, 3xTF32) dense pass, csc_tc.cu
 constexpr int kTcMaxKC = 104;  // filters per k-split held resident in shared memory

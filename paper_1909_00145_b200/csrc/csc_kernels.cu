@@ -999,6 +999,44 @@ cudaError_t launch_count_nonzero(const float* v, int64_t n, uint64_t* out, cudaS
   return cudaGetLastError();
 }
 
+// new images from a staging buffer with the residual moved along (csc_iterate_staged): r += x_old - x_new,
+// x <- x_new in one pass (float4 when every pointer is 16-B aligned and n % 4 == 0)
+__global__ void stage_swap_kernel(const float* __restrict__ xn, float* __restrict__ x, float* __restrict__ r,
+                                  int64_t n, int shift, int vec) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (vec) {
+    const float4* xn4 = reinterpret_cast<const float4*>(xn);
+    float4* x4 = reinterpret_cast<float4*>(x);
+    float4* r4 = reinterpret_cast<float4*>(r);
+    for (int64_t i = t0; i < n / 4; i += stride) {
+      const float4 a = xn4[i];
+      if (shift) {
+        const float4 o = x4[i];
+        float4 rv = r4[i];
+        rv.x = (rv.x + o.x) - a.x; rv.y = (rv.y + o.y) - a.y; rv.z = (rv.z + o.z) - a.z; rv.w = (rv.w + o.w) - a.w;
+        r4[i] = rv;
+      }
+      x4[i] = a;
+    }
+    return;
+  }
+  for (int64_t i = t0; i < n; i += stride) {
+    const float a = xn[i];
+    if (shift) r[i] = (r[i] + x[i]) - a;
+    x[i] = a;
+  }
+}
+
+cudaError_t launch_stage_swap(const float* xn, float* x, float* r, int64_t n, bool shift, cudaStream_t st) {
+  const int vec = ((reinterpret_cast<uintptr_t>(xn) | reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r)) & 15u) == 0 &&
+                          n % 4 == 0
+                      ? 1
+                      : 0;
+  stage_swap_kernel<<<kFinalizeBlocks, 256, 0, st>>>(xn, x, r, n, shift ? 1 : 0, vec);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_resid_shift(const float* x, float* r, int64_t n, float sign, cudaStream_t st) {
   axpy_sign_kernel<<<kFinalizeBlocks, 256, 0, st>>>(x, r, n, sign);
   return cudaGetLastError();

@@ -476,3 +476,53 @@ def test_iterate_staged_double_buffered(torch_dev):
         assert rel_err(dt.cpu().numpy(), d) < TOL, t
         assert abs(F[0] - it["F"][0]) <= TOL * abs(it["F"][0]), t
     ctx.close()
+
+
+def test_iterate_staged_async_pipelined(torch_dev):
+    """csc_iterate_staged_async returns the previous iteration's objective and step sizes while the next
+    one is queued; csc_iterate_drain returns the last.  Same kernels as csc_iterate_staged: the sequence
+    of (F, tau_z, tau_d), the codes and the filters are bit-identical to the synchronous calls, and the
+    objectives match the oracle."""
+    import torch
+    cfg = CONFIGS["tiny"]
+    p, lam, steps = 0.5, cfg.lam, 6
+    seed = mask_seed(cfg)
+    batches = [np.ascontiguousarray(make_images(cfg) * (1.0 + 0.2 * t)).astype(np.float32) for t in range(steps)]
+    hosts = [torch.from_numpy(b).pin_memory() for b in batches]
+
+    def run(use_async):
+        ctx = _ctx(cfg.N, cfg.K, cfg.s, cfg.H, cfg.W)
+        xt = _t(make_images(cfg), torch_dev)
+        dt, zt = _t(make_filters(cfg), torch_dev), _t(make_codes(cfg), torch_dev)
+        out = []
+        ctx.stage_images(hosts[0], 0)
+        for t in range(steps):
+            if t + 1 < steps:
+                ctx.stage_images(hosts[t + 1], (t + 1) % 2)
+            if use_async:
+                r = ctx.iterate_staged_async(xt, dt, zt, lam, p, seed, t + 1, t % 2)
+                assert (r is None) == (t == 0)
+                if r is not None:
+                    out.append(r)
+            else:
+                out.append(ctx.iterate_staged(xt, dt, zt, lam, p, seed, t + 1, t % 2))
+        if use_async:
+            r = ctx.iterate_drain()
+            assert r is not None
+            out.append(r)
+            assert ctx.iterate_drain() is None
+        torch.cuda.synchronize()
+        res = (out, zt.cpu().numpy(), dt.cpu().numpy())
+        ctx.close()
+        return res
+
+    sync_out, zs, ds = run(False)
+    async_out, za, da = run(True)
+    assert len(async_out) == steps
+    assert async_out == sync_out
+    assert np.array_equal(za, zs) and np.array_equal(da, ds)
+    d, z = make_filters(cfg), make_codes(cfg)
+    for t in range(steps):
+        it = oracle.iteration(batches[t], d, z, lam, p, seed, t + 1)
+        z, d = it["z"], it["d"]
+        assert abs(async_out[t][0][0] - it["F"][0]) <= TOL * abs(it["F"][0]), t
