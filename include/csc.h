@@ -234,6 +234,15 @@ csc_status csc_iterate_staged_async(csc_ctx* ctx, int slot, float* x, float* d, 
                                     double obj_prev[3], float taus_prev[2], int* have_prev);
 csc_status csc_iterate_drain(csc_ctx* ctx, double obj[3], float taus[2], int* have);
 
+/* The image half of csc_iterate_staged on its own, for CUDA-graph capture of a streaming step: enqueues
+ * on the library stream a wait for the slot's latest csc_stage_images copy, x <- the slot's images and,
+ * when the residual cache holds D z - x for this x, r <- r + x_old - x_new (no dense pass); then marks
+ * the slot free.  Inside a capture the wait and the mark are external event nodes, so each replay
+ * follows the slot's most recent staging.  Follow with csc_code_step / csc_filter_step /
+ * csc_objective_enqueue (the mask iteration through csc_set_iter_offset).  CSC_ERR_ARG for a slot
+ * that was never staged. */
+csc_status csc_load_staged(csc_ctx* ctx, int slot, float* x);
+
 /* Forget the residual cache (caller changed x, d or z outside the API). */
 csc_status csc_invalidate(csc_ctx* ctx);
 

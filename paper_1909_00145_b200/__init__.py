@@ -34,7 +34,7 @@ ABI_SYMBOLS = (
     "csc_stage_images", "csc_iterate_staged", "csc_mask_selwords", "csc_read_scalars", "csc_zg_sumsq",
     "csc_set_iter_offset", "csc_count_nonzero", "csc_set_nvtx", "csc_comm_check", "csc_profile_set_classes",
     "csc_objective_enqueue", "csc_objective_read", "csc_profile_sample", "csc_iterate_staged_async",
-    "csc_iterate_drain",
+    "csc_iterate_drain", "csc_load_staged",
 )
 
 # csc_kernel_class (include/csc.h)
@@ -80,6 +80,7 @@ def load_library(path: Optional[str] = None):
         L.csc_iterate_staged.argtypes = [vp, ctypes.c_int, vp, vp, vp, f32, f32, f32, f64, u64, u32, vp, vp]
         L.csc_iterate_staged_async.argtypes = [vp, ctypes.c_int, vp, vp, vp, f32, f32, f32, f64, u64, u32, vp, vp, vp]
         L.csc_iterate_drain.argtypes = [vp, vp, vp, vp]
+        L.csc_load_staged.argtypes = [vp, ctypes.c_int, vp]
         L.csc_filter_step_bcd.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
         L.csc_surrogate_reset.argtypes = [vp]
         L.csc_surrogate_update.argtypes = [vp, vp, vp]
@@ -331,6 +332,12 @@ class Context:
         if not have.value:
             return None
         return (float(obj[0]), float(obj[1]), float(obj[2])), (float(taus[0]), float(taus[1]))
+
+    def load_staged(self, x, slot: int):
+        """Enqueue the images of a staged slot into x (and move the residual cache), capturable
+        (include/csc.h csc_load_staged)."""
+        self._check(self._L.csc_load_staged(self._h, int(slot),
+                                            _ptr(x, "x", self.n_local * self.H * self.W) if self.n_local else 0))
 
     def iterate_drain(self):
         """The results of the last csc_iterate_staged_async call (include/csc.h csc_iterate_drain), or None."""

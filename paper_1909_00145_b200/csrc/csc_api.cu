@@ -1413,6 +1413,25 @@ static csc_status iterate_impl(csc_ctx* c, const float* x_host, int slot, float*
                                float step_z, float step_d, double p, uint64_t seed, uint32_t iter, double obj_out[3],
                                float taus_out[2]);
 
+csc_status csc_load_staged(csc_ctx* c, int slot, float* x) {
+  if (!c || slot < 0 || slot > 1 || c->stage[slot] == nullptr) return fail(c, CSC_ERR_ARG, "slot never staged");
+  if (c->g.N > 0 && !aligned4(x)) return fail(c, CSC_ERR_ARG, "x must be a device pointer");
+  CSC_CUDA(c, cudaSetDevice(c->device));
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CSC_CUDA(c, cudaStreamIsCapturing(c->st, &cs));
+  const bool cap = cs == cudaStreamCaptureStatusActive;
+  // inside a capture the events become external wait / record nodes: every replay waits for the slot's
+  // latest copy and marks the slot free for csc_stage_images
+  CSC_CUDA(c, cudaStreamWaitEvent(c->st, c->st_ready[slot], cap ? cudaEventWaitExternal : 0));
+  const bool shift = c->cache_valid && c->cx == x && c->cz != nullptr;
+  if (c->g.N > 0) CSC_LAUNCH(c, 1, csc::launch_stage_swap(c->stage[slot], x, c->r, n_pix(c->g), shift, c->st));
+  CSC_CUDA(c, cudaEventRecordWithFlags(c->st_free[slot], c->st, cap ? cudaEventRecordExternal : 0));
+  c->st_used[slot] = true;
+  c->staged[slot] = false;
+  if (!shift) c->cache_valid = false;
+  return CSC_OK;
+}
+
 csc_status csc_iterate_staged(csc_ctx* c, int slot, float* x, float* d, float* z, float lambda, float step_z,
                               float step_d, double p, uint64_t seed, uint32_t iter, double obj_out[3],
                               float taus_out[2]) {
