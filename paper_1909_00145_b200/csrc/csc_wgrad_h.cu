@@ -36,9 +36,6 @@
 #include <cstring>
 #include <cuda_runtime.h>
 
-#ifndef CSC_WH_CONV_ILP
-#define CSC_WH_CONV_ILP 1  // converters: all row loads of a chunk issued before the conversions
-#endif
 #ifndef CSC_Z_EVICT_FIRST
 #define CSC_Z_EVICT_FIRST 1  // stream z through L2 evict-first (tcx::tma_load_2d_hint): 0.390 -> 0.378 ms
 #endif
@@ -302,28 +299,6 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
         const uint8_t* rp = rawst + slot * rawbytes + (lane & 15) * 16;
         uint8_t* hip = bst + bs * 2 * bbytes + half8;
         uint8_t* lop = hip + bbytes;
-#if CSC_WH_CONV_ILP
-        // every row pair of this warp loaded first (KC <= 112: at most 6 per warp), then converted
-        constexpr int kMaxIt = (56 + kWhZWarps - 1) / kWhZWarps;
-        float4 xs[kMaxIt];
-#pragma unroll
-        for (int i = 0; i < kMaxIt; ++i) {
-          const int k = 2 * (zw + i * kWhZWarps) + (lane >> 4);
-          xs[i] = k < A.KC ? *reinterpret_cast<const float4*>(rp + k * 256) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int i = 0; i < kMaxIt; ++i) {
-          const int k = 2 * (zw + i * kWhZWarps) + (lane >> 4);
-          if (k < A.KC) {
-            uint2 hv, lv;
-            split2(xs[i].x, xs[i].y, hv.x, lv.x);
-            split2(xs[i].z, xs[i].w, hv.y, lv.y);
-            const int off = k * 128 + ((cidx ^ (k & 7)) << 4);
-            *reinterpret_cast<uint2*>(hip + off) = hv;
-            *reinterpret_cast<uint2*>(lop + off) = lv;
-          }
-        }
-#else
 #pragma unroll 3
         for (int pr = zw; pr < npairs; pr += kWhZWarps) {
           const int k = 2 * pr + (lane >> 4);
@@ -337,7 +312,6 @@ wgrad_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const WhArgs A) {
             *reinterpret_cast<uint2*>(lop + off) = lv;
           }
         }
-#endif
         fence_async_shared();  // generic writes before the MMA's async-proxy reads; raw reads before the refill
         __syncwarp();
         if (lane == 0) {
