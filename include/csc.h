@@ -25,12 +25,14 @@
  * (tests/test_gpu_graph.py).  The residual-cache decisions are taken on the host while
  * capturing, so a captured sequence must be replayed from the state it was captured in (e.g.
  * a SOCSC step: zero codes, code steps, filter step; or a whole iteration with
- * csc_objective_enqueue).  csc_objective, csc_iterate and any call with a host output synchronise
- * and are not capturable; csc_code_step_admm, the BCD and
- * surrogate updates and csc_stage_images allocate on first use.
+ * csc_objective_enqueue; or a streaming step with csc_load_staged in front).  csc_objective,
+ * csc_iterate and any call with a host output synchronise and are not capturable;
+ * csc_code_step_admm, the BCD and surrogate updates, csc_stage_images and
+ * csc_iterate_staged_async allocate on first use.
  *
  * ASYNCHRONY: everything is enqueued on dims.stream (a cudaStream_t).  Only
- * csc_objective, csc_iterate and a non-NULL step_used pointer synchronise.
+ * csc_objective, csc_iterate(_staged), csc_objective_read, csc_iterate_drain and a non-NULL
+ * step_used pointer synchronise; csc_iterate_staged_async waits for the PREVIOUS iteration only.
  *
  * COLLECTIVES (world > 1): every rank must call csc_filter_step, csc_objective
  * and csc_iterate in the same order; csc_code_step is rank-local.  The mask is a
