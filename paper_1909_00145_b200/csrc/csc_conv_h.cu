@@ -296,6 +296,7 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t) {
         const int pt = it.p0 + 128 * t;
+        const bool tile_full = pt + 128 <= it.pend;
         for (int c = 0; c < A.NCH; ++c, ++g) {
           if (static_cast<int>(g % kHNS) != (cw >> 1)) continue;
           const uint32_t slot = g % kHNS, ph = (g / kHNS) & 1u;      // hi / lo slot
@@ -328,11 +329,15 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
             *reinterpret_cast<uint2*>(lop + off) = make_uint2(pack_h2(a0 - h0, a1 - h1), pack_h2(a2 - h2, a3 - h3));
 #endif
             if (want_l1) {
-              const int kk = A.ks * A.KC + 16 * c + k;
-              const int p = pt + 4 * lane;
+              const int kk = A.ks * A.KC + 16 * c + k;  // warp-uniform: padded filter rows add nothing
               if (kk < A.K) {
-                s1 += (p < it.pend ? fabsf(x0.x) : 0.f) + (p + 1 < it.pend ? fabsf(x0.y) : 0.f) +
-                      (p + 2 < it.pend ? fabsf(x0.z) : 0.f) + (p + 3 < it.pend ? fabsf(x0.w) : 0.f);
+                if (tile_full) {  // every position of the tile is in the item: no per-value test
+                  s1 += (fabsf(x0.x) + fabsf(x0.y)) + (fabsf(x0.z) + fabsf(x0.w));
+                } else {
+                  const int p = pt + 4 * lane;
+                  s1 += (p < it.pend ? fabsf(x0.x) : 0.f) + (p + 1 < it.pend ? fabsf(x0.y) : 0.f) +
+                        (p + 2 < it.pend ? fabsf(x0.z) : 0.f) + (p + 3 < it.pend ? fabsf(x0.w) : 0.f);
+                }
               }
             }
           }
