@@ -177,12 +177,15 @@ def test_code_step_parity(torch_dev, shape, p, path, monkeypatch):
 
 @pytest.mark.parametrize("wg", ["h", "tf32", "simt"])
 @pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (1, 3, 3, 9, 9), (2, 130, 5, 36, 40),
-                                   (1, 8, 7, 26, 22), (2, 40, 11, 256, 56), (5, 24, 9, 48, 63), (1, 100, 11, 12, 300)])
+                                   (1, 8, 7, 26, 22), (2, 40, 11, 256, 56), (5, 24, 9, 48, 63), (1, 100, 11, 12, 300),
+                                   (2, 400, 11, 20, 30), (1, 1024, 11, 12, 14), (3, 9, 3, 18, 22), (2, 33, 5, 41, 60)])
 def test_filter_step_parity(torch_dev, shape, wg, monkeypatch):
     """Filter gradient g = Z^T r (tcgen05 kind::f16 3-term split kernel "h", the 3xTF32 kernel, or SIMT),
     exact line search, projection.
-    Shapes cover several k-groups (K=130), one partial chunk per row (Wc < 32), many bands,
-    rows of 9-10 chunks, and Hc*Wc % 4 != 0 (TMA view impossible: SIMT path either way)."""
+    Shapes cover several k-groups (K=130; K=400: four groups; K=1024: ten groups of 103 filters padded to
+    112), one partial chunk per row (Wc < 32), chunks spanning rows (Wc < 64; odd Wc), a row of exactly
+    one 64-position chunk, many bands, rows of 9-10 chunks, and Hc*Wc % 4 != 0 (TMA view impossible:
+    SIMT path either way)."""
     import torch
     monkeypatch.setenv("CSC_WGRAD_PATH", wg)
     N, K, s, H, W = shape
