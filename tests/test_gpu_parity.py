@@ -66,7 +66,7 @@ def test_lipschitz_parity(torch_dev):
 @pytest.mark.parametrize("conv", ["half", "ss", "tmem"])
 @pytest.mark.parametrize("shape", [(3, 5, 5, 70, 130), (2, 17, 11, 100, 100), (4, 8, 5, 32, 32),
                                    (1, 3, 1, 9, 65), (2, 6, 3, 129, 64), (1, 2, 9, 9, 9), (2, 130, 7, 41, 61),
-                                   (1, 100, 11, 150, 40)])
+                                   (1, 100, 11, 150, 40), (2, 400, 11, 20, 30), (1, 1024, 11, 12, 14)])
 def test_residual_and_objective_parity(torch_dev, shape, conv, monkeypatch):
     """Dense pass r = Dz - x and the Eq.1 objective: TMA-fed SS tensor-core kernel (default where
     Hc*Wc % 4 == 0), TMEM-fed kernel, or SIMT (s < 5, W+s-1 < 32).  Shapes: k-splits (K=130),
@@ -138,7 +138,8 @@ def test_mask_selwords_bit_exact(torch_dev, K, s, H, W, p, mode):
 @pytest.mark.parametrize("path", ["half", "tc", "simt"])
 @pytest.mark.parametrize("shape,p", [((3, 5, 5, 70, 130), 0.1), ((2, 17, 11, 100, 100), 0.2),
                                      ((4, 8, 5, 32, 32), 1.0), ((1, 9, 3, 33, 47), 0.5), ((2, 4, 11, 11, 11), 0.05),
-                                     ((2, 130, 7, 20, 300), 0.1), ((1, 100, 11, 40, 11), 0.3), ((3, 16, 9, 61, 9), 1.0)])
+                                     ((2, 130, 7, 20, 300), 0.1), ((1, 100, 11, 40, 11), 0.3), ((3, 16, 9, 61, 9), 1.0),
+                                     ((2, 400, 11, 20, 30), 0.1), ((1, 1024, 11, 12, 14), 0.1)])
 def test_code_step_parity(torch_dev, shape, p, path, monkeypatch):
     """Masked prox-gradient code step: tcgen05 dense-then-mask kernel or SIMT.  Shapes: several
     k-groups (K=130), tiles that wrap many short rows (Wc=21, 17), ragged plane tails, p=1 shortcut."""
