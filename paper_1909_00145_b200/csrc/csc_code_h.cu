@@ -221,13 +221,18 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFullMask, m, o));
     if (lane == 0) atomicMax(&dmax_sh, m);
     if (!plain) {
-      for (int k = tid; k < A.KC; k += kChThreads) {  // one thread per filter (fp32 sums: a bound only)
+      // one warp per filter: lanes sum strided taps, a shuffle tree finishes (fp32 sums: a bound only)
+      for (int k = warp; k < A.KC; k += kChWarps) {
         const int kk = kg * A.KC + k;
         if (kk >= A.K) break;
         float l1 = 0.f;
-        for (int t = 0; t < S2; ++t) l1 += fabsf(A.d[static_cast<size_t>(kk) * S2 + t]);
-        atomicMax(&dl1_sh, __float_as_uint(l1 * 1.0001f));
-        atomicMax(&tmax_sh, __float_as_uint(fabsf(A.tau[A.tau_stride ? kk : 0])));
+        for (int t = lane; t < S2; t += 32) l1 += fabsf(A.d[static_cast<size_t>(kk) * S2 + t]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(kFullMask, l1, o);
+        if (lane == 0) {
+          atomicMax(&dl1_sh, __float_as_uint(l1 * 1.0001f));
+          atomicMax(&tmax_sh, __float_as_uint(fabsf(A.tau[A.tau_stride ? kk : 0])));
+        }
       }
     }
   }
