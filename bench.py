@@ -548,11 +548,12 @@ def run_ours(args):
         if l2_flush is not None:
             l2_flush.fill_(float(it))
         if staged:
-            if i + 1 < args.steps:
-                ctx.stage_images(x_host, (i + 1) % 2)
-            # pipelined: enqueue this step, read the previous step's objective (80 B D2H per step)
+            # pipelined: enqueue this step, read the previous step's objective (80 B D2H per step), then start
+            # the next step's upload (it overlaps this step)
             if ctx.iterate_staged_async(x, d, z, cfg.lam, cfg.p, seed, it, i % 2) is not None:
                 n_obj += 1
+            if i + 1 < args.steps:
+                ctx.stage_images(x_host, (i + 1) % 2)
         else:
             step(it, x_host=x_host)
     if staged:
