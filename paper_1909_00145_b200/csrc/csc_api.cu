@@ -119,6 +119,7 @@ struct csc_ctx {
   bool tc_on = false;
   csc::TcPlan tc{};
   float* tc_part = nullptr;
+  int* tc_sched = nullptr;  // conv_h: the balanced item schedule (c->tc.sched points here)
   float* tc_bimg = nullptr;
   // fp16-split dense pass: scale bounds (float bits): [0] = bound of max|z|, [1] = max|filter|
   uint32_t* smax = nullptr;
@@ -595,6 +596,13 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
       if (!planned) c->tc = csc::conv_tc_plan(g, prop.multiProcessorCount);
       c->tc_on = true;
       ok = ok && alloc(reinterpret_cast<void**>(&c->tc_part), sizeof(float) * c->tc.part_floats);
+      if (ok && c->tc.half) {
+        std::vector<int> sched;
+        csc::conv_h_schedule(g, c->tc, sched);
+        ok = alloc(reinterpret_cast<void**>(&c->tc_sched), sizeof(int) * sched.size()) &&
+             cudaMemcpy(c->tc_sched, sched.data(), sizeof(int) * sched.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+        c->tc.sched = c->tc_sched;
+      }
       ok = ok && alloc(reinterpret_cast<void**>(&c->tc_bimg), sizeof(float) * c->tc.bimg_floats);
       ok = ok && alloc(reinterpret_cast<void**>(&c->smax), sizeof(uint32_t) * 2);
       const int need = c->tc.nks * c->tc.grid;
@@ -762,6 +770,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->adm_vec);
   cudaFree(c->lip_part);
   cudaFree(c->tc_part);
+  cudaFree(c->tc_sched);
   cudaFree(c->tc_bimg);
   cudaFree(c->smax);
   cudaFree(c->dscal);

@@ -32,7 +32,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <queue>
 #include <type_traits>
+#include <utility>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace csc {
@@ -110,6 +114,7 @@ struct HArgs {
   int KC, NCH, NT, ks;       // NCH = KC / 16
   int BR, nbands, nitems, WL;
   int precise;  // 1: hi*hi and the cross terms in separate TMEM accumulators (the ||Zg||^2 pass, reading T3)
+  const int* sched;  // [grid + 1] CTA offsets, then [nitems] items (conv_h_schedule); nullptr: round robin
   unsigned long long* dbg;  // CSC_ROLE_TIMING builds: per-CTA role cycle counters [grid][16]
 };
 
@@ -126,6 +131,21 @@ __device__ __forceinline__ HItem h_item(const HArgs& A, int item) {
   it.pend = it.u1 * A.Wc;
   it.ntiles = (it.pend - it.p0 + 127) / 128;
   return it;
+}
+
+// the items of this CTA: positions j in [j0, j1) of its list (the balanced schedule of conv_h_schedule, or
+// blockIdx.x + j * gridDim.x without one)
+__device__ __forceinline__ void h_range(const HArgs& A, int& j0, int& j1) {
+  if (A.sched != nullptr) {
+    j0 = A.sched[blockIdx.x];
+    j1 = A.sched[blockIdx.x + 1];
+  } else {
+    j0 = 0;
+    j1 = A.nitems > static_cast<int>(blockIdx.x) ? (A.nitems - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1 : 0;
+  }
+}
+__device__ __forceinline__ int h_item_at(const HArgs& A, int j) {
+  return A.sched != nullptr ? A.sched[gridDim.x + 1 + j] : static_cast<int>(blockIdx.x) + j * gridDim.x;
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -185,6 +205,8 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
   __syncthreads();
   tc_after();
   const uint32_t tbase = __shfl_sync(kFullMask, tmem_base_sh, 0);
+  int j0, j1;
+  h_range(A, j0, j1);
 
   if (warp == 0) {
     // ================================ MMA issuer
@@ -193,7 +215,8 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     const uint32_t sbh = su32(bsm), sbl = su32(bsm + bbytes), sst = su32(hls);
     uint32_t g = 0, tcount = 0;
     unsigned long long t0 = HT_NOW(), w_ae = 0, w_rd = 0;
-    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+    for (int j = j0; j < j1; ++j) {
+      const int item = h_item_at(A, j);
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
@@ -249,7 +272,8 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
 #if CSC_Z_EVICT_FIRST
       const uint64_t zpol = l2_policy_evict_first();
 #endif
-      for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+      for (int j = j0; j < j1; ++j) {
+        const int item = h_item_at(A, j);
         const HItem it = h_item(A, item);
         const int plane0 = it.n * A.K + A.ks * A.KC;
         for (int t = 0; t < it.ntiles; ++t) {
@@ -292,7 +316,8 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
       lv = *reinterpret_cast<const uint32_t*>(&lh);
     };
     (void)split2;
-    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+    for (int j = j0; j < j1; ++j) {
+      const int item = h_item_at(A, j);
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t) {
         const int pt = it.p0 + 128 * t;
@@ -372,7 +397,8 @@ conv_h_kernel(const __grid_constant__ CUtensorMap tmap_z, const HArgs A) {
     const int myph = nph == 1 ? 0 : (nph == 4 ? q : kHEpiGroups * q + h);
     uint32_t tcount = 0;
     unsigned long long e_t0 = HT_NOW(), e_wa = 0, e_red = 0, e_win = 0, e_fl = 0;
-    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+    for (int j = j0; j < j1; ++j) {
+      const int item = h_item_at(A, j);
       const HItem it = h_item(A, item);
       for (int t = 0; t < it.ntiles; ++t, ++tcount) {
         const uint32_t buf = tcount & 1u, use = tcount >> 1;
@@ -607,16 +633,54 @@ bool conv_h_supported(const Geom& g) {
          (static_cast<int64_t>(g.Hc) * g.Wc) % 4 == 0 && tc_ntaps_padded(g.S) <= 128 && tmap_available();
 }
 
+// Longest-processing-time-first assignment of the items (image, band of BR code rows; cost = its 128-position
+// tiles + one for the band's window flush) to the G persistent CTAs: each item in decreasing cost goes to the
+// least-loaded CTA (ties: lowest index).  Writes [G + 1] CTA offsets, then the items CTA by CTA (in the order
+// assigned), and returns the largest CTA load in tiles.  Round robin (item = CTA + j * G) leaves the CTA
+// with one item more than the others idle-free while the rest wait: at config 3 with BR = 8 the busiest CTA
+// had 170 tiles against a mean of 153.
+static int64_t conv_h_lpt(const Geom& g, int BR, int G, std::vector<int>* out) {
+  const int nb = ceil_div(g.Hc, BR);
+  const int nitems = g.N * nb;
+  std::vector<int64_t> cost(nb);
+  for (int b = 0; b < nb; ++b) {
+    const int u0 = b * BR, u1 = std::min(u0 + BR, g.Hc);
+    cost[b] = ceil_div((u1 - u0) * g.Wc, 128) + 1;
+  }
+  // stable order of decreasing cost (items of one cost keep their image-major order)
+  std::vector<int> order(nitems);
+  for (int i = 0; i < nitems; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a % nb] > cost[b % nb]; });
+  using E = std::pair<int64_t, int>;
+  std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+  for (int c = 0; c < G; ++c) pq.push(E(0, c));
+  std::vector<std::vector<int>> per(out ? G : 0);
+  int64_t mx = 0;
+  for (int i : order) {
+    E e = pq.top();
+    pq.pop();
+    e.first += cost[i % nb];
+    mx = std::max(mx, e.first);
+    if (out) per[e.second].push_back(i);
+    pq.push(e);
+  }
+  if (out) {
+    out->assign(G + 1 + nitems, 0);
+    int j = 0;
+    for (int c = 0; c < G; ++c) {
+      (*out)[c] = j;
+      for (int i : per[c]) (*out)[G + 1 + j++] = i;
+    }
+    (*out)[G] = j;
+  }
+  return mx;
+}
+
 bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p) {
   p = TcPlan{};
   p.NT = 128;  // taps padded to 2 atoms of 64
   p.natoms = 2;
   const int stages = kHRingBytes;
-  const int n = g.N > 0 ? g.N : 1;
-  int BR = (g.Hc * n) / (6 * num_sms);
-  BR = (BR / 4) * 4;
-  if (BR < 4) BR = 4;
-  if (BR > 32) BR = 32;
   auto wl = [&](int br) { return (br + g.P) * g.Wc + 192; };
   int kc_fit = (kHSmemMax - 2048 - stages - wl(4) * 4) / (2 * 2 * 128);
   kc_fit = kc_fit / 16 * 16;
@@ -626,8 +690,25 @@ bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p) {
   p.KC = (ceil_div(g.K, p.nks) + 15) / 16 * 16;
   p.NCH = p.KC / 16;
   const int bsm = 2 * 2 * p.KC * 128;
-  while (BR > 4 && 2048 + bsm + stages + wl(BR) * 4 > kHSmemMax) BR -= 4;
-  if (2048 + bsm + stages + wl(BR) * 4 > kHSmemMax) return false;
+  // band height: every BR that fits (BR * Wc % 4 == 0: 16-B aligned TMA box starts), the smallest busiest-CTA
+  // load under the LPT schedule; on ties the taller band (fewer halo rows in the partials the fixup reads)
+  const int G = std::max(1, std::min(num_sms, g.N * ceil_div(g.Hc, 4)));
+  int BR = 0;
+  int64_t best = 0;
+  for (int br = 1; br <= 32 && br <= std::max(g.Hc, 4); ++br) {
+    if ((static_cast<int64_t>(br) * g.Wc) % 4 != 0) continue;
+    if (2048 + bsm + stages + wl(br) * 4 > kHSmemMax) break;
+    if (g.N <= 0) {
+      BR = br;
+      continue;
+    }
+    const int64_t c = conv_h_lpt(g, br, std::min(G, g.N * ceil_div(g.Hc, br)), nullptr);
+    if (BR == 0 || c <= best) {
+      BR = br;
+      best = c;
+    }
+  }
+  if (BR == 0) return false;
   p.BR = BR;
   p.WL = wl(BR);
   p.nbands = ceil_div(g.Hc, BR);
@@ -640,6 +721,14 @@ bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p) {
   p.ss = false;
   p.half = true;
   return true;
+}
+
+void conv_h_schedule(const Geom& g, const TcPlan& p, std::vector<int>& out) {
+  if (g.N <= 0 || p.nitems <= 0) {
+    out.assign(p.grid + 1, 0);
+    return;
+  }
+  conv_h_lpt(g, p.BR, p.grid, &out);
 }
 
 cudaError_t launch_absmax(const float* x, int64_t n, uint32_t* out, cudaStream_t st) {
@@ -672,6 +761,7 @@ cudaError_t launch_conv_h(const Geom& g, const TcPlan& p, TmapCache* tmc, const 
   a.KC = p.KC; a.NCH = p.NCH; a.NT = p.NT;
   a.BR = p.BR; a.nbands = p.nbands; a.nitems = p.nitems; a.WL = p.WL;
   a.precise = precise ? 1 : 0;
+  a.sched = p.sched;
   for (int ks = 0; ks < p.nks; ++ks) {
     a.ks = ks;
     switch (g.S) {

@@ -2,6 +2,7 @@
 // and the sm_100a kernels (csc_kernels.cu).  Not part of the public ABI.
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -139,6 +140,7 @@ struct TcPlan {
   int WL;    // SS kernels: band window length (floats)
   bool ss;   // true: the TMA-fed SS kernel (csc_conv_ss.cu) runs this plan
   bool half; // true: the fp16-split SS kernel (csc_conv_h.cu) runs this plan
+  const int* sched = nullptr;  // half: device copy of conv_h_schedule (owned by the context), or round robin
 };
 int tc_ntaps_padded(int S);
 // filter taps -> B image bimg[nks][hi|lo][natoms][KC][32] (MN-major SWIZZLE_128B_BASE32B)
@@ -152,6 +154,8 @@ cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, TmapCache* tmc, const
 // (float bits, device); fmax: written with max|filt| (float bits, device).
 bool conv_h_supported(const Geom& g);
 bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p);
+// the balanced item schedule of a conv_h plan: [grid + 1] CTA offsets, then the items CTA by CTA
+void conv_h_schedule(const Geom& g, const TcPlan& p, std::vector<int>& out);
 // build_b = false reuses the fp16 filter image (and fmax) of the previous call with the same filt.
 // precise: hi*hi and the cross products accumulate in separate TMEM accumulators (the ||Zg||^2 pass,
 // DESIGN.md reading T3).  tmc: the context's cached tensor map of z.

@@ -570,9 +570,25 @@ __global__ void tc_fixup_kernel(const float* __restrict__ part, int N, int H, in
   }
 }
 
-// The fixup's reductions in its last block (one launch less per dense pass): the block sums of r^2 in
-// block order -> *out_sq, and the ||z||_1 partials of the dense pass (if any) in order -> *out_l1; the
-// block counter (zero at allocation) is cleared for the next launch.
+// The fixup's reductions in its last block (one launch less per dense pass): the block sums of r^2 ->
+// *out_sq, and the ||z||_1 partials of the dense pass (if any) -> *out_l1, each in a fixed order (thread t
+// sums partials t, t + blockDim, ... in turn, then the block's tree; deterministic, and the last block no
+// longer walks the 592 partials one dependent L2 load at a time); the block counter (zero at allocation)
+// is cleared for the next launch.
+__device__ double block_sum_fixed(const double* v, int n) {
+  __shared__ double red[32];
+  double t = 0.0;
+  for (int b = threadIdx.x; b < n; b += blockDim.x) t += __ldcg(v + b);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFullMask, t, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w];
+  return s;
+}
+
 __device__ void fixup_finish(const double* sq_part, const FixupSums& fs) {
   __shared__ bool last;
   __syncthreads();
@@ -581,17 +597,15 @@ __device__ void fixup_finish(const double* sq_part, const FixupSums& fs) {
     last = atomicAdd(fs.counter, 1ull) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
-  double t = 0.0;
-  for (int b = 0; b < static_cast<int>(gridDim.x); ++b) t += __ldcg(sq_part + b);
-  *fs.out_sq = t;
+  const double t = block_sum_fixed(sq_part, static_cast<int>(gridDim.x));
+  if (threadIdx.x == 0) *fs.out_sq = t;
   if (fs.l1_part != nullptr) {
-    double u = 0.0;
-    for (int b = 0; b < fs.nl1; ++b) u += __ldcg(fs.l1_part + b);
-    *fs.out_l1 = u;
+    const double u = block_sum_fixed(fs.l1_part, fs.nl1);
+    if (threadIdx.x == 0) *fs.out_l1 = u;
   }
-  *fs.counter = 0ull;
+  if (threadIdx.x == 0) *fs.counter = 0ull;
 }
 
 // Same as tc_fixup_kernel for W % 4 == 0 with 16-B aligned buffers: a thread takes 4 consecutive
