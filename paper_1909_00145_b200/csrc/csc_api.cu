@@ -120,6 +120,7 @@ struct csc_ctx {
   csc::TcPlan tc{};
   float* tc_part = nullptr;
   int* tc_sched = nullptr;  // conv_h: the balanced item schedule (c->tc.sched points here)
+  int* ct_sched = nullptr;  // code_h: the balanced item schedule (c->ct.sched points here)
   float* tc_bimg = nullptr;
   // fp16-split dense pass: scale bounds (float bits): [0] = bound of max|z|, [1] = max|filter|
   uint32_t* smax = nullptr;
@@ -565,6 +566,13 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
         c->ct_on = true;
         ok = ok && alloc(reinterpret_cast<void**>(&c->mwords), sizeof(uint32_t) * c->ct.sw_words);
         if (c->ct.half) ok = ok && alloc(reinterpret_cast<void**>(&c->a3_part), sizeof(float) * c->ct.a3_floats);
+        if (ok && c->ct.half) {
+          std::vector<int> sched;
+          csc::code_h_schedule(g, c->ct, sched);
+          ok = alloc(reinterpret_cast<void**>(&c->ct_sched), sizeof(int) * sched.size()) &&
+               cudaMemcpy(c->ct_sched, sched.data(), sizeof(int) * sched.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+          c->ct.sched = c->ct_sched;
+        }
         ok = ok && alloc(reinterpret_cast<void**>(&c->rmax), sizeof(uint32_t) * 4);
       }
     }
@@ -771,6 +779,7 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->lip_part);
   cudaFree(c->tc_part);
   cudaFree(c->tc_sched);
+  cudaFree(c->ct_sched);
   cudaFree(c->tc_bimg);
   cudaFree(c->smax);
   cudaFree(c->dscal);

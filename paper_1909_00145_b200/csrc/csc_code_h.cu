@@ -37,7 +37,9 @@
 
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -157,6 +159,7 @@ struct ChArgs {
   int plain;             // 1: z <- c at every position (no z read, no step / shrinkage / mask / a3')
   int tau_stride;        // 0: tau[0] for every filter; 1: tau[k] per filter (ESO rule)
   int precise;           // plain mode: hi*hi and the cross terms in separate accumulators
+  const int* sched;      // [G + 1] CTA offsets, then [nitems] items (code_h_schedule); nullptr: round robin
   unsigned long long* dbg;  // CSC_ROLE_TIMING: [grid][4 roles][8] cycle counters
   int dbgflags;             // CSC_ROLE_TIMING builds: CSC_CH_DBG experiment switches
 };
@@ -164,7 +167,9 @@ struct ChArgs {
 struct ChItem {
   int n, u0, u1, p0, p1, ntiles, band;
 };
-__device__ __forceinline__ ChItem ch_item(const ChArgs& A, int item) {
+// j: a position in the item list (the schedule's list, or the item itself without one)
+__device__ __forceinline__ ChItem ch_item(const ChArgs& A, int j) {
+  const int item = A.sched != nullptr ? A.sched[A.G + 1 + j] : j;
   ChItem it;
   it.n = item / A.nbands;
   it.band = item - it.n * A.nbands;
@@ -189,6 +194,10 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
 
   const int tid = threadIdx.x, warp = __shfl_sync(kFullMask, tid >> 5, 0), lane = tid & 31;
   const int gi = blockIdx.x % A.G, kg = blockIdx.x / A.G;
+  // this CTA's item-list positions: jbeg, jbeg + jstep, ... < jend
+  const int jbeg = A.sched != nullptr ? A.sched[gi] : gi;
+  const int jend = A.sched != nullptr ? A.sched[gi + 1] : A.nitems;
+  const int jstep = A.sched != nullptr ? 1 : A.G;
   const bool plain = A.plain != 0;
   const bool a3p = !plain && A.part != nullptr;
   // plain mode (ADMM's D^T e) with separate hi*hi / cross accumulators, single-buffered (T3)
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       mma_commit_elect(&acc_empty[bu]);
     };
     uint32_t g = 0, tcount = 0;
-    for (int item = gi; item < A.nitems; item += A.G) {
+    for (int item = jbeg; item < jend; item += jstep) {
       const ChItem it = ch_item(A, item);
       for (int tl = 0; tl < it.ntiles; ++tl, ++tcount) {
         const uint32_t buf = prec ? 0u : (tcount & 1u), use = prec ? tcount : (tcount >> 1);
@@ -386,21 +395,21 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       return nv >= 16 ? 0xFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
     };
     // tile cursors: the current tile and the next (its slices are loaded one tile ahead)
-    int item = gi, tl = 0;
-    ChItem it = ch_item(A, item < A.nitems ? item : 0);
+    int item = jbeg, tl = 0;
+    ChItem it = ch_item(A, item < jend ? item : 0);
     int ni = item, ntl = 0;
     ChItem nit = it;
     auto step = [&](int& itm, int& t, ChItem& c) {
       if (++t >= c.ntiles) {
         t = 0;
-        itm += A.G;
-        if (itm < A.nitems) c = ch_item(A, itm);
+        itm += jstep;
+        if (itm < jend) c = ch_item(A, itm);
       }
     };
     // TMA of chunk s (group (jq + tc) mod E + E s, E = epilogue warps per quarter) of tile (itm, t): the {32 positions, 16 filters}
     // code slice and the 32 selection words; an empty arrival when the group does not exist
     auto issue = [&](int itm, int t, const ChItem& c, uint32_t tc, int s) {
-      if (plain || itm >= A.nitems) return;
+      if (plain || itm >= jend) return;
       const int g = static_cast<int>((jq + tc) % kChEpiPerQ) + kChEpiPerQ * s;
       if (lane == 0) {
         if (g < A.ngroups) {
@@ -417,8 +426,8 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     RoleClock rc;
     uint32_t tcount = 0;
     for (int s0 = 0; s0 < kChChunks; ++s0) issue(item, tl, it, 0u, s0);
-    if (ni < A.nitems) step(ni, ntl, nit);
-    while (item < A.nitems) {
+    if (ni < jend) step(ni, ntl, nit);
+    while (item < jend) {
       const uint32_t buf = prec ? 0u : (tcount & 1u), use = prec ? tcount : (tcount >> 1);
       const int p = it.p0 + tl * kChTile + 32 * q + lane;
       const bool pok = p < it.p1;
@@ -553,7 +562,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
         if (lane == 0) mbar_arrive(&acc_empty[buf]);
       }
       step(item, tl, it);
-      if (ni < A.nitems) step(ni, ntl, nit);
+      if (ni < jend) step(ni, ntl, nit);
       ++tcount;
     }
     if (ew == 0 && lane == 0) RT_DUMP(rc, A.dbg, 2);
@@ -753,8 +762,8 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
     };
     // per tile t: the im2col of tile t+1 (the tensor pipe needs it right after C(t)), then the col2im of
     // tile t-1 (its Y is ready once GEMM 2 of t-1, issued after C(t), completes)
-    int item = gi;
-    if (item < A.nitems) {
+    int item = jbeg;
+    if (item < jend) {
       ChItem it = ch_item(A, item);
       int tl = 0;
       ChItem pit = it;
@@ -764,8 +773,8 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       auto step = [&](int& itm, int& t, ChItem& c) {
         if (++t >= c.ntiles) {
           t = 0;
-          itm += A.G;
-          if (itm < A.nitems) c = ch_item(A, itm);
+          itm += jstep;
+          if (itm < jend) c = ch_item(A, itm);
         }
       };
       fill(it);
@@ -773,8 +782,8 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
       convert(it, 0, 0u);
       step(nitem, ntl, nit);
       uint32_t tcount = 0;
-      while (item < A.nitems) {
-        if (nitem < A.nitems) {
+      while (item < jend) {
+        if (nitem < jend) {
           if (nitem != item) {  // a new band: every helper is past its last use of the residual pairs
             RT_WAIT(rc, 3, named_sync(1, 32 * kChHelpWarps));
             fill(nit);
@@ -791,7 +800,7 @@ __global__ void __launch_bounds__(kChThreads, 1) code_h_kernel(const __grid_cons
         item = nitem;
         tl = ntl;
         it = nit;
-        if (nitem < A.nitems) step(nitem, ntl, nit);
+        if (nitem < jend) step(nitem, ntl, nit);
         ++tcount;
       }
       if (a3p && tcount > 0) {
@@ -917,15 +926,15 @@ CodeTcPlan code_h_plan(const Geom& g, int num_sms) {
     const int wl = (br + g.P) * g.Wc + 192;
     return smem_fixed + 2 * rs * 4 + wl * 4;
   };
-  // band height: the fewest rounds of items over the G CTAs x rows per band (tail balance), largest on ties
+  // band height: the smallest busiest-CTA cost (128-position tiles + 2 per band for the residual staging and
+  // the window flush) under the LPT schedule of code_h_schedule, the taller band on ties
   int best = 0;
   int64_t best_cost = 0;
   for (int br = 1; br <= 32 && br <= g.Hc; ++br) {
     if (smem_for(br) > kChSmemMax) break;
     if ((br * g.Wc) % 4 != 0) continue;  // every band starts 16-B aligned (TMA box starts)
     const int nb = ceil_div(g.Hc, br);
-    const int64_t rounds = ceil_div(n * nb, G);
-    const int64_t cost = rounds * (br + 1);  // +1: per-band staging / flush overhead in row units
+    const int64_t cost = g.N > 0 ? lpt_bands(g, br, std::min(G, n * nb), 2, nullptr) : br;
     if (best == 0 || cost <= best_cost) {
       best = br;
       best_cost = cost;
@@ -948,6 +957,14 @@ CodeTcPlan code_h_plan(const Geom& g, int num_sms) {
   p.ok = p.smem <= kChSmemMax;
   p.half = true;
   return p;
+}
+
+void code_h_schedule(const Geom& g, const CodeTcPlan& p, std::vector<int>& out) {
+  if (g.N <= 0 || p.nitems <= 0) {
+    out.assign(p.G + 1, 0);
+    return;
+  }
+  lpt_bands(g, p.BR, p.G, 2, &out);
 }
 
 cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, TmapCache* tmc, const float* r, const float* d,
@@ -976,6 +993,7 @@ cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, TmapCache* tmc, co
   a.plain = plain ? 1 : 0;
   a.precise = plain ? 1 : 0;  // the plain correlation (ADMM) always takes the precise accumulation
   a.tau_stride = tau_stride;
+  a.sched = p.sched;
   if (plain) {
     a.mask = nullptr;
     a.zmax = nullptr;

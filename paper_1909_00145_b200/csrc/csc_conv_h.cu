@@ -634,18 +634,18 @@ bool conv_h_supported(const Geom& g) {
 }
 
 // Longest-processing-time-first assignment of the items (image, band of BR code rows; cost = its 128-position
-// tiles + one for the band's window flush) to the G persistent CTAs: each item in decreasing cost goes to the
+// tiles + overhead for the band's staging / window flush) to the G persistent CTAs: each item in decreasing cost goes to the
 // least-loaded CTA (ties: lowest index).  Writes [G + 1] CTA offsets, then the items CTA by CTA (in the order
 // assigned), and returns the largest CTA load in tiles.  Round robin (item = CTA + j * G) leaves the CTA
 // with one item more than the others idle-free while the rest wait: at config 3 with BR = 8 the busiest CTA
 // had 170 tiles against a mean of 153.
-static int64_t conv_h_lpt(const Geom& g, int BR, int G, std::vector<int>* out) {
+int64_t lpt_bands(const Geom& g, int BR, int G, int overhead, std::vector<int>* out) {
   const int nb = ceil_div(g.Hc, BR);
   const int nitems = g.N * nb;
   std::vector<int64_t> cost(nb);
   for (int b = 0; b < nb; ++b) {
     const int u0 = b * BR, u1 = std::min(u0 + BR, g.Hc);
-    cost[b] = ceil_div((u1 - u0) * g.Wc, 128) + 1;
+    cost[b] = ceil_div((u1 - u0) * g.Wc, 128) + overhead;
   }
   // stable order of decreasing cost (items of one cost keep their image-major order)
   std::vector<int> order(nitems);
@@ -702,7 +702,7 @@ bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p) {
       BR = br;
       continue;
     }
-    const int64_t c = conv_h_lpt(g, br, std::min(G, g.N * ceil_div(g.Hc, br)), nullptr);
+    const int64_t c = lpt_bands(g, br, std::min(G, g.N * ceil_div(g.Hc, br)), 1, nullptr);
     if (BR == 0 || c <= best) {
       BR = br;
       best = c;
@@ -728,7 +728,7 @@ void conv_h_schedule(const Geom& g, const TcPlan& p, std::vector<int>& out) {
     out.assign(p.grid + 1, 0);
     return;
   }
-  conv_h_lpt(g, p.BR, p.grid, &out);
+  lpt_bands(g, p.BR, p.grid, 1, &out);
 }
 
 cudaError_t launch_absmax(const float* x, int64_t n, uint32_t* out, cudaStream_t st) {

@@ -154,6 +154,9 @@ cudaError_t launch_conv_ss(const Geom& g, const TcPlan& p, TmapCache* tmc, const
 // (float bits, device); fmax: written with max|filt| (float bits, device).
 bool conv_h_supported(const Geom& g);
 bool conv_h_plan(const Geom& g, int num_sms, TcPlan& p);
+// LPT assignment of the (image, band of BR code rows) items to G CTAs, cost = 128-position tiles + overhead:
+// returns the busiest CTA's cost; out (if any) = [G + 1] CTA offsets, then the items CTA by CTA
+int64_t lpt_bands(const Geom& g, int BR, int G, int overhead, std::vector<int>* out);
 // the balanced item schedule of a conv_h plan: [grid + 1] CTA offsets, then the items CTA by CTA
 void conv_h_schedule(const Geom& g, const TcPlan& p, std::vector<int>& out);
 // build_b = false reuses the fp16 filter image (and fmax) of the previous call with the same filt.
@@ -220,6 +223,7 @@ struct CodeTcPlan {
   // a3' band partials [nkg][N][nbands][BR+P][W] (a3_floats)
   int ngroups, BR, nbands, WL;
   size_t a3_floats;
+  const int* sched = nullptr;  // device copy of code_h_schedule (owned by the context), or round robin
 };
 bool code_tc_supported(const Geom& g);
 CodeTcPlan code_tc_plan(const Geom& g, int num_sms);
@@ -229,6 +233,8 @@ cudaError_t launch_mask_selwords(const Geom& g, const CodeTcPlan& p, uint64_t se
 // fp16-split variant (csc_code_h.cu): Hc*Wc % 4 == 0 (TMA view of z); rmax = max|r| (float bits).
 bool code_h_supported(const Geom& g);
 CodeTcPlan code_h_plan(const Geom& g, int num_sms);
+// the balanced item schedule of a code_h plan (the G CTAs of one filter group; every group runs the same list)
+void code_h_schedule(const Geom& g, const CodeTcPlan& p, std::vector<int>& out);
 // a3_part != nullptr (and !plain): the incremental residual r' = r + D dz is written as band partials
 // [nkg][N][nbands][BR+P][W]; launch_code_a3_fixup then adds them to r (a3').
 cudaError_t launch_code_h(const Geom& g, const CodeTcPlan& p, TmapCache* tmc, const float* r, const float* d,
