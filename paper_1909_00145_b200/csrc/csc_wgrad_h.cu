@@ -30,7 +30,9 @@
 
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -641,6 +643,36 @@ WhPlan wgrad_h_plan(const Geom& g, int num_sms) {
   while (nr < 4 && smem_for(nb, nr + 1, L) <= kWhSmemMax) ++nr;
   while (nb < 4 && smem_for(nb + 1, nr, L) <= kWhSmemMax) ++nb;
   while (L > 64 && smem_for(nb, nr, L) > kWhSmemMax) L -= 64;
+  // the segment length among those with the same staged residual rows (same shared memory): the smallest
+  // busiest-CTA load under the round-robin item order, in chunks + 2 per item (the residual staging); at
+  // config 3 L = 832 -> 960: the busiest CTA 360 -> 340 chunk units
+  if (g.N > 0) {
+    auto load = [&](int64_t len) {
+      const int64_t ns = (plane + len - 1) / len;
+      const int64_t ni = static_cast<int64_t>(g.N) * ns;
+      const int64_t Gi = std::min<int64_t>(G, ni);
+      // CTA c takes items c, c + Gi, ...
+      std::vector<int64_t> ld(static_cast<size_t>(Gi), 0);
+      for (int64_t i = 0; i < ni; ++i) {
+        const int64_t sg = i % ns, l = std::min<int64_t>(len, plane - sg * len);
+        ld[static_cast<size_t>(i % Gi)] += (l + kWhChunk - 1) / kWhChunk + 2;
+      }
+      int64_t mx = 0;
+      for (int64_t v : ld) mx = std::max(mx, v);
+      return mx;
+    };
+    const int rows0 = rows_for(L);
+    int64_t bestL = L, best = load(L);
+    for (int64_t l2 = 256; l2 <= 4096; l2 += 64) {
+      if (rows_for(l2) > rows0) continue;
+      const int64_t c = load(l2);
+      if (c < best || (c == best && l2 > bestL)) {
+        best = c;
+        bestL = l2;
+      }
+    }
+    L = bestL;
+  }
   p.NB = nb;
   p.NR = nr;
   p.L = static_cast<int>(L);
