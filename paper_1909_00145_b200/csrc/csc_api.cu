@@ -74,6 +74,7 @@ constexpr double kBcdRidge = 1e-10;  // DESIGN.md reading B2
 // csc_count_nonzero (host mirror only)
 enum DSlot { kSqR = 0, kL1 = 1, kZg2 = 2, kGG = 3, kLhat = 4, kCounter = 6, kCnt = 7, kNumD = 8 };
 enum FSlot { kTauZ = 0, kTauD = 1, kNumF = 4 };
+constexpr size_t kScalBytes = sizeof(double) * kNumD + sizeof(float) * kNumF;  // dscal then fscal, one block
 
 }  // namespace
 
@@ -585,11 +586,12 @@ csc_status csc_init(const csc_dims* dims, csc_ctx** out) {
   ok = ok && alloc(reinterpret_cast<void**>(&c->tauk), sizeof(float) * g.K);
   ok = ok && alloc(reinterpret_cast<void**>(&c->colw), sizeof(uint32_t) * static_cast<size_t>(g.K) * NB * g.Wc);
   ok = ok && alloc(reinterpret_cast<void**>(&c->lip_part), sizeof(double) * (64 * 64 * csc::ceil_div(g.K, 2) + 64));
-  ok = ok && alloc(reinterpret_cast<void**>(&c->dscal), sizeof(double) * kNumD);
+  // the fp64 and fp32 scalars share one block (fscal follows dscal): one D2H copy reads both
+  ok = ok && alloc(reinterpret_cast<void**>(&c->dscal), kScalBytes);
+  if (ok) c->fscal = reinterpret_cast<float*>(c->dscal + kNumD);
   ok = ok && alloc(reinterpret_cast<void**>(&c->gf_scratch), sizeof(double) * (csc::ceil_div(g.K * g.S * g.S, 256) + 1));
-  ok = ok && alloc(reinterpret_cast<void**>(&c->fscal), sizeof(float) * kNumF);
-  ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_dscal), sizeof(double) * kNumD) == cudaSuccess;
-  ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_fscal), sizeof(float) * kNumF) == cudaSuccess;
+  ok = ok && cudaMallocHost(reinterpret_cast<void**>(&c->h_dscal), kScalBytes) == cudaSuccess;
+  if (ok) c->h_fscal = reinterpret_cast<float*>(c->h_dscal + kNumD);
   // tensor-core dense path unless CSC_DENSE_PATH=simt
   {
     const char* ev = std::getenv("CSC_DENSE_PATH");
@@ -782,13 +784,10 @@ csc_status csc_destroy(csc_ctx* c) {
   cudaFree(c->ct_sched);
   cudaFree(c->tc_bimg);
   cudaFree(c->smax);
-  cudaFree(c->dscal);
-  cudaFree(c->fscal);
+  cudaFree(c->dscal);  // fscal, h_fscal and h_res_f point into the dscal / h_dscal / h_res_d blocks
   cudaFreeHost(c->h_dscal);
-  cudaFreeHost(c->h_fscal);
   for (int i = 0; i < 2; ++i) {
     cudaFreeHost(c->h_res_d[i]);
-    cudaFreeHost(c->h_res_f[i]);
     if (c->res_ev[i]) cudaEventDestroy(c->res_ev[i]);
   }
   delete c;
@@ -1365,8 +1364,7 @@ static csc_status objective_enqueue(csc_ctx* c, const float* x, const float* d, 
   if (s != CSC_OK) return s;
   s = allreduce_d(c, c->dscal + kSqR, 2);
   if (s != CSC_OK) return s;
-  CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal, c->dscal, sizeof(double) * kNumD, cudaMemcpyDeviceToHost, c->st));
-  CSC_CUDA(c, cudaMemcpyAsync(c->h_fscal, c->fscal, sizeof(float) * kNumF, cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_dscal, c->dscal, kScalBytes, cudaMemcpyDeviceToHost, c->st));
   return CSC_OK;
 }
 
@@ -1540,8 +1538,8 @@ csc_status csc_iterate_staged_async(csc_ctx* c, int slot, float* x, float* d, fl
   CSC_CUDA(c, cudaSetDevice(c->device));
   if (c->h_res_d[0] == nullptr) {
     for (int i = 0; i < 2; ++i) {
-      CSC_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_res_d[i]), sizeof(double) * kNumD));
-      CSC_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_res_f[i]), sizeof(float) * kNumF));
+      CSC_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_res_d[i]), kScalBytes));
+      c->h_res_f[i] = reinterpret_cast<float*>(c->h_res_d[i] + kNumD);
       CSC_CUDA(c, cudaEventCreateWithFlags(&c->res_ev[i], cudaEventDisableTiming));
     }
   }
@@ -1551,8 +1549,7 @@ csc_status csc_iterate_staged_async(csc_ctx* c, int slot, float* x, float* d, fl
   (void)dummy;
   csc_status s = iterate_impl(c, nullptr, slot, x, d, z, lambda, step_z, step_d, p, seed, iter, nullptr, nullptr);
   if (s != CSC_OK) return s;
-  CSC_CUDA(c, cudaMemcpyAsync(c->h_res_d[k], c->dscal, sizeof(double) * kNumD, cudaMemcpyDeviceToHost, c->st));
-  CSC_CUDA(c, cudaMemcpyAsync(c->h_res_f[k], c->fscal, sizeof(float) * kNumF, cudaMemcpyDeviceToHost, c->st));
+  CSC_CUDA(c, cudaMemcpyAsync(c->h_res_d[k], c->dscal, kScalBytes, cudaMemcpyDeviceToHost, c->st));
   CSC_CUDA(c, cudaEventRecord(c->res_ev[k], c->st));
   c->res_lam[k] = lambda;
   const int prev = c->res_pending;
